@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 gate-application hot path (driver contract: one JSON line).
+
+Metric (BASELINE.json): "sec/gate & effective HBM GB/s vs roofline at N
+qubits, 1/2/4/8 B200; adder circuit time".
+
+Workload at N=1 GPU = BASELINE config[1]: "Hadamard + random 1q/2q gate
+layers, N=33 FP64 on 1xB200 (128 GiB state)": H on all 33 qubits followed by
+random layers drawn with the reference's generator (tests/circuits.py
+random_circuit, depth 33 per layer, every gate kind).  One *step* = one
+layer of 33 gates applied to the 2**33-amplitude state resident in HBM.
+
+  value      = effective HBM GB/s over the timed steps: the algorithmic bytes
+               of every gate (2*16*L read+write per non-diagonal gate,
+               2*16*L/2**k for a diagonal on k qubits),
+               summed over all GPUs, divided by the device time (CUDA events,
+               max over ranks).  Gates are fused into tile passes, so this can
+               exceed the HBM peak; roofline.* reports the per-pass truth.
+  roofline   = the dominant kernel (k_fused, one read + one write of the
+               state per launch), its algorithmic bytes / average launch time
+               from CUDA events bracketing every launch on its own stream.
+  e2e        = the same metric through the public API: run_circuit() on a
+               Circuit built on the host (layer + measure-all), state
+               allocated and zeroed by the call, report copied back.
+  cpu_baseline = the reference algorithm (numpy port in oracle/, threaded over
+               the box's cores) on a bounded sample of the same layers at N=24.
+
+`--impl reference` runs only that CPU arm (rank 0) and prints its own line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sec/gate & effective HBM GB/s vs roofline at N qubits, 1/2/4/8 B200; adder circuit time"
+SEED = 20240817
+CPU_SAMPLE_N = 24
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def workload_layers(n: int, n_layers: int):
+    """H on every qubit, then random layers (depth n) — the BASELINE config[1] circuit."""
+    from tests.circuits import random_circuit
+    from oracle.ref_gates import OGate
+    rng = np.random.default_rng(SEED)
+    layers = [tuple(OGate("H", (q,)) for q in range(n))]
+    for _ in range(n_layers - 1):
+        layers.append(random_circuit(rng, n, n, measured=False).gates)
+    return layers
+
+
+def layer_bytes(layer, n: int, bpe: int = 16) -> int:
+    from oracle.cpu_baseline import gate_bytes
+    return sum(gate_bytes(g, n, bpe) for g in layer)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def dist_init(world):
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    return dist
+
+
+def max_over_ranks(dist, value: float) -> float:
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(dist, value: float) -> float:
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# --------------------------------------------------------------------------------------------
+def cpu_baseline(steps: int, n_layers: int, sample_n: int = CPU_SAMPLE_N):
+    from oracle.cpu_baseline import time_layers
+    layers = workload_layers(sample_n, n_layers)
+    chosen = [layers[i % len(layers)] for i in range(steps)]
+    res, threads = time_layers(chosen, sample_n)
+    secs = sum(r[0] for r in res)
+    byts = sum(r[1] for r in res)
+    gates = sum(r[2] for r in res)
+    return {"value": byts / secs / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+            "sec_per_gate": secs / gates,
+            "sample": f"{len(chosen)} layer(s) x {n_layers}-layer workload at N={sample_n} FP64 "
+                      f"({gates} gates, {secs:.1f} s), numpy port of svsim/kernels.py in oracle/, "
+                      f"{threads} threads"}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.cpu_baseline import time_layers
+    layers = workload_layers(CPU_SAMPLE_N, args.layers)
+    seq = [layers[i % len(layers)] for i in range(args.warmup + args.steps)]
+    res, threads = time_layers(seq, CPU_SAMPLE_N)
+    timed = res[args.warmup:]
+    secs = sum(r[0] for r in timed)
+    byts = sum(r[1] for r in timed)
+    gates = sum(r[2] for r in timed)
+    val = byts / secs / 1e9
+    line = {
+        "metric": METRIC, "value": round(val, 4), "unit": "GB/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(secs / max(1, len(timed)) * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+        "data": "synthetic", "sec_per_gate": secs / gates,
+        "config": {"workload": f"C2 layers sampled at N={CPU_SAMPLE_N} (reference CPU path cannot hold "
+                               f"N={args.n}: 128 GiB + copies)", "n_qubits": CPU_SAMPLE_N,
+                   "layer_gates": CPU_SAMPLE_N, "precision": "fp64"},
+        "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{len(timed)} timed layers at N={CPU_SAMPLE_N}, numpy port of "
+                                   f"svsim/kernels.py (oracle/), {threads} threads"},
+        "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------------
+def run_b200(args):
+    rank, world, local = dist_env()
+    dist = dist_init(world)
+    import paper_2511_03359_b200 as pb
+    from paper_2511_03359_b200 import _native as nat
+    from paper_2511_03359_b200.device import DeviceState
+    from paper_2511_03359_b200.engine import gate_to_op
+    from tests.circuits import to_product
+    from oracle.ref_builders import OCircuit
+
+    device = local if world > 1 else 0
+    n = args.n
+    layers_o = workload_layers(n, args.layers)
+    layers = [to_product(OCircuit(n, tuple(l))).gates for l in layers_o]
+    lbytes = [layer_bytes(l, n) for l in layers_o]
+    step_layers = [i % len(layers) for i in range(args.warmup + args.steps)]
+
+    dev = DeviceState(n, pb.PrecisionMode.FP64, device=device)
+    dev.zero(0)
+    ops = [[gate_to_op(g) for g in layer] for layer in layers]
+    for i in step_layers[:args.warmup]:
+        dev.apply_fused(ops[i], args.tile_bits)
+    dev.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ev0, ev1 = nat.Event(), nat.Event()
+    launches0 = nat.launch_count()
+    nat.pass_timing(True)
+    nat.pass_timing_read()
+    with ClockSampler(device) as clk:
+        ev0.record(dev.stream)
+        for i in step_layers[args.warmup:]:
+            dev.apply_fused(ops[i], args.tile_bits)
+        ev1.record(dev.stream)
+        dev.synchronize()
+    nat.pass_timing(False)
+    passes, pass_ms, pass_bytes = nat.pass_timing_read()
+    launches = nat.launch_count() - launches0
+    ms = ev0.elapsed_ms(ev1)
+    if dist is not None:
+        dist.barrier()
+    ms_max = max_over_ranks(dist, ms)
+    timed_bytes = sum(lbytes[i] for i in step_layers[args.warmup:])
+    timed_gates = sum(len(layers[i]) for i in step_layers[args.warmup:])
+    total_bytes = sum_over_ranks(dist, timed_bytes)
+    value = total_bytes / (ms_max / 1e3) / 1e9
+    peak, peak_src = peaks()
+    achieved = pass_bytes / (pass_ms / 1e3) / 1e9 if pass_ms > 0 else 0.0
+
+    # single-gate streaming kernel (no fusion): the per-gate roofline the north star names
+    single = {}
+    if args.single_gate:
+        h = pb.gates.H_MATRIX
+        for q in (0, 1, n // 2, n - 1):
+            e0, e1 = nat.Event(), nat.Event()
+            dev.apply_1q(q, h)
+            e0.record(dev.stream)
+            for _ in range(3):
+                dev.apply_1q(q, h)
+            e1.record(dev.stream)
+            t = e0.elapsed_ms(e1) / 3
+            single[f"q{q}"] = {"ms": round(t, 3), "GB/s": round(2 * 16 * dev.size / (t / 1e3) / 1e9, 1)}
+    dev.free()
+    del dev
+
+    # end to end through the public API (host-built circuit in, report out)
+    e2e = None
+    if args.e2e_steps > 0:
+        h2d0, d2h0 = nat.transfer_bytes()
+        t_e2e = 0.0
+        e2e_bytes = 0
+        for j in range(args.e2e_steps):
+            li = 1 + j % (len(layers) - 1) if len(layers) > 1 else 0
+            circ = pb.Circuit(n, tuple(layers[li]) + (pb.gates.measure_all(),))
+            t0 = time.perf_counter()
+            res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
+            _ = res.report.qz[0]
+            t_e2e += time.perf_counter() - t0
+            e2e_bytes += lbytes[li]
+            del res
+        h2d1, d2h1 = nat.transfer_bytes()
+        t_e2e = max_over_ranks(dist, t_e2e)
+        e2e = {"value": round(sum_over_ranks(dist, e2e_bytes) / t_e2e / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": (h2d1 - h2d0) // args.e2e_steps,
+               "d2h_bytes_per_step": (d2h1 - d2h0) // args.e2e_steps,
+               "what": "run_circuit(layer + M): allocate + zero 2^N state, fused layer, measure-all, "
+                       "report to host; wall clock per call"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(max(1, args.cpu_layers), args.layers)
+
+    clocks = clk.summary()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic",
+            "sec_per_gate": round(ms_max / 1e3 / timed_gates, 6),
+            "config": {"workload": f"C2: H layer + random 1q/2q/diag layers (depth {n}), N={n} FP64 "
+                                   f"per GPU, {2 ** n * 16 / 2 ** 30:.0f} GiB state",
+                       "n_qubits_per_gpu": n, "n_qubits_total": n + (world.bit_length() - 1),
+                       "gates_per_step": n, "layers": args.layers, "tile_bits": args.tile_bits,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs (128 GiB) >> 126 MB L2; no flush needed"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "kernel": "k_fused<c64s,12>", "launches_timed": passes,
+                         "bytes_per_launch": 2 * 16 * 2 ** n},
+            "gpu_launches": launches,
+            "fused_passes_per_step": round(passes / args.steps, 2),
+            "clocks": clocks,
+        }
+        if single:
+            line["single_gate_h"] = single
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=33, help="qubits per GPU")
+    ap.add_argument("--layers", type=int, default=9, help="H layer + random layers in the workload")
+    ap.add_argument("--tile-bits", type=int, default=12)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-layers", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--single-gate", action="store_true", default=True)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,137 @@
+/*
+ * svb200.h — C ABI of the B200-native gate-application hot path.
+ *
+ * Drop-in boundary for the reference package `svsim`
+ * (/root/reference/pkg/src/svsim).  The reference is pure Python + numpy and
+ * has no FFI of its own; the entry points below are what its hot-path
+ * operators bind to when they are re-pointed at this library (the ctypes
+ * binding lives in paper_2511_03359_b200/_native.py; INTEGRATION.md shows
+ * the stub a reference maintainer would add).  Each entry point names the
+ * reference interface it replaces.
+ *
+ * Conventions
+ *   - plain C types only: pointers, sizes, int status codes;
+ *   - every function returns SV_OK (0) or a negative SV_E* code, and the
+ *     message of the last failure on the calling thread is available from
+ *     sv_last_error();
+ *   - SV_EINDEX maps to Python IndexError, SV_EVALUE to ValueError,
+ *     SV_ECUDA / SV_ENOMEM to RuntimeError / MemoryError, matching the
+ *     reference's exception types (kernels.py:23-24, 34-35, 49-52);
+ *   - amplitude storage: SV_FP64 = interleaved complex128 (16 B),
+ *     SV_FP32 = interleaved complex64 (8 B) (state.py:20-27);
+ *   - a matrix is row-major complex entries as (re, im) doubles:
+ *     2x2 -> 8 doubles, 4x4 -> 32 doubles, basis index bit(qa) + 2*bit(qb)
+ *     (gates.py:24, kernels.py:46).
+ *   - "svk_*" functions take raw device pointers and a cudaStream_t (passed
+ *     as void*), "sv_*" functions take a state handle that owns its device
+ *     memory and stream.
+ */
+#ifndef SVB200_H
+#define SVB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SV_ABI_VERSION 1
+
+enum { SV_OK = 0, SV_EINDEX = -1, SV_EVALUE = -2, SV_ECUDA = -3, SV_ENOMEM = -4 };
+enum { SV_FP64 = 0, SV_FP32 = 1, SV_BYTE = 2 };              /* state.py:20-27 PrecisionMode */
+enum { SV_OP_1Q = 1, SV_OP_2Q = 2, SV_OP_DIAG = 3 };
+
+typedef struct sv_state* sv_handle;
+
+/* One gate of a fused pass (see sv_apply_fused). */
+typedef struct {
+    int32_t kind;          /* SV_OP_1Q / SV_OP_2Q / SV_OP_DIAG */
+    int32_t qa, qb;        /* local qubits (qb unused for 1Q; unused for DIAG) */
+    int32_t reserved;
+    uint64_t diag_mask;    /* DIAG: local-index bits that must all read 1 */
+    double m[32];          /* 1Q: 8 doubles, 2Q: 32 doubles, DIAG: factor (re, im) */
+} sv_op;
+
+/* ---- library -------------------------------------------------------- */
+int sv_abi_version(void);
+const char* sv_last_error(void);
+int sv_device_count(int* count);
+int sv_sm_count(int device, int* count);
+
+/* ---- raw device-pointer kernels (one call = one kernel launch) ------ */
+/* kernels.py:30-40 apply_single: in-place 2x2 on pairs (i, i + 2^q) of a
+ * buffer of n_elems amplitudes (n_elems a multiple of 2^(q+1)). */
+int svk_apply_1q(void* psi, uint64_t n_elems, int mode, int q, const double* m8, void* stream);
+/* kernels.py:43-64 apply_two: in-place 4x4 on the quadruples of (qa, qb). */
+int svk_apply_2q(void* psi, uint64_t n_elems, int mode, int qa, int qb, const double* m32,
+                 void* stream);
+/* kernels.py:67-81 apply_diagonal: multiply (array first) where all bits of
+ * mask are 1; mask == 0 scales the whole buffer. */
+int svk_apply_diag(void* psi, uint64_t n_elems, int mode, uint64_t mask, const double* f2,
+                   void* stream);
+/* kernels.py:84-88 apply_pair_arrays, in place over two aligned buffers
+ * (a1 may be a peer-GPU pointer: the exchange-fused update). */
+int svk_pair_update(void* a0, void* a1, uint64_t count, int mode, const double* m8, void* stream);
+/* kernels.py:91-98 apply_quad_arrays, in place over four aligned buffers. */
+int svk_quad_update(void* const* parts, uint64_t count, int mode, const double* m32,
+                    void* stream);
+/* engine.py:166-180 run of local gates as ONE pass over HBM: ops applied in
+ * order, each with the reference arithmetic, on tiles of 2^tile_bits
+ * amplitudes staged in shared memory. n_elems must be a power of two. */
+int svk_apply_fused(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_ops,
+                    int tile_bits, void* stream);
+/* measure.py:51-56 + 59-109: norm, per-qubit one-weights and cross sums of
+ * a buffer of 2^n amplitudes.  ones[n], cross[2n] (re, im). */
+int svk_measure(const void* psi, uint64_t n_elems, int mode, double* norm, double* ones,
+                double* cross, void* stream);
+
+/* ---- state handles (state.py:34-103 LocalState) --------------------- */
+int sv_create(int device, int n_qubits, int mode, sv_handle* out);
+int sv_destroy(sv_handle h);
+/* state.py:49-63 zero_state: all zeros, amplitude 1 at index `unit` (-1: none) */
+int sv_zero_state(sv_handle h, int64_t unit);
+int sv_info(sv_handle h, int* device, int* n_qubits, int* mode, void** dev_ptr, void** stream);
+int sv_apply_1q(sv_handle h, int q, const double* m8);
+int sv_apply_2q(sv_handle h, int qa, int qb, const double* m32);
+int sv_apply_diag(sv_handle h, uint64_t mask, const double* f2);
+int sv_apply_fused(sv_handle h, const sv_op* ops, int n_ops, int tile_bits);
+int sv_measure(sv_handle h, double* norm, double* ones, double* cross);
+/* raw storage elements [first, first+count) <-> host memory */
+int sv_export(sv_handle h, void* host, uint64_t first, uint64_t count);
+int sv_import(sv_handle h, const void* host, uint64_t first, uint64_t count);
+int sv_synchronize(sv_handle h);
+
+/* ---- raw device buffers (for the array-level operator API) --------- */
+int sv_buffer_alloc(int device, uint64_t bytes, void** ptr);
+int sv_buffer_free(int device, void* ptr);
+int sv_copy_h2d(void* dst, const void* src, uint64_t bytes, void* stream);
+int sv_copy_d2h(void* dst, const void* src, uint64_t bytes, void* stream);
+int sv_stream_create(int device, void** stream);
+int sv_stream_destroy(void* stream);
+
+/* ---- instrumentation ------------------------------------------------ */
+/* number of kernels this library has launched in the process */
+int sv_launch_count(uint64_t* count);
+/* host<->device bytes this library has moved (copies plus the kernel-
+ * parameter blocks of fused passes, which the driver ships per launch) */
+int sv_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
+/* per-launch CUDA-event timing of fused passes (off by default): when on,
+ * every fused-pass kernel is bracketed by events on its own stream */
+int sv_pass_timing(int enable);
+/* passes timed since the last call, their summed device time (ms) and the
+ * summed algorithmic bytes (one read + one write of the buffer per pass);
+ * synchronises on the recorded events and resets the record */
+int sv_pass_timing_read(uint64_t* passes, double* ms, double* bytes);
+
+/* ---- device timing (CUDA events on the handle's / given stream) ------ */
+int sv_event_create(void** ev);
+int sv_event_destroy(void* ev);
+int sv_event_record(void* ev, void* stream);
+int sv_event_elapsed_ms(void* start, void* stop, float* ms);
+int sv_stream_synchronize(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVB200_H */

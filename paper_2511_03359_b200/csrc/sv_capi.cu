@@ -1,0 +1,681 @@
+// extern "C" boundary of libsvb200.so (declared in include/svb200.h).
+//
+// Validation and error texts follow the reference operators they replace
+// (/root/reference/pkg/src/svsim/kernels.py:23-24, 34-35, 49-52) so the
+// Python layer can re-raise the same exception types with the same messages.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <atomic>
+#include <mutex>
+
+#include "sv_common.cuh"
+#include "sv_kernels.cuh"
+
+using namespace sv;
+
+namespace sv { uint64_t launch_total(); }
+
+namespace {
+
+thread_local std::string g_err;
+
+std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
+inline void count_h2d(uint64_t b) { g_h2d.fetch_add(b, std::memory_order_relaxed); }
+inline void count_d2h(uint64_t b) { g_d2h.fetch_add(b, std::memory_order_relaxed); }
+
+struct TimedPass { cudaEvent_t a, b; double bytes; };
+bool g_timing = false;
+std::mutex g_timing_mu;
+std::vector<TimedPass> g_timed;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    cudaGetLastError();  // clear sticky-free errors
+    return fail(e == cudaErrorMemoryAllocation ? SV_ENOMEM : SV_ECUDA, "%s: %s (%s)", what,
+                cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define CUDA_TRY(expr, what)                               \
+    do {                                                   \
+        cudaError_t _e = (expr);                           \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
+inline bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
+inline int log2u(uint64_t x) { return 63 - __builtin_clzll(x); }
+inline size_t elem_bytes(int mode) { return mode == SV_FP32 ? 8 : 16; }
+inline bool valid_fp_mode(int mode) { return mode == SV_FP64 || mode == SV_FP32; }
+
+// ---- scalar fallbacks for tiny / unaligned / non-power-of-two buffers -----
+template <typename S>
+__global__ void k_gate1_scalar(S* psi, uint64_t n_pairs, int q, cplx m0, cplx m1, cplx m2, cplx m3) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_pairs;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i0 = insert0(t, q), i1 = i0 | (1ull << q);
+        const cplx a0 = Store<S>::get(psi[i0]), a1 = Store<S>::get(psi[i1]);
+        psi[i0] = Store<S>::put(row2(m0, m1, a0, a1));
+        psi[i1] = Store<S>::put(row2(m2, m3, a0, a1));
+    }
+}
+
+template <typename S>
+__global__ void k_diag_all(S* psi, uint64_t n, uint64_t mask, cplx f) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        if ((i & mask) == mask) psi[i] = Store<S>::put(cmul(Store<S>::get(psi[i]), f));
+}
+
+unsigned small_grid(uint64_t items) {
+    uint64_t g = (items + 255) / 256;
+    if (g < 1) g = 1;
+    if (g > 4096) g = 4096;
+    return (unsigned)g;
+}
+
+int check_1q(uint64_t n, int q) {
+    if (q < 0 || q >= 63 || (1ull << q) >= n)
+        return fail(SV_EINDEX, "qubit %d outside local array of %llu amplitudes", q,
+                    (unsigned long long)n);
+    if (n % (2ull << q))
+        return fail(SV_EVALUE, "array of %llu amplitudes does not split into pairs of stride %llu",
+                    (unsigned long long)n, (unsigned long long)(1ull << q));
+    return SV_OK;
+}
+
+int check_2q(uint64_t n, int qa, int qb) {
+    if (qa == qb) return fail(SV_EVALUE, "two-qubit gate requires distinct qubits");
+    if (qa < 0 || qb < 0 || qa >= 63 || qb >= 63 || (1ull << qa) >= n || (1ull << qb) >= n)
+        return fail(SV_EINDEX, "qubits (%d, %d) outside local array of %llu amplitudes", qa, qb,
+                    (unsigned long long)n);
+    const int hi = qa > qb ? qa : qb;
+    if (n % (2ull << hi))
+        return fail(SV_EVALUE, "array of %llu amplitudes does not split into quadruples",
+                    (unsigned long long)n);
+    return SV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// fused-pass planning: greedy grouping of consecutive ops whose non-diagonal
+// qubits fit one tile of 2^k amplitudes; the tile always contains the lowest
+// qubits so HBM runs stay contiguous (>= 2^5 amplitudes = 512 B in FP64).
+struct PassPlan {
+    std::vector<int> ops;       // indices into the op list
+    uint64_t qmask = 0;         // qubits that must be in the tile
+    int mdata = 0;
+};
+
+int op_mdata(int kind) { return kind == SV_OP_2Q ? 32 : (kind == SV_OP_1Q ? 8 : 2); }
+
+int popcount64(uint64_t x) { return __builtin_popcountll(x); }
+
+uint64_t tile_mask_for(uint64_t qmask, int n, int k) {
+    // required qubits plus the lowest ones, k in total
+    uint64_t t = qmask;
+    for (int q = 0; q < n && popcount64(t) < k; ++q) t |= 1ull << q;
+    return t;
+}
+
+int build_params(const sv_op* ops, const PassPlan& pp, int n, int k, FusedParams& P) {
+    std::memset(&P, 0, sizeof(P));
+    const uint64_t tmask = tile_mask_for(pp.qmask, n, k);
+    P.n = n;
+    P.k = k;
+    P.tile_mask = tmask;
+    P.out_mask = ((n == 64) ? ~0ull : ((1ull << n) - 1ull)) & ~tmask;
+    P.n_tiles = 1ull << (n - k);
+    int pos_of[64];
+    int j = 0;
+    for (int q = 0; q < n; ++q) {
+        pos_of[q] = -1;
+        if ((tmask >> q) & 1) {
+            pos_of[q] = j;
+            P.tq[j++] = (int8_t)q;
+        }
+    }
+    int b = 0;
+    while (b < k && P.tq[b] == b) ++b;
+    P.b = b;
+    int md = 0;
+    P.n_ops = (int)pp.ops.size();
+    for (int i = 0; i < P.n_ops; ++i) {
+        const sv_op& o = ops[pp.ops[i]];
+        P.kind[i] = (uint8_t)o.kind;
+        P.moff[i] = (uint16_t)md;
+        const int cnt = op_mdata(o.kind);
+        for (int c = 0; c < cnt; ++c) P.mdata[md + c] = o.m[c];
+        md += cnt;
+        if (o.kind == SV_OP_1Q) {
+            P.pa[i] = (uint8_t)pos_of[o.qa];
+        } else if (o.kind == SV_OP_2Q) {
+            P.pa[i] = (uint8_t)pos_of[o.qa];
+            P.pb[i] = (uint8_t)pos_of[o.qb];
+        } else {
+            uint32_t mt = 0;
+            for (int q = 0; q < n; ++q)
+                if (((o.diag_mask >> q) & 1) && pos_of[q] >= 0) mt |= 1u << pos_of[q];
+            P.dmask_t[i] = mt;
+            P.dmask_o[i] = o.diag_mask & ~tmask;
+        }
+    }
+    return SV_OK;
+}
+
+int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_ops, int tile_bits,
+               cudaStream_t st) {
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "fused passes need FP64 or FP32 storage");
+    if (!is_pow2(n_elems)) return fail(SV_EVALUE, "fused pass needs a power-of-two buffer");
+    if ((reinterpret_cast<uintptr_t>(psi) & 31) != 0)
+        return fail(SV_EVALUE, "fused pass needs a 32-byte aligned buffer");
+    const int n = log2u(n_elems);
+    if (tile_bits <= 0) tile_bits = 12;
+    const int k = tile_bits < n ? tile_bits : n;
+    if (k < 1 || k > kMaxTileBits) return fail(SV_EVALUE, "tile bits %d out of range", tile_bits);
+    const int bmin = k >= 5 ? 5 : k;
+    const uint64_t lowfix = (1ull << bmin) - 1ull;
+    for (int i = 0; i < n_ops; ++i) {
+        const sv_op& o = ops[i];
+        if (o.kind == SV_OP_1Q) {
+            if (int rc = check_1q(n_elems, o.qa)) return rc;
+        } else if (o.kind == SV_OP_2Q) {
+            if (int rc = check_2q(n_elems, o.qa, o.qb)) return rc;
+        } else if (o.kind == SV_OP_DIAG) {
+            if (n < 64 && (o.diag_mask >> n))
+                return fail(SV_EINDEX, "diagonal mask 0x%llx outside local array of %llu amplitudes",
+                            (unsigned long long)o.diag_mask, (unsigned long long)n_elems);
+        } else {
+            return fail(SV_EVALUE, "unknown op kind %d", o.kind);
+        }
+    }
+    PassPlan cur;
+    auto flush = [&]() -> int {
+        if (cur.ops.empty()) return SV_OK;
+        FusedParams P;
+        build_params(ops, cur, n, k, P);
+        cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+        if (g_timing) {
+            cudaEventCreate(&ev0);
+            cudaEventCreate(&ev1);
+            cudaEventRecord(ev0, st);
+        }
+        cudaError_t e = launch_fused(psi, mode, P, st);
+        count_h2d(sizeof(FusedParams));
+        if (g_timing) {
+            cudaEventRecord(ev1, st);
+            std::lock_guard<std::mutex> lk(g_timing_mu);
+            g_timed.push_back({ev0, ev1, 2.0 * (double)n_elems * (mode == SV_FP32 ? 8.0 : 16.0)});
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "fused pass launch");
+        cur = PassPlan();
+        return SV_OK;
+    };
+    for (int i = 0; i < n_ops; ++i) {
+        const sv_op& o = ops[i];
+        uint64_t need = 0;
+        if (o.kind == SV_OP_1Q) need = 1ull << o.qa;
+        if (o.kind == SV_OP_2Q) need = (1ull << o.qa) | (1ull << o.qb);
+        const uint64_t merged = cur.qmask | need;
+        const bool fits = popcount64(merged | (lowfix & ((n >= 64) ? ~0ull : ((1ull << n) - 1)))) <= k;
+        if (!fits || (int)cur.ops.size() >= kMaxOps || cur.mdata + op_mdata(o.kind) > kMaxMData) {
+            if (int rc = flush()) return rc;
+        }
+        cur.qmask |= need;
+        cur.ops.push_back(i);
+        cur.mdata += op_mdata(o.kind);
+    }
+    return flush();
+}
+
+int measure_impl(const void* psi, uint64_t n_elems, int mode, double* norm, double* ones,
+                 double* cross, double* dev_partials, size_t partial_cap, cudaStream_t st) {
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "measurement needs FP64 or FP32 storage");
+    if (!is_pow2(n_elems)) return fail(SV_EVALUE, "measurement needs a power-of-two buffer");
+    const int n = log2u(n_elems);
+    if (n > 52) return fail(SV_EVALUE, "buffer too large");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int k = n < 12 ? n : 12;
+    if (n == 0) {  // a single amplitude: no qubits, just the norm
+        double h[2];
+        CUDA_TRY(cudaMemcpyAsync(h, psi, 16, cudaMemcpyDeviceToHost, st), "measure copy");
+        CUDA_TRY(cudaStreamSynchronize(st), "measure sync");
+        *norm = h[0] * h[0] + h[1] * h[1];
+        return SV_OK;
+    }
+    const int bmin = k >= 5 ? 5 : k;
+    const int grid_cap = measure_grid(dev);
+    const int slots_max = measure_slots(k, n);
+    double* partials = dev_partials;
+    const size_t need = (size_t)grid_cap * slots_max;
+    bool owned = false;
+    if (partials == nullptr || partial_cap < need) {
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&partials), need * sizeof(double), st),
+                 "measure scratch");
+        owned = true;
+    }
+    std::vector<double> host(need);
+    for (int q = 0; q < n; ++q) { ones[q] = 0; cross[2 * q] = cross[2 * q + 1] = 0; }
+    *norm = 0;
+    // pass list: first {0..k-1}, then blocks of (k - bmin) higher qubits
+    std::vector<uint64_t> passes;
+    passes.push_back((1ull << k) - 1ull);
+    for (int q = k; q < n;) {
+        uint64_t t = (1ull << bmin) - 1ull;
+        int c = 0;
+        while (q < n && c < k - bmin) { t |= 1ull << q; ++q; ++c; }
+        for (int f = bmin; popcount64(t) < k; ++f) t |= 1ull << f;   // fill (always < first new q)
+        passes.push_back(t);
+    }
+    uint64_t done = 0;
+    int rc = SV_OK;
+    for (size_t pi = 0; pi < passes.size() && rc == SV_OK; ++pi) {
+        MeasureParams P;
+        std::memset(&P, 0, sizeof(P));
+        const uint64_t tmask = passes[pi];
+        P.n = n; P.k = k;
+        P.tile_mask = tmask;
+        P.out_mask = ((1ull << n) - 1ull) & ~tmask;
+        P.n_tiles = 1ull << (n - k);
+        P.want_ones = pi == 0;
+        int j = 0, o = 0;
+        int tq[64];
+        for (int q = 0; q < n; ++q) {
+            if ((tmask >> q) & 1) { P.tq[j] = (int8_t)q; tq[j] = q; ++j; }
+            else P.oq[o++] = (int8_t)q;
+        }
+        int b = 0;
+        while (b < k && P.tq[b] == b) ++b;
+        P.b = b;
+        uint32_t cp = 0;
+        for (int i = 0; i < k; ++i)
+            if (!((done >> tq[i]) & 1)) cp |= 1u << i;
+        P.cross_pos = cp;
+        const int grid = (int)((P.n_tiles < (uint64_t)grid_cap) ? P.n_tiles : grid_cap);
+        const int slots = measure_slots(k, n);
+        cudaError_t e = launch_measure(psi, mode, P, partials, grid, st);
+        if (e != cudaSuccess) { rc = cuda_fail(e, "measure launch"); break; }
+        e = cudaMemcpyAsync(host.data(), partials, sizeof(double) * grid * slots, cudaMemcpyDeviceToHost, st);
+        count_d2h(sizeof(double) * grid * slots);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) { rc = cuda_fail(e, "measure readback"); break; }
+        // fixed-order host reduction over CTAs
+        for (int g = 0; g < grid; ++g) {
+            const double* row = host.data() + (size_t)g * slots;
+            if (pi == 0) {
+                *norm += row[0];
+                for (int i = 0; i < k; ++i) ones[tq[i]] += row[1 + i];
+                for (int jj = 0; jj < n - k; ++jj) ones[P.oq[jj]] += row[1 + k + jj];
+            }
+            for (int i = 0; i < k; ++i) {
+                if (!((cp >> i) & 1)) continue;
+                cross[2 * tq[i]] += row[1 + n + 2 * i];
+                cross[2 * tq[i] + 1] += row[2 + n + 2 * i];
+            }
+        }
+        for (int i = 0; i < k; ++i)
+            if ((cp >> i) & 1) done |= 1ull << tq[i];
+    }
+    if (owned) cudaFreeAsync(partials, st);
+    return rc;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct sv_state {
+    int device;
+    int n;
+    int mode;
+    void* ptr;
+    cudaStream_t stream;
+    double* partials;
+    size_t partial_cap;
+};
+
+namespace {
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+}  // namespace
+
+extern "C" {
+
+int sv_abi_version(void) { return SV_ABI_VERSION; }
+const char* sv_last_error(void) { return g_err.c_str(); }
+
+int sv_device_count(int* count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return cuda_fail(e, "cudaGetDeviceCount");
+    }
+    *count = c;
+    return SV_OK;
+}
+
+int sv_sm_count(int device, int* count) {
+    *count = sm_count(device);
+    return SV_OK;
+}
+
+int svk_apply_1q(void* psi, uint64_t n, int mode, int q, const double* m8, void* stream) {
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "apply_1q needs FP64 or FP32 storage");
+    if (int rc = check_1q(n, q)) return rc;
+    const bool vec_ok = is_pow2(n) && n >= 64 && (reinterpret_cast<uintptr_t>(psi) & 31) == 0;
+    cudaError_t e;
+    if (vec_ok) {
+        e = launch_gate1(psi, n, mode, q, m8, as_stream(stream));
+    } else {
+        const cplx m0 = {m8[0], m8[1]}, m1 = {m8[2], m8[3]}, m2 = {m8[4], m8[5]}, m3 = {m8[6], m8[7]};
+        if (mode == SV_FP32)
+            k_gate1_scalar<c32s><<<small_grid(n / 2), 256, 0, as_stream(stream)>>>(
+                static_cast<c32s*>(psi), n / 2, q, m0, m1, m2, m3);
+        else
+            k_gate1_scalar<c64s><<<small_grid(n / 2), 256, 0, as_stream(stream)>>>(
+                static_cast<c64s*>(psi), n / 2, q, m0, m1, m2, m3);
+        e = cudaGetLastError();
+        count_launch();
+    }
+    return e == cudaSuccess ? SV_OK : cuda_fail(e, "apply_1q launch");
+}
+
+int svk_apply_2q(void* psi, uint64_t n, int mode, int qa, int qb, const double* m32, void* stream) {
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "apply_2q needs FP64 or FP32 storage");
+    if (int rc = check_2q(n, qa, qb)) return rc;
+    cudaError_t e = launch_gate2(psi, n, mode, qa, qb, m32, as_stream(stream));
+    return e == cudaSuccess ? SV_OK : cuda_fail(e, "apply_2q launch");
+}
+
+int svk_apply_diag(void* psi, uint64_t n, int mode, uint64_t mask, const double* f2, void* stream) {
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "apply_diag needs FP64 or FP32 storage");
+    if (n == 0) return SV_OK;
+    const bool structured = is_pow2(n) && n >= 64 && (reinterpret_cast<uintptr_t>(psi) & 31) == 0;
+    if (structured && (mask & ~(n - 1)))
+        return fail(SV_EINDEX, "diagonal mask 0x%llx outside local array of %llu amplitudes",
+                    (unsigned long long)mask, (unsigned long long)n);
+    cudaError_t e;
+    if (structured) {
+        e = launch_diag(psi, n, mode, mask, f2, as_stream(stream));
+    } else {
+        const cplx f = {f2[0], f2[1]};
+        if (mode == SV_FP32)
+            k_diag_all<c32s><<<small_grid(n), 256, 0, as_stream(stream)>>>(static_cast<c32s*>(psi), n, mask, f);
+        else
+            k_diag_all<c64s><<<small_grid(n), 256, 0, as_stream(stream)>>>(static_cast<c64s*>(psi), n, mask, f);
+        e = cudaGetLastError();
+        count_launch();
+    }
+    return e == cudaSuccess ? SV_OK : cuda_fail(e, "apply_diag launch");
+}
+
+int svk_pair_update(void* a0, void* a1, uint64_t count, int mode, const double* m8, void* stream) {
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "pair update needs FP64 or FP32 storage");
+    if (count == 0) return SV_OK;
+    cudaError_t e = launch_pair(a0, a1, count, mode, m8, as_stream(stream));
+    return e == cudaSuccess ? SV_OK : cuda_fail(e, "pair update launch");
+}
+
+int svk_quad_update(void* const* parts, uint64_t count, int mode, const double* m32, void* stream) {
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "quad update needs FP64 or FP32 storage");
+    if (count == 0) return SV_OK;
+    cudaError_t e = launch_quad(parts, count, mode, m32, as_stream(stream));
+    return e == cudaSuccess ? SV_OK : cuda_fail(e, "quad update launch");
+}
+
+int svk_apply_fused(void* psi, uint64_t n, int mode, const sv_op* ops, int n_ops, int tile_bits,
+                    void* stream) {
+    if (n_ops <= 0) return SV_OK;
+    return fused_impl(psi, n, mode, ops, n_ops, tile_bits, as_stream(stream));
+}
+
+int svk_measure(const void* psi, uint64_t n, int mode, double* norm, double* ones, double* cross,
+                void* stream) {
+    return measure_impl(psi, n, mode, norm, ones, cross, nullptr, 0, as_stream(stream));
+}
+
+// ---- handles ---------------------------------------------------------------
+int sv_create(int device, int n_qubits, int mode, sv_handle* out) {
+    *out = nullptr;
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "handle storage mode %d not supported here", mode);
+    if (n_qubits < 0 || n_qubits > 40) return fail(SV_EVALUE, "n_qubits %d out of range", n_qubits);
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) return fail(SV_EVALUE, "device %d not present (%d visible)", device, ndev);
+    DeviceGuard g(device);
+    sv_state* h = new sv_state();
+    h->device = device;
+    h->n = n_qubits;
+    h->mode = mode;
+    h->partials = nullptr;
+    h->partial_cap = 0;
+    const size_t bytes = (size_t)elem_bytes(mode) << n_qubits;
+    cudaError_t e = cudaMalloc(&h->ptr, bytes < 256 ? 256 : bytes);
+    if (e != cudaSuccess) {
+        delete h;
+        return cuda_fail(e, "state allocation");
+    }
+    e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        cudaFree(h->ptr);
+        delete h;
+        return cuda_fail(e, "stream creation");
+    }
+    const size_t cap = (size_t)measure_grid(device) * measure_slots(12, 40 > n_qubits ? n_qubits : 40);
+    e = cudaMalloc(reinterpret_cast<void**>(&h->partials), cap * sizeof(double));
+    if (e == cudaSuccess) h->partial_cap = cap;
+    else { h->partials = nullptr; cudaGetLastError(); }
+    *out = h;
+    return SV_OK;
+}
+
+int sv_destroy(sv_handle h) {
+    if (!h) return SV_OK;
+    DeviceGuard g(h->device);
+    cudaStreamSynchronize(h->stream);
+    if (h->partials) cudaFree(h->partials);
+    cudaFree(h->ptr);
+    cudaStreamDestroy(h->stream);
+    delete h;
+    return SV_OK;
+}
+
+int sv_info(sv_handle h, int* device, int* n_qubits, int* mode, void** dev_ptr, void** stream) {
+    if (!h) return fail(SV_EVALUE, "null handle");
+    if (device) *device = h->device;
+    if (n_qubits) *n_qubits = h->n;
+    if (mode) *mode = h->mode;
+    if (dev_ptr) *dev_ptr = h->ptr;
+    if (stream) *stream = reinterpret_cast<void*>(h->stream);
+    return SV_OK;
+}
+
+int sv_zero_state(sv_handle h, int64_t unit) {
+    DeviceGuard g(h->device);
+    const size_t eb = elem_bytes(h->mode);
+    const uint64_t n = 1ull << h->n;
+    CUDA_TRY(cudaMemsetAsync(h->ptr, 0, eb * n, h->stream), "zero state");
+    if (unit >= 0) {
+        if ((uint64_t)unit >= n) return fail(SV_EINDEX, "unit index %lld outside %llu amplitudes",
+                                             (long long)unit, (unsigned long long)n);
+        static const double one64[2] = {1.0, 0.0};
+        static const float one32[2] = {1.0f, 0.0f};
+        const void* src = h->mode == SV_FP32 ? static_cast<const void*>(one32) : static_cast<const void*>(one64);
+        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(h->ptr) + eb * unit, src, eb, cudaMemcpyHostToDevice,
+                                 h->stream), "unit amplitude");
+        count_h2d(eb);
+    }
+    return SV_OK;
+}
+
+int sv_apply_1q(sv_handle h, int q, const double* m8) {
+    DeviceGuard g(h->device);
+    return svk_apply_1q(h->ptr, 1ull << h->n, h->mode, q, m8, h->stream);
+}
+int sv_apply_2q(sv_handle h, int qa, int qb, const double* m32) {
+    DeviceGuard g(h->device);
+    return svk_apply_2q(h->ptr, 1ull << h->n, h->mode, qa, qb, m32, h->stream);
+}
+int sv_apply_diag(sv_handle h, uint64_t mask, const double* f2) {
+    DeviceGuard g(h->device);
+    return svk_apply_diag(h->ptr, 1ull << h->n, h->mode, mask, f2, h->stream);
+}
+int sv_apply_fused(sv_handle h, const sv_op* ops, int n_ops, int tile_bits) {
+    DeviceGuard g(h->device);
+    return svk_apply_fused(h->ptr, 1ull << h->n, h->mode, ops, n_ops, tile_bits, h->stream);
+}
+int sv_measure(sv_handle h, double* norm, double* ones, double* cross) {
+    DeviceGuard g(h->device);
+    return measure_impl(h->ptr, 1ull << h->n, h->mode, norm, ones, cross, h->partials, h->partial_cap,
+                        h->stream);
+}
+
+int sv_export(sv_handle h, void* host, uint64_t first, uint64_t count) {
+    DeviceGuard g(h->device);
+    const uint64_t n = 1ull << h->n;
+    if (first > n || count > n - first) return fail(SV_EINDEX, "export range outside the state");
+    const size_t eb = elem_bytes(h->mode);
+    CUDA_TRY(cudaMemcpyAsync(host, static_cast<char*>(h->ptr) + eb * first, eb * count,
+                             cudaMemcpyDeviceToHost, h->stream), "export");
+    count_d2h(eb * count);
+    CUDA_TRY(cudaStreamSynchronize(h->stream), "export sync");
+    return SV_OK;
+}
+
+int sv_import(sv_handle h, const void* host, uint64_t first, uint64_t count) {
+    DeviceGuard g(h->device);
+    const uint64_t n = 1ull << h->n;
+    if (first > n || count > n - first) return fail(SV_EINDEX, "import range outside the state");
+    const size_t eb = elem_bytes(h->mode);
+    CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(h->ptr) + eb * first, host, eb * count,
+                             cudaMemcpyHostToDevice, h->stream), "import");
+    count_h2d(eb * count);
+    CUDA_TRY(cudaStreamSynchronize(h->stream), "import sync");
+    return SV_OK;
+}
+
+int sv_synchronize(sv_handle h) {
+    DeviceGuard g(h->device);
+    CUDA_TRY(cudaStreamSynchronize(h->stream), "synchronize");
+    return SV_OK;
+}
+
+int sv_launch_count(uint64_t* count) {
+    *count = sv::launch_total();
+    return SV_OK;
+}
+
+int sv_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
+    *h2d = g_h2d.load();
+    *d2h = g_d2h.load();
+    return SV_OK;
+}
+
+int sv_pass_timing(int enable) {
+    g_timing = enable != 0;
+    return SV_OK;
+}
+
+int sv_pass_timing_read(uint64_t* passes, double* ms, double* bytes) {
+    std::vector<TimedPass> v;
+    {
+        std::lock_guard<std::mutex> lk(g_timing_mu);
+        v.swap(g_timed);
+    }
+    double tot = 0.0, by = 0.0;
+    for (auto& t : v) {
+        float m = 0.f;
+        cudaEventSynchronize(t.b);
+        if (cudaEventElapsedTime(&m, t.a, t.b) == cudaSuccess) tot += m;
+        by += t.bytes;
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+    }
+    *passes = v.size();
+    *ms = tot;
+    *bytes = by;
+    return SV_OK;
+}
+
+int sv_buffer_alloc(int device, uint64_t bytes, void** ptr) {
+    DeviceGuard g(device);
+    CUDA_TRY(cudaMalloc(ptr, bytes ? bytes : 256), "buffer allocation");
+    return SV_OK;
+}
+int sv_buffer_free(int device, void* ptr) {
+    DeviceGuard g(device);
+    CUDA_TRY(cudaFree(ptr), "buffer free");
+    return SV_OK;
+}
+int sv_copy_h2d(void* dst, const void* src, uint64_t bytes, void* stream) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream)), "h2d copy");
+    count_h2d(bytes);
+    CUDA_TRY(cudaStreamSynchronize(as_stream(stream)), "h2d sync");
+    return SV_OK;
+}
+int sv_copy_d2h(void* dst, const void* src, uint64_t bytes, void* stream) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream)), "d2h copy");
+    count_d2h(bytes);
+    CUDA_TRY(cudaStreamSynchronize(as_stream(stream)), "d2h sync");
+    return SV_OK;
+}
+int sv_stream_create(int device, void** stream) {
+    DeviceGuard g(device);
+    cudaStream_t s;
+    CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
+    *stream = reinterpret_cast<void*>(s);
+    return SV_OK;
+}
+int sv_stream_destroy(void* stream) {
+    cudaStreamDestroy(as_stream(stream));
+    return SV_OK;
+}
+
+int sv_event_create(void** ev) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e), "event create");
+    *ev = reinterpret_cast<void*>(e);
+    return SV_OK;
+}
+int sv_event_destroy(void* ev) {
+    cudaEventDestroy(reinterpret_cast<cudaEvent_t>(ev));
+    return SV_OK;
+}
+int sv_event_record(void* ev, void* stream) {
+    CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev), as_stream(stream)), "event record");
+    return SV_OK;
+}
+int sv_event_elapsed_ms(void* start, void* stop, float* ms) {
+    CUDA_TRY(cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(stop)), "event sync");
+    CUDA_TRY(cudaEventElapsedTime(ms, reinterpret_cast<cudaEvent_t>(start), reinterpret_cast<cudaEvent_t>(stop)),
+             "event elapsed");
+    return SV_OK;
+}
+int sv_stream_synchronize(void* stream) {
+    CUDA_TRY(cudaStreamSynchronize(as_stream(stream)), "stream synchronize");
+    return SV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// Launch-side declarations shared by the .cu translation units.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/svb200.h"
+
+namespace sv {
+
+// Fused-pass parameters travel as one kernel-parameter block (constant bank:
+// broadcast reads, no per-CTA global loads).  Kept well under the 32 KB
+// kernel-parameter limit of sm_70+ with CUDA >= 12.1.
+constexpr int kMaxOps = 128;
+constexpr int kMaxMData = 1536;         // doubles
+constexpr int kMaxTileBits = 12;
+
+struct FusedParams {
+    uint64_t n_tiles;
+    uint64_t out_mask;                  // local-index bits NOT in the tile
+    uint64_t tile_mask;                 // local-index bits in the tile
+    int n;                              // local qubits of the buffer
+    int k;                              // tile bits
+    int b;                              // contiguous low tile bits (T[i] == i for i < b)
+    int n_ops;
+    int8_t tq[kMaxTileBits];            // tile position -> qubit
+    uint8_t kind[kMaxOps];              // SV_OP_*
+    uint8_t pa[kMaxOps];                // tile positions (1Q: pa; 2Q: pa = pos(qa), pb = pos(qb))
+    uint8_t pb[kMaxOps];
+    uint16_t moff[kMaxOps];             // offset into mdata
+    uint32_t dmask_t[kMaxOps];          // DIAG: required tile-position bits
+    uint64_t dmask_o[kMaxOps];          // DIAG: required out-of-tile local-index bits
+    double mdata[kMaxMData];
+};
+
+// mode: SV_FP64 / SV_FP32 storage
+cudaError_t launch_gate1(void* psi, uint64_t n_elems, int mode, int q, const double* m8,
+                         cudaStream_t st);
+cudaError_t launch_gate2(void* psi, uint64_t n_elems, int mode, int qa, int qb, const double* m32,
+                         cudaStream_t st);
+cudaError_t launch_diag(void* psi, uint64_t n_elems, int mode, uint64_t mask, const double* f2,
+                        cudaStream_t st);
+cudaError_t launch_pair(void* a0, void* a1, uint64_t count, int mode, const double* m8,
+                        cudaStream_t st);
+cudaError_t launch_quad(void* const* parts, uint64_t count, int mode, const double* m32,
+                        cudaStream_t st);
+cudaError_t launch_fused(void* psi, int mode, const FusedParams& p, cudaStream_t st);
+
+// measurement: partial sums per CTA; see sv_measure.cu
+struct MeasureParams {
+    uint64_t n_tiles;
+    uint64_t out_mask;
+    uint64_t tile_mask;
+    int n, k, b;
+    int want_ones;                      // first pass: norm + ones for every local qubit
+    int8_t tq[kMaxTileBits];
+    uint32_t cross_pos;                 // tile positions whose cross terms are wanted
+    int8_t oq[64];                      // out-of-tile qubits (ascending), count n - k
+};
+int measure_slots(int k, int n);        // doubles per CTA partial row
+cudaError_t launch_measure(const void* psi, int mode, const MeasureParams& p, double* partials,
+                           int grid, cudaStream_t st);
+int measure_grid(int device);
+
+int sm_count(int device);
+void count_launch(uint64_t n = 1);
+
+}  // namespace sv

@@ -1,0 +1,252 @@
+"""Circuit execution on the B200 (``svsim.engine`` surface).
+
+Mirrors /root/reference/pkg/src/svsim/engine.py: ``RunResult`` (40-79) and
+``run_circuit`` (82-105) with the same keyword arguments, validation and
+error wrapping (``RuntimeError("gate {ordinal} ({kind}): ...")`` for a
+transport failure, 161-162).
+
+Execution model (single process, one GPU):
+  * all 2**(N-N') rank slices live in ONE HBM buffer in rank order, so rank r
+    owns elements [r*L, (r+1)*L) exactly as in the reference layout
+    (layout.py:26-47).  A gate on a global qubit is then an ordinary strided
+    update over the whole buffer — the reference's pairwise / quad exchange
+    rounds (engine.py:246-363) compute the same per-element expressions, so
+    the amplitudes are bit-identical and nothing needs to cross a link;
+  * the control plane still walks the reference choreography message by
+    message through the transport, so ledgers, partners, failure injection
+    and rank-order shuffling behave exactly as in the reference;
+  * consecutive gates are queued and flushed as fused tile passes
+    (svk_apply_fused): every gate keeps its own rounding, so fusion changes
+    the number of HBM passes, never the results.
+Multi-GPU execution (one process per GPU, NVLink exchanges) is in
+distributed.py.
+"""
+from __future__ import annotations
+
+import random
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from . import gates as g
+from .circuit import Circuit, validate_circuit
+from .device import gate_op
+from .layout import PartitionLayout, TrafficLedger, plan_exchange
+from .measure import ExpectationReport, charge_measurement, report_from_sums
+from .state import LocalState, PrecisionMode
+from .transport import ExchangeToken, Transport, TransportError
+
+FUSE_QUEUE_LIMIT = 1024
+
+
+@dataclass
+class RunResult:
+    circuit: Circuit
+    layout: PartitionLayout
+    mode: PrecisionMode
+    states: list
+    ledgers: list
+    report: ExpectationReport | None
+    codebook: object
+    tier_accounts: list | None
+    wall_time_seconds: float
+    device_stats: dict = field(default_factory=dict)
+
+    @property
+    def gate_operations(self) -> int:
+        return self.ledgers[0].gate_operations
+
+    @property
+    def total_bytes_sent(self) -> int:
+        return sum(led.inter_rank_bytes_sent for led in self.ledgers)
+
+    @property
+    def total_messages(self) -> int:
+        return sum(led.inter_rank_messages for led in self.ledgers)
+
+    @property
+    def total_tier_bytes(self) -> int:
+        return sum(led.tier_bytes_moved for led in self.ledgers)
+
+    @property
+    def total_tier_transfers(self) -> int:
+        return sum(led.tier_transfer_count for led in self.ledgers)
+
+    def gathered_state(self) -> np.ndarray:
+        """Global state vector (complex128) assembled from the rank slices."""
+        dev = self.states[0].device_state
+        if self.mode is PrecisionMode.BYTE:
+            return dev.decode_all(self.codebook)
+        return dev.export().astype(np.complex128)
+
+    def report_in_program_labels(self) -> ExpectationReport | None:
+        if self.report is None:
+            return None
+        return self.report.relabelled(self.circuit.label_permutation)
+
+
+def gate_to_op(gate: g.Gate):
+    """One gate as an sv_op over the global index (all ranks in one buffer)."""
+    if g.is_diagonal(gate):
+        mask = 0
+        for q in gate.qubits:
+            mask |= 1 << q
+        f = g.diagonal_factor(gate)
+        return gate_op(nat.SV_OP_DIAG, mask=mask, data=(f.real, f.imag))
+    m = nat.mat_buffer(g.unitary_matrix(gate))
+    if len(gate.qubits) == 1:
+        return gate_op(nat.SV_OP_1Q, qa=gate.qubits[0], data=m)
+    return gate_op(nat.SV_OP_2Q, qa=gate.qubits[0], qb=gate.qubits[1], data=m)
+
+
+def run_circuit(circuit: Circuit, *, ranks: int = 1, local_qubits: int | None = None,
+                mode: PrecisionMode = PrecisionMode.FP64, tier_config=None,
+                rank_order_seed: int | None = None, transport_factory=Transport,
+                device: int = 0, fuse: bool = True, tile_bits: int = 12) -> RunResult:
+    validate_circuit(circuit)
+    if ranks < 1 or ranks & (ranks - 1):
+        raise ValueError("rank count must be a power of two")
+    if local_qubits is None:
+        local_qubits = circuit.n_qubits - (ranks.bit_length() - 1)
+    layout = PartitionLayout(circuit.n_qubits, local_qubits)
+    if layout.rank_count != ranks:
+        raise ValueError(f"{ranks} ranks with {local_qubits} local qubits does not cover "
+                         f"{circuit.n_qubits} qubits")
+    if tier_config is not None:
+        raise NotImplementedError("the two-tier staging model (tier.py) is out of scope on B200: "
+                                  "every configuration stays resident in HBM")
+    start = time.perf_counter()
+    eng = _Engine(circuit, layout, mode, rank_order_seed, transport_factory, device, fuse, tile_bits)
+    eng.run()
+    return RunResult(circuit, layout, mode, eng.states, eng.ledgers, eng.report, eng.codebook,
+                     None, time.perf_counter() - start, eng.stats())
+
+
+class _Engine:
+    def __init__(self, circuit, layout, mode, rank_order_seed, transport_factory, device, fuse,
+                 tile_bits):
+        self.circuit = circuit
+        self.layout = layout
+        self.mode = mode
+        self.fuse = fuse
+        self.tile_bits = tile_bits
+        n = layout.rank_count
+        self.ledgers = [TrafficLedger() for _ in range(n)]
+        self.transport = transport_factory(n, self.ledgers)
+        self.order = list(range(n))
+        if rank_order_seed is not None:
+            random.Random(rank_order_seed).shuffle(self.order)
+        self.report = None
+        self.codebook = None
+        if mode is PrecisionMode.BYTE:
+            from .codec import ByteEngineState
+            self.dev = ByteEngineState(circuit.n_qubits, layout, device=device)
+            self.codebook = self.dev.codebook
+        else:
+            from .device import DeviceState
+            self.dev = DeviceState(circuit.n_qubits, mode, device=device)
+        self.dev.zero(0)
+        L = layout.local_size
+        self.states = [LocalState(layout.local_qubits, mode, _device_state=self.dev, _offset=r * L)
+                       for r in range(n)]
+        self.pending = []
+        self.gates_applied = 0
+
+    # -- device queue ----------------------------------------------------------------
+    def _enqueue(self, gate):
+        if self.mode is PrecisionMode.BYTE:
+            self.dev.apply_gate(gate, self.layout)
+            return
+        self.pending.append(gate_to_op(gate))
+        self.gates_applied += 1
+        if not self.fuse or len(self.pending) >= FUSE_QUEUE_LIMIT:
+            self._flush()
+
+    def _flush(self):
+        if not self.pending:
+            return
+        if self.fuse:
+            self.dev.apply_fused(self.pending, self.tile_bits)
+        else:
+            for op in self.pending:
+                self._apply_single_op(op)
+        self.pending = []
+
+    def _apply_single_op(self, op):
+        m = np.array(op.m[:32])
+        if op.kind == nat.SV_OP_1Q:
+            nat.check(nat.load().sv_apply_1q(self.dev.handle, op.qa, nat.dptr(m)))
+        elif op.kind == nat.SV_OP_2Q:
+            nat.check(nat.load().sv_apply_2q(self.dev.handle, op.qa, op.qb, nat.dptr(m)))
+        else:
+            nat.check(nat.load().sv_apply_diag(self.dev.handle, op.diag_mask, nat.dptr(m)))
+        self.dev._touch()
+
+    # -- control plane -----------------------------------------------------------------
+    def _exchange_messages(self, plan, ordinal):
+        """The reference's send phase then receive phase (engine.py:246-363)."""
+        L = self.layout.local_size
+        if plan.kind == "pairwise":
+            mask = plan.masks[0]
+            for rank in self.order:
+                tok = ExchangeToken(ordinal, rank, rank ^ mask, 0, plan.element_count)
+                self.transport.send(rank, rank ^ mask, tok, plan.bytes_per_rank)
+            for rank in self.order:
+                self.transport.recv(rank, rank ^ mask)
+            return
+        ma, mb = plan.masks
+        quarter = L // 4
+
+        def member(rank, pos):
+            return (rank & ~(ma | mb)) | (ma if pos & 1 else 0) | (mb if pos & 2 else 0)
+
+        for rank in self.order:
+            for pos in range(4):
+                dst = member(rank, pos)
+                if dst != rank:
+                    tok = ExchangeToken(ordinal, rank, dst, pos * quarter, quarter)
+                    self.transport.send(rank, dst, tok, quarter * plan.bytes_per_element)
+        for rank in self.order:
+            for pos in range(4):
+                src = member(rank, pos)
+                if src != rank:
+                    self.transport.recv(rank, src)
+
+    def _measure(self, ordinal):
+        self._flush()
+        P = self.layout.rank_count
+        self.transport.collective([None] * P)
+        charge_measurement(self.layout, self.transport, self.mode.bytes_per_element, self.order, ordinal)
+        if self.mode is PrecisionMode.BYTE:
+            norm, ones, cross = self.dev.measure_sums()
+        else:
+            norm, ones, cross = self.dev.measure()
+        for _ in range(self.layout.total_qubits):
+            self.transport.collective([None] * P)
+            self.transport.collective([None] * P)
+        self.report = report_from_sums(norm, ones, cross)
+
+    def run(self):
+        for ordinal, gate in enumerate(self.circuit.gates):
+            plan = plan_exchange(self.layout, gate, self.mode)
+            try:
+                if gate.kind == "M":
+                    self._measure(ordinal)
+                else:
+                    if plan.kind != "none":
+                        self._exchange_messages(plan, ordinal)
+                    self._enqueue(gate)
+            except TransportError as exc:
+                raise RuntimeError(f"gate {ordinal} ({gate.kind}): {exc}") from exc
+            for led in self.ledgers:
+                led.gate_operations += 1
+        self._flush()
+        self.dev.synchronize()
+        self.transport.assert_drained()
+
+    def stats(self) -> dict:
+        return {"device": self.dev.device, "kernel_launches": self.dev.launches,
+                "gates_applied": self.gates_applied, "fused": self.fuse,
+                "physical_link_bytes": 0}

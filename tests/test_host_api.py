@@ -1,0 +1,179 @@
+"""CPU tests of the product's host logic against the reference goldens.
+
+No GPU is touched here: planner / layout / ledger / builders / gate constants /
+parser / transport, plus the C ABI library loading and exporting every
+symbol include/svb200.h declares.
+"""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2511_03359_b200 as pb
+from paper_2511_03359_b200 import _native, gates as g
+from paper_2511_03359_b200.layout import gibibytes_exchanged
+from tests.circuits import random_circuit, to_product, unpack
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+MODES = {"fp64": pb.PrecisionMode.FP64, "fp32": pb.PrecisionMode.FP32, "be": pb.PrecisionMode.BYTE}
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.load(require_device=False)
+    header = open(os.path.join(ROOT, "include", "svb200.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(sv\w+)\(", header, re.M))
+    assert declared, "no declarations parsed"
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(_native.exported_symbols())
+    assert lib.sv_abi_version() == 1
+
+
+def test_gate_constants_bit_exact(golden):
+    k = golden("kernels.npz")
+    assert np.array_equal(g.H_MATRIX, k["H"])
+    for e in (1, 2, 3, 4, -1, -2, -3, -4, 7, 16, 25):
+        f = np.complex128(g.diagonal_factor(g.phase(0, e)))
+        assert f.tobytes() == k[f"factor_{e}"].tobytes(), e
+    assert g.diagonal_factor(g.z(0)) == -1.0 + 0.0j
+    assert g.phase_angle(2) == np.pi / 2 and g.phase_angle(-2) == -np.pi / 2
+    with pytest.raises(ValueError):
+        g.phase_angle(0)
+
+
+def test_gate_validation_messages():
+    with pytest.raises(ValueError, match="out of range"):
+        g.validate_gate(g.h(5), 4)
+    with pytest.raises(ValueError, match="distinct"):
+        g.validate_gate(g.cphase(2, 2, 1), 4)
+    with pytest.raises(ValueError, match="not unitary"):
+        g.validate_gate(g.u2(0, np.diag([1.0, 2.0])), 2)
+    with pytest.raises(ValueError):
+        g.validate_gate(g.Gate("M", (0,)), 2)
+    for gate in (g.h(0), g.x(0), g.y(0), g.cnot(0, 1)):
+        assert g.unitarity_residual(g.unitary_matrix(gate)) < 1e-15
+
+
+def test_plans_match_reference(golden):
+    for e in golden("planner.json")["plans"]:
+        gate = g.Gate(e["kind"], tuple(e["qubits"]))
+        p = pb.plan_exchange(pb.PartitionLayout(e["n"], e["local"]), gate, MODES[e["mode"]])
+        assert (p.kind, list(p.masks), p.element_count, p.bytes_per_element) == \
+            (e["plan_kind"], e["masks"], e["count"], e["bpe"]), e
+    for e in golden("planner.json")["memory"]:
+        assert pb.memory_bytes(e["n"], MODES[e["mode"]]) == e["bytes"]
+
+
+def _workload(name):
+    if name == "adder16":
+        return pb.build_adder(16, [47302, 18233])[0]
+    if name == "adder19":
+        return pb.build_adder(19, [374982, 149305])[0]
+    if name == "adder25":
+        return pb.build_adder(25, [21346502, 12207929])[0]
+    if name.startswith("bench"):
+        return pb.build_benchmark(int(name[5:]))
+    return None
+
+
+def test_optimize_labels_matches_reference(golden):
+    for e in golden("planner.json")["optimize"]:
+        circ = _workload(e["name"])
+        if circ is None:
+            d = {k: np.array(v) for k, v in e["circuit"].items()}
+            d["mats"] = np.zeros((len(d["kinds"]), 4, 4), dtype=np.complex128)
+            circ = to_product(unpack(d))
+        layout = pb.PartitionLayout(circ.n_qubits, e["local"])
+        perm = pb.optimize_labels(circ, layout)
+        assert list(perm) == e["perm"], e["name"]
+        assert pb.predicted_exchange_bytes(circ, layout) == e["identity_bytes"]
+        assert pb.predicted_exchange_bytes(pb.relabel(circ, perm), layout) == e["optimized_bytes"]
+        assert pb.predicted_exchange_bytes(circ, layout, pb.PrecisionMode.BYTE) == e["identity_bytes_be"]
+
+
+def test_builders_match_oracle_restatement():
+    from oracle.ref_builders import adder, benchmark
+    for n in (8, 12, 36):
+        a, b = pb.build_benchmark(n), benchmark(n)
+        assert [(x.kind, x.qubits) for x in a.gates] == [(x.kind, x.qubits) for x in b.gates]
+        assert len(a.gates) == n + 7
+    for width, vals in ((2, [1, 2]), (5, [11, 19]), (16, [47302, 18233]), (3, [1, 5, 6])):
+        (a, regs), (b, _) = pb.build_adder(width, vals), adder(width, vals)
+        assert [(x.kind, x.qubits, x.k) for x in a.gates] == [(x.kind, x.qubits, x.k) for x in b.gates]
+    assert len(pb.build_adder(25, [21346502, 12207929])[0].gates) == 1001
+    assert len(pb.build_adder(16, [47302, 18233])[0].gates) == 425
+    with pytest.raises(ValueError, match="fit"):
+        pb.build_adder(3, [8, 1])
+    with pytest.raises(ValueError):
+        pb.build_benchmark(7)
+
+
+def test_parser_round_trip(rng):
+    for _ in range(10):
+        circ = to_product(random_circuit(rng, int(rng.integers(2, 7)), 12))
+        text = pb.serialize_circuit(circ)
+        again = pb.parse_circuit(text)
+        assert pb.serialize_circuit(again) == text
+    c = pb.parse_circuit("qubits 3\nRELABEL 2 1 0\nH 0\nM\n")
+    assert c.gates[0].qubits == (2,) and c.label_permutation == (2, 1, 0)
+    for bad in ["", "qubits 0", "qubits 2\nCPHASE 0 0 1", "qubits 2\nU2 0 1 2", "qubits 2\nM 0",
+                "qubits 2\nRELABEL 0 0", "qubits 2\nH 9\n", "qubits 2\nFROB 1", "H 0\n"]:
+        with pytest.raises(pb.ParseError):
+            pb.parse_circuit(bad)
+
+
+def test_ledger_and_transport_semantics():
+    led = pb.TrafficLedger()
+    led.count_send(3 << 30)
+    led.count_receive(3 << 30)
+    assert gibibytes_exchanged(led) == 6
+    leds = [pb.TrafficLedger() for _ in range(2)]
+    t = pb.Transport(2, leds)
+    with pytest.raises(pb.TransportError):
+        t.send(0, 0, None, 1)
+    with pytest.raises(pb.TransportError):
+        t.recv(1, 0)
+    t.send(0, 1, "x", 32)
+    with pytest.raises(pb.TransportError):
+        t.assert_drained()
+    assert t.recv(1, 0) == "x"
+    t.assert_drained()
+    assert leds[0].inter_rank_bytes_sent == 32 and leds[1].inter_rank_bytes_received == 32
+    with pytest.raises(pb.TransportError):
+        t.collective([1])
+
+
+def test_run_circuit_validation_without_gpu():
+    c = pb.Circuit(4, (g.h(0),))
+    with pytest.raises(ValueError, match="power of two"):
+        pb.run_circuit(c, ranks=3)
+    with pytest.raises(ValueError):
+        pb.run_circuit(c, ranks=2, local_qubits=4)
+    with pytest.raises(ValueError):
+        pb.run_circuit(pb.Circuit(2, (g.h(5),)))
+
+
+def test_no_cpu_fallback_without_device():
+    if _native.load(require_device=False).sv_device_count is None:
+        pytest.skip("library not loadable")
+    import ctypes
+    n = ctypes.c_int(0)
+    _native.load(require_device=False).sv_device_count(ctypes.byref(n))
+    if n.value > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(_native.NativeUnavailable):
+        pb.run_circuit(pb.build_benchmark(8))
+    with pytest.raises(_native.NativeUnavailable):
+        pb.kernels.apply_single(np.zeros(4, dtype=np.complex128), 0, g.H_MATRIX) \
+            if hasattr(pb, "kernels") else __import__("paper_2511_03359_b200.kernels").kernels.apply_single(
+                np.zeros(4, dtype=np.complex128), 0, g.H_MATRIX)
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2511_03359_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                text = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle\b", text, re.M), f
