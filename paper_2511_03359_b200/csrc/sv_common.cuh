@@ -43,11 +43,17 @@ struct __align__(8) c32s { float re, im; };
 template <typename S> struct Store;
 template <> struct Store<c64s> {
     static constexpr int V = 2;                   // amplitudes per 32 B vector
+    // value as it would read back after a store (identity for FP64 storage)
+    __device__ __forceinline__ static cplx round(cplx c) { return c; }
     __device__ __forceinline__ static cplx get(c64s s) { return {s.re, s.im}; }
     __device__ __forceinline__ static c64s put(cplx c) { return {c.re, c.im}; }
 };
 template <> struct Store<c32s> {
     static constexpr int V = 4;
+    // FP32 storage rounds after every gate (kernels.py:36-40 store into complex64)
+    __device__ __forceinline__ static cplx round(cplx c) {
+        return {(double)__double2float_rn(c.re), (double)__double2float_rn(c.im)};
+    }
     __device__ __forceinline__ static cplx get(c32s s) { return {(double)s.re, (double)s.im}; }
     __device__ __forceinline__ static c32s put(cplx c) {
         return {__double2float_rn(c.re), __double2float_rn(c.im)};

@@ -275,8 +275,8 @@ __global__ void __launch_bounds__(256) k_fused(S* __restrict__ psi, const __grid
                     const int e0 = (int)insert0((uint64_t)w, pos);
                     const int e1 = e0 | (1 << pos);
                     const cplx a0 = s[e0], a1 = s[e1];
-                    s[e0] = row2(m0, m1, a0, a1);
-                    s[e1] = row2(m2, m3, a0, a1);
+                    s[e0] = Store<S>::round(row2(m0, m1, a0, a1));
+                    s[e1] = Store<S>::round(row2(m2, m3, a0, a1));
                 }
             } else if (kind == SV_OP_2Q) {
                 if (prev_kind != 0) __syncthreads();
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(256) k_fused(S* __restrict__ psi, const __grid
                     const int idx[4] = {e, e | (1 << pa), e | (1 << pb), e | (1 << pa) | (1 << pb)};
                     const cplx a0 = s[idx[0]], a1 = s[idx[1]], a2 = s[idx[2]], a3 = s[idx[3]];
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) s[idx[r]] = row4(&m[4 * r], a0, a1, a2, a3);
+                    for (int r = 0; r < 4; ++r) s[idx[r]] = Store<S>::round(row4(&m[4 * r], a0, a1, a2, a3));
                 }
             } else {  // SV_OP_DIAG: elementwise; same element->thread map as other diags
                 if (prev_kind != 0 && prev_kind != SV_OP_DIAG) __syncthreads();
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(256) k_fused(S* __restrict__ psi, const __grid
                     const uint32_t mt = p.dmask_t[o];
                     const cplx f = {md[0], md[1]};
                     for (int e = threadIdx.x; e < TILE; e += NT)
-                        if (((uint32_t)e & mt) == mt) s[e] = cmul(s[e], f);
+                        if (((uint32_t)e & mt) == mt) s[e] = Store<S>::round(cmul(s[e], f));
                 }
             }
             prev_kind = kind;
@@ -335,7 +335,7 @@ static cudaError_t gate1_t(S* psi, uint64_t n, int q, const Mat2& m, cudaStream_
         k_gate1_hi<S, U><<<grid_for(items, 256 * U, 8), 256, 0, st>>>(psi, items, q, m);
     } else {
         const uint64_t vecs = n / V;
-        k_gate1_lo<S, U><<<grid_for(vecs, 256 * U, 8), 256, 0, st>>>(psi, vecs, q, m);
+        k_gate1_lo<S, 4><<<grid_for(vecs, 256 * 4, 8), 256, 0, st>>>(psi, vecs, q, m);
     }
     count_launch();
     return cudaGetLastError();

@@ -157,8 +157,9 @@ static cudaError_t measure_k(const S* psi, const MeasureParams& p, double* parti
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !configured[dev]) {
+        const size_t worst = tile_bytes + sizeof(double) * (size_t)measure_slots(K, 64) * 8;
         cudaError_t e = cudaFuncSetAttribute(k_measure<S, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             96 * 1024);
+                                             (int)worst);
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
