@@ -221,6 +221,8 @@ def run_b200(args):
     from oracle.ref_builders import OCircuit
 
     device = local if world > 1 else 0
+    nat.check(nat.load().sv_fused_variant(args.fused))
+    nat.check(nat.load().sv_fused_segment_limit(args.seg_limit))
     n = args.n
     layers_o = workload_layers(n, args.layers)
     layers = [to_product(OCircuit(n, tuple(l))).gates for l in layers_o]
@@ -319,7 +321,10 @@ def run_b200(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None,
-                         "kernel": "k_fused<c64s,12>", "launches_timed": passes,
+                         "kernel": {0: "k_fused<c64s,12>", 1: "k_fused3<12,4,1>", 2: "k_fused3<11,3,2>",
+                                    3: "k_fused3<12,3,1>", 4: "k_fused3<11,3,3>",
+                                    5: "k_fused3<10,3,4>"}[args.fused],
+                         "launches_timed": passes,
                          "bytes_per_launch": 2 * 16 * 2 ** n},
             "gpu_launches": launches,
             "fused_passes_per_step": round(passes / args.steps, 2),
@@ -345,7 +350,10 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=33, help="qubits per GPU")
     ap.add_argument("--layers", type=int, default=9, help="H layer + random layers in the workload")
-    ap.add_argument("--tile-bits", type=int, default=12)
+    ap.add_argument("--tile-bits", type=int, default=12, help="v1 tile bits / upper bound")
+    ap.add_argument("--fused", type=int, default=5, choices=[0, 1, 2, 3, 4, 5],
+                    help="fused-pass kernel: 0 smem-per-gate v1, 1-3 register-resident v3 configs")
+    ap.add_argument("--seg-limit", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-layers", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")

@@ -116,6 +116,14 @@ int sv_launch_count(uint64_t* count);
 /* host<->device bytes this library has moved (copies plus the kernel-
  * parameter blocks of fused passes, which the driver ships per launch) */
 int sv_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
+/* select the fused-pass kernel (FP64): 0 = shared-memory-per-gate v1;
+ * register-resident cp.async-pipelined v3 with 1 = 2^12 tiles x 16 amplitudes
+ * per thread, 2 = 2^11 tiles x 8 per thread (2 CTAs/SM), 3 = 2^12 tiles x 8
+ * per thread (512 threads).  FP32 storage always uses v1. */
+int sv_fused_variant(int v2);
+/* passes whose v3 plan needs more than `limit` register segments use v1
+ * instead (0 = no limit) */
+int sv_fused_segment_limit(int limit);
 /* per-launch CUDA-event timing of fused passes (off by default): when on,
  * every fused-pass kernel is bracketed by events on its own stream */
 int sv_pass_timing(int enable);

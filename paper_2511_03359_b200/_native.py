@@ -68,6 +68,8 @@ _SIGNATURES = {
     "sv_stream_destroy": ([_P], _I),
     "sv_launch_count": ([ctypes.POINTER(_U64)], _I),
     "sv_transfer_bytes": ([ctypes.POINTER(_U64), ctypes.POINTER(_U64)], _I),
+    "sv_fused_variant": ([_I], _I),
+    "sv_fused_segment_limit": ([_I], _I),
     "sv_pass_timing": ([_I], _I),
     "sv_pass_timing_read": ([ctypes.POINTER(_U64), _D, _D], _I),
     "sv_event_create": ([ctypes.POINTER(_P)], _I),

@@ -29,6 +29,8 @@ inline void count_d2h(uint64_t b) { g_d2h.fetch_add(b, std::memory_order_relaxed
 
 struct TimedPass { cudaEvent_t a, b; double bytes; };
 bool g_timing = false;
+int g_fused_v2 = 5;      // default: 2^10 tiles, 8 amplitudes/thread, 4 CTAs/SM (best measured)
+int g_seg_limit = 0;        // > 0: passes needing more segments fall back to v1
 std::mutex g_timing_mu;
 std::vector<TimedPass> g_timed;
 
@@ -173,6 +175,185 @@ int build_params(const sv_op* ops, const PassPlan& pp, int n, int k, FusedParams
     return SV_OK;
 }
 
+// ---- v2 planner: 12-bit register-resident tiles (sv_fused2.cu) -----------------
+// unit code of a matrix entry: 0 -> 1, 1 -> i, 2 -> -1, 3 -> -i, -1 -> not a unit
+int unit_code(double re, double im) {
+    if (im == 0.0 && re == 1.0) return 0;
+    if (re == 0.0 && im == 1.0) return 1;
+    if (im == 0.0 && re == -1.0) return 2;
+    if (re == 0.0 && im == -1.0) return 3;
+    return -1;
+}
+
+// classify a dim x dim row-major complex matrix: 0 generic, 1 real, 2 monomial (units)
+int classify(const double* m, int dim, uint32_t* mono) {
+    bool real = true;
+    for (int i = 0; i < dim * dim; ++i) real = real && m[2 * i + 1] == 0.0;
+    uint32_t code = 0;
+    bool monomial = true;
+    for (int r = 0; r < dim && monomial; ++r) {
+        int src = -1, u = -1, nz = 0;
+        for (int c = 0; c < dim; ++c) {
+            const double re = m[2 * (r * dim + c)], im = m[2 * (r * dim + c) + 1];
+            if (re != 0.0 || im != 0.0) {
+                ++nz;
+                src = c;
+                u = unit_code(re, im);
+            }
+        }
+        if (nz != 1 || u < 0) monomial = false;
+        else code |= (uint32_t)(src | (u << 2)) << (4 * r);
+    }
+    if (monomial) {
+        *mono = code;
+        return 2;
+    }
+    return real ? 1 : 0;
+}
+
+int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Params& P) {
+    std::memset(&P, 0, sizeof(P));
+    const int K = (cfg == 2 || cfg == 4) ? 11 : (cfg == 5 ? 10 : 12);
+    const int RB = cfg == 1 ? 4 : 3;
+    const int NTH = 1 << (K - RB);
+    P.cfg = cfg;
+    P.kbits = K;
+    P.rbits = RB;
+    const uint64_t tmask = tile_mask_for(pp.qmask, n, K);
+    P.n = n;
+    P.tile_mask = tmask;
+    P.n_tiles = 1ull << (n - K);
+    int pos_of[64];
+    int j = 0;
+    for (int q = 0; q < n; ++q) {
+        pos_of[q] = -1;
+        if ((tmask >> q) & 1) { pos_of[q] = j; P.tq[j++] = (int8_t)q; }
+    }
+    int b = 0;
+    while (b < K && P.tq[b] == b) ++b;
+    P.b = b;
+    // segments: greedy, at most 4 distinct tile positions in registers
+    const int nops = (int)pp.ops.size();
+    std::vector<uint32_t> seg_sets;
+    std::vector<int> seg_end;
+    uint32_t cur = 0;
+    for (int i = 0; i < nops; ++i) {
+        const sv_op& o = ops[pp.ops[i]];
+        uint32_t need = 0;
+        if (o.kind == SV_OP_1Q) need = 1u << pos_of[o.qa];
+        if (o.kind == SV_OP_2Q) need = (1u << pos_of[o.qa]) | (1u << pos_of[o.qb]);
+        if (__builtin_popcount(cur | need) > RB) {
+            seg_sets.push_back(cur);
+            seg_end.push_back(i);
+            cur = 0;
+        }
+        cur |= need;
+    }
+    seg_sets.push_back(cur);
+    seg_end.push_back(nops);
+    if ((int)seg_sets.size() > kMaxSegs) return -1;
+    P.n_segs = (int)seg_sets.size();
+    P.n_ops = nops;
+    std::vector<int> seg_of(nops);
+    for (int sgi = 0, i = 0; sgi < P.n_segs; ++sgi)
+        for (; i < seg_end[sgi]; ++i) seg_of[i] = sgi;
+    int regbit_of[kMaxSegs][12];
+    for (int sgi = 0; sgi < P.n_segs; ++sgi) {
+        uint32_t set = seg_sets[sgi];
+        for (int pos = K - 1; pos >= 0 && __builtin_popcount(set) < RB; --pos)   // fill from the top
+            if (!((set >> pos) & 1)) set |= 1u << pos;
+        int r = 0, t = 0;
+        for (int pos = 0; pos < K; ++pos) {
+            regbit_of[sgi][pos] = -1;
+            if ((set >> pos) & 1) { P.seg_reg[sgi][r] = (uint8_t)pos; regbit_of[sgi][pos] = r; ++r; }
+            else P.seg_thr[sgi][t++] = (uint8_t)pos;
+        }
+        P.seg_end[sgi] = (uint16_t)seg_end[sgi];
+    }
+    auto lanes_contiguous = [&](int sgi) {
+        return b >= 5 && P.seg_reg[sgi][0] >= 5;   // lanes = the 5 lowest (contiguous) positions
+    };
+    // linear helpers: shared-memory swizzle and HBM offset of a set of tile positions
+    auto swz_h = [](int e) {
+        const int g = (((e >> 3) & 1) * 7) ^ (((e >> 4) & 1) * 3) ^ (((e >> 5) & 1) * 5) ^ (((e >> 6) & 1) * 6);
+        return e ^ g;
+    };
+    auto gofs = [&](int e) {
+        uint64_t o = 0;
+        for (int pos = 0; pos < K; ++pos)
+            if ((e >> pos) & 1) o += 1ull << P.tq[pos];
+        return o;
+    };
+    for (int sgi = 0; sgi < P.n_segs; ++sgi)
+        for (int i = 0; i < (1 << RB); ++i) {
+            int e = 0;
+            for (int bit = 0; bit < RB; ++bit)
+                if ((i >> bit) & 1) e |= 1 << P.seg_reg[sgi][bit];
+            P.seg_rsw[sgi][i] = (uint16_t)swz_h(e);
+            if (sgi == P.n_segs - 1) P.last_rgo[i] = gofs(e);
+        }
+    for (int jj = 0; jj < (1 << RB); ++jj) P.pf_go[jj] = gofs(jj * NTH);
+    {
+        // deposit tables: tile index byte -> local index bits outside the tile
+        int outpos[64], no = 0;
+        for (int q = 0; q < n; ++q)
+            if (!((tmask >> q) & 1)) outpos[no++] = q;
+        if (no > 32) return -1;
+        for (int byte = 0; byte < 4; ++byte)
+            for (int v = 0; v < 256; ++v) {
+                uint64_t d = 0;
+                for (int bit = 0; bit < 8; ++bit) {
+                    const int src = byte * 8 + bit;
+                    if (((v >> bit) & 1) && src < no) d |= 1ull << outpos[src];
+                }
+                P.base_tab[byte][v] = d;
+            }
+    }
+    P.direct_in = lanes_contiguous(0);
+    P.direct_out = lanes_contiguous(P.n_segs - 1);
+    int md = 0;
+    for (int i = 0; i < nops; ++i) {
+        const sv_op& o = ops[pp.ops[i]];
+        const int sgi = seg_of[i];
+        P.moff[i] = (uint16_t)md;
+        if (o.kind == SV_OP_1Q) {
+            uint32_t mono = 0;
+            const int cls = classify(o.m, 2, &mono);
+            P.kind[i] = (uint8_t)(cls == 2 ? F2_1Q_MONO : (cls == 1 ? F2_1Q_REAL : F2_1Q));
+            P.mono[i] = (uint16_t)mono;
+            P.ra[i] = (uint8_t)regbit_of[sgi][pos_of[o.qa]];
+            for (int c = 0; c < 8; ++c) P.mdata[md + c] = o.m[c];
+            md += 8;
+        } else if (o.kind == SV_OP_2Q) {
+            uint32_t mono = 0;
+            const int cls = classify(o.m, 4, &mono);
+            P.kind[i] = (uint8_t)(cls == 2 ? F2_2Q_MONO : F2_2Q);   // real 4x4: generic path (exact)
+            P.mono[i] = (uint16_t)mono;
+            P.ra[i] = (uint8_t)regbit_of[sgi][pos_of[o.qa]];
+            P.rb[i] = (uint8_t)regbit_of[sgi][pos_of[o.qb]];
+            for (int c = 0; c < 32; ++c) P.mdata[md + c] = o.m[c];
+            md += 32;
+        } else {
+            const bool neg = o.m[0] == -1.0 && o.m[1] == 0.0;
+            P.kind[i] = (uint8_t)(neg ? F2_DIAG_NEG : F2_DIAG);
+            uint32_t dreg = 0, dthr = 0;
+            for (int q = 0; q < n; ++q) {
+                if (!((o.diag_mask >> q) & 1) || pos_of[q] < 0) continue;
+                const int rb = regbit_of[sgi][pos_of[q]];
+                if (rb >= 0) dreg |= 1u << rb;
+                else dthr |= 1u << pos_of[q];
+            }
+            P.dreg[i] = (uint8_t)dreg;
+            P.dthr[i] = (uint16_t)dthr;
+            P.dout[i] = o.diag_mask & ~tmask;
+            P.mdata[md] = o.m[0];
+            P.mdata[md + 1] = o.m[1];
+            md += 2;
+        }
+    }
+    return 0;
+}
+
 int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_ops, int tile_bits,
                cudaStream_t st) {
     if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "fused passes need FP64 or FP32 storage");
@@ -181,7 +362,9 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
         return fail(SV_EVALUE, "fused pass needs a 32-byte aligned buffer");
     const int n = log2u(n_elems);
     if (tile_bits <= 0) tile_bits = 12;
-    const int k = tile_bits < n ? tile_bits : n;
+    const int kv3 = (g_fused_v2 == 2 || g_fused_v2 == 4) ? 11 : (g_fused_v2 == 5 ? 10 : 12);
+    const bool use_v3 = g_fused_v2 != 0 && mode == SV_FP64 && n >= kv3 && tile_bits >= kv3;
+    const int k = use_v3 ? kv3 : (tile_bits < n ? tile_bits : n);
     if (k < 1 || k > kMaxTileBits) return fail(SV_EVALUE, "tile bits %d out of range", tile_bits);
     const int bmin = k >= 5 ? 5 : k;
     const uint64_t lowfix = (1ull << bmin) - 1ull;
@@ -202,16 +385,24 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
     PassPlan cur;
     auto flush = [&]() -> int {
         if (cur.ops.empty()) return SV_OK;
-        FusedParams P;
-        build_params(ops, cur, n, k, P);
         cudaEvent_t ev0 = nullptr, ev1 = nullptr;
         if (g_timing) {
             cudaEventCreate(&ev0);
             cudaEventCreate(&ev1);
             cudaEventRecord(ev0, st);
         }
-        cudaError_t e = launch_fused(psi, mode, P, st);
-        count_h2d(sizeof(FusedParams));
+        cudaError_t e;
+        static thread_local Fused2Params P2;
+        if (use_v3 && build_params2(ops, cur, n, g_fused_v2, P2) == 0 &&
+            (g_seg_limit <= 0 || P2.n_segs <= g_seg_limit)) {
+            e = launch_fused2(psi, mode, P2, st);
+            count_h2d(sizeof(Fused2Params));
+        } else {
+            static thread_local FusedParams P;
+            build_params(ops, cur, n, k, P);
+            e = launch_fused(psi, mode, P, st);
+            count_h2d(sizeof(FusedParams));
+        }
         if (g_timing) {
             cudaEventRecord(ev1, st);
             std::lock_guard<std::mutex> lk(g_timing_mu);
@@ -590,6 +781,17 @@ int sv_launch_count(uint64_t* count) {
 int sv_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
     *h2d = g_h2d.load();
     *d2h = g_d2h.load();
+    return SV_OK;
+}
+
+int sv_fused_variant(int v2) {
+    if (v2 < 0 || v2 > 5) return fail(SV_EVALUE, "fused variant %d not in 0..5", v2);
+    g_fused_v2 = v2;
+    return SV_OK;
+}
+
+int sv_fused_segment_limit(int limit) {
+    g_seg_limit = limit;
     return SV_OK;
 }
 

@@ -32,6 +32,38 @@ struct FusedParams {
     double mdata[kMaxMData];
 };
 
+// v2 fused passes: register-resident 2^12-amplitude tiles (sv_fused2.cu)
+enum {
+    F2_1Q = 1, F2_1Q_REAL = 2, F2_1Q_MONO = 3,
+    F2_2Q = 4, F2_2Q_REAL = 5, F2_2Q_MONO = 6,
+    F2_DIAG = 7, F2_DIAG_NEG = 8
+};
+constexpr int kMaxSegs = 48;
+struct Fused2Params {
+    uint64_t n_tiles;
+    uint64_t tile_mask;
+    int n, b, n_ops, n_segs;
+    int direct_in, direct_out;
+    int cfg, kbits, rbits;              // kernel configuration (tile bits, register bits)
+    int8_t tq[12];
+    uint8_t seg_reg[kMaxSegs][4];       // register bit j -> tile position
+    uint8_t seg_thr[kMaxSegs][9];       // thread-id bit j -> tile position
+    uint16_t seg_end[kMaxSegs];         // one past the segment's last op
+    uint16_t seg_rsw[kMaxSegs][16];     // swizzled shared-memory offset of register slot i
+    uint64_t last_rgo[16];              // HBM offset of register slot i in the last segment
+    uint64_t pf_go[16];                 // HBM offset of tile element 256*j (prefetch chunks)
+    uint64_t base_tab[4][256];          // tile index byte k -> local-index bits (deposit tables)
+    uint8_t kind[kMaxOps];
+    uint8_t ra[kMaxOps], rb[kMaxOps];   // register bits of qa / qb
+    uint8_t dreg[kMaxOps];              // DIAG: register-bit mask
+    uint16_t dthr[kMaxOps];             // DIAG: tile-position mask covered by thread bits
+    uint16_t moff[kMaxOps];
+    uint16_t mono[kMaxOps];             // monomial rows: per row src (2 bits) | unit (2 bits) << 2
+    uint64_t dout[kMaxOps];             // DIAG: out-of-tile local-index mask
+    double mdata[kMaxMData];
+};
+cudaError_t launch_fused2(void* psi, int mode, const Fused2Params& p, cudaStream_t st);
+
 // mode: SV_FP64 / SV_FP32 storage
 cudaError_t launch_gate1(void* psi, uint64_t n_elems, int mode, int q, const double* m8,
                          cudaStream_t st);
