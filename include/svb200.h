@@ -102,6 +102,60 @@ int sv_export(sv_handle h, void* host, uint64_t first, uint64_t count);
 int sv_import(sv_handle h, const void* host, uint64_t first, uint64_t count);
 int sv_synchronize(sv_handle h);
 
+/* ---- BYTE mode: adaptive two-byte polar encoding (codec.py) ---------- */
+typedef struct sv_bstate* sv_bhandle;
+
+/* One gate pass over a BYTE state (engine.py:186-215, 229-377). */
+typedef struct {
+    int32_t kind;          /* SV_OP_1Q / SV_OP_2Q / SV_OP_DIAG */
+    int32_t qa, qb;
+    int32_t n_local;       /* reference rank layout: local qubits per rank */
+    uint64_t diag_mask;
+    double m[32];          /* matrix (1Q/2Q) or diagonal factor (re, im) */
+    int32_t xkind;         /* 0 none, 1 pairwise 1q, 2 pairwise 2q, 3 quad (engine.py choreography) */
+    int32_t qlow_top;      /* pairwise 2q: the local qubit is the top local bit */
+    uint64_t xmask_a, xmask_b;
+    int32_t producer;      /* -1 all work items; r: only those reference rank r computes */
+    int32_t collect;       /* collect codebook proposals (codec.py:137-152) */
+    int32_t want_mag, want_ph;   /* which tables can still change */
+    double mag_cut, ph_cut;      /* collect only values below the cut (overflow retry) */
+} svb_gate_desc;
+
+int svb_create(int device, int n_qubits, sv_bhandle* out);
+int svb_destroy(sv_bhandle h);
+int svb_info(sv_bhandle h, int* device, int* n_qubits, void** stream);
+/* state.py:49-63: all zero bytes, magnitude index 1 (= 1.0) at `unit` */
+int svb_zero_state(sv_bhandle h, int64_t unit);
+/* upload the codebook (append order, codec.py:100-106); sorted copies are
+ * built here with a stable argsort (codec.py:112-120) */
+int svb_set_tables(sv_bhandle h, const double* mags, int n_mag, const double* thetas, const double* ux,
+                   const double* uy, int n_ph);
+/* one pass: reads the current planes, writes the pending planes */
+int svb_gate(sv_bhandle h, const svb_gate_desc* g);
+/* candidates of the passes since the last reset: distinct magnitudes and,
+ * per distinct theta, (re, im, ux, uy) of its smallest-(ux, uy) value
+ * (duplicates possible).  flags: 1 = a buffer overflowed (retry with a cut),
+ * 2 = at least one magnitude candidate was seen */
+int svb_candidates(sv_bhandle h, double* mags, uint64_t cap_m, uint64_t* n_m, double* ph4, uint64_t cap_p,
+                   uint64_t* n_p, int* flags);
+/* amplitudes whose phase decision was inside the atan2 margin */
+int svb_unsure(sv_bhandle h, uint64_t* idx, double* vals, uint64_t cap, uint64_t* n);
+int svb_reset(sv_bhandle h);
+/* overwrite bytes of the pending planes (host-resolved uncertain amplitudes) */
+int svb_patch(sv_bhandle h, const uint64_t* idx, const uint8_t* mi, const uint8_t* pi, uint64_t n);
+/* pending planes become current */
+int svb_commit(sv_bhandle h);
+int svb_export(sv_bhandle h, uint8_t* mi, uint8_t* pi, uint64_t first, uint64_t count);
+int svb_import(sv_bhandle h, const uint8_t* mi, const uint8_t* pi, uint64_t first, uint64_t count);
+/* decoded complex128 amplitudes [first, first+count) to host */
+int svb_decode(sv_bhandle h, double* out, uint64_t first, uint64_t count);
+/* measure.py on the decoded state (FP64 sums) */
+int svb_measure(sv_bhandle h, double* norm, double* ones, double* cross);
+/* array-level codec: encode n complex128 host values with the handle's tables
+ * (codec.py:193-201); with collect != 0 also gather proposals into the
+ * handle's candidate buffers (codec.py:137-152) */
+int svb_encode_values(sv_bhandle h, const double* vals, uint64_t n, uint8_t* mi, uint8_t* pi, int collect);
+
 /* ---- raw device buffers (for the array-level operator API) --------- */
 int sv_buffer_alloc(int device, uint64_t bytes, void** ptr);
 int sv_buffer_free(int device, void* ptr);

@@ -60,6 +60,23 @@ _SIGNATURES = {
     "sv_export": ([_P, _P, _U64, _U64], _I),
     "sv_import": ([_P, _P, _U64, _U64], _I),
     "sv_synchronize": ([_P], _I),
+    "svb_create": ([_I, _I, ctypes.POINTER(_P)], _I),
+    "svb_destroy": ([_P], _I),
+    "svb_info": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_P)], _I),
+    "svb_zero_state": ([_P, ctypes.c_int64], _I),
+    "svb_set_tables": ([_P, _D, _I, _D, _D, _D, _I], _I),
+    "svb_gate": ([_P, _P], _I),
+    "svb_candidates": ([_P, _D, _U64, ctypes.POINTER(_U64), _D, _U64, ctypes.POINTER(_U64),
+                        ctypes.POINTER(_I)], _I),
+    "svb_unsure": ([_P, ctypes.POINTER(_U64), _D, _U64, ctypes.POINTER(_U64)], _I),
+    "svb_reset": ([_P], _I),
+    "svb_patch": ([_P, ctypes.POINTER(_U64), _P, _P, _U64], _I),
+    "svb_commit": ([_P], _I),
+    "svb_export": ([_P, _P, _P, _U64, _U64], _I),
+    "svb_import": ([_P, _P, _P, _U64, _U64], _I),
+    "svb_decode": ([_P, _D, _U64, _U64], _I),
+    "svb_measure": ([_P, _D, _D, _D], _I),
+    "svb_encode_values": ([_P, _D, _U64, _P, _P, _I], _I),
     "sv_buffer_alloc": ([_I, _U64, ctypes.POINTER(_P)], _I),
     "sv_buffer_free": ([_I, _P], _I),
     "sv_copy_h2d": ([_P, _P, _U64, _P], _I),

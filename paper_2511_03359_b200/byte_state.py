@@ -1,0 +1,336 @@
+"""HBM-resident BYTE (two-plane uint8) state and the per-gate codebook barrier.
+
+``ByteDeviceState`` wraps an ``sv_bhandle`` (include/svb200.h): current and
+pending (magnitude, phase) index planes, the device codebook tables and the
+candidate buffers.  ``ByteEngineState`` adds the reference's per-gate
+protocol (engine.py:186-225, 365-377):
+
+  1. one device pass per reference rank (its "produced" values, as the
+     reference's exchange choreography assigns them) decodes, applies the
+     gate, encodes against the current tables into the pending planes and
+     reduces that rank's not-yet-representable values to candidates;
+  2. the host turns every rank's candidates into its proposal and merges
+     them (codec.py:137-191) — identical tables on every rank by construction;
+  3. if a table grew, one more pass re-encodes from the untouched current
+     planes with the new tables;
+  4. atan2-ambiguous amplitudes are re-encoded with numpy and patched in;
+  5. pending planes become current.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as nat
+from . import gates as g
+from .codec import CAPACITY, Codebook
+
+_BIG = 1e308
+_CAP = 1 << 20
+
+
+class SvbGateDesc(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("qa", ctypes.c_int32), ("qb", ctypes.c_int32),
+                ("n_local", ctypes.c_int32), ("diag_mask", ctypes.c_uint64), ("m", ctypes.c_double * 32),
+                ("xkind", ctypes.c_int32), ("qlow_top", ctypes.c_int32),
+                ("xmask_a", ctypes.c_uint64), ("xmask_b", ctypes.c_uint64),
+                ("producer", ctypes.c_int32), ("collect", ctypes.c_int32),
+                ("want_mag", ctypes.c_int32), ("want_ph", ctypes.c_int32),
+                ("mag_cut", ctypes.c_double), ("ph_cut", ctypes.c_double)]
+
+
+class ByteDeviceState:
+    """2**n amplitudes as (magnitude index, phase index) byte planes in HBM."""
+
+    mode_code = nat.SV_BYTE
+
+    def __init__(self, n_qubits: int, codebook: Codebook | None = None, device: int = 0):
+        lib = nat.load()
+        self.n_qubits = int(n_qubits)
+        self.device = device
+        h = ctypes.c_void_p()
+        nat.check(lib.svb_create(device, self.n_qubits, ctypes.byref(h)))
+        self.handle = h
+        s = ctypes.c_void_p()
+        nat.check(lib.svb_info(h, None, None, ctypes.byref(s)))
+        self.stream = s
+        self.codebook = codebook if codebook is not None else Codebook()
+        self._tables_version = None
+        self.version = 0
+        self.launches = 0
+
+    @property
+    def size(self) -> int:
+        return 1 << self.n_qubits
+
+    def sync_tables(self) -> None:
+        cb = self.codebook
+        key = (cb.version, len(cb.mags), len(cb.thetas))
+        if key == self._tables_version:
+            return
+        mags = np.ascontiguousarray(cb.mags, dtype=np.float64)
+        th = np.ascontiguousarray(cb.thetas, dtype=np.float64)
+        ux = np.ascontiguousarray(cb.ux, dtype=np.float64)
+        uy = np.ascontiguousarray(cb.uy, dtype=np.float64)
+        nat.check(nat.load().svb_set_tables(self.handle, nat.dptr(mags), len(mags), nat.dptr(th), nat.dptr(ux),
+                                            nat.dptr(uy), len(th)))
+        self._tables_version = key
+
+    def zero(self, unit_index: int | None = 0) -> None:
+        nat.check(nat.load().svb_zero_state(self.handle, -1 if unit_index is None else unit_index))
+        self.version += 1
+
+    def export_storage(self, first: int, count: int):
+        mi = np.empty(count, dtype=np.uint8)
+        pi = np.empty(count, dtype=np.uint8)
+        nat.check(nat.load().svb_export(self.handle, mi.ctypes.data_as(ctypes.c_void_p),
+                                        pi.ctypes.data_as(ctypes.c_void_p), first, count))
+        return mi, pi
+
+    def import_storage(self, parts, first: int = 0) -> None:
+        mi = np.ascontiguousarray(parts[0], dtype=np.uint8)
+        pi = np.ascontiguousarray(parts[1], dtype=np.uint8)
+        nat.check(nat.load().svb_import(self.handle, mi.ctypes.data_as(ctypes.c_void_p),
+                                        pi.ctypes.data_as(ctypes.c_void_p), first, mi.size))
+        self.version += 1
+
+    def decode(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        self.sync_tables()
+        count = self.size - first if count is None else count
+        out = np.empty(count, dtype=np.complex128)
+        nat.check(nat.load().svb_decode(self.handle, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                        first, count))
+        self.launches += 1
+        return out
+
+    def decode_all(self, codebook=None) -> np.ndarray:
+        return self.decode()
+
+    def measure_sums(self, codebook=None):
+        self.sync_tables()
+        n = self.n_qubits
+        norm = np.zeros(1)
+        ones = np.zeros(max(n, 1))
+        cross = np.zeros(2 * max(n, 1))
+        nat.check(nat.load().svb_measure(self.handle, nat.dptr(norm), nat.dptr(ones), nat.dptr(cross)))
+        self.launches += 2
+        return float(norm[0]), ones[:n].copy(), cross[0:2 * n:2] + 1j * cross[1:2 * n:2]
+
+    def measure_range(self, first: int, count: int):
+        vals = self.decode(first, count)
+        from .kernels import norm_squared
+        return norm_squared(vals), None, None
+
+    def synchronize(self) -> None:
+        nat.check(nat.load().sv_stream_synchronize(self.stream))
+
+    # -- candidate plumbing -----------------------------------------------------------
+    def read_candidates(self):
+        lib = nat.load()
+        mags = np.empty(_CAP, dtype=np.float64)
+        ph = np.empty((_CAP, 4), dtype=np.float64)
+        nm, npp = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        flags = ctypes.c_int(0)
+        nat.check(lib.svb_candidates(self.handle, nat.dptr(mags), _CAP, ctypes.byref(nm),
+                                     ph.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _CAP, ctypes.byref(npp),
+                                     ctypes.byref(flags)))
+        ph = ph[:npp.value]
+        return mags[:nm.value].copy(), (ph[:, 0] + 1j * ph[:, 1]), flags.value
+
+    def read_unsure(self):
+        idx = np.empty(_CAP, dtype=np.uint64)
+        vals = np.empty(2 * _CAP, dtype=np.float64)
+        n = ctypes.c_uint64(0)
+        nat.check(nat.load().svb_unsure(self.handle, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                        nat.dptr(vals), _CAP, ctypes.byref(n)))
+        k = n.value
+        return idx[:k].copy(), vals[0:2 * k:2] + 1j * vals[1:2 * k:2]
+
+    def reset(self):
+        nat.check(nat.load().svb_reset(self.handle))
+
+    def patch(self, idx, mi, pi):
+        if len(idx) == 0:
+            return
+        idx = np.ascontiguousarray(idx, dtype=np.uint64)
+        mi = np.ascontiguousarray(mi, dtype=np.uint8)
+        pi = np.ascontiguousarray(pi, dtype=np.uint8)
+        nat.check(nat.load().svb_patch(self.handle, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                       mi.ctypes.data_as(ctypes.c_void_p), pi.ctypes.data_as(ctypes.c_void_p),
+                                       idx.size))
+        self.launches += 1
+
+    def commit(self):
+        nat.check(nat.load().svb_commit(self.handle))
+        self.version += 1
+
+    def gate_pass(self, desc: SvbGateDesc):
+        nat.check(nat.load().svb_gate(self.handle, ctypes.byref(desc)))
+        self.launches += 1
+
+    # -- array-level codec -----------------------------------------------------------
+    def encode_values(self, v: np.ndarray):
+        self.sync_tables()
+        n = v.size
+        mi = np.empty(n, dtype=np.uint8)
+        pi = np.empty(n, dtype=np.uint8)
+        self.reset()
+        nat.check(nat.load().svb_encode_values(self.handle, v.view(np.float64).ctypes.data_as(
+            ctypes.POINTER(ctypes.c_double)), n, mi.ctypes.data_as(ctypes.c_void_p),
+            pi.ctypes.data_as(ctypes.c_void_p), 0))
+        idx, vals = self.read_unsure()
+        self.reset()
+        if len(idx):
+            fm, fp = self.codebook.host_encode(vals)
+            mi[idx.astype(np.int64)] = fm
+            pi[idx.astype(np.int64)] = fp
+        return mi, pi
+
+    def collect_values(self, v: np.ndarray):
+        self.sync_tables()
+        n = v.size
+        mi = np.empty(max(n, 1), dtype=np.uint8)
+        pi = np.empty(max(n, 1), dtype=np.uint8)
+        self.reset()
+        nat.check(nat.load().svb_encode_values(self.handle, v.view(np.float64).ctypes.data_as(
+            ctypes.POINTER(ctypes.c_double)), n, mi.ctypes.data_as(ctypes.c_void_p),
+            pi.ctypes.data_as(ctypes.c_void_p), 1))
+        mags, ph, flags = self.read_candidates()
+        self.reset()
+        if flags & 1:
+            raise RuntimeError("codebook candidate buffer overflow in propose()")
+        return mags, ph
+
+    def free(self):
+        if getattr(self, "handle", None):
+            nat.load(require_device=False).svb_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _exchange_fields(desc: SvbGateDesc, gate, layout, plan) -> None:
+    loc = layout.local_qubits
+    desc.n_local = loc
+    if plan.kind == "pairwise" and len(gate.qubits) == 1:
+        desc.xkind, desc.xmask_a = 1, plan.masks[0]
+    elif plan.kind == "pairwise":
+        desc.xkind, desc.xmask_a = 2, plan.masks[0]
+        (ql,) = [q for q in gate.qubits if q < loc]
+        desc.qlow_top = 1 if ql == loc - 1 else 0
+    elif plan.kind == "quad":
+        desc.xkind, desc.xmask_a, desc.xmask_b = 3, plan.masks[0], plan.masks[1]
+    else:
+        desc.xkind = 0
+
+
+class ByteEngineState(ByteDeviceState):
+    """The engine's whole-register BYTE state (all rank slices in one buffer)."""
+
+    def __init__(self, n_qubits: int, layout, device: int = 0):
+        super().__init__(n_qubits, Codebook(), device)
+        self.layout = layout
+        self.passes = 0
+        self.reencodes = 0
+        self.host_fixes = 0
+
+    def _desc(self, gate, plan) -> SvbGateDesc:
+        d = SvbGateDesc()
+        if g.is_diagonal(gate):
+            d.kind = nat.SV_OP_DIAG
+            mask = 0
+            for q in gate.qubits:
+                mask |= 1 << q
+            d.diag_mask = mask
+            f = g.diagonal_factor(gate)
+            d.m[0], d.m[1] = f.real, f.imag
+        else:
+            m = nat.mat_buffer(g.unitary_matrix(gate))
+            for i, v in enumerate(m):
+                d.m[i] = v
+            d.kind = nat.SV_OP_1Q if len(gate.qubits) == 1 else nat.SV_OP_2Q
+            d.qa = gate.qubits[0]
+            d.qb = gate.qubits[1] if len(gate.qubits) == 2 else 0
+        _exchange_fields(d, gate, self.layout, plan)
+        d.producer = -1
+        d.mag_cut = d.ph_cut = _BIG
+        return d
+
+    def _collect_rank(self, d: SvbGateDesc, rank: int):
+        """One pass restricted to `rank`'s work items; returns (mag cands, phase values, unsure)."""
+        d.producer = rank
+        d.collect = 1
+        cb = self.codebook
+        while True:
+            self.reset()
+            self.gate_pass(d)
+            self.passes += 1
+            mags, ph, flags = self.read_candidates()
+            unsure = self.read_unsure()
+            if not flags & 1:
+                return mags, ph, unsure
+            # candidate buffer overflowed: keep only the smallest values (merge can only
+            # append the smallest `room` of them) and run again
+            k = 4 * (CAPACITY + 1)
+            um = np.unique(mags)
+            if len(um) > k:
+                d.mag_cut = float(um[k])
+            _, th, _, _ = __import__("paper_2511_03359_b200.codec", fromlist=["canonicalize"]).canonicalize(ph)
+            ut = np.unique(th)
+            if len(ut) > k:
+                d.ph_cut = float(ut[k]) + 1e-13
+            if len(um) <= k and len(ut) <= k:
+                raise RuntimeError("codebook candidate buffer overflow without a usable cut")
+
+    def apply_gate(self, gate, layout=None) -> None:
+        from .layout import plan_exchange
+        from .state import PrecisionMode
+        plan = plan_exchange(self.layout, gate, PrecisionMode.BYTE)
+        cb = self.codebook
+        self.sync_tables()
+        sat_mag, sat_ph = cb.tables_saturated
+        d = self._desc(gate, plan)
+        d.want_mag = 0 if sat_mag else 1
+        d.want_ph = 0 if sat_ph else 1
+        unsure_idx, unsure_val = [], []
+        if sat_mag and sat_ph:
+            d.collect = 0
+            self.reset()
+            self.gate_pass(d)
+            self.passes += 1
+            ui, uv = self.read_unsure()
+            unsure_idx.append(ui)
+            unsure_val.append(uv)
+        else:
+            proposals = []
+            ranks = self.layout.rank_count
+            for r in range(ranks):
+                mags, ph, (ui, uv) = self._collect_rank(d, r if ranks > 1 else -1)
+                proposals.append(cb.finalize_proposal(mags, ph))
+                unsure_idx.append(ui)
+                unsure_val.append(uv)
+            version = cb.version
+            cb.merge(proposals)
+            if cb.version != version:
+                self.sync_tables()
+                d.producer = -1
+                d.collect = 0
+                self.reset()
+                self.gate_pass(d)
+                self.passes += 1
+                self.reencodes += 1
+                ui, uv = self.read_unsure()
+                unsure_idx, unsure_val = [ui], [uv]
+        self.reset()
+        idx = np.concatenate(unsure_idx) if unsure_idx else np.zeros(0, dtype=np.uint64)
+        if len(idx):
+            vals = np.concatenate(unsure_val)
+            mi, pi = cb.host_encode(vals)
+            self.patch(idx, mi, pi)
+            self.host_fixes += len(idx)
+        self.commit()

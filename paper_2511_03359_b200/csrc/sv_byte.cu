@@ -1,0 +1,484 @@
+// Adaptive two-byte polar encoding on the B200 (sm_100a).
+//
+// Reference: /root/reference/pkg/src/svsim/codec.py and engine.py:186-225.
+// A BYTE state is two uint8 planes (magnitude index, phase index) per
+// amplitude.  One gate = one kernel pass that, per amplitude group,
+//   decodes   mags[mi] * (ux[pi] + i uy[pi])           (codec.py:203-206)
+//   applies   the gate with numpy's FP64 operand order  (kernels.py)
+//   canonicalises each produced value                   (codec.py:33-53)
+//   encodes   it against the CURRENT tables, nearest entry, ties to the
+//             smaller original index                    (codec.py:56-71, 193-201)
+//   proposes  values whose magnitude / phase is not representable
+//             (codec.py:122-152) into per-CTA shared-memory hash sets,
+//             flushed to a global candidate buffer at the end of the pass.
+// so compressed amplitudes never round-trip HBM in FP64 (2 B read + 2 B
+// written per amplitude).  The pass writes a second pair of planes; if the
+// host-side merge of the candidates (the reference's per-gate barrier) grows
+// a table, the pass is re-run from the untouched input planes with the new
+// tables before the planes are swapped.
+//
+// Exactness.  |v| is numpy's complex abs (L*sqrt(fma(S/L,S/L,1))), ux/uy are
+// IEEE divisions: bit-identical to numpy.  The angle is numpy's SVML atan2 in
+// the reference, which is not reproducible on the GPU, so theta is computed
+// with CUDA atan2 (<= 2 ulp) EXCEPT on the axes (im == 0 or re == 0), where
+// both libraries return the exact IEEE special values.  Every decision that
+// depends on theta (nearest phase entry, 1e-12 representability, the 2*pi
+// wrap) is taken with a margin; amplitudes inside the margin are listed as
+// "uncertain" and resolved on the host with numpy, so the produced bytes are
+// the reference's bytes.
+#include <algorithm>
+#include <cstring>
+
+#include "sv_byte.cuh"
+#include "sv_common.cuh"
+#include "sv_kernels.cuh"
+
+namespace sv {
+
+namespace {
+constexpr double TWO_PI = 6.283185307179586;        // 2.0 * math.pi
+constexpr double MAG_RTOL = 1e-12, PHASE_ATOL = 1e-12;
+constexpr double TH_MARGIN = 1e-14;                 // >> |atan2_cuda - atan2_svml| (a few ulp of 2pi)
+constexpr int NT = 256;
+
+struct STables {
+    double dmag[256], dux[256], duy[256];
+    double smag[256], sth[256];
+    uint8_t smag_idx[256], sth_idx[256];
+    int n_mag, n_ph;
+};
+
+__device__ __forceinline__ cplx decode(const STables& t, uint8_t mi, uint8_t pi) {
+    if (mi == 0) return {0.0, 0.0};
+    const double m = t.dmag[mi];
+    return {__dmul_rn(m, t.dux[pi]), __dmul_rn(m, t.duy[pi])};
+}
+
+struct Polar {
+    double r, th, ux, uy;
+    bool th_exact;      // theta bit-identical to numpy (axis values, zero)
+    bool wrap_unsure;   // the 2*pi wrap decision is inside the margin
+};
+
+__device__ __forceinline__ Polar canon(cplx v) {
+    Polar p;
+    const double ax = fabs(v.re), ay = fabs(v.im);
+    const double L = fmax(ax, ay), S = fmin(ax, ay);
+    if (L == 0.0) {
+        p.r = 0.0;
+    } else {
+        const double q = __ddiv_rn(S, L);
+        p.r = __dmul_rn(L, __dsqrt_rn(__fma_rn(q, q, 1.0)));
+    }
+    p.wrap_unsure = false;
+    if (p.r == 0.0) {
+        p.th = 0.0; p.ux = 1.0; p.uy = 0.0; p.th_exact = true;
+        return p;
+    }
+    double a;
+    if (v.im == 0.0) {            // atan2(+-0, x): +-0 or +-pi (exact in every libm)
+        a = v.re > 0.0 ? 0.0 : (signbit(v.im) ? -3.141592653589793 : 3.141592653589793);
+        p.th_exact = true;
+    } else if (v.re == 0.0) {     // atan2(y, +-0) = +-pi/2
+        a = v.im > 0.0 ? 1.5707963267948966 : -1.5707963267948966;
+        p.th_exact = true;
+    } else {
+        a = atan2(v.im, v.re);
+        p.th_exact = false;
+    }
+    double th = (a == 0.0) ? 0.0 : (a < 0.0 ? __dadd_rn(a, TWO_PI) : a);   // np.mod(a, 2pi)
+    const double gap = __dsub_rn(TWO_PI, th);
+    if (gap < PHASE_ATOL) th = 0.0;
+    if (!p.th_exact && fabs(gap - PHASE_ATOL) <= TH_MARGIN) p.wrap_unsure = true;
+    p.th = th;
+    p.ux = __dadd_rn(__ddiv_rn(v.re, p.r), 0.0);
+    p.uy = __dadd_rn(__ddiv_rn(v.im, p.r), 0.0);
+    return p;
+}
+
+// numpy.searchsorted(side='left'): first i with s[i] >= x
+__device__ __forceinline__ int lower_bound(const double* s, int n, double x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// codec.py:56-71; returns index, and sets *unsure if a perturbation of x by
+// `margin` could change the answer
+__device__ __forceinline__ int nearest(const double* s, const uint8_t* orig, int n, double x, bool circular,
+                                       double margin, bool* unsure) {
+    const int pos = lower_bound(s, n, x);
+    const int last = n - 1;
+    int cand[4];
+    int nc = 2;
+    cand[0] = min(max(pos - 1, 0), last);
+    cand[1] = min(max(pos, 0), last);
+    if (circular && last > 0) { cand[2] = 0; cand[3] = last; nc = 4; }
+    double d[4];
+    double best = 1e300;
+    for (int c = 0; c < nc; ++c) {
+        double dd = fabs(__dsub_rn(s[cand[c]], x));
+        if (circular) dd = fmin(dd, __dsub_rn(TWO_PI, dd));
+        d[c] = dd;
+        best = fmin(best, dd);
+    }
+    int idx = 1 << 30;
+    for (int c = 0; c < nc; ++c)
+        if (d[c] == best) idx = min(idx, (int)orig[cand[c]]);
+    if (margin > 0.0) {
+        for (int c = 0; c < nc; ++c)
+            if ((int)orig[cand[c]] != idx && d[c] - best <= 2.0 * margin) *unsure = true;
+    }
+    return idx;
+}
+
+// codec.py:122-135 for one value: 1 representable, 0 not, -1 inside the margin
+__device__ __forceinline__ int representable(const double* s, int n, double x, bool mag, double margin) {
+    const int pos = lower_bound(s, n, x);
+    const int last = n - 1;
+    const int c0 = min(max(pos - 1, 0), last), c1 = min(max(pos, 0), last);
+    int verdict = 0;
+    for (int k = 0; k < 2; ++k) {
+        const double e = s[k == 0 ? c0 : c1];
+        double d = fabs(__dsub_rn(e, x));
+        double tol;
+        if (mag) {
+            tol = __dmul_rn(MAG_RTOL, fmax(fabs(x), fabs(e)));
+        } else {
+            d = fmin(d, __dsub_rn(TWO_PI, d));
+            tol = PHASE_ATOL;
+        }
+        if (d <= tol - margin) return 1;
+        if (d <= tol + margin) verdict = -1;
+    }
+    return verdict;
+}
+
+// ---- per-CTA candidate sets ----------------------------------------------------
+constexpr int MAG_SLOTS = 1024;
+constexpr int PH_SLOTS = 512;
+constexpr unsigned long long EMPTY = ~0ull;
+
+struct CtaSets {
+    unsigned long long mag_key[MAG_SLOTS];
+    unsigned long long ph_key[PH_SLOTS];
+    double ph_ux[PH_SLOTS], ph_uy[PH_SLOTS], ph_re[PH_SLOTS], ph_im[PH_SLOTS];
+    int ph_lock[PH_SLOTS];
+    int mag_count, ph_count;
+    int full;                       // a set ran out of slots: flush at the next barrier
+};
+
+__device__ __forceinline__ unsigned hash64(unsigned long long k) {
+    k ^= k >> 33; k *= 0xff51afd7ed558ccdull; k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ull; k ^= k >> 33;
+    return (unsigned)k;
+}
+
+__device__ void global_mag(ByteCand* out, double r) {
+    const unsigned long long slot = atomicAdd(&out->n_mag, 1ull);
+    if (slot < out->cap_mag) out->mag[slot] = r;
+    else out->overflow = 1;
+}
+
+__device__ void global_phase(ByteCand* out, const Polar& p, cplx v) {
+    const unsigned long long slot = atomicAdd(&out->n_ph, 1ull);
+    if (slot < out->cap_ph) {
+        out->ph[4 * slot + 0] = v.re;
+        out->ph[4 * slot + 1] = v.im;
+        out->ph[4 * slot + 2] = p.ux;
+        out->ph[4 * slot + 3] = p.uy;
+    } else {
+        out->overflow = 1;
+    }
+}
+
+// shared-memory set first; a full set spills straight to the global buffer
+// (duplicates there are harmless: the host takes unique values / first per theta)
+__device__ void insert_mag(CtaSets& s, ByteCand* out, double r) {
+    const unsigned long long key = (unsigned long long)__double_as_longlong(r);
+    unsigned h = hash64(key) & (MAG_SLOTS - 1);
+    for (int probe = 0; probe < 64; ++probe) {
+        const unsigned long long cur = s.mag_key[h];
+        if (cur == key) return;
+        if (cur == EMPTY) {
+            const unsigned long long prev = atomicCAS(&s.mag_key[h], EMPTY, key);
+            if (prev == EMPTY) { atomicAdd(&s.mag_count, 1); return; }
+            if (prev == key) return;
+        }
+        h = (h + 1) & (MAG_SLOTS - 1);
+    }
+    global_mag(out, r);
+}
+
+__device__ __forceinline__ bool lex_less(double ax, double ay, double bx, double by) {
+    return ax < bx || (ax == bx && ay < by);
+}
+
+__device__ void insert_phase(CtaSets& s, ByteCand* out, const Polar& p, cplx v) {
+    const unsigned long long key = (unsigned long long)__double_as_longlong(p.th);
+    unsigned h = hash64(key ^ 0x9e3779b97f4a7c15ull) & (PH_SLOTS - 1);
+    for (int probe = 0; probe < 64; ++probe) {
+        unsigned long long cur = s.ph_key[h];
+        if (cur == EMPTY) {
+            cur = atomicCAS(&s.ph_key[h], EMPTY, key);
+            if (cur == EMPTY) { atomicAdd(&s.ph_count, 1); cur = key; }
+        }
+        if (cur == key) {
+            // keep the lexicographically smallest (ux, uy) per exact theta (codec.py:144-148);
+            // the stored ux only decreases, so a strictly larger ux can never win
+            if (p.ux > *(volatile double*)&s.ph_ux[h]) return;
+            while (atomicCAS(&s.ph_lock[h], 0, 1) != 0) {}
+            if (lex_less(p.ux, p.uy, s.ph_ux[h], s.ph_uy[h])) {
+                s.ph_ux[h] = p.ux; s.ph_uy[h] = p.uy; s.ph_re[h] = v.re; s.ph_im[h] = v.im;
+            }
+            __threadfence_block();
+            atomicExch(&s.ph_lock[h], 0);
+            return;
+        }
+        h = (h + 1) & (PH_SLOTS - 1);
+    }
+    global_phase(out, p, v);
+}
+
+__device__ void sets_clear(CtaSets& s) {
+    for (int i = threadIdx.x; i < MAG_SLOTS; i += blockDim.x) s.mag_key[i] = EMPTY;
+    for (int i = threadIdx.x; i < PH_SLOTS; i += blockDim.x) {
+        s.ph_key[i] = EMPTY; s.ph_ux[i] = 1e300; s.ph_uy[i] = 1e300; s.ph_lock[i] = 0;
+    }
+    if (threadIdx.x == 0) { s.mag_count = 0; s.ph_count = 0; s.full = 0; }
+}
+
+__device__ void sets_flush(CtaSets& s, ByteCand* out) {
+    for (int i = threadIdx.x; i < MAG_SLOTS; i += blockDim.x) {
+        if (s.mag_key[i] == EMPTY) continue;
+        const unsigned long long slot = atomicAdd(&out->n_mag, 1ull);
+        if (slot < out->cap_mag) out->mag[slot] = __longlong_as_double((long long)s.mag_key[i]);
+        else out->overflow = 1;
+    }
+    for (int i = threadIdx.x; i < PH_SLOTS; i += blockDim.x) {
+        if (s.ph_key[i] == EMPTY) continue;
+        const unsigned long long slot = atomicAdd(&out->n_ph, 1ull);
+        if (slot < out->cap_ph) {
+            out->ph[4 * slot + 0] = s.ph_re[i];
+            out->ph[4 * slot + 1] = s.ph_im[i];
+            out->ph[4 * slot + 2] = s.ph_ux[i];
+            out->ph[4 * slot + 3] = s.ph_uy[i];
+        } else {
+            out->overflow = 1;
+        }
+    }
+}
+
+// producer rank of a work item in the reference's exchange choreography
+__device__ __forceinline__ int producer_of(const ByteGate& g, uint64_t i0) {
+    const int nl = g.n_local;
+    const uint64_t rank = i0 >> nl;
+    const uint64_t off = i0 & ((1ull << nl) - 1ull);
+    switch (g.xkind) {
+        case 1: {   // pairwise, single-qubit gate on global qubit
+            return (int)((off >> (nl - 1)) & 1 ? (rank | g.xmask_a) : (rank & ~g.xmask_a));
+        }
+        case 2: {   // pairwise, two-qubit gate with one global qubit
+            const int side = g.qlow_top ? (int)((off >> (nl - 2)) & 1) : (int)((off >> (nl - 1)) & 1);
+            return (int)(side ? (rank | g.xmask_a) : (rank & ~g.xmask_a));
+        }
+        case 3: {   // quad: rank at position p computes quarter p
+            const int pos = (int)(off >> (nl - 2));
+            const uint64_t base = rank & ~(g.xmask_a | g.xmask_b);
+            return (int)(base | ((pos & 1) ? g.xmask_a : 0) | ((pos & 2) ? g.xmask_b : 0));
+        }
+        default:
+            return (int)rank;
+    }
+}
+
+struct Emitter {
+    const STables& t;
+    const ByteGate& g;
+    CtaSets& sets;
+    ByteCand* cand;
+    uint8_t* mo;
+    uint8_t* po;
+    bool collect;
+
+    __device__ void emit(uint64_t idx, cplx v) const {
+        const Polar p = canon(v);
+        bool unsure = p.wrap_unsure;
+        const int mi = nearest(t.smag, t.smag_idx, t.n_mag, p.r, false, 0.0, &unsure);
+        int pi = nearest(t.sth, t.sth_idx, t.n_ph, p.th, true, p.th_exact ? 0.0 : TH_MARGIN, &unsure);
+        if (mi == 0) pi = 0;
+        mo[idx] = (uint8_t)mi;
+        po[idx] = (uint8_t)pi;
+        if (unsure && mi != 0) {
+            const unsigned long long slot = atomicAdd(&cand->n_unsure, 1ull);
+            if (slot < cand->cap_unsure) {
+                cand->unsure_idx[slot] = idx;
+                cand->unsure_val[2 * slot] = v.re;
+                cand->unsure_val[2 * slot + 1] = v.im;
+            } else {
+                cand->overflow = 1;
+            }
+        }
+        if (!collect) return;
+        if (g.want_mag && p.r < g.mag_cut && representable(t.smag, t.n_mag, p.r, true, 0.0) == 0) {
+            cand->any_mag = 1;
+            insert_mag(sets, cand, p.r);
+        }
+        if (g.want_ph && p.th < g.ph_cut &&
+            representable(t.sth, t.n_ph, p.th, false, p.th_exact ? 0.0 : TH_MARGIN) != 1) {
+            insert_phase(sets, cand, p, v);
+        }
+    }
+};
+
+__device__ void load_tables(STables& t, const ByteTables* gt) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        t.dmag[i] = gt->dmag[i]; t.dux[i] = gt->dux[i]; t.duy[i] = gt->duy[i];
+        t.smag[i] = gt->smag[i]; t.sth[i] = gt->sth[i];
+        t.smag_idx[i] = gt->smag_idx[i]; t.sth_idx[i] = gt->sth_idx[i];
+    }
+    if (threadIdx.x == 0) { t.n_mag = gt->n_mag; t.n_ph = gt->n_ph; }
+}
+}  // namespace
+
+// One BYTE gate pass.  Work items: pairs (1Q), quadruples (2Q) or single
+// amplitudes (DIAG, and COPY for untouched amplitudes of a diagonal gate).
+__global__ void __launch_bounds__(NT) k_byte_gate(const uint8_t* __restrict__ mi_in, const uint8_t* __restrict__ pi_in,
+                                                  uint8_t* __restrict__ mi_out, uint8_t* __restrict__ pi_out,
+                                                  const ByteTables* __restrict__ gtab, const __grid_constant__ ByteGate g,
+                                                  ByteCand* cand) {
+    __shared__ STables t;
+    __shared__ CtaSets sets;
+    load_tables(t, gtab);
+    const bool collect = g.collect != 0;
+    if (collect) sets_clear(sets);
+    __syncthreads();
+    const Emitter em{t, g, sets, cand, mi_out, pi_out, collect};
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g.kind == SV_OP_1Q) {
+        const cplx m0 = {g.m[0], g.m[1]}, m1 = {g.m[2], g.m[3]}, m2 = {g.m[4], g.m[5]}, m3 = {g.m[6], g.m[7]};
+        const uint64_t n_items = g.n_elems >> 1;
+        for (uint64_t w = first; w < n_items; w += step) {
+            const uint64_t i0 = insert0(w, g.qa), i1 = i0 | (1ull << g.qa);
+            if (g.producer >= 0 && producer_of(g, i0) != g.producer) continue;
+            const cplx a0 = decode(t, mi_in[i0], pi_in[i0]);
+            const cplx a1 = decode(t, mi_in[i1], pi_in[i1]);
+            em.emit(i0, row2(m0, m1, a0, a1));
+            em.emit(i1, row2(m2, m3, a0, a1));
+        }
+    } else if (g.kind == SV_OP_2Q) {
+        cplx m[16];
+        for (int i = 0; i < 16; ++i) m[i] = {g.m[2 * i], g.m[2 * i + 1]};
+        const int lo = min(g.qa, g.qb), hi = max(g.qa, g.qb);
+        const uint64_t n_items = g.n_elems >> 2;
+        for (uint64_t w = first; w < n_items; w += step) {
+            const uint64_t e = insert0(insert0(w, lo), hi);
+            if (g.producer >= 0 && producer_of(g, e) != g.producer) continue;
+            const uint64_t idx[4] = {e, e | (1ull << g.qa), e | (1ull << g.qb), e | (1ull << g.qa) | (1ull << g.qb)};
+            cplx a[4];
+            for (int c = 0; c < 4; ++c) a[c] = decode(t, mi_in[idx[c]], pi_in[idx[c]]);
+            cplx o[4];
+            for (int r = 0; r < 4; ++r) o[r] = row4(&m[4 * r], a[0], a[1], a[2], a[3]);
+            for (int r = 0; r < 4; ++r) em.emit(idx[r], o[r]);
+        }
+    } else {   // DIAG: masked amplitudes re-encoded, the rest copied
+        const cplx f = {g.m[0], g.m[1]};
+        for (uint64_t i = first; i < g.n_elems; i += step) {
+            if ((i & g.mask) == g.mask) {
+                if (g.producer >= 0 && producer_of(g, i) != g.producer) continue;
+                em.emit(i, cmul(decode(t, mi_in[i], pi_in[i]), f));
+            } else if (g.producer < 0 || (int)(i >> g.n_local) == g.producer) {
+                mi_out[i] = mi_in[i];
+                pi_out[i] = pi_in[i];
+            }
+        }
+    }
+    if (collect) {
+        __syncthreads();
+        sets_flush(sets, cand);
+    }
+}
+
+// Decode into complex128 (export, host mirrors, measurement of small states).
+__global__ void k_byte_decode(const uint8_t* __restrict__ mi, const uint8_t* __restrict__ pi, const ByteTables* gtab,
+                              double* __restrict__ out, uint64_t n) {
+    __shared__ STables t;
+    load_tables(t, gtab);
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const cplx v = decode(t, mi[i], pi[i]);
+        out[2 * i] = v.re;
+        out[2 * i + 1] = v.im;
+    }
+}
+
+// Encode complex128 values (Codebook.encode on device) with the same uncertain-
+// theta reporting as the gate pass; optionally collect proposals (Codebook.propose).
+__global__ void __launch_bounds__(NT) k_byte_encode(const double* __restrict__ vals, uint64_t n, const ByteTables* gtab,
+                                                    uint8_t* __restrict__ mi, uint8_t* __restrict__ pi,
+                                                    const __grid_constant__ ByteGate g, ByteCand* cand) {
+    __shared__ STables t;
+    __shared__ CtaSets sets;
+    load_tables(t, gtab);
+    const bool collect = g.collect != 0;
+    if (collect) sets_clear(sets);
+    __syncthreads();
+    const Emitter em{t, g, sets, cand, mi, pi, collect};
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        em.emit(i, {vals[2 * i], vals[2 * i + 1]});
+    if (collect) {
+        __syncthreads();
+        sets_flush(sets, cand);
+    }
+}
+
+__global__ void k_byte_patch(uint8_t* mi, uint8_t* pi, const uint64_t* idx, const uint8_t* nm, const uint8_t* np_,
+                             uint64_t n) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        mi[idx[k]] = nm[k];
+        pi[idx[k]] = np_[k];
+    }
+}
+
+static unsigned byte_grid(uint64_t items) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t cap = (uint64_t)sm_count(dev) * 4;
+    const uint64_t want = (items + NT - 1) / NT;
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
+}
+
+cudaError_t launch_byte_gate(const uint8_t* mi_in, const uint8_t* pi_in, uint8_t* mi_out, uint8_t* pi_out,
+                             const ByteTables* tab, const ByteGate& g, ByteCand* cand, cudaStream_t st) {
+    const uint64_t items = g.kind == SV_OP_1Q ? g.n_elems / 2 : (g.kind == SV_OP_2Q ? g.n_elems / 4 : g.n_elems);
+    k_byte_gate<<<byte_grid(items), NT, 0, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g, cand);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_byte_decode(const uint8_t* mi, const uint8_t* pi, const ByteTables* tab, double* out, uint64_t n,
+                               cudaStream_t st) {
+    k_byte_decode<<<byte_grid(n), NT, 0, st>>>(mi, pi, tab, out, n);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_byte_encode(const double* vals, uint64_t n, const ByteTables* tab, uint8_t* mi, uint8_t* pi,
+                               const ByteGate& g, ByteCand* cand, cudaStream_t st) {
+    k_byte_encode<<<byte_grid(n), NT, 0, st>>>(vals, n, tab, mi, pi, g, cand);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_byte_patch(uint8_t* mi, uint8_t* pi, const uint64_t* idx, const uint8_t* nm, const uint8_t* np_,
+                              uint64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_byte_patch<<<byte_grid(n), NT, 0, st>>>(mi, pi, idx, nm, np_, n);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace sv

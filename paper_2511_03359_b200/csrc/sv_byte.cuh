@@ -1,0 +1,56 @@
+// BYTE-mode device structures shared by sv_byte.cu and the C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/svb200.h"
+
+namespace sv {
+
+// Codebook tables as the kernels read them: decode tables by original index
+// (codec.py:203-206) and the ascending copies + original indices used by the
+// nearest-entry search (codec.py:110-120, 193-201).
+struct ByteTables {
+    double dmag[256], dux[256], duy[256];
+    double smag[256], sth[256];
+    uint8_t smag_idx[256], sth_idx[256];
+    int n_mag, n_ph;
+};
+
+// One gate pass (fields mirror svb_gate_desc in include/svb200.h).
+struct ByteGate {
+    int kind, qa, qb;
+    uint64_t mask;
+    double m[32];
+    uint64_t n_elems;
+    int n_local;
+    int xkind;                  // 0 none, 1 pairwise-1q, 2 pairwise-2q, 3 quad (reference choreography)
+    uint64_t xmask_a, xmask_b;  // partner rank masks
+    int qlow_top;               // pairwise-2q: the local qubit is the top local bit
+    int producer;               // -1: every work item; r: only items the reference's rank r computes
+    int collect, want_mag, want_ph;
+    int mag_room, ph_room;      // free table entries (informational)
+    double mag_cut, ph_cut;     // only values below the cut are collected (overflow retry)
+};
+
+// Candidate / uncertain-amplitude output of a pass (device memory).
+struct ByteCand {
+    unsigned long long n_mag, n_ph, n_unsure;
+    unsigned long long cap_mag, cap_ph, cap_unsure;
+    double* mag;                // distinct unrepresentable magnitudes
+    double* ph;                 // per distinct theta: (re, im, ux, uy) of the min-(ux, uy) value
+    unsigned long long* unsure_idx;
+    double* unsure_val;         // (re, im)
+    int overflow, any_mag, any_ph, pad;
+};
+
+cudaError_t launch_byte_gate(const uint8_t* mi_in, const uint8_t* pi_in, uint8_t* mi_out, uint8_t* pi_out,
+                             const ByteTables* tab, const ByteGate& g, ByteCand* cand, cudaStream_t st);
+cudaError_t launch_byte_decode(const uint8_t* mi, const uint8_t* pi, const ByteTables* tab, double* out, uint64_t n,
+                               cudaStream_t st);
+cudaError_t launch_byte_encode(const double* vals, uint64_t n, const ByteTables* tab, uint8_t* mi, uint8_t* pi,
+                               const ByteGate& g, ByteCand* cand, cudaStream_t st);
+cudaError_t launch_byte_patch(uint8_t* mi, uint8_t* pi, const uint64_t* idx, const uint8_t* nm, const uint8_t* np_,
+                              uint64_t n, cudaStream_t st);
+
+}  // namespace sv

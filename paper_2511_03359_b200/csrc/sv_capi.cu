@@ -524,6 +524,15 @@ int measure_impl(const void* psi, uint64_t n_elems, int mode, double* norm, doub
 
 }  // namespace
 
+namespace sv {
+int capi_fail(int code, const char* msg) { return fail(code, "%s", msg); }
+int capi_cuda_fail(cudaError_t e, const char* what) { return cuda_fail(e, what); }
+int capi_measure(const void* psi, uint64_t n, int mode, double* norm, double* ones, double* cross,
+                 cudaStream_t st) {
+    return measure_impl(psi, n, mode, norm, ones, cross, nullptr, 0, st);
+}
+}  // namespace sv
+
 // ---------------------------------------------------------------------------
 struct sv_state {
     int device;

@@ -78,7 +78,7 @@ class RunResult:
         """Global state vector (complex128) assembled from the rank slices."""
         dev = self.states[0].device_state
         if self.mode is PrecisionMode.BYTE:
-            return dev.decode_all(self.codebook)
+            return dev.decode()
         return dev.export().astype(np.complex128)
 
     def report_in_program_labels(self) -> ExpectationReport | None:
@@ -141,7 +141,7 @@ class _Engine:
         self.report = None
         self.codebook = None
         if mode is PrecisionMode.BYTE:
-            from .codec import ByteEngineState
+            from .byte_state import ByteEngineState
             self.dev = ByteEngineState(circuit.n_qubits, layout, device=device)
             self.codebook = self.dev.codebook
         else:
@@ -158,6 +158,7 @@ class _Engine:
     def _enqueue(self, gate):
         if self.mode is PrecisionMode.BYTE:
             self.dev.apply_gate(gate, self.layout)
+            self.gates_applied += 1
             return
         self.pending.append(gate_to_op(gate))
         self.gates_applied += 1
@@ -247,6 +248,10 @@ class _Engine:
         self.transport.assert_drained()
 
     def stats(self) -> dict:
-        return {"device": self.dev.device, "kernel_launches": self.dev.launches,
-                "gates_applied": self.gates_applied, "fused": self.fuse,
-                "physical_link_bytes": 0}
+        out = {"device": self.dev.device, "kernel_launches": self.dev.launches,
+               "gates_applied": self.gates_applied, "fused": self.fuse and self.mode is not PrecisionMode.BYTE,
+               "physical_link_bytes": 0}
+        if self.mode is PrecisionMode.BYTE:
+            out.update(byte_passes=self.dev.passes, byte_reencodes=self.dev.reencodes,
+                       byte_host_fixes=self.dev.host_fixes)
+        return out

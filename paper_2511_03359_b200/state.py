@@ -140,7 +140,7 @@ class LocalState:
 
 def _new_storage(n_local: int, mode: PrecisionMode, device: int):
     if mode is PrecisionMode.BYTE:
-        from .codec import ByteDeviceState
+        from .byte_state import ByteDeviceState
         return ByteDeviceState(n_local, device=device)
     from .device import DeviceState
     return DeviceState(n_local, mode, device=device)
