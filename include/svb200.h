@@ -156,6 +156,21 @@ int svb_measure(sv_bhandle h, double* norm, double* ones, double* cross);
  * handle's candidate buffers (codec.py:137-152) */
 int svb_encode_values(sv_bhandle h, const double* vals, uint64_t n, uint8_t* mi, uint8_t* pi, int collect);
 
+/* ---- multi-GPU: CUDA IPC + NVLink peer kernels ------------------------ */
+/* 64-byte IPC handle of the handle's state buffer */
+int sv_ipc_handle(sv_handle h, void* out64);
+/* map a peer's state buffer into this process (device = this rank's GPU) */
+int sv_ipc_open(int device, const void* handle64, void** peer_ptr);
+int sv_ipc_close(int device, void* peer_ptr);
+/* global<->local qubit swap with the partner rank (the remap planner's move):
+ * this rank has global bit `side`; its amplitudes with local bit l = 1-side
+ * trade places with the partner's amplitudes with bit l = side.  Both ranks
+ * call it; each moves half of the pairs.  n_local_elems = 2^n'. */
+int svk_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l, int side, void* stream);
+/* sum conj(a0[i]) * a1[i] over count elements (a1 may be a peer pointer):
+ * measure.py:83-101 cross term of a global qubit; out2 = (re, im) */
+int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, double* out2, void* stream);
+
 /* ---- raw device buffers (for the array-level operator API) --------- */
 int sv_buffer_alloc(int device, uint64_t bytes, void** ptr);
 int sv_buffer_free(int device, void* ptr);

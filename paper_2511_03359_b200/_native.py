@@ -77,6 +77,11 @@ _SIGNATURES = {
     "svb_decode": ([_P, _D, _U64, _U64], _I),
     "svb_measure": ([_P, _D, _D, _D], _I),
     "svb_encode_values": ([_P, _D, _U64, _P, _P, _I], _I),
+    "sv_ipc_handle": ([_P, _P], _I),
+    "sv_ipc_open": ([_I, _P, ctypes.POINTER(_P)], _I),
+    "sv_ipc_close": ([_I, _P], _I),
+    "svk_swap_peer": ([_P, _P, _U64, _I, _I, _I, _P], _I),
+    "svk_pair_dot": ([_P, _P, _U64, _I, _D, _P], _I),
     "sv_buffer_alloc": ([_I, _U64, ctypes.POINTER(_P)], _I),
     "sv_buffer_free": ([_I, _P], _I),
     "sv_copy_h2d": ([_P, _P, _U64, _P], _I),

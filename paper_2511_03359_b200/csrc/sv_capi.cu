@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 
@@ -827,6 +828,58 @@ int sv_pass_timing_read(uint64_t* passes, double* ms, double* bytes) {
     *passes = v.size();
     *ms = tot;
     *bytes = by;
+    return SV_OK;
+}
+
+int sv_ipc_handle(sv_handle h, void* out64) {
+    DeviceGuard g(h->device);
+    cudaIpcMemHandle_t ih;
+    CUDA_TRY(cudaIpcGetMemHandle(&ih, h->ptr), "cudaIpcGetMemHandle");
+    static_assert(sizeof(ih) == 64, "IPC handle size");
+    std::memcpy(out64, &ih, 64);
+    return SV_OK;
+}
+
+int sv_ipc_open(int device, const void* handle64, void** peer_ptr) {
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, handle64, 64);
+    CUDA_TRY(cudaIpcOpenMemHandle(peer_ptr, ih, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    return SV_OK;
+}
+
+int sv_ipc_close(int device, void* peer_ptr) {
+    DeviceGuard g(device);
+    CUDA_TRY(cudaIpcCloseMemHandle(peer_ptr), "cudaIpcCloseMemHandle");
+    return SV_OK;
+}
+
+int svk_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l, int side, void* stream) {
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "swap needs FP64 or FP32 storage");
+    if (!is_pow2(n_local_elems) || n_local_elems < 4) return fail(SV_EVALUE, "swap needs a power-of-two slice >= 4");
+    if (l < 0 || (1ull << l) >= n_local_elems) return fail(SV_EINDEX, "swap qubit %d outside the slice", l);
+    if (side != 0 && side != 1) return fail(SV_EVALUE, "side must be 0 or 1");
+    cudaError_t e = launch_swap_peer(own, peer, n_local_elems, mode, l, side, as_stream(stream));
+    return e == cudaSuccess ? SV_OK : cuda_fail(e, "swap launch");
+}
+
+int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, double* out2, void* stream) {
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "pair dot needs FP64 or FP32 storage");
+    out2[0] = out2[1] = 0.0;
+    if (count == 0) return SV_OK;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int grid = (int)std::min<uint64_t>((count + 255) / 256, (uint64_t)sm_count(dev) * 4);
+    double* part = nullptr;
+    cudaStream_t st = as_stream(stream);
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), 16 * grid, st), "pair dot scratch");
+    cudaError_t e = launch_pair_dot(a0, a1, count, mode, part, grid, st);
+    std::vector<double> h(2 * grid);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), part, 16 * grid, cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(part, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "pair dot");
+    for (int b = 0; b < grid; ++b) { out2[0] += h[2 * b]; out2[1] += h[2 * b + 1]; }
     return SV_OK;
 }
 

@@ -94,6 +94,9 @@ cudaError_t launch_measure(const void* psi, int mode, const MeasureParams& p, do
 int measure_grid(int device);
 
 int sm_count(int device);
+cudaError_t launch_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l, int c, cudaStream_t st);
+cudaError_t launch_pair_dot(const void* a0, const void* a1, uint64_t n, int mode, double* partials, int grid,
+                            cudaStream_t st);
 void count_launch(uint64_t n = 1);
 
 }  // namespace sv

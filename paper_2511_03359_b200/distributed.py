@@ -1,0 +1,277 @@
+"""Multi-GPU execution: one process per GPU, NVLink 5 / NVSwitch exchanges.
+
+Launch with torchrun (``python -m torch.distributed.run --nproc-per-node P``)
+and call ``run_circuit_distributed`` on every rank.  Rank r owns the 2**N'
+amplitudes whose top log2(P) index bits equal r (svsim/layout.py:26-47),
+in its own GPU's HBM.
+
+Control plane: ``torch.distributed`` (gloo, CPU) for rendezvous, the CUDA IPC
+handle exchange, barriers and the few scalars of a measurement.  Data plane:
+libsvb200 kernels on IPC-mapped peer memory —
+  * gates whose qubits are local: fused tile passes (same kernels as 1 GPU);
+  * a non-diagonal gate on a global qubit: the remap planner (remap.py)
+    swaps it with a local qubit first (svk_swap_peer: every amplitude that has
+    to move crosses NVLink once, L/2 per direction per rank pair);
+  * diagonal gates: no data movement, global bits select the active ranks
+    (layout.py:81-82);
+  * measure-all: local tiled passes for local qubits, svk_pair_dot over
+    NVLink for the cross terms of global qubits (measure.py:83-101), then
+    one all-reduce of 3N + 1 scalars.
+The reference's ledgers are still charged exactly as svsim would
+(layout.plan_exchange per gate, one L/2 message per global qubit at
+measurement); the bytes that physically crossed NVLink are reported next to
+them.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from . import gates as g
+from .circuit import Circuit, validate_circuit
+from .device import gate_op
+from .layout import PartitionLayout, TrafficLedger, plan_exchange
+from .measure import ExpectationReport, report_from_sums
+from .remap import Measure, PhysGate, RemapPlanner, Swap
+from .state import PrecisionMode
+
+
+def phys_op(gate, phys: tuple, n_local: int, rank: int):
+    """sv_op for a gate on physical positions; None if this rank is inactive (diagonal)."""
+    if g.is_diagonal(gate):
+        mask = 0
+        for p in phys:
+            if p >= n_local:
+                if not (rank >> (p - n_local)) & 1:
+                    return None
+            else:
+                mask |= 1 << p
+        f = g.diagonal_factor(gate)
+        return gate_op(nat.SV_OP_DIAG, mask=mask, data=(f.real, f.imag))
+    m = nat.mat_buffer(g.unitary_matrix(gate))
+    if len(phys) == 1:
+        return gate_op(nat.SV_OP_1Q, qa=phys[0], data=m)
+    return gate_op(nat.SV_OP_2Q, qa=phys[0], qb=phys[1], data=m)
+
+
+class CudaBackend:
+    """This rank's slice in HBM plus IPC-mapped slices of every other rank."""
+
+    def __init__(self, dist, n_local: int, mode: PrecisionMode, device: int, tile_bits: int = 12):
+        from .device import DeviceState
+        self.dist = dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.n_local = n_local
+        self.mode = mode
+        self.tile_bits = tile_bits
+        self.dev = DeviceState(n_local, mode, device=device)
+        self.dev.zero(0 if self.rank == 0 else None)
+        self.bpe = mode.bytes_per_element
+        handle = (ctypes.c_char * 64)()
+        nat.check(nat.load().sv_ipc_handle(self.dev.handle, handle))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle))
+        self.peers = {}
+        for r, hb in enumerate(handles):
+            if r == self.rank:
+                continue
+            p = ctypes.c_void_p()
+            buf = (ctypes.c_char * 64).from_buffer_copy(hb)
+            nat.check(nat.load().sv_ipc_open(device, buf, ctypes.byref(p)))
+            self.peers[r] = p
+        self.link_bytes = 0
+        dist.barrier()
+
+    def apply_local(self, ops):
+        self.dev.apply_fused(ops, self.tile_bits)
+
+    def _sync_all(self):
+        self.dev.synchronize()
+        self.dist.barrier()
+
+    def swap(self, global_pos: int, local_pos: int):
+        bit = global_pos - self.n_local
+        partner = self.rank ^ (1 << bit)
+        side = (self.rank >> bit) & 1
+        self._sync_all()
+        nat.check(nat.load().svk_swap_peer(self.dev.ptr, self.peers[partner], self.dev.size, self.dev.mode_code,
+                                           local_pos, side, self.dev.stream))
+        self._sync_all()
+        self.dev._touch()
+        self.link_bytes += 2 * (self.dev.size // 4) * self.bpe      # this rank's reads + writes over NVLink
+
+    def measure_local(self):
+        return self.dev.measure()
+
+    def pair_dot(self, global_pos: int) -> complex:
+        """This rank's share of sum conj(a0) a1 for a global qubit (measure.py:92-99)."""
+        bit = global_pos - self.n_local
+        partner = self.rank ^ (1 << bit)
+        low = ((self.rank >> bit) & 1) == 0
+        half = self.dev.size // 2
+        esz = np.dtype(self.dev.dtype).itemsize
+        self._sync_all()
+        out = np.zeros(2)
+        if low:
+            a0, a1 = self.dev.ptr, self.peers[partner]
+            off = 0
+        else:
+            a0, a1 = self.peers[partner], self.dev.ptr
+            off = half
+        p0 = ctypes.c_void_p(a0.value + off * esz)
+        p1 = ctypes.c_void_p(a1.value + off * esz)
+        nat.check(nat.load().svk_pair_dot(p0, p1, half, self.dev.mode_code, nat.dptr(out), self.dev.stream))
+        self.link_bytes += half * self.bpe
+        return complex(out[0], out[1])
+
+    def export(self) -> np.ndarray:
+        return self.dev.export()
+
+    def close(self):
+        self.dev.synchronize()
+        self.dist.barrier()
+        for p in self.peers.values():
+            nat.load().sv_ipc_close(self.dev.device, p)
+        self.peers = {}
+
+
+@dataclass
+class DistRunResult:
+    circuit: Circuit
+    layout: PartitionLayout
+    mode: PrecisionMode
+    rank: int
+    ledgers: list
+    report: ExpectationReport | None
+    perm: tuple                       # logical qubit -> physical position at the end
+    wall_time_seconds: float
+    device_stats: dict = field(default_factory=dict)
+    backend: object = None
+
+    def local_slice(self) -> np.ndarray:
+        """This rank's slice in PHYSICAL order (after remapping)."""
+        return self.backend.export()
+
+    def gathered_state(self, dist) -> np.ndarray | None:
+        """Logical-order global state on rank 0 (collective; small N only)."""
+        mine = self.local_slice().astype(np.complex128)
+        parts = [None] * dist.get_world_size()
+        dist.all_gather_object(parts, mine)
+        if self.rank != 0:
+            return None
+        phys = np.concatenate(parts)
+        idx = np.arange(phys.size)
+        src = np.zeros_like(idx)
+        for q, p in enumerate(self.perm):
+            src |= ((idx >> q) & 1) << p
+        return phys[src]
+
+
+def _charge_reference(layout, ledgers, gate, mode):
+    """The reference ledger entries of one gate (transport.py:30-35 via engine.py)."""
+    plan = plan_exchange(layout, gate, mode)
+    L = layout.local_size
+    P = layout.rank_count
+    if plan.kind == "pairwise":
+        for r in range(P):
+            ledgers[r].count_send(plan.bytes_per_rank)
+            ledgers[r ^ plan.masks[0]].count_receive(plan.bytes_per_rank)
+    elif plan.kind == "quad":
+        ma, mb = plan.masks
+        for r in range(P):
+            base = r & ~(ma | mb)
+            for pos in range(4):
+                dst = base | (ma if pos & 1 else 0) | (mb if pos & 2 else 0)
+                if dst != r:
+                    ledgers[r].count_send((L // 4) * plan.bytes_per_element)
+                    ledgers[dst].count_receive((L // 4) * plan.bytes_per_element)
+
+
+def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = PrecisionMode.FP64,
+                            remap: bool = True, device: int | None = None, backend_factory=None,
+                            tile_bits: int = 12, fuse_limit: int = 1024) -> DistRunResult:
+    """Run `circuit` with one rank per process of the torch.distributed group `dist`."""
+    validate_circuit(circuit)
+    if mode is PrecisionMode.BYTE:
+        raise NotImplementedError("BYTE mode across GPUs is not wired yet: use run_circuit (one GPU)")
+    P = dist.get_world_size()
+    rank = dist.get_rank()
+    if P & (P - 1):
+        raise ValueError("rank count must be a power of two")
+    n = circuit.n_qubits
+    n_local = n - (P.bit_length() - 1)
+    layout = PartitionLayout(n, n_local)
+    if not remap:
+        raise NotImplementedError("reference-choreography exchanges: use remap=True")
+    start = time.perf_counter()
+    if backend_factory is None:
+        be = CudaBackend(dist, n_local, mode, rank if device is None else device, tile_bits)
+    else:
+        be = backend_factory(dist, n_local, mode)
+    ledgers = [TrafficLedger() for _ in range(P)]
+    planner = RemapPlanner(n, n_local, remap=remap)
+    steps = planner.plan(circuit.gates)
+    pending = []
+    report = None
+    swaps = 0
+
+    def flush():
+        nonlocal pending
+        if pending:
+            be.apply_local(pending)
+            pending = []
+
+    for step in steps:
+        if isinstance(step, Swap):
+            flush()
+            be.swap(step.global_pos, step.local_pos)
+            swaps += 1
+        elif isinstance(step, PhysGate):
+            _charge_reference(layout, ledgers, step.gate, mode)
+            op = phys_op(step.gate, step.qubits, n_local, rank)
+            if op is not None:
+                pending.append(op)
+                if len(pending) >= fuse_limit:
+                    flush()
+            for led in ledgers:
+                led.gate_operations += 1
+        elif isinstance(step, Measure):
+            flush()
+            report = _measure(be, layout, ledgers, step.perm, rank, mode, dist)
+            for led in ledgers:
+                led.gate_operations += 1
+    flush()
+    stats = {"swaps": swaps, "physical_link_bytes": be.link_bytes, "planner": "remap" if remap else "reference"}
+    return DistRunResult(circuit, layout, mode, rank, ledgers, report, tuple(planner.pos),
+                         time.perf_counter() - start, stats, be)
+
+
+def _measure(be, layout, ledgers, perm, rank, mode, dist):
+    import torch
+    n, n_local = layout.total_qubits, layout.local_qubits
+    half_bytes = (layout.local_size // 2) * mode.bytes_per_element
+    for q in range(n_local, n):        # reference accounting: one L/2 message per global qubit
+        m = 1 << (q - n_local)
+        for r in range(layout.rank_count):
+            ledgers[r].count_send(half_bytes)
+            ledgers[r ^ m].count_receive(half_bytes)
+    norm, ones_l, cross_l = be.measure_local()
+    ones_p = np.zeros(n)
+    cross_p = np.zeros(n, dtype=np.complex128)
+    ones_p[:n_local] = ones_l
+    cross_p[:n_local] = cross_l
+    for p in range(n_local, n):
+        cross_p[p] = be.pair_dot(p)
+        ones_p[p] = norm if (rank >> (p - n_local)) & 1 else 0.0
+    vec = torch.tensor(np.concatenate([[norm], ones_p, cross_p.real, cross_p.imag]), dtype=torch.float64)
+    dist.all_reduce(vec)
+    v = vec.numpy()
+    norm_t, ones_t = float(v[0]), v[1:1 + n]
+    cross_t = v[1 + n:1 + 2 * n] + 1j * v[1 + 2 * n:1 + 3 * n]
+    ones = [ones_t[perm[q]] for q in range(n)]
+    cross = [cross_t[perm[q]] for q in range(n)]
+    return report_from_sums(norm_t, ones, cross)
