@@ -58,6 +58,8 @@ int sv_abi_version(void);
 const char* sv_last_error(void);
 int sv_device_count(int* count);
 int sv_sm_count(int device, int* count);
+/* make `device` current on the calling thread (svk_* launch on the current device) */
+int sv_set_device(int device);
 
 /* ---- raw device-pointer kernels (one call = one kernel launch) ------ */
 /* kernels.py:30-40 apply_single: in-place 2x2 on pairs (i, i + 2^q) of a

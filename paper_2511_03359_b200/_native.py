@@ -40,6 +40,7 @@ _SIGNATURES = {
     "sv_last_error": ([], ctypes.c_char_p),
     "sv_device_count": ([ctypes.POINTER(_I)], _I),
     "sv_sm_count": ([_I, ctypes.POINTER(_I)], _I),
+    "sv_set_device": ([_I], _I),
     "svk_apply_1q": ([_P, _U64, _I, _I, _D, _P], _I),
     "svk_apply_2q": ([_P, _U64, _I, _I, _I, _D, _P], _I),
     "svk_apply_diag": ([_P, _U64, _I, _U64, _D, _P], _I),

@@ -577,6 +577,11 @@ int sv_device_count(int* count) {
     return SV_OK;
 }
 
+int sv_set_device(int device) {
+    CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
+    return SV_OK;
+}
+
 int sv_sm_count(int device, int* count) {
     *count = sm_count(device);
     return SV_OK;

@@ -63,6 +63,7 @@ class CudaBackend:
 
     def __init__(self, dist, n_local: int, mode: PrecisionMode, device: int, tile_bits: int = 12):
         from .device import DeviceState
+        nat.check(nat.load().sv_set_device(device))
         self.dist = dist
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
         self.n_local = n_local

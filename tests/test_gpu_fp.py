@@ -254,3 +254,21 @@ def test_local_state_api():
     assert w.dtype == np.complex128
     st.store(np.full(16, 0.25, dtype=np.complex128))
     assert np.allclose(st.psi, 0.25)
+
+
+def test_multi_gpu_torchrun_parity():
+    """2-GPU remapped execution vs the oracle (skipped on single-GPU boxes)."""
+    import ctypes
+    import os
+    import subprocess
+    import sys
+    from paper_2511_03359_b200 import _native
+    n = ctypes.c_int(0)
+    _native.load().sv_device_count(ctypes.byref(n))
+    if n.value < 2:
+        pytest.skip("needs 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+           "--master-port", "29533", os.path.join(root, "tests", "dist_gpu_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
