@@ -85,6 +85,8 @@ class CudaBackend:
             nat.check(nat.load().sv_ipc_open(device, buf, ctypes.byref(p)))
             self.peers[r] = p
         self.link_bytes = 0
+        self.swap_timing = False
+        self.swap_events = []
         dist.barrier()
 
     def apply_local(self, ops):
@@ -99,8 +101,14 @@ class CudaBackend:
         partner = self.rank ^ (1 << bit)
         side = (self.rank >> bit) & 1
         self._sync_all()
+        if self.swap_timing:
+            e0, e1 = nat.Event(), nat.Event()
+            e0.record(self.dev.stream)
         nat.check(nat.load().svk_swap_peer(self.dev.ptr, self.peers[partner], self.dev.size, self.dev.mode_code,
                                            local_pos, side, self.dev.stream))
+        if self.swap_timing:
+            e1.record(self.dev.stream)
+            self.swap_events.append((e0, e1))
         self._sync_all()
         self.dev._touch()
         self.link_bytes += 2 * (self.dev.size // 4) * self.bpe      # this rank's reads + writes over NVLink
