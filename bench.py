@@ -45,7 +45,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "sec/gate & effective HBM GB/s vs roofline at N qubits, 1/2/4/8 B200; adder circuit time"
 SEED = 20240817
-CPU_SAMPLE_N = 24
+CPU_SAMPLE_N = 26
 
 
 def peaks():
@@ -326,7 +326,8 @@ def run_b200(args):
                          "frac": round(achieved / peak, 4), "traffic": None,
                          "kernel": {0: "k_fused<c64s,12>", 1: "k_fused3<12,4,1>", 2: "k_fused3<11,3,2>",
                                     3: "k_fused3<12,3,1>", 4: "k_fused3<11,3,3>",
-                                    5: "k_fused3<10,3,4>"}[args.fused],
+                                    5: "k_fused3<10,3,4>", 6: "k_fused3<11,4,3>",
+                                    7: "k_fused3<10,4,6>"}[args.fused],
                          "launches_timed": passes,
                          "bytes_per_launch": 2 * 16 * 2 ** n},
             "gpu_launches": launches,
@@ -471,11 +472,11 @@ def main():
     ap.add_argument("--n", type=int, default=33, help="qubits per GPU")
     ap.add_argument("--layers", type=int, default=9, help="H layer + random layers in the workload")
     ap.add_argument("--tile-bits", type=int, default=12, help="v1 tile bits / upper bound")
-    ap.add_argument("--fused", type=int, default=5, choices=[0, 1, 2, 3, 4, 5],
+    ap.add_argument("--fused", type=int, default=6, choices=[0, 1, 2, 3, 4, 5, 6, 7],
                     help="fused-pass kernel: 0 smem-per-gate v1, 1-3 register-resident v3 configs")
     ap.add_argument("--seg-limit", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-layers", type=int, default=2)
+    ap.add_argument("--cpu-layers", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--single-gate", action="store_true", default=True)
     args = ap.parse_args()

@@ -30,7 +30,7 @@ inline void count_d2h(uint64_t b) { g_d2h.fetch_add(b, std::memory_order_relaxed
 
 struct TimedPass { cudaEvent_t a, b; double bytes; };
 bool g_timing = false;
-int g_fused_v2 = 5;      // default: 2^10 tiles, 8 amplitudes/thread, 4 CTAs/SM (best measured)
+int g_fused_v2 = 6;      // default: 2^11 tiles, 16 amplitudes/thread, 3 CTAs/SM (best measured)
 int g_seg_limit = 0;        // > 0: passes needing more segments fall back to v1
 std::mutex g_timing_mu;
 std::vector<TimedPass> g_timed;
@@ -214,8 +214,8 @@ int classify(const double* m, int dim, uint32_t* mono) {
 
 int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Params& P) {
     std::memset(&P, 0, sizeof(P));
-    const int K = (cfg == 2 || cfg == 4) ? 11 : (cfg == 5 ? 10 : 12);
-    const int RB = cfg == 1 ? 4 : 3;
+    const int K = (cfg == 2 || cfg == 4 || cfg == 6) ? 11 : ((cfg == 5 || cfg == 7) ? 10 : 12);
+    const int RB = (cfg == 1 || cfg == 6 || cfg == 7) ? 4 : 3;
     const int NTH = 1 << (K - RB);
     P.cfg = cfg;
     P.kbits = K;
@@ -363,7 +363,8 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
         return fail(SV_EVALUE, "fused pass needs a 32-byte aligned buffer");
     const int n = log2u(n_elems);
     if (tile_bits <= 0) tile_bits = 12;
-    const int kv3 = (g_fused_v2 == 2 || g_fused_v2 == 4) ? 11 : (g_fused_v2 == 5 ? 10 : 12);
+    const int kv3 = (g_fused_v2 == 2 || g_fused_v2 == 4 || g_fused_v2 == 6) ? 11
+                    : ((g_fused_v2 == 5 || g_fused_v2 == 7) ? 10 : 12);
     const bool use_v3 = g_fused_v2 != 0 && mode == SV_FP64 && n >= kv3 && tile_bits >= kv3;
     const int k = use_v3 ? kv3 : (tile_bits < n ? tile_bits : n);
     if (k < 1 || k > kMaxTileBits) return fail(SV_EVALUE, "tile bits %d out of range", tile_bits);
@@ -800,7 +801,7 @@ int sv_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
 }
 
 int sv_fused_variant(int v2) {
-    if (v2 < 0 || v2 > 5) return fail(SV_EVALUE, "fused variant %d not in 0..5", v2);
+    if (v2 < 0 || v2 > 7) return fail(SV_EVALUE, "fused variant %d not in 0..7", v2);
     g_fused_v2 = v2;
     return SV_OK;
 }

@@ -297,6 +297,8 @@ cudaError_t launch_fused2(void* psi, int mode, const Fused2Params& p, cudaStream
         case 3: return fused3_cfg<12, 3, 1>(psi, p, st);
         case 4: return fused3_cfg<11, 3, 3>(psi, p, st);
         case 5: return fused3_cfg<10, 3, 4>(psi, p, st);
+        case 6: return fused3_cfg<11, 4, 3>(psi, p, st);
+        case 7: return fused3_cfg<10, 4, 6>(psi, p, st);
         default: return fused3_cfg<12, 4, 1>(psi, p, st);
     }
 }

@@ -108,12 +108,11 @@ __global__ void __launch_bounds__(256) k_gate1_hi(S* __restrict__ psi, uint64_t 
 }
 
 // single-qubit gate, q < log2(V): the pair partners share a 32-byte vector.
-template <typename S, int U>
-__global__ void __launch_bounds__(256) k_gate1_lo(S* __restrict__ psi, uint64_t n_vecs, int q,
-                                                  Mat2 m) {
+template <typename S, int U, int Q>
+__global__ void __launch_bounds__(256) k_gate1_lo(S* __restrict__ psi, uint64_t n_vecs, Mat2 m) {
     constexpr int V = Store<S>::V;
     const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
-    const int off = 1 << q;
+    constexpr int off = 1 << Q;
     for (uint64_t w0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w0 < n_vecs; w0 += U * step) {
         Vec<S> x[U];
 #pragma unroll
@@ -335,7 +334,10 @@ static cudaError_t gate1_t(S* psi, uint64_t n, int q, const Mat2& m, cudaStream_
         k_gate1_hi<S, U><<<grid_for(items, 256 * U, 8), 256, 0, st>>>(psi, items, q, m);
     } else {
         const uint64_t vecs = n / V;
-        k_gate1_lo<S, 4><<<grid_for(vecs, 256 * 4, 8), 256, 0, st>>>(psi, vecs, q, m);
+        if (q == 0)
+            k_gate1_lo<S, 4, 0><<<grid_for(vecs, 256 * 4, 8), 256, 0, st>>>(psi, vecs, m);
+        else
+            k_gate1_lo<S, 4, 1><<<grid_for(vecs, 256 * 4, 8), 256, 0, st>>>(psi, vecs, m);
     }
     count_launch();
     return cudaGetLastError();
