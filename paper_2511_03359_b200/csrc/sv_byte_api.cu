@@ -16,6 +16,7 @@ int capi_fail(int code, const char* msg);                 // sv_capi.cu
 int capi_cuda_fail(cudaError_t e, const char* what);      // sv_capi.cu
 int capi_measure(const void* psi, uint64_t n, int mode, double* norm, double* ones, double* cross,
                  cudaStream_t st);                        // sv_capi.cu
+int capi_measure_byte(const void* src, uint64_t n, double* norm, double* ones, double* cross, cudaStream_t st);
 }
 
 #define BTRY(expr, what)                                        \
@@ -266,14 +267,16 @@ int svb_decode(sv_bhandle h, double* out, uint64_t first, uint64_t count) {
 int svb_measure(sv_bhandle h, double* norm, double* ones, double* cross) {
     Guard gd(h->device);
     const uint64_t n = 1ull << h->n;
-    double* d = nullptr;
-    BTRY(cudaMallocAsync(reinterpret_cast<void**>(&d), 16 * n, h->stream), "measure decode buffer");
-    cudaError_t e = launch_byte_decode(h->plane[h->cur][0], h->plane[h->cur][1], h->tab, d, n, h->stream);
-    if (e != cudaSuccess) { cudaFreeAsync(d, h->stream); return capi_cuda_fail(e, "measure decode"); }
-    const int rc = capi_measure(d, n, SV_FP64, norm, ones, cross, h->stream);
-    cudaFreeAsync(d, h->stream);
-    cudaStreamSynchronize(h->stream);
-    return rc;
+    if (h->n == 0) {   // one amplitude: decode it on the host side of the copy
+        double v[2];
+        if (int rc = svb_decode(h, v, 0, 1)) return rc;
+        *norm = v[0] * v[0] + v[1] * v[1];
+        return SV_OK;
+    }
+    // decoded on the fly inside the tiled measurement passes (no FP64 copy of the state)
+    struct { const uint8_t* mi; const uint8_t* pi; const double* tab; } src = {
+        h->plane[h->cur][0], h->plane[h->cur][1], reinterpret_cast<const double*>(h->tab)};
+    return capi_measure_byte(&src, n, norm, ones, cross, h->stream);
 }
 
 int svb_encode_values(sv_bhandle h, const double* vals, uint64_t n, uint8_t* mi, uint8_t* pi, int collect) {

@@ -433,13 +433,14 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
 
 int measure_impl(const void* psi, uint64_t n_elems, int mode, double* norm, double* ones,
                  double* cross, double* dev_partials, size_t partial_cap, cudaStream_t st) {
-    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "measurement needs FP64 or FP32 storage");
+    if (!valid_fp_mode(mode) && mode != SV_BYTE) return fail(SV_EVALUE, "unknown storage mode");
     if (!is_pow2(n_elems)) return fail(SV_EVALUE, "measurement needs a power-of-two buffer");
     const int n = log2u(n_elems);
     if (n > 52) return fail(SV_EVALUE, "buffer too large");
     int dev = 0;
     cudaGetDevice(&dev);
     const int k = n < 12 ? n : 12;
+    if (n == 0 && mode == SV_BYTE) return fail(SV_EVALUE, "BYTE measurement needs >= 2 amplitudes");
     if (n == 0) {  // a single amplitude: no qubits, just the norm
         double h[2];
         CUDA_TRY(cudaMemcpyAsync(h, psi, 16, cudaMemcpyDeviceToHost, st), "measure copy");
@@ -532,6 +533,10 @@ int capi_cuda_fail(cudaError_t e, const char* what) { return cuda_fail(e, what);
 int capi_measure(const void* psi, uint64_t n, int mode, double* norm, double* ones, double* cross,
                  cudaStream_t st) {
     return measure_impl(psi, n, mode, norm, ones, cross, nullptr, 0, st);
+}
+// psi = host pointer to {mi plane, pi plane, decode tables} (sv_measure.cu ByteSrc)
+int capi_measure_byte(const void* src, uint64_t n, double* norm, double* ones, double* cross, cudaStream_t st) {
+    return measure_impl(src, n, SV_BYTE, norm, ones, cross, nullptr, 0, st);
 }
 }  // namespace sv
 

@@ -22,10 +22,19 @@ int measure_slots(int k, int n) { return 1 + n + 2 * k; }
 
 constexpr int kMaxOut = 40;
 
-template <typename S, int K>
+// BYTE storage (two uint8 planes) is decoded on the fly: mags[mi] * (ux[pi], uy[pi])
+// with the same single rounding as codec.py:203-206, so a BYTE state is measured
+// without ever materialising it in FP64.
+struct ByteSrc {
+    const uint8_t* mi;
+    const uint8_t* pi;
+    const double* tab;      // dmag[256], dux[256], duy[256] (ByteTables prefix)
+};
+
+template <typename S, int K, bool BYTE>
 __global__ void __launch_bounds__(256) k_measure(const S* __restrict__ psi,
                                                  const __grid_constant__ MeasureParams p,
-                                                 double* __restrict__ partials) {
+                                                 double* __restrict__ partials, const ByteSrc bsrc) {
     constexpr int NT = 256;
     constexpr int TILE = 1 << K;
     constexpr int V = Store<S>::V;
@@ -35,8 +44,11 @@ __global__ void __launch_bounds__(256) k_measure(const S* __restrict__ psi,
     // per-warp one-weights of the out-of-tile qubits (constant bit per tile)
     double* ow = reinterpret_cast<double*>(smem_raw + sizeof(cplx) * TILE + sizeof(uint64_t) * TILE);
     double* red = ow + (NT / 32) * kMaxOut;             // block-reduction scratch
+    double* dtab = red + 8 * (1 + 64 + 2 * 12);         // BYTE decode tables (768 doubles)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < (NT / 32) * kMaxOut; i += NT) ow[i] = 0.0;
+    if constexpr (BYTE)
+        for (int i = threadIdx.x; i < 768; i += NT) dtab[i] = bsrc.tab[i];
 
     const int b = p.b;
     const int nhi = 1 << (K - b);
@@ -58,7 +70,14 @@ __global__ void __launch_bounds__(256) k_measure(const S* __restrict__ psi,
 
     for (uint64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
         const uint64_t base = insert_zeros(tile, p.tile_mask);
-        if constexpr (TILE >= NT * V) {
+        if constexpr (BYTE) {
+            for (int e = threadIdx.x; e < TILE; e += NT) {
+                const uint64_t i = base + off_hi[e >> b] + (e & lowmask);
+                const uint8_t mi = bsrc.mi[i], pi = bsrc.pi[i];
+                s[e] = mi == 0 ? cplx{0.0, 0.0}
+                               : cplx{__dmul_rn(dtab[mi], dtab[256 + pi]), __dmul_rn(dtab[mi], dtab[512 + pi])};
+            }
+        } else if constexpr (TILE >= NT * V) {
             constexpr int PER = TILE / (NT * V);
             Vec<S> buf[PER];
 #pragma unroll
@@ -145,53 +164,63 @@ __global__ void __launch_bounds__(256) k_measure(const S* __restrict__ psi,
 
 int measure_grid(int device) { return sm_count(device) * 2; }
 
-template <typename S, int K>
+template <typename S, int K, bool BYTE>
 static cudaError_t measure_k(const S* psi, const MeasureParams& p, double* partials, int grid,
-                             cudaStream_t st) {
-    const int nslots = measure_slots(K, p.n);
+                             cudaStream_t st, const ByteSrc& bsrc) {
     const size_t tile_bytes = sizeof(cplx) * (1u << K) + sizeof(uint64_t) * (1u << K) +
                               sizeof(double) * 8 * kMaxOut;
-    const size_t red_bytes = sizeof(double) * (size_t)nslots * 8;
-    const size_t smem = tile_bytes + red_bytes;
+    const size_t red_bytes = sizeof(double) * (size_t)(1 + 64 + 2 * 12) * 8;
+    const size_t smem = tile_bytes + red_bytes + (BYTE ? sizeof(double) * 768 : 0);
     static bool configured[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !configured[dev]) {
-        const size_t worst = tile_bytes + sizeof(double) * (size_t)measure_slots(K, 64) * 8;
-        cudaError_t e = cudaFuncSetAttribute(k_measure<S, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)worst);
+        cudaError_t e = cudaFuncSetAttribute(k_measure<S, K, BYTE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(tile_bytes + red_bytes + sizeof(double) * 768));
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
-    k_measure<S, K><<<grid, 256, smem, st>>>(psi, p, partials);
+    k_measure<S, K, BYTE><<<grid, 256, smem, st>>>(psi, p, partials, bsrc);
     count_launch();
     return cudaGetLastError();
 }
 
-template <typename S>
+template <typename S, bool BYTE>
 static cudaError_t measure_t(const S* psi, const MeasureParams& p, double* partials, int grid,
-                             cudaStream_t st) {
+                             cudaStream_t st, const ByteSrc& bsrc) {
     switch (p.k) {
-        case 1: return measure_k<S, 1>(psi, p, partials, grid, st);
-        case 2: return measure_k<S, 2>(psi, p, partials, grid, st);
-        case 3: return measure_k<S, 3>(psi, p, partials, grid, st);
-        case 4: return measure_k<S, 4>(psi, p, partials, grid, st);
-        case 5: return measure_k<S, 5>(psi, p, partials, grid, st);
-        case 6: return measure_k<S, 6>(psi, p, partials, grid, st);
-        case 7: return measure_k<S, 7>(psi, p, partials, grid, st);
-        case 8: return measure_k<S, 8>(psi, p, partials, grid, st);
-        case 9: return measure_k<S, 9>(psi, p, partials, grid, st);
-        case 10: return measure_k<S, 10>(psi, p, partials, grid, st);
-        case 11: return measure_k<S, 11>(psi, p, partials, grid, st);
-        case 12: return measure_k<S, 12>(psi, p, partials, grid, st);
+        case 1: return measure_k<S, 1, BYTE>(psi, p, partials, grid, st, bsrc);
+        case 2: return measure_k<S, 2, BYTE>(psi, p, partials, grid, st, bsrc);
+        case 3: return measure_k<S, 3, BYTE>(psi, p, partials, grid, st, bsrc);
+        case 4: return measure_k<S, 4, BYTE>(psi, p, partials, grid, st, bsrc);
+        case 5: return measure_k<S, 5, BYTE>(psi, p, partials, grid, st, bsrc);
+        case 6: return measure_k<S, 6, BYTE>(psi, p, partials, grid, st, bsrc);
+        case 7: return measure_k<S, 7, BYTE>(psi, p, partials, grid, st, bsrc);
+        case 8: return measure_k<S, 8, BYTE>(psi, p, partials, grid, st, bsrc);
+        case 9: return measure_k<S, 9, BYTE>(psi, p, partials, grid, st, bsrc);
+        case 10: return measure_k<S, 10, BYTE>(psi, p, partials, grid, st, bsrc);
+        case 11: return measure_k<S, 11, BYTE>(psi, p, partials, grid, st, bsrc);
+        case 12: return measure_k<S, 12, BYTE>(psi, p, partials, grid, st, bsrc);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t launch_measure(const void* psi, int mode, const MeasureParams& p, double* partials,
                            int grid, cudaStream_t st) {
-    return mode == SV_FP32 ? measure_t(static_cast<const c32s*>(psi), p, partials, grid, st)
-                           : measure_t(static_cast<const c64s*>(psi), p, partials, grid, st);
+    const ByteSrc none{nullptr, nullptr, nullptr};
+    if (mode == SV_BYTE) {
+        const ByteSrc* b = static_cast<const ByteSrc*>(psi);
+        return measure_t<c64s, true>(nullptr, p, partials, grid, st, *b);
+    }
+    return mode == SV_FP32 ? measure_t<c32s, false>(static_cast<const c32s*>(psi), p, partials, grid, st, none)
+                           : measure_t<c64s, false>(static_cast<const c64s*>(psi), p, partials, grid, st, none);
+}
+
+// BYTE measurement entry: planes + decode tables
+cudaError_t launch_measure_byte(const uint8_t* mi, const uint8_t* pi, const double* tab, const MeasureParams& p,
+                                double* partials, int grid, cudaStream_t st) {
+    const ByteSrc b{mi, pi, tab};
+    return measure_t<c64s, true>(nullptr, p, partials, grid, st, b);
 }
 
 }  // namespace sv
