@@ -121,6 +121,8 @@ typedef struct {
     int32_t collect;       /* collect codebook proposals (codec.py:137-152) */
     int32_t want_mag, want_ph;   /* which tables can still change */
     double mag_cut, ph_cut;      /* collect only values below the cut (overflow retry) */
+    int32_t scan_only;           /* 1: only collect candidates, write nothing */
+    int32_t reserved;
 } svb_gate_desc;
 
 int svb_create(int device, int n_qubits, sv_bhandle* out);

@@ -37,7 +37,8 @@ class SvbGateDesc(ctypes.Structure):
                 ("xmask_a", ctypes.c_uint64), ("xmask_b", ctypes.c_uint64),
                 ("producer", ctypes.c_int32), ("collect", ctypes.c_int32),
                 ("want_mag", ctypes.c_int32), ("want_ph", ctypes.c_int32),
-                ("mag_cut", ctypes.c_double), ("ph_cut", ctypes.c_double)]
+                ("mag_cut", ctypes.c_double), ("ph_cut", ctypes.c_double),
+                ("scan_only", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class ByteDeviceState:
@@ -238,6 +239,7 @@ class ByteEngineState(ByteDeviceState):
         self.passes = 0
         self.reencodes = 0
         self.host_fixes = 0
+        self.scan_first = False         # the previous gate grew a table: scan before encoding
 
     def _desc(self, gate, plan) -> SvbGateDesc:
         d = SvbGateDesc()
@@ -287,7 +289,22 @@ class ByteEngineState(ByteDeviceState):
             if len(um) <= k and len(ut) <= k:
                 raise RuntimeError("codebook candidate buffer overflow without a usable cut")
 
+    def _write_pass(self, d: SvbGateDesc):
+        d.producer = -1
+        d.collect = 0
+        d.scan_only = 0
+        self.reset()
+        self.gate_pass(d)
+        self.passes += 1
+        return self.read_unsure()
+
     def apply_gate(self, gate, layout=None) -> None:
+        """One gate with the reference's per-gate codebook barrier (engine.py:186-225).
+
+        Pass policy: tables that can no longer change -> one encode pass; after a
+        gate that grew a table -> candidate scan first (reads only), merge, then
+        one encode pass; otherwise encode speculatively while collecting and
+        re-encode only if the merge grew a table."""
         from .layout import plan_exchange
         from .state import PrecisionMode
         plan = plan_exchange(self.layout, gate, PrecisionMode.BYTE)
@@ -297,40 +314,32 @@ class ByteEngineState(ByteDeviceState):
         d = self._desc(gate, plan)
         d.want_mag = 0 if sat_mag else 1
         d.want_ph = 0 if sat_ph else 1
-        unsure_idx, unsure_val = [], []
         if sat_mag and sat_ph:
-            d.collect = 0
-            self.reset()
-            self.gate_pass(d)
-            self.passes += 1
-            ui, uv = self.read_unsure()
-            unsure_idx.append(ui)
-            unsure_val.append(uv)
+            ui, uv = self._write_pass(d)
         else:
-            proposals = []
+            scan = self.scan_first
+            proposals, unsure = [], []
             ranks = self.layout.rank_count
+            d.scan_only = 1 if scan else 0
             for r in range(ranks):
-                mags, ph, (ui, uv) = self._collect_rank(d, r if ranks > 1 else -1)
+                mags, ph, u = self._collect_rank(d, r if ranks > 1 else -1)
                 proposals.append(cb.finalize_proposal(mags, ph))
-                unsure_idx.append(ui)
-                unsure_val.append(uv)
+                unsure.append(u)
             version = cb.version
             cb.merge(proposals)
-            if cb.version != version:
+            grew = cb.version != version
+            self.scan_first = grew
+            if scan or grew:
                 self.sync_tables()
-                d.producer = -1
-                d.collect = 0
-                self.reset()
-                self.gate_pass(d)
-                self.passes += 1
-                self.reencodes += 1
-                ui, uv = self.read_unsure()
-                unsure_idx, unsure_val = [ui], [uv]
+                ui, uv = self._write_pass(d)
+                if grew and not scan:
+                    self.reencodes += 1
+            else:
+                ui = np.concatenate([u[0] for u in unsure])
+                uv = np.concatenate([u[1] for u in unsure])
         self.reset()
-        idx = np.concatenate(unsure_idx) if unsure_idx else np.zeros(0, dtype=np.uint64)
-        if len(idx):
-            vals = np.concatenate(unsure_val)
-            mi, pi = cb.host_encode(vals)
-            self.patch(idx, mi, pi)
-            self.host_fixes += len(idx)
+        if len(ui):
+            mi, pi = cb.host_encode(uv)
+            self.patch(ui, mi, pi)
+            self.host_fixes += len(ui)
         self.commit()

@@ -44,6 +44,8 @@ constexpr int NT = 256;
 struct STables {
     double dmag[256], dux[256], duy[256];
     double smag[256], sth[256];
+    double sqmid[256];      // squared midpoints of consecutive sorted magnitudes (+inf sentinel)
+    double sqmag[256];      // squared sorted magnitudes
     uint8_t smag_idx[256], sth_idx[256];
     int n_mag, n_ph;
 };
@@ -294,6 +296,40 @@ __device__ __forceinline__ int producer_of(const ByteGate& g, uint64_t i0) {
     }
 }
 
+// exact numpy complex abs (codec.py:41 via np.abs)
+__device__ __forceinline__ double exact_abs(cplx v) {
+    const double ax = fabs(v.re), ay = fabs(v.im);
+    const double L = fmax(ax, ay), S = fmin(ax, ay);
+    if (L == 0.0) return 0.0;
+    const double q = __ddiv_rn(S, L);
+    return __dmul_rn(L, __dsqrt_rn(__fma_rn(q, q, 1.0)));
+}
+
+// theta as canonicalize computes it; exact on the axes
+__device__ __forceinline__ double theta_of(cplx v, bool* exact, bool* wrap_unsure) {
+    double a;
+    *exact = true;
+    if (v.im == 0.0) {
+        a = v.re > 0.0 ? 0.0 : (signbit(v.im) ? -3.141592653589793 : 3.141592653589793);
+    } else if (v.re == 0.0) {
+        a = v.im > 0.0 ? 1.5707963267948966 : -1.5707963267948966;
+    } else {
+        a = atan2(v.im, v.re);
+        *exact = false;
+    }
+    double th = (a == 0.0) ? 0.0 : (a < 0.0 ? __dadd_rn(a, TWO_PI) : a);
+    const double gap = __dsub_rn(TWO_PI, th);
+    if (gap < PHASE_ATOL) th = 0.0;
+    *wrap_unsure = !*exact && fabs(gap - PHASE_ATOL) <= TH_MARGIN;
+    return th;
+}
+
+constexpr double SQ_EPS = 1e-13;      // relative margin on |v|^2 decisions (fast path)
+
+struct ThreadCache {                  // last candidate values seen by this thread
+    double mre, mim, pre, pim;
+};
+
 struct Emitter {
     const STables& t;
     const ByteGate& g;
@@ -302,33 +338,94 @@ struct Emitter {
     uint8_t* mo;
     uint8_t* po;
     bool collect;
+    bool write;
 
-    __device__ void emit(uint64_t idx, cplx v) const {
-        const Polar p = canon(v);
-        bool unsure = p.wrap_unsure;
-        const int mi = nearest(t.smag, t.smag_idx, t.n_mag, p.r, false, 0.0, &unsure);
-        int pi = nearest(t.sth, t.sth_idx, t.n_ph, p.th, true, p.th_exact ? 0.0 : TH_MARGIN, &unsure);
-        if (mi == 0) pi = 0;
-        mo[idx] = (uint8_t)mi;
-        po[idx] = (uint8_t)pi;
-        if (unsure && mi != 0) {
-            const unsigned long long slot = atomicAdd(&cand->n_unsure, 1ull);
-            if (slot < cand->cap_unsure) {
-                cand->unsure_idx[slot] = idx;
-                cand->unsure_val[2 * slot] = v.re;
-                cand->unsure_val[2 * slot + 1] = v.im;
-            } else {
-                cand->overflow = 1;
+    __device__ void unsure_push(uint64_t idx, cplx v) const {
+        const unsigned long long slot = atomicAdd(&cand->n_unsure, 1ull);
+        if (slot < cand->cap_unsure) {
+            cand->unsure_idx[slot] = idx;
+            cand->unsure_val[2 * slot] = v.re;
+            cand->unsure_val[2 * slot + 1] = v.im;
+        } else {
+            cand->overflow = 1;
+        }
+    }
+
+    __device__ void emit(uint64_t idx, cplx v, ThreadCache& tc) const {
+        if (v.re == 0.0 && v.im == 0.0) {          // r == 0: indices (0, 0), always representable
+            if (write) { mo[idx] = 0; po[idx] = 0; }
+            return;
+        }
+        const double x2 = __fma_rn(v.re, v.re, __dmul_rn(v.im, v.im));
+        // ---- magnitude: nearest sorted entry from squared midpoints; exact |v| only near a boundary
+        bool slow = !(x2 > 1e-280);
+        int lo = 0, hi = t.n_mag - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (t.sqmid[mid] < x2) lo = mid + 1; else hi = mid;
+        }
+        const int k = lo;
+        if (k > 0 && x2 - t.sqmid[k - 1] <= SQ_EPS * x2) slow = true;
+        if (k < t.n_mag - 1 && t.sqmid[k] - x2 <= SQ_EPS * x2) slow = true;
+        // representability by the nearest entry: |r - m| <= 1e-12 max(r, m)  <=>  |x2 - m^2| ~ 2e-12 m^2
+        const double m2 = t.sqmag[k];
+        const double dd = fabs(x2 - m2);
+        int mag_rep = (dd < 1.98e-12 * m2) ? 1 : ((dd > 2.02e-12 * m2) ? 0 : -1);
+        if (m2 == 0.0) mag_rep = 0;
+        double r = 0.0;
+        bool have_r = false;
+        int mi;
+        if (slow) {
+            r = exact_abs(v);
+            have_r = true;
+            bool dummy = false;
+            mi = nearest(t.smag, t.smag_idx, t.n_mag, r, false, 0.0, &dummy);
+            mag_rep = representable(t.smag, t.n_mag, r, true, 0.0);
+        } else {
+            mi = t.smag_idx[k];
+            if (mag_rep < 0) {
+                r = exact_abs(v);
+                have_r = true;
+                mag_rep = representable(t.smag, t.n_mag, r, true, 0.0);
             }
         }
-        if (!collect) return;
-        if (g.want_mag && p.r < g.mag_cut && representable(t.smag, t.n_mag, p.r, true, 0.0) == 0) {
-            cand->any_mag = 1;
-            insert_mag(sets, cand, p.r);
+        // ---- phase: a single-entry table needs no angle to encode
+        bool th_exact = true, wrap_unsure = false, have_th = false;
+        double th = 0.0;
+        int pi = 0;
+        bool unsure = false;
+        if (t.n_ph > 1 && mi != 0) {
+            th = theta_of(v, &th_exact, &wrap_unsure);
+            have_th = true;
+            unsure = wrap_unsure;
+            pi = nearest(t.sth, t.sth_idx, t.n_ph, th, true, th_exact ? 0.0 : TH_MARGIN, &unsure);
         }
-        if (g.want_ph && p.th < g.ph_cut &&
-            representable(t.sth, t.n_ph, p.th, false, p.th_exact ? 0.0 : TH_MARGIN) != 1) {
-            insert_phase(sets, cand, p, v);
+        if (mi == 0) pi = 0;
+        if (write) {
+            mo[idx] = (uint8_t)mi;
+            po[idx] = (uint8_t)pi;
+            if (unsure && mi != 0) unsure_push(idx, v);
+        }
+        if (!collect) return;
+        if (g.want_mag && mag_rep == 0 && !(v.re == tc.mre && v.im == tc.mim)) {
+            if (!have_r) r = exact_abs(v);
+            if (r < g.mag_cut) {
+                cand->any_mag = 1;
+                insert_mag(sets, cand, r);
+            }
+            tc.mre = v.re; tc.mim = v.im;
+        }
+        if (g.want_ph && !(v.re == tc.pre && v.im == tc.pim)) {
+            if (!have_th) th = theta_of(v, &th_exact, &wrap_unsure);
+            if (th < g.ph_cut && representable(t.sth, t.n_ph, th, false, th_exact ? 0.0 : TH_MARGIN) != 1) {
+                if (!have_r) { r = exact_abs(v); have_r = true; }
+                Polar p;
+                p.r = r; p.th = th; p.th_exact = th_exact; p.wrap_unsure = wrap_unsure;
+                p.ux = __dadd_rn(__ddiv_rn(v.re, r), 0.0);
+                p.uy = __dadd_rn(__ddiv_rn(v.im, r), 0.0);
+                insert_phase(sets, cand, p, v);
+            }
+            tc.pre = v.re; tc.pim = v.im;
         }
     }
 };
@@ -338,6 +435,7 @@ __device__ void load_tables(STables& t, const ByteTables* gt) {
         t.dmag[i] = gt->dmag[i]; t.dux[i] = gt->dux[i]; t.duy[i] = gt->duy[i];
         t.smag[i] = gt->smag[i]; t.sth[i] = gt->sth[i];
         t.smag_idx[i] = gt->smag_idx[i]; t.sth_idx[i] = gt->sth_idx[i];
+        t.sqmid[i] = gt->sqmid[i]; t.sqmag[i] = gt->sqmag[i];
     }
     if (threadIdx.x == 0) { t.n_mag = gt->n_mag; t.n_ph = gt->n_ph; }
 }
@@ -355,19 +453,29 @@ __global__ void __launch_bounds__(NT) k_byte_gate(const uint8_t* __restrict__ mi
     const bool collect = g.collect != 0;
     if (collect) sets_clear(sets);
     __syncthreads();
-    const Emitter em{t, g, sets, cand, mi_out, pi_out, collect};
+    const bool write = g.scan_only == 0;
+    const Emitter em{t, g, sets, cand, mi_out, pi_out, collect, write};
+    ThreadCache tc{NAN, NAN, NAN, NAN};
     const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g.kind == SV_OP_1Q) {
         const cplx m0 = {g.m[0], g.m[1]}, m1 = {g.m[2], g.m[3]}, m2 = {g.m[4], g.m[5]}, m3 = {g.m[6], g.m[7]};
+        const bool real = g.m[1] == 0.0 && g.m[3] == 0.0 && g.m[5] == 0.0 && g.m[7] == 0.0;
         const uint64_t n_items = g.n_elems >> 1;
         for (uint64_t w = first; w < n_items; w += step) {
             const uint64_t i0 = insert0(w, g.qa), i1 = i0 | (1ull << g.qa);
             if (g.producer >= 0 && producer_of(g, i0) != g.producer) continue;
             const cplx a0 = decode(t, mi_in[i0], pi_in[i0]);
             const cplx a1 = decode(t, mi_in[i1], pi_in[i1]);
-            em.emit(i0, row2(m0, m1, a0, a1));
-            em.emit(i1, row2(m2, m3, a0, a1));
+            if (real) {   // numpy's +-0 imaginary products dropped (exact up to the sign of zero)
+                em.emit(i0, {__dadd_rn(__dmul_rn(m0.re, a0.re), __dmul_rn(m1.re, a1.re)),
+                             __dadd_rn(__dmul_rn(m0.re, a0.im), __dmul_rn(m1.re, a1.im))}, tc);
+                em.emit(i1, {__dadd_rn(__dmul_rn(m2.re, a0.re), __dmul_rn(m3.re, a1.re)),
+                             __dadd_rn(__dmul_rn(m2.re, a0.im), __dmul_rn(m3.re, a1.im))}, tc);
+            } else {
+                em.emit(i0, row2(m0, m1, a0, a1), tc);
+                em.emit(i1, row2(m2, m3, a0, a1), tc);
+            }
         }
     } else if (g.kind == SV_OP_2Q) {
         cplx m[16];
@@ -382,15 +490,15 @@ __global__ void __launch_bounds__(NT) k_byte_gate(const uint8_t* __restrict__ mi
             for (int c = 0; c < 4; ++c) a[c] = decode(t, mi_in[idx[c]], pi_in[idx[c]]);
             cplx o[4];
             for (int r = 0; r < 4; ++r) o[r] = row4(&m[4 * r], a[0], a[1], a[2], a[3]);
-            for (int r = 0; r < 4; ++r) em.emit(idx[r], o[r]);
+            for (int r = 0; r < 4; ++r) em.emit(idx[r], o[r], tc);
         }
     } else {   // DIAG: masked amplitudes re-encoded, the rest copied
         const cplx f = {g.m[0], g.m[1]};
         for (uint64_t i = first; i < g.n_elems; i += step) {
             if ((i & g.mask) == g.mask) {
                 if (g.producer >= 0 && producer_of(g, i) != g.producer) continue;
-                em.emit(i, cmul(decode(t, mi_in[i], pi_in[i]), f));
-            } else if (g.producer < 0 || (int)(i >> g.n_local) == g.producer) {
+                em.emit(i, cmul(decode(t, mi_in[i], pi_in[i]), f), tc);
+            } else if (write && (g.producer < 0 || (int)(i >> g.n_local) == g.producer)) {
                 mi_out[i] = mi_in[i];
                 pi_out[i] = pi_in[i];
             }
@@ -426,9 +534,10 @@ __global__ void __launch_bounds__(NT) k_byte_encode(const double* __restrict__ v
     const bool collect = g.collect != 0;
     if (collect) sets_clear(sets);
     __syncthreads();
-    const Emitter em{t, g, sets, cand, mi, pi, collect};
+    const Emitter em{t, g, sets, cand, mi, pi, collect, true};
+    ThreadCache tc{NAN, NAN, NAN, NAN};
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        em.emit(i, {vals[2 * i], vals[2 * i + 1]});
+        em.emit(i, {vals[2 * i], vals[2 * i + 1]}, tc);
     if (collect) {
         __syncthreads();
         sets_flush(sets, cand);

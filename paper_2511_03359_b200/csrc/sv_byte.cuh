@@ -11,10 +11,12 @@ namespace sv {
 // (codec.py:203-206) and the ascending copies + original indices used by the
 // nearest-entry search (codec.py:110-120, 193-201).
 struct ByteTables {
-    double dmag[256], dux[256], duy[256];
+    double dmag[256], dux[256], duy[256];    // must stay first (decode-fused measurement reads them)
     double smag[256], sth[256];
     uint8_t smag_idx[256], sth_idx[256];
     int n_mag, n_ph;
+    double sqmid[256];                         // ((s[i] + s[i+1]) / 2)^2, +inf after the last
+    double sqmag[256];                         // s[i]^2
 };
 
 // One gate pass (fields mirror svb_gate_desc in include/svb200.h).
@@ -31,6 +33,7 @@ struct ByteGate {
     int collect, want_mag, want_ph;
     int mag_room, ph_room;      // free table entries (informational)
     double mag_cut, ph_cut;     // only values below the cut are collected (overflow retry)
+    int scan_only;              // 1: collect candidates, write nothing
 };
 
 // Candidate / uncertain-amplitude output of a pass (device memory).

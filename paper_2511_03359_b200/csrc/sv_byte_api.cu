@@ -55,6 +55,7 @@ ByteGate to_gate(const svb_gate_desc& d, uint64_t n_elems) {
     g.collect = d.collect;
     g.want_mag = d.want_mag; g.want_ph = d.want_ph;
     g.mag_cut = d.mag_cut; g.ph_cut = d.ph_cut;
+    g.scan_only = d.scan_only;
     return g;
 }
 }  // namespace
@@ -151,6 +152,15 @@ int svb_set_tables(sv_bhandle h, const double* mags, int n_mag, const double* th
     for (int i = 0; i < n_ph; ++i) { t.sth[i] = thetas[q[i]]; t.sth_idx[i] = (uint8_t)q[i]; }
     t.n_mag = n_mag;
     t.n_ph = n_ph;
+    for (int i = 0; i < 256; ++i) {
+        if (i + 1 < n_mag) {
+            const double mid = 0.5 * (t.smag[i] + t.smag[i + 1]);
+            t.sqmid[i] = mid * mid;
+        } else {
+            t.sqmid[i] = 1.0 / 0.0;
+        }
+        t.sqmag[i] = i < n_mag ? t.smag[i] * t.smag[i] : 0.0;
+    }
     BTRY(cudaMemcpyAsync(h->tab, &t, sizeof(t), cudaMemcpyHostToDevice, h->stream), "table upload");
     BTRY(cudaStreamSynchronize(h->stream), "table sync");
     return SV_OK;
