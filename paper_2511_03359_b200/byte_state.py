@@ -167,7 +167,14 @@ class ByteDeviceState:
         self.version += 1
 
     def gate_pass(self, desc: SvbGateDesc):
-        nat.check(nat.load().svb_gate(self.handle, ctypes.byref(desc)))
+        if getattr(self, "time_passes", False):
+            e0, e1 = nat.Event(), nat.Event()
+            e0.record(self.stream)
+            nat.check(nat.load().svb_gate(self.handle, ctypes.byref(desc)))
+            e1.record(self.stream)
+            self.pass_events.append((desc.scan_only, e0, e1))
+        else:
+            nat.check(nat.load().svb_gate(self.handle, ctypes.byref(desc)))
         self.launches += 1
 
     # -- array-level codec -----------------------------------------------------------

@@ -48,6 +48,7 @@ struct STables {
     double sqmag[256];      // squared sorted magnitudes
     uint8_t smag_idx[256], sth_idx[256];
     int n_mag, n_ph;
+    int search_top;         // largest power of two < n_mag (branch-free search)
 };
 
 __device__ __forceinline__ cplx decode(const STables& t, uint8_t mi, uint8_t pi) {
@@ -114,24 +115,27 @@ __device__ __forceinline__ int nearest(const double* s, const uint8_t* orig, int
                                        double margin, bool* unsure) {
     const int pos = lower_bound(s, n, x);
     const int last = n - 1;
-    int cand[4];
-    int nc = 2;
-    cand[0] = min(max(pos - 1, 0), last);
-    cand[1] = min(max(pos, 0), last);
-    if (circular && last > 0) { cand[2] = 0; cand[3] = last; nc = 4; }
+    // four candidates, always (duplicates of candidate 0 when the wrap entries do not apply):
+    // a fixed shape keeps everything in registers
+    const bool wrap = circular && last > 0;
+    const int c0 = min(max(pos - 1, 0), last), c1 = min(max(pos, 0), last);
+    const int cand[4] = {c0, c1, wrap ? 0 : c0, wrap ? last : c0};
     double d[4];
     double best = 1e300;
-    for (int c = 0; c < nc; ++c) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
         double dd = fabs(__dsub_rn(s[cand[c]], x));
         if (circular) dd = fmin(dd, __dsub_rn(TWO_PI, dd));
         d[c] = dd;
         best = fmin(best, dd);
     }
     int idx = 1 << 30;
-    for (int c = 0; c < nc; ++c)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
         if (d[c] == best) idx = min(idx, (int)orig[cand[c]]);
     if (margin > 0.0) {
-        for (int c = 0; c < nc; ++c)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
             if ((int)orig[cand[c]] != idx && d[c] - best <= 2.0 * margin) *unsure = true;
     }
     return idx;
@@ -326,8 +330,10 @@ __device__ __forceinline__ double theta_of(cplx v, bool* exact, bool* wrap_unsur
 
 constexpr double SQ_EPS = 1e-13;      // relative margin on |v|^2 decisions (fast path)
 
-struct ThreadCache {                  // last candidate values seen by this thread
-    double mre, mim, pre, pim;
+struct ThreadCache {                  // last values seen by this thread
+    double mre, mim, pre, pim;        // last magnitude / phase candidate
+    double cre, cim;                  // last encoded value ...
+    unsigned ccode;                   // ... and its (certain) code
 };
 
 struct Emitter {
@@ -351,20 +357,25 @@ struct Emitter {
         }
     }
 
-    __device__ void emit(uint64_t idx, cplx v, ThreadCache& tc) const {
-        if (v.re == 0.0 && v.im == 0.0) {          // r == 0: indices (0, 0), always representable
-            if (write) { mo[idx] = 0; po[idx] = 0; }
-            return;
-        }
+    __device__ __forceinline__ void emit(uint64_t idx, cplx v, ThreadCache& tc) const {
+        const unsigned c = code(idx, v, tc);
+        if (write) { mo[idx] = (uint8_t)(c & 255); po[idx] = (uint8_t)(c >> 8); }
+    }
+
+    // (magnitude index | phase index << 8) of a produced value; candidate and
+    // uncertain-phase bookkeeping as a side effect
+    __device__ __forceinline__ unsigned code(uint64_t idx, cplx v, ThreadCache& tc) const {
+        if (v.re == 0.0 && v.im == 0.0) return 0u;   // r == 0: indices (0, 0), always representable
+        // structured states repeat values: reuse the last certain code (candidates of an
+        // identical value were already recorded)
+        if (v.re == tc.cre && v.im == tc.cim) return tc.ccode;
         const double x2 = __fma_rn(v.re, v.re, __dmul_rn(v.im, v.im));
-        // ---- magnitude: nearest sorted entry from squared midpoints; exact |v| only near a boundary
+        // ---- magnitude: nearest sorted entry from squared midpoints (branch-free search over the
+        //      +inf-padded table); exact |v| only near a boundary
         bool slow = !(x2 > 1e-280);
-        int lo = 0, hi = t.n_mag - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (t.sqmid[mid] < x2) lo = mid + 1; else hi = mid;
-        }
-        const int k = lo;
+        int k = 0;
+        for (int step = t.search_top; step > 0; step >>= 1)
+            k += (t.sqmid[k + step - 1] < x2) ? step : 0;
         if (k > 0 && x2 - t.sqmid[k - 1] <= SQ_EPS * x2) slow = true;
         if (k < t.n_mag - 1 && t.sqmid[k] - x2 <= SQ_EPS * x2) slow = true;
         // representability by the nearest entry: |r - m| <= 1e-12 max(r, m)  <=>  |x2 - m^2| ~ 2e-12 m^2
@@ -401,12 +412,10 @@ struct Emitter {
             pi = nearest(t.sth, t.sth_idx, t.n_ph, th, true, th_exact ? 0.0 : TH_MARGIN, &unsure);
         }
         if (mi == 0) pi = 0;
-        if (write) {
-            mo[idx] = (uint8_t)mi;
-            po[idx] = (uint8_t)pi;
-            if (unsure && mi != 0) unsure_push(idx, v);
-        }
-        if (!collect) return;
+        if (write && unsure && mi != 0) unsure_push(idx, v);
+        const unsigned result = (unsigned)mi | ((unsigned)pi << 8);
+        if (!unsure) { tc.cre = v.re; tc.cim = v.im; tc.ccode = result; }
+        if (!collect) return result;
         if (g.want_mag && mag_rep == 0 && !(v.re == tc.mre && v.im == tc.mim)) {
             if (!have_r) r = exact_abs(v);
             if (r < g.mag_cut) {
@@ -427,8 +436,21 @@ struct Emitter {
             }
             tc.pre = v.re; tc.pim = v.im;
         }
+        return result;
     }
 };
+
+__device__ __forceinline__ void load8(const uint8_t* p, uint8_t (&b)[8]) {
+    const uint2 w = *reinterpret_cast<const uint2*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { b[i] = (w.x >> (8 * i)) & 255; b[4 + i] = (w.y >> (8 * i)) & 255; }
+}
+__device__ __forceinline__ void store8(uint8_t* p, const uint8_t (&b)[8]) {
+    uint2 w;
+    w.x = b[0] | (b[1] << 8) | (b[2] << 16) | ((unsigned)b[3] << 24);
+    w.y = b[4] | (b[5] << 8) | (b[6] << 16) | ((unsigned)b[7] << 24);
+    *reinterpret_cast<uint2*>(p) = w;
+}
 
 __device__ void load_tables(STables& t, const ByteTables* gt) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
@@ -437,13 +459,19 @@ __device__ void load_tables(STables& t, const ByteTables* gt) {
         t.smag_idx[i] = gt->smag_idx[i]; t.sth_idx[i] = gt->sth_idx[i];
         t.sqmid[i] = gt->sqmid[i]; t.sqmag[i] = gt->sqmag[i];
     }
-    if (threadIdx.x == 0) { t.n_mag = gt->n_mag; t.n_ph = gt->n_ph; }
+    if (threadIdx.x == 0) {
+        t.n_mag = gt->n_mag;
+        t.n_ph = gt->n_ph;
+        int top = 0;                       // smallest power of two with 2*top >= n_mag
+        while (2 * top < gt->n_mag) top = top ? 2 * top : 1;
+        t.search_top = top;
+    }
 }
 }  // namespace
 
 // One BYTE gate pass.  Work items: pairs (1Q), quadruples (2Q) or single
 // amplitudes (DIAG, and COPY for untouched amplitudes of a diagonal gate).
-__global__ void __launch_bounds__(NT) k_byte_gate(const uint8_t* __restrict__ mi_in, const uint8_t* __restrict__ pi_in,
+__global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__ mi_in, const uint8_t* __restrict__ pi_in,
                                                   uint8_t* __restrict__ mi_out, uint8_t* __restrict__ pi_out,
                                                   const ByteTables* __restrict__ gtab, const __grid_constant__ ByteGate g,
                                                   ByteCand* cand) {
@@ -455,13 +483,69 @@ __global__ void __launch_bounds__(NT) k_byte_gate(const uint8_t* __restrict__ mi
     __syncthreads();
     const bool write = g.scan_only == 0;
     const Emitter em{t, g, sets, cand, mi_out, pi_out, collect, write};
-    ThreadCache tc{NAN, NAN, NAN, NAN};
+    ThreadCache tc{NAN, NAN, NAN, NAN, NAN, NAN, 0u};
     const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g.kind == SV_OP_1Q) {
         const cplx m0 = {g.m[0], g.m[1]}, m1 = {g.m[2], g.m[3]}, m2 = {g.m[4], g.m[5]}, m3 = {g.m[6], g.m[7]};
         const bool real = g.m[1] == 0.0 && g.m[3] == 0.0 && g.m[5] == 0.0 && g.m[7] == 0.0;
         const uint64_t n_items = g.n_elems >> 1;
+        if (g.qa >= 4 && g.n_elems >= 32) {
+            // 16 consecutive pairs per work item (16-byte loads/stores of every plane); the next
+            // item's bytes are loaded before the current one is computed (latency hiding)
+            const uint64_t n_chunks = n_items >> 4;
+            const uint64_t off = 1ull << g.qa;
+            uint4 nxt[4];
+            auto fetch = [&](uint64_t w, uint4 (&b)[4]) {
+                const uint64_t i0 = insert0(w << 4, g.qa);
+                b[0] = *reinterpret_cast<const uint4*>(mi_in + i0);
+                b[1] = *reinterpret_cast<const uint4*>(pi_in + i0);
+                b[2] = *reinterpret_cast<const uint4*>(mi_in + i0 + off);
+                b[3] = *reinterpret_cast<const uint4*>(pi_in + i0 + off);
+            };
+            uint64_t w = first;
+            if (w < n_chunks) fetch(w, nxt);
+            for (; w < n_chunks; w += step) {
+                uint4 cur[4] = {nxt[0], nxt[1], nxt[2], nxt[3]};
+                if (w + step < n_chunks) fetch(w + step, nxt);
+                const uint64_t i0 = insert0(w << 4, g.qa), i1 = i0 + off;
+                if (g.producer >= 0 && producer_of(g, i0) != g.producer) continue;
+                uint4 out[4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
+                auto byte_of = [](const uint4& v, int j) -> unsigned {
+                    const unsigned w = j < 4 ? v.x : (j < 8 ? v.y : (j < 12 ? v.z : v.w));
+                    return (w >> (8 * (j & 3))) & 255u;
+                };
+                auto put_byte = [](uint4& v, int j, unsigned b) {
+                    const unsigned sh = 8 * (j & 3);
+                    if (j < 4) v.x |= b << sh; else if (j < 8) v.y |= b << sh;
+                    else if (j < 12) v.z |= b << sh; else v.w |= b << sh;
+                };
+#pragma unroll 4
+                for (int j = 0; j < 16; ++j) {
+                    const cplx a0 = decode(t, byte_of(cur[0], j), byte_of(cur[1], j));
+                    const cplx a1 = decode(t, byte_of(cur[2], j), byte_of(cur[3], j));
+                    cplx r0, r1;
+                    if (real) {
+                        r0 = {__dadd_rn(__dmul_rn(m0.re, a0.re), __dmul_rn(m1.re, a1.re)),
+                              __dadd_rn(__dmul_rn(m0.re, a0.im), __dmul_rn(m1.re, a1.im))};
+                        r1 = {__dadd_rn(__dmul_rn(m2.re, a0.re), __dmul_rn(m3.re, a1.re)),
+                              __dadd_rn(__dmul_rn(m2.re, a0.im), __dmul_rn(m3.re, a1.im))};
+                    } else {
+                        r0 = row2(m0, m1, a0, a1);
+                        r1 = row2(m2, m3, a0, a1);
+                    }
+                    const unsigned c0 = em.code(i0 + j, r0, tc), c1 = em.code(i1 + j, r1, tc);
+                    put_byte(out[0], j, c0 & 255u); put_byte(out[1], j, c0 >> 8);
+                    put_byte(out[2], j, c1 & 255u); put_byte(out[3], j, c1 >> 8);
+                }
+                if (write) {
+                    *reinterpret_cast<uint4*>(mi_out + i0) = out[0];
+                    *reinterpret_cast<uint4*>(pi_out + i0) = out[1];
+                    *reinterpret_cast<uint4*>(mi_out + i1) = out[2];
+                    *reinterpret_cast<uint4*>(pi_out + i1) = out[3];
+                }
+            }
+        } else
         for (uint64_t w = first; w < n_items; w += step) {
             const uint64_t i0 = insert0(w, g.qa), i1 = i0 | (1ull << g.qa);
             if (g.producer >= 0 && producer_of(g, i0) != g.producer) continue;
@@ -491,6 +575,35 @@ __global__ void __launch_bounds__(NT) k_byte_gate(const uint8_t* __restrict__ mi
             cplx o[4];
             for (int r = 0; r < 4; ++r) o[r] = row4(&m[4 * r], a[0], a[1], a[2], a[3]);
             for (int r = 0; r < 4; ++r) em.emit(idx[r], o[r], tc);
+        }
+    } else if (g.n_elems >= 16) {   // DIAG, 8 amplitudes per work item
+        const cplx f = {g.m[0], g.m[1]};
+        const uint64_t n_chunks = g.n_elems >> 3;
+        for (uint64_t w = first; w < n_chunks; w += step) {
+            const uint64_t i = w << 3;
+            const bool own = g.producer < 0 || (int)(i >> g.n_local) == g.producer;
+            if (!own) continue;
+            if (((i | 7ull) & g.mask) != g.mask) {           // no amplitude of the chunk is active
+                if (write) {
+                    *reinterpret_cast<uint2*>(mi_out + i) = *reinterpret_cast<const uint2*>(mi_in + i);
+                    *reinterpret_cast<uint2*>(pi_out + i) = *reinterpret_cast<const uint2*>(pi_in + i);
+                }
+                continue;
+            }
+            uint8_t bm[8], bp[8];
+            load8(mi_in + i, bm);
+            load8(pi_in + i, bp);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (((i + j) & g.mask) != g.mask) continue;
+                const unsigned c = em.code(i + j, cmul(decode(t, bm[j], bp[j]), f), tc);
+                bm[j] = c & 255;
+                bp[j] = c >> 8;
+            }
+            if (write) {
+                store8(mi_out + i, bm);
+                store8(pi_out + i, bp);
+            }
         }
     } else {   // DIAG: masked amplitudes re-encoded, the rest copied
         const cplx f = {g.m[0], g.m[1]};
@@ -535,7 +648,7 @@ __global__ void __launch_bounds__(NT) k_byte_encode(const double* __restrict__ v
     if (collect) sets_clear(sets);
     __syncthreads();
     const Emitter em{t, g, sets, cand, mi, pi, collect, true};
-    ThreadCache tc{NAN, NAN, NAN, NAN};
+    ThreadCache tc{NAN, NAN, NAN, NAN, NAN, NAN, 0u};
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         em.emit(i, {vals[2 * i], vals[2 * i + 1]}, tc);
     if (collect) {

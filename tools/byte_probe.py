@@ -20,6 +20,8 @@ else:
 layout = PartitionLayout(circ.n_qubits, circ.n_qubits)
 st = ByteEngineState(circ.n_qubits, layout)
 st.zero(0)
+st.time_passes = True
+st.pass_events = []
 times = []
 for gate in circ.gates:
     if gate.kind == "M":
@@ -33,6 +35,10 @@ for gate in circ.gates:
     times.append((gate.kind, time.perf_counter() - t0))
 byt = 4 * (1 << circ.n_qubits)
 ts = np.array([t for _, t in times])
+scan = [a.elapsed_ms(b) for sc, a, b in st.pass_events if sc]
+wr = [a.elapsed_ms(b) for sc, a, b in st.pass_events if not sc]
+print(f"  device: scan passes {len(scan)} median {np.median(scan) if scan else 0:.2f} ms; "
+      f"write passes {len(wr)} median {np.median(wr):.2f} ms -> {byt / (np.median(wr) / 1e3) / 1e9:.0f} GB/s")
 print(f"BYTE {which} N={circ.n_qubits}: {len(ts)} gates, median {np.median(ts)*1e3:.2f} ms/gate "
       f"({byt / np.median(ts) / 1e9:.0f} GB/s eff), mean {ts.mean()*1e3:.2f} ms, max {ts.max()*1e3:.1f} ms; "
       f"passes {st.passes} reencodes {st.reencodes} host fixes {st.host_fixes}; measure {tm*1e3:.1f} ms "
