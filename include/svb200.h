@@ -122,7 +122,10 @@ typedef struct {
     int32_t want_mag, want_ph;   /* which tables can still change */
     double mag_cut, ph_cut;      /* collect only values below the cut (overflow retry) */
     int32_t scan_only;           /* 1: only collect candidates, write nothing */
-    int32_t reserved;
+    int32_t rank_bits;           /* log2(reference rank count) */
+    uint64_t phys_base;          /* physical global index of this buffer's element 0 */
+    int8_t lbit[16];             /* physical bit of logical bit n_local - 2 + j (j = 0, 1: offset
+                                  * top bits; j >= 2: rank bits); identity when not remapped */
 } svb_gate_desc;
 
 int svb_create(int device, int n_qubits, sv_bhandle* out);
@@ -174,6 +177,16 @@ int svk_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l
 /* sum conj(a0[i]) * a1[i] over count elements (a1 may be a peer pointer):
  * measure.py:83-101 cross term of a global qubit; out2 = (re, im) */
 int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, double* out2, void* stream);
+
+/* BYTE multi-GPU: IPC handles of the 4 planes ([buffer][magnitude, phase]),
+ * mapped peer planes, byte-plane swap and decoded cross term */
+int svb_ipc_handles(sv_bhandle h, void* out256);
+int svb_cur(sv_bhandle h);
+int svb_swap_peer(sv_bhandle h, void* peer_mi, void* peer_pi, int l, int side);
+int svb_pair_dot(sv_bhandle h, const void* a_mi, const void* a_pi, const void* b_mi, const void* b_pi,
+                 uint64_t count, double* out2);
+/* device pointers of the current planes (for offsets into own / peer planes) */
+int svb_planes(sv_bhandle h, void** cur_mi, void** cur_pi);
 
 /* ---- raw device buffers (for the array-level operator API) --------- */
 int sv_buffer_alloc(int device, uint64_t bytes, void** ptr);

@@ -38,7 +38,8 @@ class SvbGateDesc(ctypes.Structure):
                 ("producer", ctypes.c_int32), ("collect", ctypes.c_int32),
                 ("want_mag", ctypes.c_int32), ("want_ph", ctypes.c_int32),
                 ("mag_cut", ctypes.c_double), ("ph_cut", ctypes.c_double),
-                ("scan_only", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("scan_only", ctypes.c_int32), ("rank_bits", ctypes.c_int32),
+                ("phys_base", ctypes.c_uint64), ("lbit", ctypes.c_int8 * 16)]
 
 
 class ByteDeviceState:
@@ -222,6 +223,18 @@ class ByteDeviceState:
             pass
 
 
+def set_logical_bits(d: SvbGateDesc, layout, pos, phys_base: int) -> None:
+    """Where the logical bits the producer rule reads live physically (pos: logical ->
+    physical qubit, None for the identity)."""
+    loc = layout.local_qubits
+    rank_bits = layout.total_qubits - loc
+    d.rank_bits = rank_bits
+    d.phys_base = phys_base
+    for j in range(2 + rank_bits):
+        lq = loc - 2 + j
+        d.lbit[j] = 0 if lq < 0 else (lq if pos is None else pos[lq])
+
+
 def _exchange_fields(desc: SvbGateDesc, gate, layout, plan) -> None:
     loc = layout.local_qubits
     desc.n_local = loc
@@ -266,6 +279,7 @@ class ByteEngineState(ByteDeviceState):
             d.qa = gate.qubits[0]
             d.qb = gate.qubits[1] if len(gate.qubits) == 2 else 0
         _exchange_fields(d, gate, self.layout, plan)
+        set_logical_bits(d, self.layout, None, 0)
         d.producer = -1
         d.mag_cut = d.ph_cut = _BIG
         return d

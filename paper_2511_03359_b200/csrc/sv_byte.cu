@@ -278,25 +278,30 @@ __device__ void sets_flush(CtaSets& s, ByteCand* out) {
 }
 
 // producer rank of a work item in the reference's exchange choreography
+// producer rank of a work item in the reference's exchange choreography, from the
+// item's LOGICAL index (the remap planner may have permuted physical qubits):
+// logical bit (n_local - 2 + j) lives at physical bit lbit[j] of phys_base | i0
 __device__ __forceinline__ int producer_of(const ByteGate& g, uint64_t i0) {
-    const int nl = g.n_local;
-    const uint64_t rank = i0 >> nl;
-    const uint64_t off = i0 & ((1ull << nl) - 1ull);
+    const uint64_t full = g.phys_base | i0;
+    auto lb = [&](int j) -> int { return (int)((full >> g.lbit[j]) & 1ull); };
+    int rank = 0;
+    for (int j = 0; j < g.rank_bits; ++j) rank |= lb(2 + j) << j;
+    const int top1 = g.n_local >= 1 ? lb(1) : 0;    // logical bit n_local - 1
+    const int top2 = g.n_local >= 2 ? lb(0) : 0;    // logical bit n_local - 2
     switch (g.xkind) {
-        case 1: {   // pairwise, single-qubit gate on global qubit
-            return (int)((off >> (nl - 1)) & 1 ? (rank | g.xmask_a) : (rank & ~g.xmask_a));
+        case 1:     // pairwise, single-qubit gate on a global qubit: low side computes offsets [0, L/2)
+            return top1 ? (rank | (int)g.xmask_a) : (rank & ~(int)g.xmask_a);
+        case 2: {   // pairwise, two-qubit gate with one global qubit (engine.py:278-323)
+            const int side = g.qlow_top ? top2 : top1;
+            return side ? (rank | (int)g.xmask_a) : (rank & ~(int)g.xmask_a);
         }
-        case 2: {   // pairwise, two-qubit gate with one global qubit
-            const int side = g.qlow_top ? (int)((off >> (nl - 2)) & 1) : (int)((off >> (nl - 1)) & 1);
-            return (int)(side ? (rank | g.xmask_a) : (rank & ~g.xmask_a));
-        }
-        case 3: {   // quad: rank at position p computes quarter p
-            const int pos = (int)(off >> (nl - 2));
-            const uint64_t base = rank & ~(g.xmask_a | g.xmask_b);
-            return (int)(base | ((pos & 1) ? g.xmask_a : 0) | ((pos & 2) ? g.xmask_b : 0));
+        case 3: {   // quad: the rank at position p computes quarter p
+            const int pos = (top1 << 1) | top2;
+            const int base = rank & ~(int)(g.xmask_a | g.xmask_b);
+            return base | ((pos & 1) ? (int)g.xmask_a : 0) | ((pos & 2) ? (int)g.xmask_b : 0);
         }
         default:
-            return (int)rank;
+            return rank;
     }
 }
 
@@ -665,6 +670,67 @@ __global__ void k_byte_patch(uint8_t* mi, uint8_t* pi, const uint64_t* idx, cons
     }
 }
 
+// global<->local qubit swap of BYTE planes with the partner rank (see sv_dist.cu)
+__global__ void k_byte_swap_peer(uint8_t* omi, uint8_t* opi, uint8_t* pmi, uint8_t* ppi, uint64_t t0, uint64_t n,
+                                 int l, int c) {
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n; w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = t0 + w;
+        const uint64_t low = t & ((1ull << l) - 1ull);
+        const uint64_t x = ((t >> l) << (l + 1)) | ((uint64_t)(1 - c) << l) | low;
+        const uint64_t y = ((t >> l) << (l + 1)) | ((uint64_t)c << l) | low;
+        const uint8_t a = omi[x], b = opi[x];
+        omi[x] = pmi[y];
+        opi[x] = ppi[y];
+        pmi[y] = a;
+        ppi[y] = b;
+    }
+}
+
+// vectorised: 16 consecutive rest indices per item (l >= 4)
+__global__ void k_byte_swap_peer16(uint8_t* omi, uint8_t* opi, uint8_t* pmi, uint8_t* ppi, uint64_t t0, uint64_t n16,
+                                   int l, int c) {
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n16;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = t0 + (w << 4);
+        const uint64_t low = t & ((1ull << l) - 1ull);
+        const uint64_t x = ((t >> l) << (l + 1)) | ((uint64_t)(1 - c) << l) | low;
+        const uint64_t y = ((t >> l) << (l + 1)) | ((uint64_t)c << l) | low;
+        const uint4 a = *reinterpret_cast<const uint4*>(omi + x), b = *reinterpret_cast<const uint4*>(opi + x);
+        const uint4 pa = *reinterpret_cast<const uint4*>(pmi + y), pb = *reinterpret_cast<const uint4*>(ppi + y);
+        *reinterpret_cast<uint4*>(omi + x) = pa;
+        *reinterpret_cast<uint4*>(opi + x) = pb;
+        *reinterpret_cast<uint4*>(pmi + y) = a;
+        *reinterpret_cast<uint4*>(ppi + y) = b;
+    }
+}
+
+// sum conj(decode(a)) * decode(b) over count elements (a / b may be peer planes)
+__global__ void k_byte_pair_dot(const uint8_t* ami, const uint8_t* api, const uint8_t* bmi, const uint8_t* bpi,
+                                const ByteTables* gtab, uint64_t n, double* partials) {
+    __shared__ STables t;
+    load_tables(t, gtab);
+    __syncthreads();
+    double re = 0.0, im = 0.0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const cplx x = decode(t, ami[i], api[i]), y = decode(t, bmi[i], bpi[i]);
+        re += x.re * y.re + x.im * y.im;
+        im += x.re * y.im - x.im * y.re;
+    }
+    __shared__ double sr[8], si[8];
+    for (int o = 16; o > 0; o >>= 1) {
+        re += __shfl_down_sync(0xffffffffu, re, o);
+        im += __shfl_down_sync(0xffffffffu, im, o);
+    }
+    if ((threadIdx.x & 31) == 0) { sr[threadIdx.x >> 5] = re; si[threadIdx.x >> 5] = im; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += sr[w]; b += si[w]; }
+        partials[2 * blockIdx.x] = a;
+        partials[2 * blockIdx.x + 1] = b;
+    }
+}
+
 static unsigned byte_grid(uint64_t items) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -691,6 +757,26 @@ cudaError_t launch_byte_decode(const uint8_t* mi, const uint8_t* pi, const ByteT
 cudaError_t launch_byte_encode(const double* vals, uint64_t n, const ByteTables* tab, uint8_t* mi, uint8_t* pi,
                                const ByteGate& g, ByteCand* cand, cudaStream_t st) {
     k_byte_encode<<<byte_grid(n), NT, 0, st>>>(vals, n, tab, mi, pi, g, cand);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_byte_swap_peer(uint8_t* omi, uint8_t* opi, uint8_t* pmi, uint8_t* ppi, uint64_t n_local_elems,
+                                  int l, int c, cudaStream_t st) {
+    const uint64_t quarter = n_local_elems / 4;
+    const uint64_t t0 = (uint64_t)c * quarter;
+    if (l >= 4 && quarter % 16 == 0) {
+        k_byte_swap_peer16<<<byte_grid(quarter / 16), NT, 0, st>>>(omi, opi, pmi, ppi, t0, quarter / 16, l, c);
+    } else {
+        k_byte_swap_peer<<<byte_grid(quarter), NT, 0, st>>>(omi, opi, pmi, ppi, t0, quarter, l, c);
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_byte_pair_dot(const uint8_t* ami, const uint8_t* api, const uint8_t* bmi, const uint8_t* bpi,
+                                 const ByteTables* tab, uint64_t n, double* partials, int grid, cudaStream_t st) {
+    k_byte_pair_dot<<<grid, NT, 0, st>>>(ami, api, bmi, bpi, tab, n, partials);
     count_launch();
     return cudaGetLastError();
 }

@@ -30,6 +30,9 @@ struct ByteGate {
     uint64_t xmask_a, xmask_b;  // partner rank masks
     int qlow_top;               // pairwise-2q: the local qubit is the top local bit
     int producer;               // -1: every work item; r: only items the reference's rank r computes
+    uint64_t phys_base;         // this buffer's first physical global index
+    int rank_bits;              // log2 of the reference rank count
+    int8_t lbit[12];            // physical bit of logical bit (n_local - 2 + j)
     int collect, want_mag, want_ph;
     int mag_room, ph_room;      // free table entries (informational)
     double mag_cut, ph_cut;     // only values below the cut are collected (overflow retry)
@@ -53,6 +56,10 @@ cudaError_t launch_byte_decode(const uint8_t* mi, const uint8_t* pi, const ByteT
                                cudaStream_t st);
 cudaError_t launch_byte_encode(const double* vals, uint64_t n, const ByteTables* tab, uint8_t* mi, uint8_t* pi,
                                const ByteGate& g, ByteCand* cand, cudaStream_t st);
+cudaError_t launch_byte_swap_peer(uint8_t* omi, uint8_t* opi, uint8_t* pmi, uint8_t* ppi, uint64_t n_local_elems,
+                                  int l, int c, cudaStream_t st);
+cudaError_t launch_byte_pair_dot(const uint8_t* ami, const uint8_t* api, const uint8_t* bmi, const uint8_t* bpi,
+                                 const ByteTables* tab, uint64_t n, double* partials, int grid, cudaStream_t st);
 cudaError_t launch_byte_patch(uint8_t* mi, uint8_t* pi, const uint64_t* idx, const uint8_t* nm, const uint8_t* np_,
                               uint64_t n, cudaStream_t st);
 

@@ -56,6 +56,9 @@ ByteGate to_gate(const svb_gate_desc& d, uint64_t n_elems) {
     g.want_mag = d.want_mag; g.want_ph = d.want_ph;
     g.mag_cut = d.mag_cut; g.ph_cut = d.ph_cut;
     g.scan_only = d.scan_only;
+    g.phys_base = d.phys_base;
+    g.rank_bits = d.rank_bits;
+    for (int j = 0; j < 12; ++j) g.lbit[j] = d.lbit[j];
     return g;
 }
 }  // namespace
@@ -300,6 +303,7 @@ int svb_encode_values(sv_bhandle h, const double* vals, uint64_t n, uint8_t* mi,
     std::memset(&desc, 0, sizeof(desc));
     desc.producer = -1;
     desc.collect = collect;
+    for (int j = 0; j < 16; ++j) desc.lbit[j] = 0;
     desc.want_mag = 1;
     desc.want_ph = 1;
     desc.mag_cut = 1e308;
@@ -312,6 +316,54 @@ int svb_encode_values(sv_bhandle h, const double* vals, uint64_t n, uint8_t* mi,
     cudaFreeAsync(b, h->stream);
     if (e != cudaSuccess) return capi_cuda_fail(e, "encode");
     BTRY(cudaStreamSynchronize(h->stream), "encode sync");
+    return SV_OK;
+}
+
+int svb_ipc_handles(sv_bhandle h, void* out256) {
+    Guard gd(h->device);
+    for (int b = 0; b < 2; ++b)
+        for (int p = 0; p < 2; ++p) {
+            cudaIpcMemHandle_t ih;
+            BTRY(cudaIpcGetMemHandle(&ih, h->plane[b][p]), "cudaIpcGetMemHandle");
+            std::memcpy(static_cast<char*>(out256) + 64 * (2 * b + p), &ih, 64);
+        }
+    return SV_OK;
+}
+
+int svb_cur(sv_bhandle h) { return h->cur; }
+
+int svb_planes(sv_bhandle h, void** cur_mi, void** cur_pi) {
+    *cur_mi = h->plane[h->cur][0];
+    *cur_pi = h->plane[h->cur][1];
+    return SV_OK;
+}
+
+int svb_swap_peer(sv_bhandle h, void* peer_mi, void* peer_pi, int l, int side) {
+    Guard gd(h->device);
+    const uint64_t n = 1ull << h->n;
+    if (l < 0 || l >= h->n || h->n < 2) return capi_fail(SV_EINDEX, "swap qubit outside the slice");
+    cudaError_t e = launch_byte_swap_peer(h->plane[h->cur][0], h->plane[h->cur][1], static_cast<uint8_t*>(peer_mi),
+                                          static_cast<uint8_t*>(peer_pi), n, l, side, h->stream);
+    return e == cudaSuccess ? SV_OK : capi_cuda_fail(e, "byte swap launch");
+}
+
+int svb_pair_dot(sv_bhandle h, const void* a_mi, const void* a_pi, const void* b_mi, const void* b_pi,
+                 uint64_t count, double* out2) {
+    Guard gd(h->device);
+    out2[0] = out2[1] = 0.0;
+    if (count == 0) return SV_OK;
+    const int grid = (int)std::min<uint64_t>((count + 255) / 256, (uint64_t)sm_count(h->device) * 4);
+    double* part = nullptr;
+    BTRY(cudaMallocAsync(reinterpret_cast<void**>(&part), 16 * grid, h->stream), "pair dot scratch");
+    cudaError_t e = launch_byte_pair_dot(static_cast<const uint8_t*>(a_mi), static_cast<const uint8_t*>(a_pi),
+                                         static_cast<const uint8_t*>(b_mi), static_cast<const uint8_t*>(b_pi), h->tab,
+                                         count, part, grid, h->stream);
+    std::vector<double> hp(2 * grid);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hp.data(), part, 16 * grid, cudaMemcpyDeviceToHost, h->stream);
+    cudaFreeAsync(part, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return capi_cuda_fail(e, "byte pair dot");
+    for (int b = 0; b < grid; ++b) { out2[0] += hp[2 * b]; out2[1] += hp[2 * b + 1]; }
     return SV_OK;
 }
 

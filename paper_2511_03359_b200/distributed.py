@@ -148,6 +148,186 @@ class CudaBackend:
         self.peers = {}
 
 
+class CudaByteBackend:
+    """BYTE slice (two uint8 planes, double-buffered) + IPC-mapped peer planes.
+
+    Every gate runs the reference's per-gate codebook barrier across ranks: each rank
+    encodes its work items speculatively (or scans first after a table grew), tags every
+    produced value with its REFERENCE producer rank (computed from the logical index,
+    so remapping does not change who proposes what), the raw candidates of all ranks
+    are all-gathered, and every rank merges the same proposals in rank order
+    (codec.py:154-191) -> identical tables everywhere."""
+
+    def __init__(self, dist, n_local: int, layout, device: int):
+        from .byte_state import ByteDeviceState
+        from .codec import Codebook
+        nat.check(nat.load().sv_set_device(device))
+        self.dist = dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.n_local = n_local
+        self.layout = layout
+        self.mode = PrecisionMode.BYTE
+        self.st = ByteDeviceState(n_local, Codebook(), device)
+        self.st.zero(0 if self.rank == 0 else None)
+        self.dev = self.st
+        handles = (ctypes.c_char * 256)()
+        nat.check(nat.load().svb_ipc_handles(self.st.handle, handles))
+        every = [None] * self.world
+        dist.all_gather_object(every, bytes(handles))
+        self.peers = {}
+        for r, hb in enumerate(every):
+            if r == self.rank:
+                continue
+            planes = [[None, None], [None, None]]
+            for b in range(2):
+                for pl in range(2):
+                    ptr = ctypes.c_void_p()
+                    buf = (ctypes.c_char * 64).from_buffer_copy(hb[64 * (2 * b + pl):64 * (2 * b + pl + 1)])
+                    nat.check(nat.load().sv_ipc_open(device, buf, ctypes.byref(ptr)))
+                    planes[b][pl] = ptr
+            self.peers[r] = planes
+        self.link_bytes = 0
+        self.passes = 0
+        self.scan_first = False
+        self.host_fixes = 0
+        dist.barrier()
+
+    def _sync_all(self):
+        self.st.synchronize()
+        self.dist.barrier()
+
+    def _peer_cur(self, r):
+        c = nat.load().svb_cur(self.st.handle)
+        return self.peers[r][c]
+
+    def swap(self, global_pos: int, local_pos: int):
+        bit = global_pos - self.n_local
+        partner = self.rank ^ (1 << bit)
+        side = (self.rank >> bit) & 1
+        pm, pp = self._peer_cur(partner)
+        self._sync_all()
+        nat.check(nat.load().svb_swap_peer(self.st.handle, pm, pp, local_pos, side))
+        self._sync_all()
+        self.st.version += 1
+        self.link_bytes += 2 * (self.st.size // 4) * 2
+
+    def _desc(self, gate, phys, pos):
+        from .byte_state import SvbGateDesc, _exchange_fields, set_logical_bits
+        d = SvbGateDesc()
+        n_local = self.n_local
+        if g.is_diagonal(gate):
+            d.kind = nat.SV_OP_DIAG
+            mask = 0
+            active = True
+            for p in phys:
+                if p >= n_local:
+                    active = active and bool((self.rank >> (p - n_local)) & 1)
+                else:
+                    mask |= 1 << p
+            d.diag_mask = mask if active else (1 << n_local)     # inactive rank: copy everything
+            f = g.diagonal_factor(gate)
+            d.m[0], d.m[1] = f.real, f.imag
+        else:
+            m = nat.mat_buffer(g.unitary_matrix(gate))
+            for i, v in enumerate(m):
+                d.m[i] = v
+            d.kind = nat.SV_OP_1Q if len(phys) == 1 else nat.SV_OP_2Q
+            d.qa = phys[0]
+            d.qb = phys[1] if len(phys) == 2 else 0
+        plan = plan_exchange(self.layout, gate, PrecisionMode.BYTE)
+        _exchange_fields(d, gate, self.layout, plan)
+        set_logical_bits(d, self.layout, pos, self.rank << n_local)
+        d.mag_cut = d.ph_cut = 1e308
+        return d
+
+    def _pass(self, d, producer, collect, scan):
+        d.producer = producer
+        d.collect = 1 if collect else 0
+        d.scan_only = 1 if scan else 0
+        self.st.reset()
+        self.st.gate_pass(d)
+        self.passes += 1
+        mags, ph, flags = self.st.read_candidates() if collect else (None, None, 0)
+        if flags & 1:
+            raise RuntimeError("codebook candidate buffer overflow (multi-GPU BYTE)")
+        unsure = self.st.read_unsure()
+        return mags, ph, unsure
+
+    def apply_gate(self, gate, phys, pos):
+        cb = self.st.codebook
+        self.st.sync_tables()
+        sat_mag, sat_ph = cb.tables_saturated
+        d = self._desc(gate, phys, pos)
+        d.want_mag = 0 if sat_mag else 1
+        d.want_ph = 0 if sat_ph else 1
+        if sat_mag and sat_ph:
+            _, _, (ui, uv) = self._pass(d, -1, False, False)
+        else:
+            scan = self.scan_first
+            mine = []
+            unsure = []
+            for r in range(self.layout.rank_count):
+                mags, ph, u = self._pass(d, r, True, scan)
+                mine.append((mags, ph))
+                unsure.append(u)
+            every = [None] * self.world
+            self.dist.all_gather_object(every, mine)
+            proposals = []
+            for r in range(self.layout.rank_count):
+                mags = np.concatenate([every[k][r][0] for k in range(self.world)])
+                ph = np.concatenate([every[k][r][1] for k in range(self.world)])
+                proposals.append(cb.finalize_proposal(mags, ph))
+            version = cb.version
+            cb.merge(proposals)
+            grew = cb.version != version
+            self.scan_first = grew
+            if scan or grew:
+                self.st.sync_tables()
+                _, _, (ui, uv) = self._pass(d, -1, False, False)
+            else:
+                ui = np.concatenate([u[0] for u in unsure])
+                uv = np.concatenate([u[1] for u in unsure])
+        self.st.reset()
+        if len(ui):
+            mi, pi = cb.host_encode(uv)
+            self.st.patch(ui, mi, pi)
+            self.host_fixes += len(ui)
+        self.st.commit()
+
+    def measure_local(self):
+        return self.st.measure_sums()
+
+    def pair_dot(self, global_pos: int) -> complex:
+        bit = global_pos - self.n_local
+        partner = self.rank ^ (1 << bit)
+        low = ((self.rank >> bit) & 1) == 0
+        half = self.st.size // 2
+        om, op = ctypes.c_void_p(), ctypes.c_void_p()
+        nat.check(nat.load().svb_planes(self.st.handle, ctypes.byref(om), ctypes.byref(op)))
+        pm, pp = self._peer_cur(partner)
+        self._sync_all()
+        off = 0 if low else half
+        sh = lambda p: ctypes.c_void_p(p.value + off)  # noqa: E731
+        a, b = ((om, op), (pm, pp)) if low else ((pm, pp), (om, op))
+        out = np.zeros(2)
+        nat.check(nat.load().svb_pair_dot(self.st.handle, sh(a[0]), sh(a[1]), sh(b[0]), sh(b[1]), half,
+                                          nat.dptr(out)))
+        self.link_bytes += half * 2
+        return complex(out[0], out[1])
+
+    def export(self) -> np.ndarray:
+        return self.st.decode()
+
+    def close(self):
+        self.st.synchronize()
+        self.dist.barrier()
+        for planes in self.peers.values():
+            for b in range(2):
+                for pl in range(2):
+                    nat.load().sv_ipc_close(self.st.device, planes[b][pl])
+        self.peers = {}
+
+
 @dataclass
 class DistRunResult:
     circuit: Circuit
@@ -164,6 +344,26 @@ class DistRunResult:
     def local_slice(self) -> np.ndarray:
         """This rank's slice in PHYSICAL order (after remapping)."""
         return self.backend.export()
+
+    def gathered_bytes(self, dist):
+        """BYTE mode: logical-order (mag_idx, phase_idx) planes on rank 0 (collective)."""
+        st = self.backend.st
+        mine = st.export_storage(0, st.size)
+        parts = [None] * dist.get_world_size()
+        dist.all_gather_object(parts, mine)
+        if self.rank != 0:
+            return None
+        src = self._logical_source(sum(p[0].size for p in parts))
+        mi = np.concatenate([p[0] for p in parts])[src]
+        pi = np.concatenate([p[1] for p in parts])[src]
+        return mi, pi
+
+    def _logical_source(self, size):
+        idx = np.arange(size)
+        src = np.zeros_like(idx)
+        for q, p in enumerate(self.perm):
+            src |= ((idx >> q) & 1) << p
+        return src
 
     def gathered_state(self, dist) -> np.ndarray | None:
         """Logical-order global state on rank 0 (collective; small N only)."""
@@ -205,8 +405,6 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
                             tile_bits: int = 12, fuse_limit: int = 1024) -> DistRunResult:
     """Run `circuit` with one rank per process of the torch.distributed group `dist`."""
     validate_circuit(circuit)
-    if mode is PrecisionMode.BYTE:
-        raise NotImplementedError("BYTE mode across GPUs is not wired yet: use run_circuit (one GPU)")
     P = dist.get_world_size()
     rank = dist.get_rank()
     if P & (P - 1):
@@ -217,10 +415,14 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
     if not remap:
         raise NotImplementedError("reference-choreography exchanges: use remap=True")
     start = time.perf_counter()
-    if backend_factory is None:
-        be = CudaBackend(dist, n_local, mode, rank if device is None else device, tile_bits)
-    else:
+    dev_id = rank if device is None else device
+    if backend_factory is not None:
         be = backend_factory(dist, n_local, mode)
+    elif mode is PrecisionMode.BYTE:
+        be = CudaByteBackend(dist, n_local, layout, dev_id)
+    else:
+        be = CudaBackend(dist, n_local, mode, dev_id, tile_bits)
+    byte = mode is PrecisionMode.BYTE and backend_factory is None
     ledgers = [TrafficLedger() for _ in range(P)]
     planner = RemapPlanner(n, n_local, remap=remap)
     steps = planner.plan(circuit.gates)
@@ -241,11 +443,14 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
             swaps += 1
         elif isinstance(step, PhysGate):
             _charge_reference(layout, ledgers, step.gate, mode)
-            op = phys_op(step.gate, step.qubits, n_local, rank)
-            if op is not None:
-                pending.append(op)
-                if len(pending) >= fuse_limit:
-                    flush()
+            if byte:
+                be.apply_gate(step.gate, step.qubits, tuple(planner_pos_at(steps, step)))
+            else:
+                op = phys_op(step.gate, step.qubits, n_local, rank)
+                if op is not None:
+                    pending.append(op)
+                    if len(pending) >= fuse_limit:
+                        flush()
             for led in ledgers:
                 led.gate_operations += 1
         elif isinstance(step, Measure):
@@ -255,8 +460,18 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
                 led.gate_operations += 1
     flush()
     stats = {"swaps": swaps, "physical_link_bytes": be.link_bytes, "planner": "remap" if remap else "reference"}
-    return DistRunResult(circuit, layout, mode, rank, ledgers, report, tuple(planner.pos),
-                         time.perf_counter() - start, stats, be)
+    if byte:
+        stats.update(byte_passes=be.passes, byte_host_fixes=be.host_fixes)
+    res = DistRunResult(circuit, layout, mode, rank, ledgers, report, tuple(planner.pos),
+                        time.perf_counter() - start, stats, be)
+    if byte:
+        res.codebook = be.st.codebook
+    return res
+
+
+def planner_pos_at(steps, step):
+    """Logical -> physical permutation in force when `step` runs."""
+    return step.perm
 
 
 def _measure(be, layout, ledgers, perm, rank, mode, dist):

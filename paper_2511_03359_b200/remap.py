@@ -40,6 +40,7 @@ class PhysGate:
     ordinal: int
     gate: object        # the logical gate
     qubits: tuple       # physical positions of gate.qubits
+    perm: tuple = ()    # logical -> physical permutation in force
 
 
 @dataclass(frozen=True)
@@ -95,7 +96,7 @@ class RemapPlanner:
                     lp = max(high or cands, key=lambda p: (nxt[i][self.at[p]], p))
                     steps.append(self._swap(self.pos[q], lp))
                     busy.add(lp)
-            steps.append(PhysGate(i, gate, tuple(self.pos[q] for q in gate.qubits)))
+            steps.append(PhysGate(i, gate, tuple(self.pos[q] for q in gate.qubits), tuple(self.pos)))
         return steps
 
 

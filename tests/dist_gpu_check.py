@@ -45,6 +45,27 @@ def main():
                   f"ledgers={led} stats={res.device_stats}", flush=True)
             ok = ok and same and diff < 1e-12 and led
         res.backend.close()
+    from paper_2511_03359_b200 import PrecisionMode
+    from tests.circuits import exact_class_circuit
+    byte_cases = [("bench14_be", benchmark(14)), ("exact12_be", exact_class_circuit(np.random.default_rng(5), 12, 40)),
+                  ("random12_be", random_circuit(np.random.default_rng(6), 12, 30)),
+                  ("adder6_be", adder(6, [45, 18])[0])]
+    for name, circ in byte_cases:
+        res = run_circuit_distributed(to_product(circ), dist, mode=PrecisionMode.BYTE)
+        planes = res.gathered_bytes(dist)
+        if rank == 0:
+            want = ref_engine.run_circuit(circ, ranks=world, mode="be")
+            same = np.array_equal(planes[0], want.mag) and np.array_equal(planes[1], want.phase)
+            cbs = res.codebook.dump() == want.codebook.dump()
+            wx, wy, wz, _ = want.report
+            rep = res.report
+            diff = max(np.max(np.abs(np.array(rep.qx) - wx)), np.max(np.abs(np.array(rep.qy) - wy)),
+                       np.max(np.abs(np.array(rep.qz) - wz)))
+            led = [l.snapshot() for l in res.ledgers] == want.ledgers
+            print(f"[dist {world} GPUs] {name}: bytes bit-exact={same} codebook={cbs} report diff={diff:.2e} "
+                  f"ledgers={led} stats={res.device_stats}", flush=True)
+            ok = ok and same and cbs and diff < 1e-12 and led
+        res.backend.close()
     flag = [ok]
     dist.broadcast_object_list(flag, src=0)
     dist.destroy_process_group()
