@@ -303,6 +303,46 @@ def run_b200(args):
                "what": "run_circuit(layer + M): allocate + zero 2^N state, fused layer, measure-all, "
                        "report to host; wall clock per call"}
 
+    # adder circuit time (BASELINE config 3: build_adder(16, [47302, 18233]), N=32 FP64, public API)
+    adder = None
+    if args.adder:
+        circ, regs = pb.build_adder(16, [47302, 18233])
+        pb.run_circuit(pb.build_adder(4, [3, 12])[0], device=device)          # warm the code paths
+        t0 = time.perf_counter()
+        res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
+        t_adder = time.perf_counter() - t0
+        kat = all(abs(res.report.qz[q] - 1.0) < 1e-12 for q in regs["R2"])
+        adder = {"circuit": "build_adder(16, [47302, 18233])", "n_qubits": 32, "gates": len(circ.gates),
+                 "seconds": round(t_adder, 4), "sec_per_gate": round(t_adder / len(circ.gates), 6),
+                 "kat_all_ones_R2": kat, "kernel_launches": res.device_stats.get("kernel_launches"),
+                 "what": "run_circuit wall clock incl. allocation, zero state, fused passes, measure-all"}
+        del res
+    # byte-encoded benchmark (BASELINE config 5 shape on one GPU): time per gate
+    byte = None
+    if args.byte_n > 0:
+        from paper_2511_03359_b200.byte_state import ByteEngineState
+        from paper_2511_03359_b200.layout import PartitionLayout
+        bc = pb.build_benchmark(args.byte_n)
+        bst = ByteEngineState(args.byte_n, PartitionLayout(args.byte_n, args.byte_n), device=device)
+        bst.zero(0)
+        t0 = time.perf_counter()
+        for gte in bc.gates[:-1]:
+            bst.apply_gate(gte)
+        bst.synchronize()
+        t_gates = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        norm, _, _ = bst.measure_sums()
+        t_meas = time.perf_counter() - t0
+        ng = len(bc.gates) - 1
+        byte = {"circuit": f"build_benchmark({args.byte_n}) BYTE", "gates": ng,
+                "sec_per_gate": round(t_gates / ng, 5),
+                "effective_GBps": round(ng * 4 * 2 ** args.byte_n / t_gates / 1e9, 1),
+                "measure_s": round(t_meas, 4), "norm": norm, "passes": bst.passes,
+                "codebook": [len(bst.codebook.mags), len(bst.codebook.thetas)],
+                "what": "apply_gate wall clock (passes + per-gate codebook barrier), 4 B/amplitude/gate"}
+        bst.free()
+        del bst
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(max(1, args.cpu_layers), args.layers)
@@ -340,6 +380,10 @@ def run_b200(args):
             line["e2e"] = e2e
         if cpu:
             line["cpu_baseline"] = cpu
+        if adder:
+            line["adder"] = adder
+        if byte:
+            line["byte_mode"] = byte
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
@@ -478,6 +522,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-layers", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--adder", type=int, default=1, help="time the N=32 adder circuit (1 GPU line)")
+    ap.add_argument("--byte-n", type=int, default=32, help="BYTE benchmark size for the 1 GPU line (0: skip)")
     ap.add_argument("--single-gate", action="store_true", default=True)
     args = ap.parse_args()
     if args.impl == "reference":

@@ -118,8 +118,10 @@ def run_circuit(circuit: Circuit, *, ranks: int = 1, local_qubits: int | None = 
         raise NotImplementedError("the two-tier staging model (tier.py) is out of scope on B200: "
                                   "every configuration stays resident in HBM")
     start = time.perf_counter()
+    launches0 = nat.launch_count()
     eng = _Engine(circuit, layout, mode, rank_order_seed, transport_factory, device, fuse, tile_bits)
     eng.run()
+    eng.launches = nat.launch_count() - launches0
     return RunResult(circuit, layout, mode, eng.states, eng.ledgers, eng.report, eng.codebook,
                      None, time.perf_counter() - start, eng.stats())
 
@@ -248,7 +250,7 @@ class _Engine:
         self.transport.assert_drained()
 
     def stats(self) -> dict:
-        out = {"device": self.dev.device, "kernel_launches": self.dev.launches,
+        out = {"device": self.dev.device, "kernel_launches": getattr(self, "launches", self.dev.launches),
                "gates_applied": self.gates_applied, "fused": self.fuse and self.mode is not PrecisionMode.BYTE,
                "physical_link_bytes": 0}
         if self.mode is PrecisionMode.BYTE:
