@@ -502,6 +502,8 @@ def run_b200_multi(args, dist, rank, world, device):
             "gpu_launches": launches,
             "clocks": clocks,
         }
+        if e2e:
+            line["e2e"] = e2e
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
