@@ -483,6 +483,34 @@ def run_b200_multi(args, dist, rank, world, device):
               "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
               "physical_link_bytes_this_rank_timed": be.link_bytes - link0 - 2 * len(probe_ms) * (be.dev.size // 4) * 16}
     be.close()
+    be.dev.free()
+    del be
+    # end to end through the public API: run_circuit_distributed(layer + M) per step
+    e2e = None
+    if args.e2e_steps > 0:
+        from paper_2511_03359_b200.distributed import run_circuit_distributed
+        h2d0, d2h0 = nat.transfer_bytes()
+        t_e2e, e2e_bytes = 0.0, 0
+        for j in range(args.e2e_steps):
+            li = 1 + j % (len(layers) - 1) if len(layers) > 1 else 0
+            circ = pb.Circuit(N, tuple(layers[li]) + (pb.gates.measure_all(),))
+            dist.barrier()
+            t0 = time.perf_counter()
+            res = run_circuit_distributed(circ, dist, device=device, tile_bits=args.tile_bits)
+            _ = res.report.qz[0]
+            dist.barrier()
+            t_e2e += time.perf_counter() - t0
+            e2e_bytes += lbytes[li]
+            res.backend.close()
+            res.backend.dev.free()
+            del res
+        h2d1, d2h1 = nat.transfer_bytes()
+        t_e2e = max_over_ranks(dist, t_e2e)
+        e2e = {"value": round(e2e_bytes / t_e2e / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": (h2d1 - h2d0) // args.e2e_steps,
+               "d2h_bytes_per_step": (d2h1 - d2h0) // args.e2e_steps,
+               "what": "run_circuit_distributed(layer + M) per step: allocate + zero + IPC map, remapped "
+                       "layer, measure-all, report on every rank; wall clock max over ranks"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
