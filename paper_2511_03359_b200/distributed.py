@@ -113,6 +113,27 @@ class CudaBackend:
         self.dev._touch()
         self.link_bytes += 2 * (self.dev.size // 4) * self.bpe      # this rank's reads + writes over NVLink
 
+    def pair_gate(self, global_pos: int, matrix) -> None:
+        """The reference's pairwise round for a single-qubit gate on a global qubit
+        (engine.py:246-269), fused with the exchange: the low rank updates offsets
+        [0, L/2) of both slices, the high rank [L/2, L), reading and writing the
+        partner's HBM directly (svk_pair_update with a peer pointer)."""
+        bit = global_pos - self.n_local
+        partner = self.rank ^ (1 << bit)
+        low = ((self.rank >> bit) & 1) == 0
+        half = self.dev.size // 2
+        esz = np.dtype(self.dev.dtype).itemsize
+        off = 0 if low else half
+        own = ctypes.c_void_p(self.dev.ptr.value + off * esz)
+        peer = ctypes.c_void_p(self.peers[partner].value + off * esz)
+        a0, a1 = (own, peer) if low else (peer, own)
+        m = nat.mat_buffer(matrix)
+        self._sync_all()
+        nat.check(nat.load().svk_pair_update(a0, a1, half, self.dev.mode_code, nat.dptr(m), self.dev.stream))
+        self._sync_all()
+        self.dev._touch()
+        self.link_bytes += 2 * half * self.bpe
+
     def measure_local(self):
         return self.dev.measure()
 
@@ -412,8 +433,8 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
     n = circuit.n_qubits
     n_local = n - (P.bit_length() - 1)
     layout = PartitionLayout(n, n_local)
-    if not remap:
-        raise NotImplementedError("reference-choreography exchanges: use remap=True")
+    if not remap and mode is PrecisionMode.BYTE:
+        raise NotImplementedError("BYTE runs use the remap planner (remap=True)")
     start = time.perf_counter()
     dev_id = rank if device is None else device
     if backend_factory is not None:
@@ -445,6 +466,9 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
             _charge_reference(layout, ledgers, step.gate, mode)
             if byte:
                 be.apply_gate(step.gate, step.qubits, tuple(planner_pos_at(steps, step)))
+            elif not remap and not g.is_diagonal(step.gate) and any(p >= n_local for p in step.qubits):
+                flush()
+                _reference_exchange(be, step, n_local, rank)
             else:
                 op = phys_op(step.gate, step.qubits, n_local, rank)
                 if op is not None:
@@ -467,6 +491,30 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
     if byte:
         res.codebook = be.st.codebook
     return res
+
+
+def _reference_exchange(be, step, n_local, rank):
+    """remap=False: the reference's exchange per global gate.  Single-qubit gates use
+    the exchange-fused pair update; two-qubit gates borrow local qubits for the
+    duration of the gate (swap in, apply, swap back)."""
+    gate, phys = step.gate, step.qubits
+    if len(phys) == 1:
+        be.pair_gate(phys[0], g.unitary_matrix(gate))
+        return
+    busy = set(phys)
+    temps, moved = [], list(phys)
+    for i, p in enumerate(phys):
+        if p >= n_local:
+            lp = next(q for q in range(n_local - 1, -1, -1) if q not in busy)
+            busy.add(lp)
+            be.swap(p, lp)
+            temps.append((p, lp))
+            moved[i] = lp
+    op = phys_op(gate, tuple(moved), n_local, rank)
+    if op is not None:
+        be.apply_local([op])
+    for p, lp in reversed(temps):
+        be.swap(p, lp)
 
 
 def planner_pos_at(steps, step):

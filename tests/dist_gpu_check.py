@@ -45,6 +45,19 @@ def main():
                   f"ledgers={led} stats={res.device_stats}", flush=True)
             ok = ok and same and diff < 1e-12 and led
         res.backend.close()
+    # reference choreography (no remapping): exchange-fused pair updates over NVLink
+    for name, circ in [("random14_ref", random_circuit(np.random.default_rng(11), 14, 80)),
+                       ("bench16_ref", benchmark(16))]:
+        res = run_circuit_distributed(to_product(circ), dist, remap=False)
+        state = res.gathered_state(dist)
+        if rank == 0:
+            want = ref_engine.run_circuit(circ, ranks=world)
+            same = np.array_equal(state, want.gathered_state())
+            led = [l.snapshot() for l in res.ledgers] == want.ledgers
+            print(f"[dist {world} GPUs] {name}: state bit-exact={same} ledgers={led} stats={res.device_stats}",
+                  flush=True)
+            ok = ok and same and led
+        res.backend.close()
     from paper_2511_03359_b200 import PrecisionMode
     from tests.circuits import exact_class_circuit
     byte_cases = [("bench14_be", benchmark(14)), ("exact12_be", exact_class_circuit(np.random.default_rng(5), 12, 40)),

@@ -25,6 +25,13 @@ cases = {
     "8xU2@20-27": [u2(q) for q in range(20, 28)],
     "2xU4": [u4(20, 21), u4(22, 23)],
     "4xU4": [u4(20, 21), u4(22, 23), u4(24, 25), u4(26, 20)],
+    "8xU2@20-23x2": [u2(q) for q in (20, 21, 22, 23)] * 2,
+    "8xH@20-27": [g.h(q) for q in range(20, 28)],
+    "16xU2@20-23x4": [u2(q) for q in (20, 21, 22, 23)] * 4,
+    "6xH@20-25": [g.h(q) for q in range(20, 26)],
+    "6xU2@20-25": [u2(q) for q in range(20, 26)],
+    "6xH@20-25x2": [g.h(q) for q in range(20, 26)] * 2,
+    "3xU4@20-25": [u4(20, 21), u4(22, 23), u4(24, 25)],
     "mix8": [g.h(20), u2(21), g.cnot(22, 23), u4(24, 20), g.cphase(21, 25, 3), g.x(26), g.phase(22, 2), u2(25)],
 }
 if len(sys.argv) > 3:
