@@ -174,6 +174,12 @@ int sv_ipc_close(int device, void* peer_ptr);
  * trade places with the partner's amplitudes with bit l = side.  Both ranks
  * call it; each moves half of the pairs.  n_local_elems = 2^n'. */
 int svk_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l, int side, void* stream);
+/* batched remap (k global qubits at once, one member pair of the 2^k group):
+ * this rank's amplitudes whose bits under victim_mask equal own_pattern trade
+ * places with the peer's amplitudes whose victim bits equal peer_pattern, for
+ * the remaining-bit indices [t_begin, t_begin + t_count). */
+int svk_swap_group(void* own, void* peer, uint64_t n_local_elems, int mode, uint64_t victim_mask,
+                   uint64_t own_pattern, uint64_t peer_pattern, uint64_t t_begin, uint64_t t_count, void* stream);
 /* sum conj(a0[i]) * a1[i] over count elements (a1 may be a peer pointer):
  * measure.py:83-101 cross term of a global qubit; out2 = (re, im) */
 int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, double* out2, void* stream);
@@ -183,6 +189,9 @@ int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, doubl
 int svb_ipc_handles(sv_bhandle h, void* out256);
 int svb_cur(sv_bhandle h);
 int svb_swap_peer(sv_bhandle h, void* peer_mi, void* peer_pi, int l, int side);
+/* BYTE planes form of svk_swap_group (current planes of this rank and the peer) */
+int svb_swap_group(sv_bhandle h, void* peer_mi, void* peer_pi, uint64_t victim_mask, uint64_t own_pattern,
+                   uint64_t peer_pattern, uint64_t t_begin, uint64_t t_count);
 int svb_pair_dot(sv_bhandle h, const void* a_mi, const void* a_pi, const void* b_mi, const void* b_pi,
                  uint64_t count, double* out2);
 /* device pointers of the current planes (for offsets into own / peer planes) */

@@ -704,6 +704,31 @@ __global__ void k_byte_swap_peer16(uint8_t* omi, uint8_t* opi, uint8_t* pmi, uin
     }
 }
 
+// batched remap of k global qubits (see k_swap_group in sv_dist.cu): 16 rest
+// indices per item when the lowest victim bit is >= 4
+template <int W>
+__global__ void k_byte_swap_group(uint8_t* omi, uint8_t* opi, uint8_t* pmi, uint8_t* ppi, uint64_t t0, uint64_t n,
+                                  uint64_t vmask, uint64_t own_pat, uint64_t peer_pat) {
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n; w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t base = insert_zeros(t0 + w * W, vmask);
+        const uint64_t x = base | own_pat, y = base | peer_pat;
+        if constexpr (W == 16) {
+            const uint4 a = *reinterpret_cast<const uint4*>(omi + x), b = *reinterpret_cast<const uint4*>(opi + x);
+            const uint4 pa = *reinterpret_cast<const uint4*>(pmi + y), pb = *reinterpret_cast<const uint4*>(ppi + y);
+            *reinterpret_cast<uint4*>(omi + x) = pa;
+            *reinterpret_cast<uint4*>(opi + x) = pb;
+            *reinterpret_cast<uint4*>(pmi + y) = a;
+            *reinterpret_cast<uint4*>(ppi + y) = b;
+        } else {
+            const uint8_t a = omi[x], b = opi[x];
+            omi[x] = pmi[y];
+            opi[x] = ppi[y];
+            pmi[y] = a;
+            ppi[y] = b;
+        }
+    }
+}
+
 // sum conj(decode(a)) * decode(b) over count elements (a / b may be peer planes)
 __global__ void k_byte_pair_dot(const uint8_t* ami, const uint8_t* api, const uint8_t* bmi, const uint8_t* bpi,
                                 const ByteTables* gtab, uint64_t n, double* partials) {
@@ -770,6 +795,17 @@ cudaError_t launch_byte_swap_peer(uint8_t* omi, uint8_t* opi, uint8_t* pmi, uint
     } else {
         k_byte_swap_peer<<<byte_grid(quarter), NT, 0, st>>>(omi, opi, pmi, ppi, t0, quarter, l, c);
     }
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_byte_swap_group(uint8_t* omi, uint8_t* opi, uint8_t* pmi, uint8_t* ppi, uint64_t t0, uint64_t n,
+                                   uint64_t vmask, uint64_t own_pat, uint64_t peer_pat, cudaStream_t st) {
+    if ((vmask & 15ull) == 0 && t0 % 16 == 0 && n % 16 == 0)
+        k_byte_swap_group<16><<<byte_grid(n / 16), NT, 0, st>>>(omi, opi, pmi, ppi, t0, n / 16, vmask, own_pat,
+                                                                peer_pat);
+    else
+        k_byte_swap_group<1><<<byte_grid(n), NT, 0, st>>>(omi, opi, pmi, ppi, t0, n, vmask, own_pat, peer_pat);
     count_launch();
     return cudaGetLastError();
 }

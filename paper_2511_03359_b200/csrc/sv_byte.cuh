@@ -56,6 +56,8 @@ cudaError_t launch_byte_decode(const uint8_t* mi, const uint8_t* pi, const ByteT
                                cudaStream_t st);
 cudaError_t launch_byte_encode(const double* vals, uint64_t n, const ByteTables* tab, uint8_t* mi, uint8_t* pi,
                                const ByteGate& g, ByteCand* cand, cudaStream_t st);
+cudaError_t launch_byte_swap_group(uint8_t* omi, uint8_t* opi, uint8_t* pmi, uint8_t* ppi, uint64_t t0, uint64_t n,
+                                   uint64_t vmask, uint64_t own_pat, uint64_t peer_pat, cudaStream_t st);
 cudaError_t launch_byte_swap_peer(uint8_t* omi, uint8_t* opi, uint8_t* pmi, uint8_t* ppi, uint64_t n_local_elems,
                                   int l, int c, cudaStream_t st);
 cudaError_t launch_byte_pair_dot(const uint8_t* ami, const uint8_t* api, const uint8_t* bmi, const uint8_t* bpi,

@@ -347,6 +347,21 @@ int svb_swap_peer(sv_bhandle h, void* peer_mi, void* peer_pi, int l, int side) {
     return e == cudaSuccess ? SV_OK : capi_cuda_fail(e, "byte swap launch");
 }
 
+int svb_swap_group(sv_bhandle h, void* peer_mi, void* peer_pi, uint64_t victim_mask, uint64_t own_pattern,
+                   uint64_t peer_pattern, uint64_t t_begin, uint64_t t_count) {
+    Guard gd(h->device);
+    const uint64_t n = 1ull << h->n;
+    if ((victim_mask & ~(n - 1)) || ((own_pattern | peer_pattern) & ~victim_mask))
+        return capi_fail(SV_EINDEX, "victim mask / patterns outside the slice");
+    const uint64_t rest = n >> __builtin_popcountll(victim_mask);
+    if (t_begin > rest || t_count > rest - t_begin) return capi_fail(SV_EINDEX, "rest range outside the slice");
+    if (t_count == 0) return SV_OK;
+    cudaError_t e = launch_byte_swap_group(h->plane[h->cur][0], h->plane[h->cur][1], static_cast<uint8_t*>(peer_mi),
+                                           static_cast<uint8_t*>(peer_pi), t_begin, t_count, victim_mask, own_pattern,
+                                           peer_pattern, h->stream);
+    return e == cudaSuccess ? SV_OK : capi_cuda_fail(e, "byte group swap launch");
+}
+
 int svb_pair_dot(sv_bhandle h, const void* a_mi, const void* a_pi, const void* b_mi, const void* b_pi,
                  uint64_t count, double* out2) {
     Guard gd(h->device);

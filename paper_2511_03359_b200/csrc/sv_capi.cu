@@ -874,6 +874,20 @@ int svk_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l
     return e == cudaSuccess ? SV_OK : cuda_fail(e, "swap launch");
 }
 
+int svk_swap_group(void* own, void* peer, uint64_t n_local_elems, int mode, uint64_t victim_mask,
+                   uint64_t own_pattern, uint64_t peer_pattern, uint64_t t_begin, uint64_t t_count, void* stream) {
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "swap needs FP64 or FP32 storage");
+    if (!is_pow2(n_local_elems)) return fail(SV_EVALUE, "swap needs a power-of-two slice");
+    if ((victim_mask & ~(n_local_elems - 1)) || ((own_pattern | peer_pattern) & ~victim_mask))
+        return fail(SV_EINDEX, "victim mask / patterns outside the slice");
+    const uint64_t rest = n_local_elems >> __builtin_popcountll(victim_mask);
+    if (t_begin > rest || t_count > rest - t_begin) return fail(SV_EINDEX, "rest range outside the slice");
+    if (t_count == 0) return SV_OK;
+    cudaError_t e = launch_swap_group(own, peer, t_begin, t_count, mode, victim_mask, own_pattern, peer_pattern,
+                                      as_stream(stream));
+    return e == cudaSuccess ? SV_OK : cuda_fail(e, "group swap launch");
+}
+
 int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, double* out2, void* stream) {
     if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "pair dot needs FP64 or FP32 storage");
     out2[0] = out2[1] = 0.0;

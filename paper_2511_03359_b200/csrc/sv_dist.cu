@@ -71,6 +71,81 @@ __global__ void __launch_bounds__(256) k_swap_peer_scalar(S* own, S* peer, uint6
     }
 }
 
+// Batched swap of k global qubits with k local victims (one member pair of the
+// 2^k-rank group): this rank's amplitudes whose victim bits read `own_pat` trade
+// places with the member's amplitudes whose victim bits read `peer_pat` (same
+// remaining bits).  t runs over the remaining-bit space [t0, t0 + n).
+template <typename S>
+__global__ void __launch_bounds__(256) k_swap_group(S* __restrict__ own, S* __restrict__ peer, uint64_t t0,
+                                                    uint64_t n, uint64_t vmask, uint64_t own_pat,
+                                                    uint64_t peer_pat) {
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n; w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t base = insert_zeros(t0 + w, vmask);
+        const uint64_t x = base | own_pat, y = base | peer_pat;
+        const S a = own[x];
+        own[x] = peer[y];
+        peer[y] = a;
+    }
+}
+
+template <typename S, int U>
+__global__ void __launch_bounds__(256) k_swap_group_vec(S* __restrict__ own, S* __restrict__ peer, uint64_t t0,
+                                                        uint64_t n_vec, uint64_t vmask, uint64_t own_pat,
+                                                        uint64_t peer_pat) {
+    constexpr int V = Store<S>::V;
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w0 < n_vec; w0 += U * step) {
+        Vec<S> a[U], b[U];
+        uint64_t x[U], y[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t w = w0 + u * step;
+            if (w < n_vec) {
+                const uint64_t base = insert_zeros(t0 + w * V, vmask);
+                x[u] = base | own_pat;
+                y[u] = base | peer_pat;
+                a[u] = vload(own + x[u]);
+                b[u] = vload(peer + y[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t w = w0 + u * step;
+            if (w < n_vec) {
+                vstore(own + x[u], b[u]);
+                vstore(peer + y[u], a[u]);
+            }
+        }
+    }
+}
+
+template <typename S>
+static cudaError_t swap_group_t(S* own, S* peer, uint64_t t0, uint64_t n, uint64_t vmask, uint64_t op, uint64_t pp,
+                                cudaStream_t st) {
+    constexpr int V = Store<S>::V;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t cap = (uint64_t)sm_count(dev) * 8;
+    const bool vec = (vmask & (uint64_t)(V - 1)) == 0 && (t0 % V) == 0 && (n % V) == 0;
+    if (vec) {
+        const uint64_t nv = n / V;
+        const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nv + 1023) / 1024, cap));
+        k_swap_group_vec<S, 4><<<g, 256, 0, st>>>(own, peer, t0, nv, vmask, op, pp);
+    } else {
+        const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, cap));
+        k_swap_group<S><<<g, 256, 0, st>>>(own, peer, t0, n, vmask, op, pp);
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_swap_group(void* own, void* peer, uint64_t t0, uint64_t n, int mode, uint64_t vmask,
+                              uint64_t own_pat, uint64_t peer_pat, cudaStream_t st) {
+    return mode == SV_FP32
+               ? swap_group_t(static_cast<c32s*>(own), static_cast<c32s*>(peer), t0, n, vmask, own_pat, peer_pat, st)
+               : swap_group_t(static_cast<c64s*>(own), static_cast<c64s*>(peer), t0, n, vmask, own_pat, peer_pat, st);
+}
+
 template <typename S>
 __global__ void __launch_bounds__(256) k_pair_dot(const S* __restrict__ a0, const S* __restrict__ a1, uint64_t n,
                                                   double* __restrict__ partials) {

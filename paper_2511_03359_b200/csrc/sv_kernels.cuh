@@ -95,6 +95,8 @@ int measure_grid(int device);
 
 int sm_count(int device);
 cudaError_t launch_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l, int c, cudaStream_t st);
+cudaError_t launch_swap_group(void* own, void* peer, uint64_t t0, uint64_t n, int mode, uint64_t vmask,
+                              uint64_t own_pat, uint64_t peer_pat, cudaStream_t st);
 cudaError_t launch_pair_dot(const void* a0, const void* a1, uint64_t n, int mode, double* partials, int grid,
                             cudaStream_t st);
 void count_launch(uint64_t n = 1);

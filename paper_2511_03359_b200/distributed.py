@@ -36,7 +36,7 @@ from .circuit import Circuit, validate_circuit
 from .device import gate_op
 from .layout import PartitionLayout, TrafficLedger, plan_exchange
 from .measure import ExpectationReport, report_from_sums
-from .remap import Measure, PhysGate, RemapPlanner, Swap
+from .remap import Measure, PhysGate, RemapPlanner, Swap, SwapGroup, group_schedule
 from .state import PrecisionMode
 
 
@@ -112,6 +112,26 @@ class CudaBackend:
         self._sync_all()
         self.dev._touch()
         self.link_bytes += 2 * (self.dev.size // 4) * self.bpe      # this rank's reads + writes over NVLink
+
+    def swap_group(self, pairs) -> None:
+        """Batched swap of k global qubits (remap.SwapGroup): one svk_swap_group launch
+        per other member of this rank's 2^k group, all ranks concurrently (every
+        launch touches a disjoint set of amplitudes)."""
+        sched = group_schedule(self.rank, pairs, self.n_local, self.dev.size)
+        self._sync_all()
+        if self.swap_timing:
+            e0, e1 = nat.Event(), nat.Event()
+            e0.record(self.dev.stream)
+        lib = nat.load()
+        for member, vmask, own_pat, peer_pat, t0, cnt in sched:
+            nat.check(lib.svk_swap_group(self.dev.ptr, self.peers[member], self.dev.size, self.dev.mode_code, vmask,
+                                         own_pat, peer_pat, t0, cnt, self.dev.stream))
+            self.link_bytes += 2 * cnt * self.bpe
+        if self.swap_timing:
+            e1.record(self.dev.stream)
+            self.swap_events.append((e0, e1))
+        self._sync_all()
+        self.dev._touch()
 
     def pair_gate(self, global_pos: int, matrix) -> None:
         """The reference's pairwise round for a single-qubit gate on a global qubit
@@ -231,6 +251,17 @@ class CudaByteBackend:
         self._sync_all()
         self.st.version += 1
         self.link_bytes += 2 * (self.st.size // 4) * 2
+
+    def swap_group(self, pairs) -> None:
+        sched = group_schedule(self.rank, pairs, self.n_local, self.st.size)
+        self._sync_all()
+        lib = nat.load()
+        for member, vmask, own_pat, peer_pat, t0, cnt in sched:
+            pm, pp = self._peer_cur(member)
+            nat.check(lib.svb_swap_group(self.st.handle, pm, pp, vmask, own_pat, peer_pat, t0, cnt))
+            self.link_bytes += 2 * cnt * 2
+        self._sync_all()
+        self.st.version += 1
 
     def _desc(self, gate, phys, pos):
         from .byte_state import SvbGateDesc, _exchange_fields, set_logical_bits
@@ -449,7 +480,7 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
     steps = planner.plan(circuit.gates)
     pending = []
     report = None
-    swaps = 0
+    swaps = groups = 0
 
     def flush():
         nonlocal pending
@@ -462,6 +493,11 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
             flush()
             be.swap(step.global_pos, step.local_pos)
             swaps += 1
+        elif isinstance(step, SwapGroup):
+            flush()
+            be.swap_group(step.pairs)
+            swaps += 1
+            groups += 1
         elif isinstance(step, PhysGate):
             _charge_reference(layout, ledgers, step.gate, mode)
             if byte:
@@ -483,7 +519,8 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
             for led in ledgers:
                 led.gate_operations += 1
     flush()
-    stats = {"swaps": swaps, "physical_link_bytes": be.link_bytes, "planner": "remap" if remap else "reference"}
+    stats = {"swaps": swaps, "swap_groups": groups, "physical_link_bytes": be.link_bytes,
+             "planner": "remap" if remap else "reference"}
     if byte:
         stats.update(byte_passes=be.passes, byte_host_fixes=be.host_fixes)
     res = DistRunResult(circuit, layout, mode, rank, ledgers, report, tuple(planner.pos),

@@ -16,6 +16,13 @@ physical positions >= MIN_VICTIM so fused tile passes keep their contiguous
 low qubits.  Diagonal gates never move data (layout.py:81-82): their global
 bits only select which ranks are active.
 
+Several global qubits needed close together are fetched in ONE batched swap
+(SwapGroup, svk_swap_group): k global qubits exchanged with k victims is an
+all-to-all inside each 2^k-rank group that moves (1 - 2^-k) L elements per
+direction per rank, against k L/2 for k single swaps.  A global qubit joins
+the batch when its next use comes before the next use of the victim it would
+evict (and within `window` gates).
+
 Results are bit-identical to the unpermuted execution (swaps are pure moves;
 each gate runs the same arithmetic on the same amplitudes); reports and
 exported states are mapped back to logical order.
@@ -36,6 +43,42 @@ class Swap:
 
 
 @dataclass(frozen=True)
+class SwapGroup:
+    pairs: tuple        # ((global_pos, local_pos), ...), k >= 2, simultaneous
+
+
+def deposit(code: int, positions) -> int:
+    """Bits of `code` (bit j) placed at positions[j]."""
+    out = 0
+    for j, p in enumerate(positions):
+        out |= ((code >> j) & 1) << p
+    return out
+
+
+def group_schedule(rank: int, pairs, n_local: int, n_local_elems: int):
+    """This rank's share of a batched swap: [(member_rank, vmask, own_pat, peer_pat,
+    t_begin, t_count)].  Rank r with group code c trades its amplitudes whose victim
+    bits read m with member m's amplitudes whose victim bits read c; the pair splits
+    the remaining-bit range in half (the lower code takes the first half)."""
+    bits = [gp - n_local for gp, _ in pairs]
+    lps = [lp for _, lp in pairs]
+    k = len(pairs)
+    vmask = deposit((1 << k) - 1, lps)
+    c = sum(((rank >> b) & 1) << j for j, b in enumerate(bits))
+    rest = n_local_elems >> k
+    half = rest // 2
+    base = rank & ~sum(1 << b for b in bits)
+    out = []
+    for m in range(1 << k):
+        if m == c:
+            continue
+        member = base | sum(((m >> j) & 1) << b for j, b in enumerate(bits))
+        t0 = 0 if c < m else half
+        out.append((member, vmask, deposit(m, lps), deposit(c, lps), t0, half))
+    return out
+
+
+@dataclass(frozen=True)
 class PhysGate:
     ordinal: int
     gate: object        # the logical gate
@@ -50,7 +93,10 @@ class Measure:
 
 
 class RemapPlanner:
-    def __init__(self, n_qubits: int, n_local: int, remap: bool = True, min_victim: int = MIN_VICTIM):
+    def __init__(self, n_qubits: int, n_local: int, remap: bool = True, min_victim: int = MIN_VICTIM,
+                 batch: bool = True, window: int = 64):
+        self.batch = batch and n_local >= 2
+        self.window = window
         self.n = n_qubits
         self.n_local = n_local
         self.remap = remap
@@ -88,18 +134,49 @@ class RemapPlanner:
             needs = [] if g.is_diagonal(gate) else [q for q in gate.qubits if self.pos[q] >= self.n_local]
             if needs and self.remap:
                 busy = {self.pos[q] for q in gate.qubits}
-                for q in needs:
+                chosen = []
+
+                def victim():
                     cands = [lp for lp in range(self.n_local) if lp not in busy]
                     high = [lp for lp in cands if lp >= self.min_victim]
                     # Belady (evict the local qubit needed latest) over the high physical
                     # positions, so tile passes keep their contiguous low qubits
-                    lp = max(high or cands, key=lambda p: (nxt[i][self.at[p]], p))
-                    steps.append(self._swap(self.pos[q], lp))
+                    return max(high or cands, key=lambda p: (nxt[i][self.at[p]], p)) if cands else None
+
+                for q in needs:
+                    lp = victim()
+                    chosen.append((self.pos[q], lp))
                     busy.add(lp)
+                if self.batch:
+                    soon = sorted((nxt[i][q], q) for q in range(self.n)
+                                  if self.pos[q] >= self.n_local and q not in gate.qubits)
+                    for when, q in soon:
+                        if when > i + self.window:
+                            break
+                        lp = victim()
+                        if lp is None or nxt[i][self.at[lp]] <= when:
+                            break
+                        chosen.append((self.pos[q], lp))
+                        busy.add(lp)
+                if len(chosen) == 1:
+                    steps.append(self._swap(*chosen[0]))
+                else:
+                    for gp, lp in chosen:
+                        self._swap(gp, lp)
+                    steps.append(SwapGroup(tuple(chosen)))
             steps.append(PhysGate(i, gate, tuple(self.pos[q] for q in gate.qubits), tuple(self.pos)))
         return steps
 
 
 def swap_traffic_elements(steps, n_local: int) -> int:
-    """Elements each rank sends over the link for the planned swaps (L/2 per swap)."""
-    return sum(1 for s in steps if isinstance(s, Swap)) * ((1 << n_local) // 2)
+    """Elements each rank sends over the link for the planned swaps (L/2 per
+    single swap, (1 - 2^-k) L per batched swap of k qubits)."""
+    L = 1 << n_local
+    total = 0
+    for s in steps:
+        if isinstance(s, Swap):
+            total += L // 2
+        elif isinstance(s, SwapGroup):
+            k = len(s.pairs)
+            total += L - (L >> k)
+    return total

@@ -55,6 +55,11 @@ class NumpyBackend:
         self.psi[sel] = other[idx[sel] ^ (1 << local_pos)]
         self.link_bytes += (self.psi.size // 2) * self.bpe
 
+    def swap_group(self, pairs):
+        # the same exchange as k sequential pairwise swaps (disjoint bit pairs)
+        for gp, lp in pairs:
+            self.swap(gp, lp)
+
     def measure_local(self):
         n = self.n_local
         norm = float(np.real(np.vdot(self.psi, self.psi)))
