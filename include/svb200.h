@@ -215,6 +215,18 @@ int sv_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
  * register-resident cp.async-pipelined v3 with 1 = 2^12 tiles x 16 amplitudes
  * per thread, 2 = 2^11 tiles x 8 per thread (2 CTAs/SM), 3 = 2^12 tiles x 8
  * per thread (512 threads).  FP32 storage always uses v1. */
+/* run-time specialised fused passes (NVRTC, one kernel per pass structure; see
+ * paper_2511_03359_b200/csrc/sv_jit.cu): mode 0 off, 1 compile-and-wait,
+ * 2 compile in the background and run the generic kernel meanwhile (default).
+ * Returns the previous mode.  Both kernels are bit-identical. */
+int sv_jit_mode(int mode);
+int sv_jit_wait(void);                        /* block until queued compiles finish */
+int sv_jit_stats(double* out6);               /* compiled, failed, jit launches, fallbacks, compile ms, cached */
+int sv_jit_available(void);                   /* 1 when NVRTC and the driver entry points resolved */
+/* CPU-side check: plan the first fused pass of ops on 2^n_qubits amplitudes, write
+ * its specialised source to src_out and, when compile_ms is non-NULL, compile it
+ * with NVRTC.  Returns the number of ops in the pass (>= 1) or an error code. */
+int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_t cap, double* compile_ms);
 int sv_fused_variant(int v2);
 /* passes whose v3 plan needs more than `limit` register segments use v1
  * instead (0 = no limit) */

@@ -83,6 +83,11 @@ _SIGNATURES = {
     "sv_ipc_close": ([_I, _P], _I),
     "svk_swap_peer": ([_P, _P, _U64, _I, _I, _I, _P], _I),
     "svk_pair_dot": ([_P, _P, _U64, _I, _D, _P], _I),
+    "sv_jit_mode": ([_I], _I),
+    "sv_jit_wait": ([], _I),
+    "sv_jit_stats": ([_D], _I),
+    "sv_jit_available": ([], _I),
+    "sv_jit_probe": ([_P, _I, _I, ctypes.c_char_p, ctypes.c_size_t, _D], _I),
     "svk_swap_group": ([_P, _P, _U64, _I, _U64, _U64, _U64, _U64, _U64, _P], _I),
     "svb_ipc_handles": ([_P, _P], _I),
     "svb_cur": ([_P], _I),

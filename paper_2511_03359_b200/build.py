@@ -42,17 +42,36 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+JIT_HEADERS = (("kJitArith", "sv_arith.cuh"), ("kJitDev", "sv_jit_dev.cuh"))
+
+
+def _jit_include() -> str:
+    """Embed the NVRTC-side headers as string literals (_obj/sv_jit_src.inc)."""
+    out = os.path.join(OBJ, "sv_jit_src.inc")
+    deps = [os.path.join(CSRC, f) for _, f in JIT_HEADERS]
+    if _stale(out, deps):
+        parts = []
+        for name, f in JIT_HEADERS:
+            text = open(os.path.join(CSRC, f)).read()
+            parts.append(f'static const char* {name} = R"SVJIT({text})SVJIT";\n')
+        with open(out, "w") as fh:
+            fh.write("".join(parts))
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    inc = _jit_include()
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "svb200.h"))
+    headers.append(inc)
     srcs = sources()
     objs = [os.path.join(OBJ, os.path.basename(s)[:-3] + ".o") for s in srcs]
     cc = nvcc()
     jobs = []
     for s, o in zip(srcs, objs):
         if force or _stale(o, [s] + headers):
-            jobs.append([cc, *ARCH, *FLAGS, "-c", s, "-o", o])
+            jobs.append([cc, *ARCH, *FLAGS, f"-I{OBJ}", "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -397,7 +397,8 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
         static thread_local Fused2Params P2;
         if (use_v3 && build_params2(ops, cur, n, g_fused_v2, P2) == 0 &&
             (g_seg_limit <= 0 || P2.n_segs <= g_seg_limit)) {
-            e = launch_fused2(psi, mode, P2, st);
+            const int jr = jit_launch_fused(psi, P2, st);
+            e = jr < 0 ? cudaErrorLaunchFailure : (jr == 0 ? cudaSuccess : launch_fused2(psi, mode, P2, st));
             count_h2d(sizeof(Fused2Params));
         } else {
             static thread_local FusedParams P;
@@ -754,6 +755,39 @@ int sv_apply_diag(sv_handle h, uint64_t mask, const double* f2) {
     DeviceGuard g(h->device);
     return svk_apply_diag(h->ptr, 1ull << h->n, h->mode, mask, f2, h->stream);
 }
+int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_t cap, double* compile_ms) {
+    // plan the FIRST fused pass of `ops` on 2^n_qubits amplitudes exactly as fused_impl
+    // does, print its specialised source, optionally compile it (CPU only)
+    const int K = 11;
+    if (n_qubits < K || n_qubits > 62 || n_ops <= 0) return fail(SV_EVALUE, "probe needs n >= 11 and ops");
+    const uint64_t lowfix = 31ull;
+    PassPlan cur;
+    for (int i = 0; i < n_ops; ++i) {
+        const sv_op& o = ops[i];
+        uint64_t need = 0;
+        if (o.kind == SV_OP_1Q) need = 1ull << o.qa;
+        if (o.kind == SV_OP_2Q) need = (1ull << o.qa) | (1ull << o.qb);
+        if (popcount64(cur.qmask | need | lowfix) > K || (int)cur.ops.size() >= kMaxOps ||
+            cur.mdata + op_mdata(o.kind) > kMaxMData)
+            break;
+        cur.qmask |= need;
+        cur.ops.push_back(i);
+        cur.mdata += op_mdata(o.kind);
+    }
+    static thread_local Fused2Params P2;
+    if (build_params2(ops, cur, n_qubits, 6, P2) != 0) return fail(SV_EVALUE, "pass does not fit the v3 kernel");
+    std::string src, log;
+    double ms = 0.0;
+    const int rc = sv::jit_probe(P2, &src, compile_ms != nullptr, &ms, &log);
+    if (compile_ms) *compile_ms = ms;
+    if (src_out && cap) {
+        std::strncpy(src_out, src.c_str(), cap - 1);
+        src_out[cap - 1] = 0;
+    }
+    if (rc) return fail(SV_EVALUE, "NVRTC compile failed: %s", log.c_str());
+    return (int)cur.ops.size();
+}
+
 int sv_apply_fused(sv_handle h, const sv_op* ops, int n_ops, int tile_bits) {
     DeviceGuard g(h->device);
     return svk_apply_fused(h->ptr, 1ull << h->n, h->mode, ops, n_ops, tile_bits, h->stream);

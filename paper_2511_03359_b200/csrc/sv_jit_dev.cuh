@@ -1,0 +1,171 @@
+// Device side of the specialised fused-pass kernels (compiled at run time by
+// NVRTC from sv_jit.cu; include-free apart from sv_arith.cuh).
+//
+// A generated pass kernel is k_fused3 (sv_fused2.cu) with every pass constant
+// folded in: tile positions, segment register/thread positions, shared-memory
+// swizzle offsets, op kinds, register bits, monomial codes and diagonal masks
+// are literals, so the per-op dispatch (switches, selects, register moves at
+// the join points, LDC of the op tables) disappears and the matrices are read
+// as constant-bank operands of the DFMA/DMUL instructions.  The arithmetic is
+// the same sequence as k_fused3 (sv_arith.cuh, reference operand order), so a
+// specialised pass is bit-identical to the generic one.
+#pragma once
+
+#include "sv_arith.cuh"
+
+namespace svj {
+
+using sv::cadd;
+using sv::cmul;
+using sv::cplx;
+using sv::row2;
+using sv::row4;
+typedef unsigned long long u64;
+
+struct __align__(16) c64s { double re, im; };
+
+// shared-memory swizzle of k_fused3 (linear in the element index)
+__device__ __forceinline__ int swz(int e) {
+    const int g = (((e >> 3) & 1) * 7) ^ (((e >> 4) & 1) * 3) ^ (((e >> 5) & 1) * 5) ^ (((e >> 6) & 1) * 6);
+    return e ^ g;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// p + off amplitudes, computed where it is used: the 16 prefetch / store addresses of
+// a tile are loop-invariant offsets from the tile base, and hoisting them out of the
+// tile loop (32 live 64-bit pointers) is what made the compiler spill
+template <typename T>
+__device__ __forceinline__ T* at(T* p, u64 off) {
+    T* r;
+    asm volatile("add.s64 %0, %1, %2;" : "=l"(r) : "l"(p), "l"(off * sizeof(T)));
+    return r;
+}
+
+__device__ __forceinline__ void stg(c64s* p, cplx v) {
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.re), "d"(v.im) : "memory");
+}
+
+template <int U>
+__device__ __forceinline__ cplx mu(cplx a) {   // U: 0 -> 1, 1 -> i, 2 -> -1, 3 -> -i
+    if constexpr (U == 0) return a;
+    else if constexpr (U == 1) return {-a.im, a.re};
+    else if constexpr (U == 2) return {-a.re, -a.im};
+    else return {a.im, -a.re};
+}
+
+__device__ __forceinline__ cplx rmul(double m, cplx a) { return {__dmul_rn(m, a.re), __dmul_rn(m, a.im)}; }
+
+// Matrix entries of the pass live in kernel parameter 1 (Args::m).  They are read
+// at the point of use through a parameter-space address that the generated kernel
+// rebuilds every tile from an opaque zero (tile >> 62): with plain (or volatile)
+// constant loads ptxas hoists every matrix of the pass out of the tile loop, the
+// uniform registers overflow into ~130 regular registers for a few U4 gates and the
+// kernel spills; a per-use LDC costs one instruction per entry per tile.
+__device__ __forceinline__ u64 mbase(u64 tile) {
+    u64 b;
+    asm("mov.u64 %0, sv_pass_param_1;" : "=l"(b));
+    return b + ((tile >> 62) << 3);
+}
+template <int OFF>
+__device__ __forceinline__ double ldm(u64 mb) {
+    double v;
+    asm volatile("ld.param.f64 %0, [%1+%2];" : "=d"(v) : "l"(mb), "n"(8 + 8 * OFF));
+    return v;
+}
+template <int OFF>
+__device__ __forceinline__ cplx ldc2(u64 mb) { return {ldm<OFF>(mb), ldm<OFF + 1>(mb)}; }
+
+// ---- single-qubit ops on register bit J ------------------------------------------
+template <int R, int J, int OFF>
+__device__ __forceinline__ void g1(cplx (&r)[R], u64 mb) {
+    const cplx m0 = ldc2<OFF>(mb), m1 = ldc2<OFF + 2>(mb), m2 = ldc2<OFF + 4>(mb), m3 = ldc2<OFF + 6>(mb);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        if (i & (1 << J)) continue;
+        const cplx a0 = r[i], a1 = r[i | (1 << J)];
+        r[i] = row2(m0, m1, a0, a1);
+        r[i | (1 << J)] = row2(m2, m3, a0, a1);
+    }
+}
+
+template <int R, int J, int OFF>
+__device__ __forceinline__ void g1r(cplx (&r)[R], u64 mb) {   // real matrix (H)
+    const double m0 = ldm<OFF>(mb), m1 = ldm<OFF + 2>(mb), m2 = ldm<OFF + 4>(mb), m3 = ldm<OFF + 6>(mb);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        if (i & (1 << J)) continue;
+        const cplx a0 = r[i], a1 = r[i | (1 << J)];
+        r[i] = cadd(rmul(m0, a0), rmul(m1, a1));
+        r[i | (1 << J)] = cadd(rmul(m2, a0), rmul(m3, a1));
+    }
+}
+
+// monomial rows: per row 2-bit source selector | 2-bit unit << 2 (k_fused3's mono code)
+template <int R, int J, unsigned MONO>
+__device__ __forceinline__ void g1m(cplx (&r)[R]) {
+    constexpr int s0 = MONO & 3, u0 = (MONO >> 2) & 3, s1 = (MONO >> 4) & 3, u1 = (MONO >> 6) & 3;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        if (i & (1 << J)) continue;
+        const cplx a0 = r[i], a1 = r[i | (1 << J)];
+        r[i] = mu<u0>(s0 ? a1 : a0);
+        r[i | (1 << J)] = mu<u1>(s1 ? a1 : a0);
+    }
+}
+
+// ---- two-qubit ops: JA = register bit of qa, JB = of qb; basis bit(qa) + 2 bit(qb) -----
+template <int R, int JA, int JB, int OFF>
+__device__ __forceinline__ void g2(cplx (&r)[R], u64 mb) {
+    const cplx mm[4][4] = {
+        {ldc2<OFF + 0>(mb), ldc2<OFF + 2>(mb), ldc2<OFF + 4>(mb), ldc2<OFF + 6>(mb)},
+        {ldc2<OFF + 8>(mb), ldc2<OFF + 10>(mb), ldc2<OFF + 12>(mb), ldc2<OFF + 14>(mb)},
+        {ldc2<OFF + 16>(mb), ldc2<OFF + 18>(mb), ldc2<OFF + 20>(mb), ldc2<OFF + 22>(mb)},
+        {ldc2<OFF + 24>(mb), ldc2<OFF + 26>(mb), ldc2<OFF + 28>(mb), ldc2<OFF + 30>(mb)}};
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        if (i & ((1 << JA) | (1 << JB))) continue;
+        const int idx[4] = {i, i | (1 << JA), i | (1 << JB), i | (1 << JA) | (1 << JB)};
+        const cplx a[4] = {r[idx[0]], r[idx[1]], r[idx[2]], r[idx[3]]};
+#pragma unroll
+        for (int row = 0; row < 4; ++row) r[idx[row]] = row4(mm[row], a[0], a[1], a[2], a[3]);
+    }
+}
+
+template <int R, int JA, int JB, unsigned MONO>
+__device__ __forceinline__ void g2m(cplx (&r)[R]) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        if (i & ((1 << JA) | (1 << JB))) continue;
+        const int idx[4] = {i, i | (1 << JA), i | (1 << JB), i | (1 << JA) | (1 << JB)};
+        const cplx a[4] = {r[idx[0]], r[idx[1]], r[idx[2]], r[idx[3]]};
+        r[idx[0]] = mu<(MONO >> 2) & 3>(a[MONO & 3]);
+        r[idx[1]] = mu<(MONO >> 6) & 3>(a[(MONO >> 4) & 3]);
+        r[idx[2]] = mu<(MONO >> 10) & 3>(a[(MONO >> 8) & 3]);
+        r[idx[3]] = mu<(MONO >> 14) & 3>(a[(MONO >> 12) & 3]);
+    }
+}
+
+// ---- diagonal factor on the registers whose bits cover MR (amplitude first) --------
+template <int R, unsigned MR, int OFF>
+__device__ __forceinline__ void gd(cplx (&r)[R], u64 mb) {
+    const cplx f = ldc2<OFF>(mb);
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+        if ((i & MR) == MR) r[i] = cmul(r[i], f);
+}
+
+template <int R, unsigned MR>
+__device__ __forceinline__ void gdn(cplx (&r)[R]) {   // factor exactly -1 (Z): exact negation
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+        if ((i & MR) == MR) r[i] = {-r[i].re, -r[i].im};
+}
+
+}  // namespace svj

@@ -63,6 +63,12 @@ struct Fused2Params {
     double mdata[kMaxMData];
 };
 cudaError_t launch_fused2(void* psi, int mode, const Fused2Params& p, cudaStream_t st);
+// run-time specialised form of the same pass (sv_jit.cu): 0 launched, 1 not ready, < 0 error
+int jit_launch_fused(void* psi, const Fused2Params& p, cudaStream_t st);
+}  // namespace sv
+#include <string>
+namespace sv {
+int jit_probe(const Fused2Params& P, std::string* src, bool compile, double* ms, std::string* log);
 
 // mode: SV_FP64 / SV_FP32 storage
 cudaError_t launch_gate1(void* psi, uint64_t n_elems, int mode, int q, const double* m8,
