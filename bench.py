@@ -235,6 +235,13 @@ def run_b200(args):
     dev = DeviceState(n, pb.PrecisionMode.FP64, device=device)
     dev.zero(0)
     ops = [[gate_to_op(g) for g in layer] for layer in layers]
+    # compile the specialised pass kernels of every layer before the warm-up (sv_jit.cu)
+    from paper_2511_03359_b200.device import jit_prepare, jit_stats, jit_wait
+    t_jit = time.perf_counter()
+    for o in ops:
+        jit_prepare(n, o, args.tile_bits)
+    jit_wait()
+    t_jit = time.perf_counter() - t_jit
     for i in step_layers[:args.warmup]:
         dev.apply_fused(ops[i], args.tile_bits)
     dev.synchronize()
@@ -253,6 +260,7 @@ def run_b200(args):
     nat.pass_timing(False)
     passes, pass_ms, pass_bytes = nat.pass_timing_read()
     launches = nat.launch_count() - launches0
+    jit = jit_stats()
     ms = ev0.elapsed_ms(ev1)
     if dist is not None:
         dist.barrier()
@@ -310,12 +318,19 @@ def run_b200(args):
         pb.run_circuit(pb.build_adder(4, [3, 12])[0], device=device)          # warm the code paths
         t0 = time.perf_counter()
         res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
+        t_first = time.perf_counter() - t0
+        del res
+        jit_wait()                       # the first run queued the adder's pass kernels
+        t0 = time.perf_counter()
+        res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
         t_adder = time.perf_counter() - t0
         kat = all(abs(res.report.qz[q] - 1.0) < 1e-12 for q in regs["R2"])
         adder = {"circuit": "build_adder(16, [47302, 18233])", "n_qubits": 32, "gates": len(circ.gates),
                  "seconds": round(t_adder, 4), "sec_per_gate": round(t_adder / len(circ.gates), 6),
+                 "first_run_seconds": round(t_first, 4),
                  "kat_all_ones_R2": kat, "kernel_launches": res.device_stats.get("kernel_launches"),
-                 "what": "run_circuit wall clock incl. allocation, zero state, fused passes, measure-all"}
+                 "what": "run_circuit wall clock incl. allocation, zero state, fused passes, measure-all "
+                         "(second run: specialised pass kernels compiled; first_run_seconds: cold)"}
         del res
     # byte-encoded benchmark (BASELINE config 5 shape on one GPU): time per gate
     byte = None
@@ -367,11 +382,13 @@ def run_b200(args):
                          "kernel": {0: "k_fused<c64s,12>", 1: "k_fused3<12,4,1>", 2: "k_fused3<11,3,2>",
                                     3: "k_fused3<12,3,1>", 4: "k_fused3<11,3,3>",
                                     5: "k_fused3<10,3,4>", 6: "k_fused3<11,4,3>",
-                                    7: "k_fused3<10,4,6>"}[args.fused],
+                                    7: "k_fused3<10,4,6>"}[args.fused] + (
+                             " as sv_pass (NVRTC-specialised per pass structure)" if jit["jit_launches"] else ""),
                          "launches_timed": passes,
                          "bytes_per_launch": 2 * 16 * 2 ** n},
             "gpu_launches": launches,
             "fused_passes_per_step": round(passes / args.steps, 2),
+            "jit": dict(jit, prepare_seconds=round(t_jit, 2)),
             "clocks": clocks,
         }
         if single:
@@ -395,7 +412,7 @@ def run_b200_multi(args, dist, rank, world, device):
     import paper_2511_03359_b200 as pb
     from paper_2511_03359_b200 import _native as nat
     from paper_2511_03359_b200.distributed import CudaBackend, phys_op
-    from paper_2511_03359_b200.remap import PhysGate, RemapPlanner, Swap
+    from paper_2511_03359_b200.remap import RemapPlanner, Swap, SwapGroup
     from tests.circuits import to_product
     from oracle.ref_builders import OCircuit
 
@@ -413,28 +430,47 @@ def run_b200_multi(args, dist, rank, world, device):
     per_step = [[] for _ in seq]
     pending_swaps = []
     for st in steps:
-        if isinstance(st, Swap):
+        if isinstance(st, (Swap, SwapGroup)):
             pending_swaps.append(st)
         else:
             k = owner[st.ordinal]
             per_step[k] += pending_swaps + [st]
             pending_swaps = []
-    be = CudaBackend(dist, n, pb.PrecisionMode.FP64, device, args.tile_bits)
-
-    def run_step(k):
-        pend = []
+    # each step as launch batches: ("swap", Swap) / ("group", SwapGroup) / ("ops", [sv_op])
+    batches = []
+    for k in range(len(seq)):
+        out, pend = [], []
         for st in per_step[k]:
-            if isinstance(st, Swap):
+            if isinstance(st, (Swap, SwapGroup)):
                 if pend:
-                    be.apply_local(pend)
+                    out.append(("ops", pend))
                     pend = []
-                be.swap(st.global_pos, st.local_pos)
+                out.append(("swap" if isinstance(st, Swap) else "group", st))
             else:
                 op = phys_op(st.gate, st.qubits, n, rank)
                 if op is not None:
                     pend.append(op)
         if pend:
-            be.apply_local(pend)
+            out.append(("ops", pend))
+        batches.append(out)
+    from paper_2511_03359_b200.device import jit_prepare, jit_stats, jit_wait
+    t_jit = time.perf_counter()
+    for out in batches:
+        for kind, item in out:
+            if kind == "ops":
+                jit_prepare(n, item, args.tile_bits)
+    jit_wait()
+    t_jit = time.perf_counter() - t_jit
+    be = CudaBackend(dist, n, pb.PrecisionMode.FP64, device, args.tile_bits)
+
+    def run_step(k):
+        for kind, item in batches[k]:
+            if kind == "ops":
+                be.apply_local(item)
+            elif kind == "swap":
+                be.swap(item.global_pos, item.local_pos)
+            else:
+                be.swap_group(item.pairs)
 
     for k in range(args.warmup):
         run_step(k)
@@ -511,6 +547,55 @@ def run_b200_multi(args, dist, rank, world, device):
                "d2h_bytes_per_step": (d2h1 - d2h0) // args.e2e_steps,
                "what": "run_circuit_distributed(layer + M) per step: allocate + zero + IPC map, remapped "
                        "layer, measure-all, report on every rank; wall clock max over ranks"}
+    jit = jit_stats()
+    # adder circuit (BASELINE config 3, N=32 FP64, strong scaling) through the public API
+    adder = None
+    if args.adder:
+        from paper_2511_03359_b200.distributed import run_circuit_distributed
+        circ, regs = pb.build_adder(16, [47302, 18233])
+        times = []
+        for rep in range(2):
+            dist.barrier()
+            t0 = time.perf_counter()
+            res = run_circuit_distributed(circ, dist, device=device, tile_bits=args.tile_bits)
+            kat = all(abs(res.report.qz[q] - 1.0) < 1e-12 for q in regs["R2"])
+            dist.barrier()
+            times.append(max_over_ranks(dist, time.perf_counter() - t0))
+            stats = res.device_stats
+            res.backend.close()
+            res.backend.dev.free()
+            del res
+            jit_wait()
+        adder = {"circuit": "build_adder(16, [47302, 18233])", "n_qubits": 32, "gates": len(circ.gates),
+                 "seconds": round(times[1], 4), "first_run_seconds": round(times[0], 4),
+                 "sec_per_gate": round(times[1] / len(circ.gates), 6), "kat_all_ones_R2": kat,
+                 "swaps": stats.get("swaps"), "swap_groups": stats.get("swap_groups"),
+                 "scaling": "strong (fixed N=32 over the GPUs)",
+                 "what": "run_circuit_distributed wall clock, max over ranks (second run: compiled kernels)"}
+    byte = None
+    if args.byte_n_multi > 0:
+        from paper_2511_03359_b200.distributed import run_circuit_distributed
+        NB = args.byte_n_multi + (world.bit_length() - 1)
+        bc = pb.build_benchmark(NB)
+        dist.barrier()
+        t0 = time.perf_counter()
+        res = run_circuit_distributed(bc, dist, mode=pb.PrecisionMode.BYTE, device=device)
+        norm_dev = res.report.norm_deviation
+        dist.barrier()
+        t_b = max_over_ranks(dist, time.perf_counter() - t0)
+        st_b = res.device_stats
+        cb = [len(res.codebook.mags), len(res.codebook.thetas)]
+        res.backend.close()
+        res.backend.st.free()
+        del res
+        ng = len(bc.gates) - 1
+        byte = {"circuit": f"build_benchmark({NB}) BYTE", "n_qubits": NB, "gates": ng,
+                "seconds": round(t_b, 3), "sec_per_gate": round(t_b / ng, 5),
+                "effective_GBps_per_gpu": round(ng * 4 * 2 ** args.byte_n_multi / t_b / 1e9, 1),
+                "codebook": cb, "norm_deviation": norm_dev, "swaps": st_b.get("swaps"), "swap_groups": st_b.get("swap_groups"),
+                "byte_passes": st_b.get("byte_passes"),
+                "what": "run_circuit_distributed(mode=BYTE) wall clock incl. allocation, per-gate codebook "
+                        "barrier across ranks, remapped byte-plane swaps, measure-all; max over ranks"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
@@ -528,10 +613,15 @@ def run_b200_multi(args, dist, rank, world, device):
                          "bytes_per_launch": 2 * 16 * 2 ** n},
             "nvlink": nvlink,
             "gpu_launches": launches,
+            "jit": dict(jit, prepare_seconds=round(t_jit, 2)),
             "clocks": clocks,
         }
         if e2e:
             line["e2e"] = e2e
+        if adder:
+            line["adder"] = adder
+        if byte:
+            line["byte_mode"] = byte
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
@@ -554,6 +644,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--adder", type=int, default=1, help="time the N=32 adder circuit (1 GPU line)")
     ap.add_argument("--byte-n", type=int, default=32, help="BYTE benchmark size for the 1 GPU line (0: skip)")
+    ap.add_argument("--byte-n-multi", type=int, default=35,
+                    help="BYTE benchmark amplitudes per GPU (2^n) for N>1 lines: N = n + log2(P), "
+                         "38 qubits on 8 GPUs = BASELINE config 5 (0: skip)")
     ap.add_argument("--single-gate", action="store_true", default=True)
     args = ap.parse_args()
     if args.impl == "reference":

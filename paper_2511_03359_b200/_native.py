@@ -85,6 +85,7 @@ _SIGNATURES = {
     "svk_pair_dot": ([_P, _P, _U64, _I, _D, _P], _I),
     "sv_jit_mode": ([_I], _I),
     "sv_jit_wait": ([], _I),
+    "sv_jit_prepare": ([_I, _P, _I, _I], _I),
     "sv_jit_stats": ([_D], _I),
     "sv_jit_available": ([], _I),
     "sv_jit_probe": ([_P, _I, _I, ctypes.c_char_p, ctypes.c_size_t, _D], _I),

@@ -5,6 +5,7 @@
 // Python layer can re-raise the same exception types with the same messages.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -355,11 +356,13 @@ int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Pa
     return 0;
 }
 
+// prepare != nullptr: plan only and queue the specialised kernels of the v3 passes for
+// compilation (sv_jit_prepare); *prepare counts them.  Nothing is launched.
 int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_ops, int tile_bits,
-               cudaStream_t st) {
+               cudaStream_t st, int* prepare = nullptr) {
     if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "fused passes need FP64 or FP32 storage");
     if (!is_pow2(n_elems)) return fail(SV_EVALUE, "fused pass needs a power-of-two buffer");
-    if ((reinterpret_cast<uintptr_t>(psi) & 31) != 0)
+    if (!prepare && (reinterpret_cast<uintptr_t>(psi) & 31) != 0)
         return fail(SV_EVALUE, "fused pass needs a 32-byte aligned buffer");
     const int n = log2u(n_elems);
     if (tile_bits <= 0) tile_bits = 12;
@@ -387,6 +390,14 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
     PassPlan cur;
     auto flush = [&]() -> int {
         if (cur.ops.empty()) return SV_OK;
+        if (prepare) {
+            static thread_local Fused2Params Pp;
+            if (use_v3 && build_params2(ops, cur, n, g_fused_v2, Pp) == 0 &&
+                (g_seg_limit <= 0 || Pp.n_segs <= g_seg_limit))
+                *prepare += jit_prepare_fused(Pp);
+            cur = PassPlan();
+            return SV_OK;
+        }
         cudaEvent_t ev0 = nullptr, ev1 = nullptr;
         if (g_timing) {
             cudaEventCreate(&ev0);
@@ -432,6 +443,129 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
     return flush();
 }
 
+// FP64 measurement with the register-resident pass (sv_measure3.cu): tiles of 2^K
+// (K = 12: 1 + ceil((n - 12) / 7) passes), segments of 4 register positions cover the
+// cross terms of the pass's new tile qubits.
+int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cross, double* dev_partials,
+                  size_t partial_cap, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static int kenv = -1;
+    if (kenv < 0) {
+        const char* e = std::getenv("SVB200_MEASURE_K");
+        kenv = (e && std::atoi(e) == 11) ? 11 : 12;
+    }
+    const int K = kenv, RB = 4, NT = 1 << (K - RB), bmin = 5;
+    const int grid_cap = measure3_grid(dev, K);
+    const int slots = measure_slots(K, n);
+    double* partials = dev_partials;
+    const size_t need = (size_t)grid_cap * slots;
+    bool owned = false;
+    if (partials == nullptr || partial_cap < need) {
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&partials), need * sizeof(double), st), "measure scratch");
+        owned = true;
+    }
+    std::vector<double> host(need);
+    for (int q = 0; q < n; ++q) { ones[q] = 0; cross[2 * q] = cross[2 * q + 1] = 0; }
+    *norm = 0;
+    std::vector<uint64_t> passes;
+    passes.push_back((1ull << K) - 1ull);
+    for (int q = K; q < n;) {
+        uint64_t t = (1ull << bmin) - 1ull;
+        int c = 0;
+        while (q < n && c < K - bmin) { t |= 1ull << q; ++q; ++c; }
+        for (int f = bmin; popcount64(t) < K; ++f) t |= 1ull << f;
+        passes.push_back(t);
+    }
+    auto swz_h = [](int e) {
+        const int g = (((e >> 3) & 1) * 7) ^ (((e >> 4) & 1) * 3) ^ (((e >> 5) & 1) * 5) ^ (((e >> 6) & 1) * 6);
+        return e ^ g;
+    };
+    uint64_t done = 0;
+    int rc = SV_OK;
+    static thread_local Measure3Params P;
+    for (size_t pi = 0; pi < passes.size() && rc == SV_OK; ++pi) {
+        std::memset(&P, 0, sizeof(P));
+        const uint64_t tmask = passes[pi];
+        P.n = n;
+        P.kbits = K;
+        P.n_tiles = 1ull << (n - K);
+        P.want_ones = pi == 0;
+        int j = 0, o = 0;
+        for (int q = 0; q < n; ++q) {
+            if ((tmask >> q) & 1) P.tq[j++] = (int8_t)q;
+            else P.oq[o++] = (int8_t)q;
+        }
+        P.n_out = o;
+        int b = 0;
+        while (b < K && P.tq[b] == b) ++b;
+        P.b = b;
+        std::vector<int> cpos;
+        for (int i = 0; i < K; ++i)
+            if (!((done >> P.tq[i]) & 1)) cpos.push_back(i);
+        P.n_segs = (int)((cpos.size() + 3) / 4);
+        if (P.n_segs < 1) P.n_segs = 1;
+        for (int sg = 0; sg < P.n_segs; ++sg) {
+            uint32_t regs = 0;
+            int cnt = 0;
+            for (size_t c = 4 * sg; c < cpos.size() && cnt < 4; ++c, ++cnt) {
+                P.seg_reg[sg][cnt] = (uint8_t)cpos[c];
+                P.cross_reg[sg] |= 1u << cnt;
+                regs |= 1u << cpos[c];
+            }
+            for (int pos = K - 1; pos >= 0 && cnt < 4; --pos)     // fill from the top
+                if (!((regs >> pos) & 1)) { P.seg_reg[sg][cnt++] = (uint8_t)pos; regs |= 1u << pos; }
+            // registers ascending by position within the segment keep the slot order simple
+            int t = 0;
+            for (int pos = 0; pos < K; ++pos)
+                if (!((regs >> pos) & 1)) P.seg_thr[sg][t++] = (uint8_t)pos;
+            for (int i = 0; i < 16; ++i) {
+                int e = 0;
+                for (int bit = 0; bit < RB; ++bit)
+                    if ((i >> bit) & 1) e |= 1 << P.seg_reg[sg][bit];
+                P.seg_rsw[sg][i] = (uint16_t)swz_h(e);
+            }
+        }
+        for (int jj = 0; jj < 16; ++jj) {
+            uint64_t off = 0;
+            for (int pos = 0; pos < K; ++pos)
+                if (((jj * NT) >> pos) & 1) off += 1ull << P.tq[pos];
+            P.pf_go[jj] = off;
+        }
+        for (int byte = 0; byte < 4; ++byte)
+            for (int v = 0; v < 256; ++v) {
+                uint64_t d = 0;
+                for (int bit = 0; bit < 8; ++bit) {
+                    const int src = byte * 8 + bit;
+                    if (((v >> bit) & 1) && src < o) d |= 1ull << P.oq[src];
+                }
+                P.base_tab[byte][v] = d;
+            }
+        const int grid = (int)((P.n_tiles < (uint64_t)grid_cap) ? P.n_tiles : grid_cap);
+        cudaError_t e = launch_measure3(psi, P, partials, grid, st);
+        if (e != cudaSuccess) { rc = cuda_fail(e, "measure launch"); break; }
+        e = cudaMemcpyAsync(host.data(), partials, sizeof(double) * grid * slots, cudaMemcpyDeviceToHost, st);
+        count_d2h(sizeof(double) * grid * slots);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) { rc = cuda_fail(e, "measure readback"); break; }
+        for (int g = 0; g < grid; ++g) {
+            const double* row = host.data() + (size_t)g * slots;
+            if (pi == 0) {
+                *norm += row[0];
+                for (int i = 0; i < K; ++i) ones[P.tq[i]] += row[1 + i];
+                for (int jj = 0; jj < o; ++jj) ones[P.oq[jj]] += row[1 + K + jj];
+            }
+            for (int i : cpos) {
+                cross[2 * P.tq[i]] += row[1 + n + 2 * i];
+                cross[2 * P.tq[i] + 1] += row[2 + n + 2 * i];
+            }
+        }
+        for (int i : cpos) done |= 1ull << P.tq[i];
+    }
+    if (owned) cudaFreeAsync(partials, st);
+    return rc;
+}
+
 int measure_impl(const void* psi, uint64_t n_elems, int mode, double* norm, double* ones,
                  double* cross, double* dev_partials, size_t partial_cap, cudaStream_t st) {
     if (!valid_fp_mode(mode) && mode != SV_BYTE) return fail(SV_EVALUE, "unknown storage mode");
@@ -449,6 +583,13 @@ int measure_impl(const void* psi, uint64_t n_elems, int mode, double* norm, doub
         *norm = h[0] * h[0] + h[1] * h[1];
         return SV_OK;
     }
+    static int use3 = -1;
+    if (use3 < 0) {
+        const char* e = std::getenv("SVB200_MEASURE3");
+        use3 = (e && std::atoi(e) == 0) ? 0 : 1;
+    }
+    if (use3 && mode == SV_FP64 && n >= 16 && (reinterpret_cast<uintptr_t>(psi) & 15) == 0)
+        return measure3_impl(psi, n, norm, ones, cross, dev_partials, partial_cap, st);
     const int bmin = k >= 5 ? 5 : k;
     const int grid_cap = measure_grid(dev);
     const int slots_max = measure_slots(k, n);
@@ -786,6 +927,13 @@ int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_
     }
     if (rc) return fail(SV_EVALUE, "NVRTC compile failed: %s", log.c_str());
     return (int)cur.ops.size();
+}
+
+int sv_jit_prepare(int n_qubits, const sv_op* ops, int n_ops, int tile_bits) {
+    if (n_qubits < 1 || n_qubits > 62) return fail(SV_EVALUE, "qubit count %d out of range", n_qubits);
+    int queued = 0;
+    if (int rc = fused_impl(nullptr, 1ull << n_qubits, SV_FP64, ops, n_ops, tile_bits, nullptr, &queued)) return rc;
+    return queued;
 }
 
 int sv_apply_fused(sv_handle h, const sv_op* ops, int n_ops, int tile_bits) {

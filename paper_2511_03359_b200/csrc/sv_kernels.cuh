@@ -65,6 +65,7 @@ struct Fused2Params {
 cudaError_t launch_fused2(void* psi, int mode, const Fused2Params& p, cudaStream_t st);
 // run-time specialised form of the same pass (sv_jit.cu): 0 launched, 1 not ready, < 0 error
 int jit_launch_fused(void* psi, const Fused2Params& p, cudaStream_t st);
+int jit_prepare_fused(const Fused2Params& p);   // queue the compile; 1 if a new kernel was queued
 }  // namespace sv
 #include <string>
 namespace sv {
@@ -95,6 +96,22 @@ struct MeasureParams {
     int8_t oq[64];                      // out-of-tile qubits (ascending), count n - k
 };
 int measure_slots(int k, int n);        // doubles per CTA partial row
+
+// register-resident FP64 measurement pass (sv_measure3.cu); same partial-row layout
+struct Measure3Params {
+    uint64_t n_tiles;
+    int n, kbits, b, want_ones, n_segs, n_out;
+    int8_t tq[12];
+    int8_t oq[64];
+    uint8_t seg_reg[3][4];              // register bit j -> tile position
+    uint8_t seg_thr[3][8];              // thread-id bit j -> tile position
+    uint16_t seg_rsw[3][16];            // swizzled shared-memory offset of register slot i
+    uint32_t cross_reg[3];              // register bits whose cross term the segment produces
+    uint64_t pf_go[16];                 // HBM offset of tile element j * threads (prefetch chunks)
+    uint64_t base_tab[4][256];          // tile index byte -> local-index bits outside the tile
+};
+cudaError_t launch_measure3(const void* psi, const Measure3Params& p, double* partials, int grid, cudaStream_t st);
+int measure3_grid(int device, int kb);
 cudaError_t launch_measure(const void* psi, int mode, const MeasureParams& p, double* partials,
                            int grid, cudaStream_t st);
 int measure_grid(int device);

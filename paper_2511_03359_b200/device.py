@@ -31,6 +31,27 @@ def ops_array(ops) -> ctypes.Array:
     return arr
 
 
+def jit_prepare(n_qubits: int, ops, tile_bits: int = 12) -> int:
+    """Queue the specialised kernels (sv_jit.cu) of the fused passes `ops` will run on
+    2**n_qubits FP64 amplitudes; returns how many new kernels were queued."""
+    if not ops:
+        return 0
+    rc = nat.load(require_device=False).sv_jit_prepare(n_qubits, ops_array(ops), len(ops), tile_bits)
+    nat.check(min(rc, 0))
+    return rc
+
+
+def jit_wait() -> None:
+    nat.check(nat.load(require_device=False).sv_jit_wait())
+
+
+def jit_stats() -> dict:
+    out = np.zeros(6)
+    nat.check(nat.load(require_device=False).sv_jit_stats(nat.dptr(out)))
+    return {"compiled": int(out[0]), "failed": int(out[1]), "jit_launches": int(out[2]),
+            "generic_fallbacks": int(out[3]), "compile_ms": round(float(out[4]), 1), "cached": int(out[5])}
+
+
 class DeviceState:
     def __init__(self, n_qubits: int, mode, device: int = 0):
         lib = nat.load()

@@ -177,3 +177,42 @@ def test_product_never_imports_oracle():
             if f.endswith(".py"):
                 text = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle\b", text, re.M), f
+
+
+def _nvrtc_present():
+    import ctypes.util
+    return any(os.path.exists(p) for p in ("/usr/local/cuda/lib64/libnvrtc.so.12",)) or ctypes.util.find_library("nvrtc")
+
+
+@pytest.mark.skipif(not _nvrtc_present(), reason="libnvrtc not in this image")
+def test_specialised_pass_source_compiles_with_nvrtc(rng):
+    """sv_jit.cu prints a fused pass as CUDA source with every constant folded and
+    compiles it for sm_100a (CPU only: NVRTC needs no device)."""
+    import ctypes
+    from paper_2511_03359_b200.device import ops_array
+    from paper_2511_03359_b200.engine import gate_to_op
+    lib = _native.load(require_device=False)
+    circ = random_circuit(rng, 14, 30, measured=False)
+    ops = [gate_to_op(gt) for gt in to_product(circ).gates]
+    buf = ctypes.create_string_buffer(1 << 20)
+    ms = np.zeros(1)
+    rc = lib.sv_jit_probe(ops_array(ops), len(ops), 14, buf, len(buf), _native.dptr(ms))
+    assert rc >= 1, lib.sv_last_error()
+    src = buf.value.decode()
+    assert 'extern "C" __global__' in src and "sv_pass" in src
+    # no op dispatch left: every op is a template call with literal arguments
+    assert not re.search(r"switch|kind\[", src)
+
+
+@pytest.mark.skipif(not _nvrtc_present(), reason="libnvrtc not in this image")
+def test_jit_prepare_queues_one_kernel_per_pass_structure():
+    from paper_2511_03359_b200.device import jit_prepare, jit_stats, jit_wait
+    from paper_2511_03359_b200.engine import gate_to_op
+    hs = [gate_to_op(g.h(q)) for q in range(16)]
+    before = jit_stats()
+    queued = jit_prepare(16, hs)
+    assert queued >= 1
+    assert jit_prepare(16, hs) == 0            # same structure: cached
+    jit_wait()
+    after = jit_stats()
+    assert after["compiled"] - before["compiled"] == queued and after["failed"] == before["failed"]
