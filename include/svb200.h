@@ -215,6 +215,10 @@ int sv_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
  * register-resident cp.async-pipelined v3 with 1 = 2^12 tiles x 16 amplitudes
  * per thread, 2 = 2^11 tiles x 8 per thread (2 CTAs/SM), 3 = 2^12 tiles x 8
  * per thread (512 threads).  FP32 storage always uses v1. */
+/* state slabs freed by sv_destroy / svb_destroy are cached per device and reused
+ * for the next allocation of the same size; release them to the driver: */
+int sv_release_cached(void);
+int sv_cached_bytes(uint64_t* out);
 /* run-time specialised fused passes (NVRTC, one kernel per pass structure; see
  * paper_2511_03359_b200/csrc/sv_jit.cu): mode 0 off, 1 compile-and-wait,
  * 2 compile in the background and run the generic kernel meanwhile (default).

@@ -74,15 +74,16 @@ int svb_create(int device, int n_qubits, sv_bhandle* out) {
     h->device = device;
     h->n = n_qubits;
     const size_t bytes = (size_t)1 << n_qubits;
+    const size_t pbytes = bytes < 256 ? 256 : bytes;
     auto fail_free = [&](cudaError_t e, const char* what) {
-        for (int b = 0; b < 2; ++b) for (int p = 0; p < 2; ++p) if (h->plane[b][p]) cudaFree(h->plane[b][p]);
+        for (int b = 0; b < 2; ++b) for (int p = 0; p < 2; ++p) if (h->plane[b][p]) sv::slab_free(h->plane[b][p], pbytes);
         if (h->tab) cudaFree(h->tab);
         delete h;
         return capi_cuda_fail(e, what);
     };
     for (int b = 0; b < 2; ++b)
         for (int p = 0; p < 2; ++p) {
-            cudaError_t e = cudaMalloc(&h->plane[b][p], bytes < 256 ? 256 : bytes);
+            cudaError_t e = sv::slab_alloc(reinterpret_cast<void**>(&h->plane[b][p]), pbytes);
             if (e != cudaSuccess) return fail_free(e, "BYTE plane allocation");
         }
     cudaError_t e = cudaMalloc(&h->tab, sizeof(ByteTables));
@@ -108,7 +109,8 @@ int svb_destroy(sv_bhandle h) {
     if (!h) return SV_OK;
     Guard gd(h->device);
     cudaStreamSynchronize(h->stream);
-    for (int b = 0; b < 2; ++b) for (int p = 0; p < 2; ++p) cudaFree(h->plane[b][p]);
+    const size_t pbytes = ((size_t)1 << h->n) < 256 ? 256 : ((size_t)1 << h->n);
+    for (int b = 0; b < 2; ++b) for (int p = 0; p < 2; ++p) sv::slab_free(h->plane[b][p], pbytes);
     cudaFree(h->tab);
     cudaFree(h->hcand.mag); cudaFree(h->hcand.ph); cudaFree(h->hcand.unsure_idx); cudaFree(h->hcand.unsure_val);
     cudaFree(h->cand);

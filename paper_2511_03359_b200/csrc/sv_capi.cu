@@ -688,6 +688,7 @@ struct sv_state {
     int n;
     int mode;
     void* ptr;
+    size_t bytes;
     cudaStream_t stream;
     double* partials;
     size_t partial_cap;
@@ -826,14 +827,15 @@ int sv_create(int device, int n_qubits, int mode, sv_handle* out) {
     h->partials = nullptr;
     h->partial_cap = 0;
     const size_t bytes = (size_t)elem_bytes(mode) << n_qubits;
-    cudaError_t e = cudaMalloc(&h->ptr, bytes < 256 ? 256 : bytes);
+    h->bytes = bytes < 256 ? 256 : bytes;
+    cudaError_t e = slab_alloc(&h->ptr, h->bytes);
     if (e != cudaSuccess) {
         delete h;
         return cuda_fail(e, "state allocation");
     }
     e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
-        cudaFree(h->ptr);
+        slab_free(h->ptr, h->bytes);
         delete h;
         return cuda_fail(e, "stream creation");
     }
@@ -850,7 +852,7 @@ int sv_destroy(sv_handle h) {
     DeviceGuard g(h->device);
     cudaStreamSynchronize(h->stream);
     if (h->partials) cudaFree(h->partials);
-    cudaFree(h->ptr);
+    slab_free(h->ptr, h->bytes);
     cudaStreamDestroy(h->stream);
     delete h;
     return SV_OK;

@@ -117,6 +117,9 @@ cudaError_t launch_measure(const void* psi, int mode, const MeasureParams& p, do
 int measure_grid(int device);
 
 int sm_count(int device);
+// caching state-slab allocator (sv_slab.cu): same-size reuse per device
+cudaError_t slab_alloc(void** p, size_t bytes);
+void slab_free(void* p, size_t bytes);
 cudaError_t launch_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l, int c, cudaStream_t st);
 cudaError_t launch_swap_group(void* own, void* peer, uint64_t t0, uint64_t n, int mode, uint64_t vmask,
                               uint64_t own_pat, uint64_t peer_pat, cudaStream_t st);

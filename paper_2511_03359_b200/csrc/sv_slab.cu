@@ -1,0 +1,117 @@
+// Caching allocator for state slabs (host side).
+//
+// run_circuit allocates a 2^N state per call; at N = 33 that is a 128 GiB
+// cudaMalloc + cudaFree per circuit (tens of ms of page-table work, and a
+// device-wide synchronisation in cudaFree).  Freed slabs of >= 1 MiB are kept
+// per device and handed back to the next request of the same size; a failed
+// cudaMalloc releases the cached slabs of that device and retries, and
+// sv_release_cached() returns everything to the driver.  Callers synchronise
+// their stream before freeing (sv_destroy / svb_destroy), so a cached slab is
+// idle when it is reused.
+#include <mutex>
+#include <vector>
+
+#include "sv_common.cuh"
+#include "sv_kernels.cuh"
+#include "svb200.h"
+
+namespace sv {
+
+namespace {
+struct Slab {
+    int device;
+    size_t bytes;
+    void* ptr;
+};
+std::mutex& slab_mu() {
+    static std::mutex* m = new std::mutex;
+    return *m;
+}
+std::vector<Slab>& slabs() {
+    static std::vector<Slab>* v = new std::vector<Slab>;
+    return *v;
+}
+constexpr size_t kMinCached = 1ull << 20;
+
+void release_device(int device) {
+    std::vector<Slab> drop;
+    {
+        std::lock_guard<std::mutex> lk(slab_mu());
+        auto& v = slabs();
+        for (size_t i = 0; i < v.size();) {
+            if (device < 0 || v[i].device == device) {
+                drop.push_back(v[i]);
+                v[i] = v.back();
+                v.pop_back();
+            } else {
+                ++i;
+            }
+        }
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (const Slab& s : drop) {
+        cudaSetDevice(s.device);
+        cudaFree(s.ptr);
+    }
+    cudaSetDevice(cur);
+}
+}  // namespace
+
+cudaError_t slab_alloc(void** p, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (bytes >= kMinCached) {
+        std::lock_guard<std::mutex> lk(slab_mu());
+        auto& v = slabs();
+        for (size_t i = 0; i < v.size(); ++i)
+            if (v[i].device == dev && v[i].bytes == bytes) {
+                *p = v[i].ptr;
+                v[i] = v.back();
+                v.pop_back();
+                return cudaSuccess;
+            }
+    }
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        release_device(dev);
+        e = cudaMalloc(p, bytes);
+    }
+    return e;
+}
+
+void slab_free(void* p, size_t bytes) {
+    if (!p) return;
+    if (bytes < kMinCached) {
+        cudaFree(p);
+        return;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(slab_mu());
+    slabs().push_back({dev, bytes, p});
+}
+
+size_t slab_cached_bytes() {
+    std::lock_guard<std::mutex> lk(slab_mu());
+    size_t t = 0;
+    for (const Slab& s : slabs()) t += s.bytes;
+    return t;
+}
+
+}  // namespace sv
+
+extern "C" {
+
+int sv_release_cached(void) {
+    sv::release_device(-1);
+    return SV_OK;
+}
+
+int sv_cached_bytes(uint64_t* out) {
+    *out = sv::slab_cached_bytes();
+    return SV_OK;
+}
+
+}  // extern "C"

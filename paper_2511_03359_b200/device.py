@@ -41,6 +41,15 @@ def jit_prepare(n_qubits: int, ops, tile_bits: int = 12) -> int:
     return rc
 
 
+def release_cached_memory() -> int:
+    """Return the cached state slabs (sv_slab.cu) to the driver; returns the bytes released."""
+    lib = nat.load(require_device=False)
+    before = ctypes.c_uint64()
+    nat.check(lib.sv_cached_bytes(ctypes.byref(before)))
+    nat.check(lib.sv_release_cached())
+    return int(before.value)
+
+
 def jit_wait() -> None:
     nat.check(nat.load(require_device=False).sv_jit_wait())
 

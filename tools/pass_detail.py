@@ -13,7 +13,7 @@ from oracle.ref_builders import OCircuit
 import bench
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 30
-only = tuple(int(x) for x in sys.argv[2].split(",")) if len(sys.argv) > 2 else None   # "layer,pass"
+only = tuple(int(x) for x in sys.argv[2].split(",")) if len(sys.argv) > 2 and sys.argv[2] != "all" else None   # "layer,pass"
 K, RB = 11, 4
 
 
@@ -52,11 +52,15 @@ def segments(ops):
     return segs
 
 
-layers_o = bench.workload_layers(n, 4)
+if len(sys.argv) > 3 and sys.argv[3] == "adder":
+    w = n // 2
+    circ, _ = pb.build_adder(w, [47302 % (1 << w), 18233 % (1 << w)])
+    layers_p = [tuple(g for g in circ.gates if g.kind != "M")]
+else:
+    layers_p = [to_product(OCircuit(n, tuple(lo))).gates for lo in bench.workload_layers(n, 4)]
 dev = DeviceState(n, pb.PrecisionMode.FP64)
 dev.zero(0)
-for li, lo in enumerate(layers_o):
-    gates = to_product(OCircuit(n, tuple(lo))).gates
+for li, gates in enumerate(layers_p):
     for pi, ops in enumerate(split([gate_to_op(g) for g in gates])):
         if only is not None and (li, pi) != only:
             continue
