@@ -369,7 +369,8 @@ struct Emitter {
 
     // (magnitude index | phase index << 8) of a produced value; candidate and
     // uncertain-phase bookkeeping as a side effect
-    __device__ __forceinline__ unsigned code(uint64_t idx, cplx v, ThreadCache& tc) const {
+    __device__ __forceinline__ unsigned code(uint64_t idx, cplx v, ThreadCache& tc, bool* sure = nullptr) const {
+        if (sure) *sure = true;
         if (v.re == 0.0 && v.im == 0.0) return 0u;   // r == 0: indices (0, 0), always representable
         // structured states repeat values: reuse the last certain code (candidates of an
         // identical value were already recorded)
@@ -420,6 +421,7 @@ struct Emitter {
         if (write && unsure && mi != 0) unsure_push(idx, v);
         const unsigned result = (unsigned)mi | ((unsigned)pi << 8);
         if (!unsure) { tc.cre = v.re; tc.cim = v.im; tc.ccode = result; }
+        if (sure) *sure = !unsure;
         if (!collect) return result;
         if (g.want_mag && mag_rep == 0 && !(v.re == tc.mre && v.im == tc.mim)) {
             if (!have_r) r = exact_abs(v);
@@ -444,6 +446,45 @@ struct Emitter {
         return result;
     }
 };
+
+// ---- per-CTA memo of input codes -> output codes -------------------------------------
+// Within one pass the tables are fixed, so the output codes of a work item are a pure
+// function of its input codes: (m0, p0, m1, p1) -> (code0, code1) for a 1Q pair,
+// (m, p) -> code for a diagonal factor.  Structured states repeat a handful of code
+// tuples, so most items are one shared-memory probe instead of decode + gate +
+// canonicalise + table search.  An entry is key << 32 | value in one 64-bit word,
+// published with a single CAS; only results without an uncertain phase are stored
+// (uncertain amplitudes must reach the host per index), and candidate collection
+// already happened when the tuple was first computed in this CTA.
+constexpr int MEMO_SLOTS = 2048;
+constexpr unsigned MEMO_NOKEY = 0xffffffffu;          // never stored (all-255 tuple)
+
+__device__ __forceinline__ unsigned memo_hash(unsigned k) {   // Fibonacci hashing, top 11 bits
+    return (k * 0x9e3779b1u) >> (32 - 11);
+}
+static_assert(MEMO_SLOTS == 2048, "memo_hash yields 11 bits");
+__device__ __forceinline__ bool memo_get(const unsigned long long* memo, unsigned key, unsigned* val) {
+    unsigned h = memo_hash(key);
+#pragma unroll
+    for (int probe = 0; probe < 4; ++probe) {
+        const unsigned long long e = memo[h];
+        if (e == ~0ull) return false;
+        if ((unsigned)(e >> 32) == key) { *val = (unsigned)e; return true; }
+        h = (h + 1) & (MEMO_SLOTS - 1);
+    }
+    return false;
+}
+__device__ __forceinline__ void memo_put(unsigned long long* memo, unsigned key, unsigned val) {
+    if (key == MEMO_NOKEY) return;
+    const unsigned long long e = ((unsigned long long)key << 32) | val;
+    unsigned h = memo_hash(key);
+#pragma unroll
+    for (int probe = 0; probe < 4; ++probe) {
+        const unsigned long long prev = atomicCAS(&memo[h], ~0ull, e);
+        if (prev == ~0ull || (unsigned)(prev >> 32) == key) return;
+        h = (h + 1) & (MEMO_SLOTS - 1);
+    }
+}
 
 __device__ __forceinline__ void load8(const uint8_t* p, uint8_t (&b)[8]) {
     const uint2 w = *reinterpret_cast<const uint2*>(p);
@@ -474,6 +515,28 @@ __device__ void load_tables(STables& t, const ByteTables* gt) {
 }
 }  // namespace
 
+// memo miss of a 1Q pair: decode, gate, encode both outputs, remember the tuple
+__device__ __noinline__ unsigned pair_slow(const STables& t, const Emitter& em, ThreadCache& tc,
+                                           unsigned long long* memo, unsigned key, uint64_t i0, uint64_t i1,
+                                           const double* m, bool real) {
+    const cplx a0 = decode(t, key & 255u, (key >> 8) & 255u), a1 = decode(t, (key >> 16) & 255u, key >> 24);
+    cplx r0, r1;
+    if (real) {   // numpy's +-0 imaginary products dropped (exact up to the sign of zero)
+        r0 = {__dadd_rn(__dmul_rn(m[0], a0.re), __dmul_rn(m[2], a1.re)),
+              __dadd_rn(__dmul_rn(m[0], a0.im), __dmul_rn(m[2], a1.im))};
+        r1 = {__dadd_rn(__dmul_rn(m[4], a0.re), __dmul_rn(m[6], a1.re)),
+              __dadd_rn(__dmul_rn(m[4], a0.im), __dmul_rn(m[6], a1.im))};
+    } else {
+        r0 = row2({m[0], m[1]}, {m[2], m[3]}, a0, a1);
+        r1 = row2({m[4], m[5]}, {m[6], m[7]}, a0, a1);
+    }
+    bool s0, s1;
+    const unsigned c0 = em.code(i0, r0, tc, &s0), c1 = em.code(i1, r1, tc, &s1);
+    const unsigned cc = c0 | (c1 << 16);
+    if (s0 && s1) memo_put(memo, key, cc);
+    return cc;
+}
+
 // One BYTE gate pass.  Work items: pairs (1Q), quadruples (2Q) or single
 // amplitudes (DIAG, and COPY for untouched amplitudes of a diagonal gate).
 __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__ mi_in, const uint8_t* __restrict__ pi_in,
@@ -482,9 +545,11 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                                                   ByteCand* cand) {
     __shared__ STables t;
     __shared__ CtaSets sets;
+    extern __shared__ unsigned long long memo[];          // MEMO_SLOTS entries (dynamic)
     load_tables(t, gtab);
     const bool collect = g.collect != 0;
     if (collect) sets_clear(sets);
+    for (int i = threadIdx.x; i < MEMO_SLOTS; i += blockDim.x) memo[i] = ~0ull;
     __syncthreads();
     const bool write = g.scan_only == 0;
     const Emitter em{t, g, sets, cand, mi_out, pi_out, collect, write};
@@ -525,23 +590,21 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                     if (j < 4) v.x |= b << sh; else if (j < 8) v.y |= b << sh;
                     else if (j < 12) v.z |= b << sh; else v.w |= b << sh;
                 };
-#pragma unroll 4
+#pragma unroll
                 for (int j = 0; j < 16; ++j) {
-                    const cplx a0 = decode(t, byte_of(cur[0], j), byte_of(cur[1], j));
-                    const cplx a1 = decode(t, byte_of(cur[2], j), byte_of(cur[3], j));
-                    cplx r0, r1;
-                    if (real) {
-                        r0 = {__dadd_rn(__dmul_rn(m0.re, a0.re), __dmul_rn(m1.re, a1.re)),
-                              __dadd_rn(__dmul_rn(m0.re, a0.im), __dmul_rn(m1.re, a1.im))};
-                        r1 = {__dadd_rn(__dmul_rn(m2.re, a0.re), __dmul_rn(m3.re, a1.re)),
-                              __dadd_rn(__dmul_rn(m2.re, a0.im), __dmul_rn(m3.re, a1.im))};
-                    } else {
-                        r0 = row2(m0, m1, a0, a1);
-                        r1 = row2(m2, m3, a0, a1);
-                    }
-                    const unsigned c0 = em.code(i0 + j, r0, tc), c1 = em.code(i1 + j, r1, tc);
-                    put_byte(out[0], j, c0 & 255u); put_byte(out[1], j, c0 >> 8);
-                    put_byte(out[2], j, c1 & 255u); put_byte(out[3], j, c1 >> 8);
+                    // key = (m0, p0, m1, p1) bytes of pair j; j is a literal after unrolling
+                    const unsigned sh = 8 * (j & 3);
+                    const unsigned w0 = j < 4 ? cur[0].x : (j < 8 ? cur[0].y : (j < 12 ? cur[0].z : cur[0].w));
+                    const unsigned w1 = j < 4 ? cur[1].x : (j < 8 ? cur[1].y : (j < 12 ? cur[1].z : cur[1].w));
+                    const unsigned w2 = j < 4 ? cur[2].x : (j < 8 ? cur[2].y : (j < 12 ? cur[2].z : cur[2].w));
+                    const unsigned w3 = j < 4 ? cur[3].x : (j < 8 ? cur[3].y : (j < 12 ? cur[3].z : cur[3].w));
+                    const unsigned key = ((w0 >> sh) & 255u) | (((w1 >> sh) & 255u) << 8) |
+                                         (((w2 >> sh) & 255u) << 16) | (((w3 >> sh) & 255u) << 24);
+                    unsigned cc;
+                    if (!memo_get(memo, key, &cc))
+                        cc = pair_slow(t, em, tc, memo, key, i0 + j, i1 + j, g.m, real);
+                    put_byte(out[0], j, cc & 255u); put_byte(out[1], j, (cc >> 8) & 255u);
+                    put_byte(out[2], j, (cc >> 16) & 255u); put_byte(out[3], j, cc >> 24);
                 }
                 if (write) {
                     *reinterpret_cast<uint4*>(mi_out + i0) = out[0];
@@ -554,16 +617,29 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
         for (uint64_t w = first; w < n_items; w += step) {
             const uint64_t i0 = insert0(w, g.qa), i1 = i0 | (1ull << g.qa);
             if (g.producer >= 0 && producer_of(g, i0) != g.producer) continue;
-            const cplx a0 = decode(t, mi_in[i0], pi_in[i0]);
-            const cplx a1 = decode(t, mi_in[i1], pi_in[i1]);
-            if (real) {   // numpy's +-0 imaginary products dropped (exact up to the sign of zero)
-                em.emit(i0, {__dadd_rn(__dmul_rn(m0.re, a0.re), __dmul_rn(m1.re, a1.re)),
-                             __dadd_rn(__dmul_rn(m0.re, a0.im), __dmul_rn(m1.re, a1.im))}, tc);
-                em.emit(i1, {__dadd_rn(__dmul_rn(m2.re, a0.re), __dmul_rn(m3.re, a1.re)),
-                             __dadd_rn(__dmul_rn(m2.re, a0.im), __dmul_rn(m3.re, a1.im))}, tc);
-            } else {
-                em.emit(i0, row2(m0, m1, a0, a1), tc);
-                em.emit(i1, row2(m2, m3, a0, a1), tc);
+            const unsigned bm0 = mi_in[i0], bp0 = pi_in[i0], bm1 = mi_in[i1], bp1 = pi_in[i1];
+            const unsigned key = bm0 | (bp0 << 8) | (bm1 << 16) | (bp1 << 24);
+            unsigned cc;
+            if (!memo_get(memo, key, &cc)) {
+                const cplx a0 = decode(t, bm0, bp0), a1 = decode(t, bm1, bp1);
+                cplx r0, r1;
+                if (real) {   // numpy's +-0 imaginary products dropped (exact up to the sign of zero)
+                    r0 = {__dadd_rn(__dmul_rn(m0.re, a0.re), __dmul_rn(m1.re, a1.re)),
+                          __dadd_rn(__dmul_rn(m0.re, a0.im), __dmul_rn(m1.re, a1.im))};
+                    r1 = {__dadd_rn(__dmul_rn(m2.re, a0.re), __dmul_rn(m3.re, a1.re)),
+                          __dadd_rn(__dmul_rn(m2.re, a0.im), __dmul_rn(m3.re, a1.im))};
+                } else {
+                    r0 = row2(m0, m1, a0, a1);
+                    r1 = row2(m2, m3, a0, a1);
+                }
+                bool s0, s1;
+                const unsigned c0 = em.code(i0, r0, tc, &s0), c1 = em.code(i1, r1, tc, &s1);
+                cc = c0 | (c1 << 16);
+                if (s0 && s1) memo_put(memo, key, cc);
+            }
+            if (write) {
+                mi_out[i0] = (uint8_t)(cc & 255u); pi_out[i0] = (uint8_t)((cc >> 8) & 255u);
+                mi_out[i1] = (uint8_t)((cc >> 16) & 255u); pi_out[i1] = (uint8_t)(cc >> 24);
             }
         }
     } else if (g.kind == SV_OP_2Q) {
@@ -601,7 +677,13 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 if (((i + j) & g.mask) != g.mask) continue;
-                const unsigned c = em.code(i + j, cmul(decode(t, bm[j], bp[j]), f), tc);
+                const unsigned key = bm[j] | ((unsigned)bp[j] << 8);
+                unsigned c;
+                if (!memo_get(memo, key, &c)) {
+                    bool sure;
+                    c = em.code(i + j, cmul(decode(t, bm[j], bp[j]), f), tc, &sure);
+                    if (sure) memo_put(memo, key, c);
+                }
                 bm[j] = c & 255;
                 bp[j] = c >> 8;
             }
@@ -767,7 +849,16 @@ static unsigned byte_grid(uint64_t items) {
 cudaError_t launch_byte_gate(const uint8_t* mi_in, const uint8_t* pi_in, uint8_t* mi_out, uint8_t* pi_out,
                              const ByteTables* tab, const ByteGate& g, ByteCand* cand, cudaStream_t st) {
     const uint64_t items = g.kind == SV_OP_1Q ? g.n_elems / 2 : (g.kind == SV_OP_2Q ? g.n_elems / 4 : g.n_elems);
-    k_byte_gate<<<byte_grid(items), NT, 0, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g, cand);
+    static bool configured[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int memo_bytes = MEMO_SLOTS * (int)sizeof(unsigned long long);
+    if (dev < 64 && !configured[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(k_byte_gate, cudaFuncAttributeMaxDynamicSharedMemorySize, memo_bytes);
+        if (e != cudaSuccess) return e;
+        configured[dev] = true;
+    }
+    k_byte_gate<<<byte_grid(items), NT, memo_bytes, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g, cand);
     count_launch();
     return cudaGetLastError();
 }
