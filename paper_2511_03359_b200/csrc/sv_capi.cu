@@ -447,7 +447,7 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
 // (K = 12: 1 + ceil((n - 12) / 7) passes), segments of 4 register positions cover the
 // cross terms of the pass's new tile qubits.
 int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cross, double* dev_partials,
-                  size_t partial_cap, cudaStream_t st) {
+                  size_t partial_cap, cudaStream_t st, bool byte = false) {
     int dev = 0;
     cudaGetDevice(&dev);
     static int kenv = -1;
@@ -455,8 +455,8 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
         const char* e = std::getenv("SVB200_MEASURE_K");
         kenv = (e && std::atoi(e) == 11) ? 11 : 12;
     }
-    const int K = kenv, RB = 4, NT = 1 << (K - RB), bmin = 5;
-    const int grid_cap = measure3_grid(dev, K);
+    const int K = byte ? 12 : kenv, RB = 4, NT = 1 << (K - RB), bmin = 5;
+    const int grid_cap = measure3_grid(dev, K, byte);
     const int slots = measure_slots(K, n);
     double* partials = dev_partials;
     const size_t need = (size_t)grid_cap * slots;
@@ -542,7 +542,8 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
                 P.base_tab[byte][v] = d;
             }
         const int grid = (int)((P.n_tiles < (uint64_t)grid_cap) ? P.n_tiles : grid_cap);
-        cudaError_t e = launch_measure3(psi, P, partials, grid, st);
+        cudaError_t e = byte ? launch_measure3_byte(*static_cast<const MeasureBytes*>(psi), P, partials, grid, st)
+                             : launch_measure3(psi, P, partials, grid, st);
         if (e != cudaSuccess) { rc = cuda_fail(e, "measure launch"); break; }
         e = cudaMemcpyAsync(host.data(), partials, sizeof(double) * grid * slots, cudaMemcpyDeviceToHost, st);
         count_d2h(sizeof(double) * grid * slots);
@@ -590,6 +591,8 @@ int measure_impl(const void* psi, uint64_t n_elems, int mode, double* norm, doub
     }
     if (use3 && mode == SV_FP64 && n >= 16 && (reinterpret_cast<uintptr_t>(psi) & 15) == 0)
         return measure3_impl(psi, n, norm, ones, cross, dev_partials, partial_cap, st);
+    if (use3 && mode == SV_BYTE && n >= 16)
+        return measure3_impl(psi, n, norm, ones, cross, dev_partials, partial_cap, st, true);
     const int bmin = k >= 5 ? 5 : k;
     const int grid_cap = measure_grid(dev);
     const int slots_max = measure_slots(k, n);

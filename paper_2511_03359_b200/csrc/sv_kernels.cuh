@@ -110,8 +110,15 @@ struct Measure3Params {
     uint64_t pf_go[16];                 // HBM offset of tile element j * threads (prefetch chunks)
     uint64_t base_tab[4][256];          // tile index byte -> local-index bits outside the tile
 };
+struct MeasureBytes {                   // BYTE planes + decode tables (dmag, dux, duy)
+    const uint8_t* mi;
+    const uint8_t* pi;
+    const double* tab;
+};
 cudaError_t launch_measure3(const void* psi, const Measure3Params& p, double* partials, int grid, cudaStream_t st);
-int measure3_grid(int device, int kb);
+cudaError_t launch_measure3_byte(const MeasureBytes& b, const Measure3Params& p, double* partials, int grid,
+                                 cudaStream_t st);
+int measure3_grid(int device, int kb, bool byte);
 cudaError_t launch_measure(const void* psi, int mode, const MeasureParams& p, double* partials,
                            int grid, cudaStream_t st);
 int measure_grid(int device);

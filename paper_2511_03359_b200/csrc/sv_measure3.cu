@@ -41,18 +41,27 @@ constexpr int kOutMax = 52;
 
 }  // namespace
 
-template <int KB, int MINB>
+// BYTE = true: the state is two uint8 planes (sv_byte.cu); each thread loads 16
+// consecutive magnitude / phase bytes of the tile (tile positions 0..3 are qubits 0..3),
+// decodes them with the reference's single rounding (codec.py:203-206) into the
+// shared-memory tile, and the next tile's bytes are already in flight in registers.
+template <int KB, int MINB, bool BYTE>
 __global__ void __launch_bounds__(1 << (KB - 4), MINB)
-    k_measure3(const c64s* __restrict__ psi, const __grid_constant__ Measure3Params p, double* __restrict__ partials) {
+    k_measure3(const c64s* __restrict__ psi, const __grid_constant__ Measure3Params p, double* __restrict__ partials,
+               const MeasureBytes bsrc) {
     constexpr int TILE = 1 << KB, R = 16, NT = TILE / R, TB = KB - 4, NW = NT / 32;
+    constexpr int NBUF = BYTE ? 1 : 2;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     cplx* bufs = reinterpret_cast<cplx*>(smem_raw);
-    double* ow = reinterpret_cast<double*>(smem_raw + 2 * sizeof(cplx) * TILE);     // [NW][kOutMax]
+    double* ow = reinterpret_cast<double*>(smem_raw + NBUF * sizeof(cplx) * TILE);  // [NW][kOutMax]
     double* red = ow + NW * kOutMax;                                                 // [NW][1 + 3 KB]
     constexpr int NSL = 1 + 3 * KB;
+    double* dtab = red + NW * NSL;                                                   // BYTE: dmag, dux, duy
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int i = tid; i < NW * kOutMax; i += NT) ow[i] = 0.0;
     for (int i = tid; i < NW * NSL; i += NT) red[i] = 0.0;
+    if constexpr (BYTE)
+        for (int i = tid; i < 768; i += NT) dtab[i] = bsrc.tab[i];
     uint64_t go_tid = 0;
 #pragma unroll
     for (int j = 0; j < TB; ++j)
@@ -77,15 +86,46 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
 #pragma unroll
         for (int j = 0; j < 4; ++j) cr[s][j] = ci[s][j] = 0.0;
 
+    // BYTE: this thread's 16-byte chunk of the tile (elements 16 tid .. 16 tid + 15)
+    uint64_t go_chunk = 0;
+    if constexpr (BYTE) {
+#pragma unroll
+        for (int j = 0; j < KB - 4; ++j)
+            if ((tid >> j) & 1) go_chunk += 1ull << p.tq[4 + j];
+    }
+    uint4 nm = {0, 0, 0, 0}, np = {0, 0, 0, 0};
+    auto fetch_bytes = [&](uint64_t t) {
+        const uint64_t a = tile_base(t) + go_chunk;
+        nm = *reinterpret_cast<const uint4*>(bsrc.mi + a);
+        np = *reinterpret_cast<const uint4*>(bsrc.pi + a);
+    };
+
     uint64_t tile = blockIdx.x;
-    if (tile < p.n_tiles) prefetch(tile, bufs);
-    cp_commit_m();
-    for (int it = 0; tile < p.n_tiles; ++it, tile += gridDim.x) {
-        cplx* S = bufs + (it & 1) * TILE;
-        const uint64_t next = tile + gridDim.x;
-        if (next < p.n_tiles) prefetch(next, bufs + ((it + 1) & 1) * TILE);
+    if constexpr (BYTE) {
+        if (tile < p.n_tiles) fetch_bytes(tile);
+    } else {
+        if (tile < p.n_tiles) prefetch(tile, bufs);
         cp_commit_m();
-        cp_wait_m<1>();
+    }
+    for (int it = 0; tile < p.n_tiles; ++it, tile += gridDim.x) {
+        cplx* S = bufs + (BYTE ? 0 : (it & 1) * TILE);
+        const uint64_t next = tile + gridDim.x;
+        if constexpr (BYTE) {
+            const uint4 cm = nm, cpp = np;
+            if (next < p.n_tiles) fetch_bytes(next);
+            const unsigned wm[4] = {cm.x, cm.y, cm.z, cm.w}, wp[4] = {cpp.x, cpp.y, cpp.z, cpp.w};
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const unsigned mi = (wm[i >> 2] >> (8 * (i & 3))) & 255u, pi = (wp[i >> 2] >> (8 * (i & 3))) & 255u;
+                const double m = dtab[mi];
+                const cplx v = mi == 0 ? cplx{0.0, 0.0} : cplx{__dmul_rn(m, dtab[256 + pi]), __dmul_rn(m, dtab[512 + pi])};
+                S[swz3(16 * tid + i)] = v;
+            }
+        } else {
+            if (next < p.n_tiles) prefetch(next, bufs + ((it + 1) & 1) * TILE);
+            cp_commit_m();
+            cp_wait_m<1>();
+        }
         __syncthreads();
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
@@ -130,9 +170,9 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
                 }
             }
         }
-        __syncthreads();   // S is the prefetch target two tiles from now
+        __syncthreads();   // S is the prefetch target two tiles from now (BYTE: the next tile)
     }
-    cp_wait_m<0>();
+    if constexpr (!BYTE) cp_wait_m<0>();
 
     // ---- deterministic reduction: warp shuffles, then fixed-order sum over warps ----
     // slots: [0] norm, [1 + pos] ones of tile position pos, [1 + KB + 2 pos (+1)] cross of pos
@@ -182,31 +222,38 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
     }
 }
 
-template <int KB, int MINB>
+template <int KB, int MINB, bool BYTE>
 static cudaError_t measure3_cfg(const c64s* psi, const Measure3Params& p, double* partials, int grid,
-                                cudaStream_t st) {
+                                cudaStream_t st, const MeasureBytes& b) {
     constexpr int TILE = 1 << KB, NW = (TILE / 16) / 32;
-    const size_t smem = 2 * sizeof(cplx) * TILE + sizeof(double) * NW * (kOutMax + 1 + 3 * KB);
+    const size_t smem = (BYTE ? 1 : 2) * sizeof(cplx) * TILE + sizeof(double) * NW * (kOutMax + 1 + 3 * KB) +
+                        (BYTE ? sizeof(double) * 768 : 0);
     static bool configured[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k_measure3<KB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_measure3<KB, MINB, BYTE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
-    k_measure3<KB, MINB><<<grid, TILE / 16, smem, st>>>(psi, p, partials);
+    k_measure3<KB, MINB, BYTE><<<grid, TILE / 16, smem, st>>>(psi, p, partials, b);
     count_launch();
     return cudaGetLastError();
 }
 
-int measure3_grid(int device, int kb) { return sm_count(device) * (kb == 12 ? 1 : 3); }
+int measure3_grid(int device, int kb, bool byte) { return sm_count(device) * (byte ? 2 : (kb == 12 ? 1 : 3)); }
 
 cudaError_t launch_measure3(const void* psi, const Measure3Params& p, double* partials, int grid, cudaStream_t st) {
+    const MeasureBytes none{nullptr, nullptr, nullptr};
     const c64s* s = static_cast<const c64s*>(psi);
-    return p.kbits == 12 ? measure3_cfg<12, 1>(s, p, partials, grid, st)
-                         : measure3_cfg<11, 3>(s, p, partials, grid, st);
+    return p.kbits == 12 ? measure3_cfg<12, 1, false>(s, p, partials, grid, st, none)
+                         : measure3_cfg<11, 3, false>(s, p, partials, grid, st, none);
+}
+
+cudaError_t launch_measure3_byte(const MeasureBytes& b, const Measure3Params& p, double* partials, int grid,
+                                 cudaStream_t st) {
+    return measure3_cfg<12, 2, true>(nullptr, p, partials, grid, st, b);
 }
 
 }  // namespace sv
