@@ -407,6 +407,41 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def nccl_probe(dist, rank, world, device, gib: int):
+    """Baseline for the exchange kernels: NCCL send/recv of `gib` GiB between rank pairs
+    (rank ^ 1) through torch.distributed (batch_isend_irecv, both directions at once).
+    Wall clock around 3 synchronised rounds, max over ranks (NCCL runs on its own
+    stream, so CUDA events on ours would not bracket it)."""
+    import torch
+    torch.cuda.set_device(device)
+    grp = dist.new_group(backend="nccl")
+    nbytes = gib << 30
+    send = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+    recv = torch.empty_like(send)
+    partner = rank ^ 1
+
+    def round_trip():
+        ops = [dist.P2POp(dist.isend, send, partner, group=grp), dist.P2POp(dist.irecv, recv, partner, group=grp)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    round_trip()
+    torch.cuda.synchronize()
+    dist.barrier()
+    reps = 3
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        round_trip()
+    torch.cuda.synchronize()
+    t = max_over_ranks(dist, time.perf_counter() - t0)
+    del send, recv
+    torch.cuda.empty_cache()
+    dist.destroy_process_group(grp)
+    gbps = nbytes * reps / t / 1e9
+    return {"what": f"NCCL send/recv {gib} GiB per direction between rank pairs (torch.distributed "
+                    f"batch_isend_irecv), wall clock max over ranks", "GBps_per_direction": round(gbps, 1),
+            "frac_of_770": round(gbps / 770.0, 4)}
+
+
 def run_b200_multi(args, dist, rank, world, device):
     """Weak scaling: 2**n amplitudes per GPU, N = n + log2(P) qubits, remapped NVLink exchanges."""
     import paper_2511_03359_b200 as pb
@@ -521,6 +556,8 @@ def run_b200_multi(args, dist, rank, world, device):
     be.close()
     be.dev.free()
     del be
+    if args.nccl_probe_gib > 0:
+        nvlink["nccl_baseline"] = nccl_probe(dist, rank, world, device, args.nccl_probe_gib)
     # end to end through the public API: run_circuit_distributed(layer + M) per step
     e2e = None
     if args.e2e_steps > 0:
@@ -644,6 +681,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--adder", type=int, default=1, help="time the N=32 adder circuit (1 GPU line)")
     ap.add_argument("--byte-n", type=int, default=32, help="BYTE benchmark size for the 1 GPU line (0: skip)")
+    ap.add_argument("--nccl-probe-gib", type=int, default=4,
+                    help="N>1: NCCL send/recv baseline next to the P2P swap kernel (0: skip)")
     ap.add_argument("--byte-n-multi", type=int, default=35,
                     help="BYTE benchmark amplitudes per GPU (2^n) for N>1 lines: N = n + log2(P), "
                          "38 qubits on 8 GPUs = BASELINE config 5 (0: skip)")

@@ -117,7 +117,8 @@ typedef struct {
     int32_t xkind;         /* 0 none, 1 pairwise 1q, 2 pairwise 2q, 3 quad (engine.py choreography) */
     int32_t qlow_top;      /* pairwise 2q: the local qubit is the top local bit */
     uint64_t xmask_a, xmask_b;
-    int32_t producer;      /* -1 all work items; r: only those reference rank r computes */
+    int32_t producer;      /* -1 all work items; r: only those reference rank r computes;
+                            * -2 all work items, candidates tagged with their reference rank */
     int32_t collect;       /* collect codebook proposals (codec.py:137-152) */
     int32_t want_mag, want_ph;   /* which tables can still change */
     double mag_cut, ph_cut;      /* collect only values below the cut (overflow retry) */
@@ -145,6 +146,9 @@ int svb_gate(sv_bhandle h, const svb_gate_desc* g);
  * 2 = at least one magnitude candidate was seen */
 int svb_candidates(sv_bhandle h, double* mags, uint64_t cap_m, uint64_t* n_m, double* ph4, uint64_t cap_p,
                    uint64_t* n_p, int* flags);
+/* producer rank of every candidate returned by svb_candidates after a pass with
+ * producer == -2 (tagged collection: one pass for all reference ranks) */
+int svb_candidate_tags(sv_bhandle h, int32_t* mag_tags, uint64_t cap_m, int32_t* ph_tags, uint64_t cap_p);
 /* amplitudes whose phase decision was inside the atan2 margin */
 int svb_unsure(sv_bhandle h, uint64_t* idx, double* vals, uint64_t cap, uint64_t* n);
 int svb_reset(sv_bhandle h);

@@ -28,6 +28,7 @@ from .codec import CAPACITY, Codebook
 
 _BIG = 1e308
 _CAP = 1 << 20
+MAX_TAGGED_RANKS = 8          # candidate set regions per CTA (sv_byte.cu CtaSets)
 
 
 class SvbGateDesc(ctypes.Structure):
@@ -139,6 +140,30 @@ class ByteDeviceState:
                                      ctypes.byref(flags)))
         ph = ph[:npp.value]
         return mags[:nm.value].copy(), (ph[:, 0] + 1j * ph[:, 1]), flags.value
+
+    def read_candidate_tags(self, n_mag: int, n_ph: int):
+        """Producer rank of each candidate of the last tagged pass (producer == -2)."""
+        mt = np.empty(max(n_mag, 1), dtype=np.int32)
+        pt = np.empty(max(n_ph, 1), dtype=np.int32)
+        nat.check(nat.load().svb_candidate_tags(self.handle, mt.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                                mt.size, pt.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                                pt.size))
+        return mt[:n_mag], pt[:n_ph]
+
+    def collect_tagged(self, d: "SvbGateDesc", ranks: int):
+        """One pass over every work item with candidates tagged by reference producer rank;
+        returns per-rank [(mags, phase values)] and the uncertain amplitudes, or None when
+        the candidate buffer overflowed (the caller then runs one pass per rank)."""
+        d.producer = -2
+        d.collect = 1
+        self.reset()
+        self.gate_pass(d)
+        mags, ph, flags = self.read_candidates()
+        if flags & 1:
+            return None
+        unsure = self.read_unsure()
+        mt, pt = self.read_candidate_tags(len(mags), len(ph))
+        return [(mags[mt == r], ph[pt == r]) for r in range(ranks)], unsure
 
     def read_unsure(self):
         idx = np.empty(_CAP, dtype=np.uint64)
@@ -342,10 +367,17 @@ class ByteEngineState(ByteDeviceState):
             proposals, unsure = [], []
             ranks = self.layout.rank_count
             d.scan_only = 1 if scan else 0
-            for r in range(ranks):
-                mags, ph, u = self._collect_rank(d, r if ranks > 1 else -1)
-                proposals.append(cb.finalize_proposal(mags, ph))
-                unsure.append(u)
+            tagged = self.collect_tagged(d, ranks) if 1 < ranks <= MAX_TAGGED_RANKS else None
+            if tagged is not None:
+                self.passes += 1
+                per_rank, u = tagged
+                proposals = [cb.finalize_proposal(m, p) for m, p in per_rank]
+                unsure = [u]
+            else:
+                for r in range(ranks):
+                    mags, ph, u = self._collect_rank(d, r if ranks > 1 else -1)
+                    proposals.append(cb.finalize_proposal(mags, ph))
+                    unsure.append(u)
             version = cb.version
             cb.merge(proposals)
             grew = cb.version != version

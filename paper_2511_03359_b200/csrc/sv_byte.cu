@@ -175,6 +175,8 @@ struct CtaSets {
     int ph_lock[PH_SLOTS];
     int mag_count, ph_count;
     int full;                       // a set ran out of slots: flush at the next barrier
+    int mag_rs, ph_rs;              // slots per producer region (tagged collection: one region
+                                    // per reference rank, so each rank's proposal stays separate)
 };
 
 __device__ __forceinline__ unsigned hash64(unsigned long long k) {
@@ -182,19 +184,24 @@ __device__ __forceinline__ unsigned hash64(unsigned long long k) {
     return (unsigned)k;
 }
 
-__device__ void global_mag(ByteCand* out, double r) {
+__device__ void global_mag(ByteCand* out, double r, int prod) {
     const unsigned long long slot = atomicAdd(&out->n_mag, 1ull);
-    if (slot < out->cap_mag) out->mag[slot] = r;
-    else out->overflow = 1;
+    if (slot < out->cap_mag) {
+        out->mag[slot] = r;
+        out->mag_tag[slot] = prod;
+    } else {
+        out->overflow = 1;
+    }
 }
 
-__device__ void global_phase(ByteCand* out, const Polar& p, cplx v) {
+__device__ void global_phase(ByteCand* out, const Polar& p, cplx v, int prod) {
     const unsigned long long slot = atomicAdd(&out->n_ph, 1ull);
     if (slot < out->cap_ph) {
         out->ph[4 * slot + 0] = v.re;
         out->ph[4 * slot + 1] = v.im;
         out->ph[4 * slot + 2] = p.ux;
         out->ph[4 * slot + 3] = p.uy;
+        out->ph_tag[slot] = prod;
     } else {
         out->overflow = 1;
     }
@@ -202,30 +209,33 @@ __device__ void global_phase(ByteCand* out, const Polar& p, cplx v) {
 
 // shared-memory set first; a full set spills straight to the global buffer
 // (duplicates there are harmless: the host takes unique values / first per theta)
-__device__ void insert_mag(CtaSets& s, ByteCand* out, double r) {
+__device__ void insert_mag(CtaSets& s, ByteCand* out, double r, int prod) {
     const unsigned long long key = (unsigned long long)__double_as_longlong(r);
-    unsigned h = hash64(key) & (MAG_SLOTS - 1);
+    const unsigned rs = (unsigned)s.mag_rs, base = (unsigned)prod * rs;
+    unsigned h = hash64(key) & (rs - 1);
     for (int probe = 0; probe < 64; ++probe) {
-        const unsigned long long cur = s.mag_key[h];
+        const unsigned long long cur = s.mag_key[base + h];
         if (cur == key) return;
         if (cur == EMPTY) {
-            const unsigned long long prev = atomicCAS(&s.mag_key[h], EMPTY, key);
+            const unsigned long long prev = atomicCAS(&s.mag_key[base + h], EMPTY, key);
             if (prev == EMPTY) { atomicAdd(&s.mag_count, 1); return; }
             if (prev == key) return;
         }
-        h = (h + 1) & (MAG_SLOTS - 1);
+        h = (h + 1) & (rs - 1);
     }
-    global_mag(out, r);
+    global_mag(out, r, prod);
 }
 
 __device__ __forceinline__ bool lex_less(double ax, double ay, double bx, double by) {
     return ax < bx || (ax == bx && ay < by);
 }
 
-__device__ void insert_phase(CtaSets& s, ByteCand* out, const Polar& p, cplx v) {
+__device__ void insert_phase(CtaSets& s, ByteCand* out, const Polar& p, cplx v, int prod) {
     const unsigned long long key = (unsigned long long)__double_as_longlong(p.th);
-    unsigned h = hash64(key ^ 0x9e3779b97f4a7c15ull) & (PH_SLOTS - 1);
+    const unsigned rs = (unsigned)s.ph_rs, base = (unsigned)prod * rs;
+    unsigned h0 = hash64(key ^ 0x9e3779b97f4a7c15ull) & (rs - 1);
     for (int probe = 0; probe < 64; ++probe) {
+        const unsigned h = base + h0;
         unsigned long long cur = s.ph_key[h];
         if (cur == EMPTY) {
             cur = atomicCAS(&s.ph_key[h], EMPTY, key);
@@ -243,25 +253,32 @@ __device__ void insert_phase(CtaSets& s, ByteCand* out, const Polar& p, cplx v) 
             atomicExch(&s.ph_lock[h], 0);
             return;
         }
-        h = (h + 1) & (PH_SLOTS - 1);
+        h0 = (h0 + 1) & (rs - 1);
     }
-    global_phase(out, p, v);
+    global_phase(out, p, v, prod);
 }
 
-__device__ void sets_clear(CtaSets& s) {
+__device__ void sets_clear(CtaSets& s, int regions) {
     for (int i = threadIdx.x; i < MAG_SLOTS; i += blockDim.x) s.mag_key[i] = EMPTY;
     for (int i = threadIdx.x; i < PH_SLOTS; i += blockDim.x) {
         s.ph_key[i] = EMPTY; s.ph_ux[i] = 1e300; s.ph_uy[i] = 1e300; s.ph_lock[i] = 0;
     }
-    if (threadIdx.x == 0) { s.mag_count = 0; s.ph_count = 0; s.full = 0; }
+    if (threadIdx.x == 0) {
+        s.mag_count = 0; s.ph_count = 0; s.full = 0;
+        s.mag_rs = MAG_SLOTS / regions; s.ph_rs = PH_SLOTS / regions;
+    }
 }
 
 __device__ void sets_flush(CtaSets& s, ByteCand* out) {
     for (int i = threadIdx.x; i < MAG_SLOTS; i += blockDim.x) {
         if (s.mag_key[i] == EMPTY) continue;
         const unsigned long long slot = atomicAdd(&out->n_mag, 1ull);
-        if (slot < out->cap_mag) out->mag[slot] = __longlong_as_double((long long)s.mag_key[i]);
-        else out->overflow = 1;
+        if (slot < out->cap_mag) {
+            out->mag[slot] = __longlong_as_double((long long)s.mag_key[i]);
+            out->mag_tag[slot] = i / s.mag_rs;
+        } else {
+            out->overflow = 1;
+        }
     }
     for (int i = threadIdx.x; i < PH_SLOTS; i += blockDim.x) {
         if (s.ph_key[i] == EMPTY) continue;
@@ -271,6 +288,7 @@ __device__ void sets_flush(CtaSets& s, ByteCand* out) {
             out->ph[4 * slot + 1] = s.ph_im[i];
             out->ph[4 * slot + 2] = s.ph_ux[i];
             out->ph[4 * slot + 3] = s.ph_uy[i];
+            out->ph_tag[slot] = i / s.ph_rs;
         } else {
             out->overflow = 1;
         }
@@ -339,6 +357,7 @@ struct ThreadCache {                  // last values seen by this thread
     double mre, mim, pre, pim;        // last magnitude / phase candidate
     double cre, cim;                  // last encoded value ...
     unsigned ccode;                   // ... and its (certain) code
+    int prod;                         // producer region the remembered candidates belong to
 };
 
 struct Emitter {
@@ -362,15 +381,20 @@ struct Emitter {
         }
     }
 
-    __device__ __forceinline__ void emit(uint64_t idx, cplx v, ThreadCache& tc) const {
-        const unsigned c = code(idx, v, tc);
+    __device__ __forceinline__ void emit(uint64_t idx, cplx v, ThreadCache& tc, int prod = 0) const {
+        const unsigned c = code(idx, v, tc, nullptr, prod);
         if (write) { mo[idx] = (uint8_t)(c & 255); po[idx] = (uint8_t)(c >> 8); }
     }
 
     // (magnitude index | phase index << 8) of a produced value; candidate and
     // uncertain-phase bookkeeping as a side effect
-    __device__ __forceinline__ unsigned code(uint64_t idx, cplx v, ThreadCache& tc, bool* sure = nullptr) const {
+    __device__ __forceinline__ unsigned code(uint64_t idx, cplx v, ThreadCache& tc, bool* sure = nullptr,
+                                             int prod = 0) const {
         if (sure) *sure = true;
+        if (collect && prod != tc.prod) {   // candidates are remembered per producer region
+            tc.mre = tc.mim = tc.pre = tc.pim = tc.cre = tc.cim = NAN;
+            tc.prod = prod;
+        }
         if (v.re == 0.0 && v.im == 0.0) return 0u;   // r == 0: indices (0, 0), always representable
         // structured states repeat values: reuse the last certain code (candidates of an
         // identical value were already recorded)
@@ -427,7 +451,7 @@ struct Emitter {
             if (!have_r) r = exact_abs(v);
             if (r < g.mag_cut) {
                 cand->any_mag = 1;
-                insert_mag(sets, cand, r);
+                insert_mag(sets, cand, r, prod);
             }
             tc.mre = v.re; tc.mim = v.im;
         }
@@ -439,7 +463,7 @@ struct Emitter {
                 p.r = r; p.th = th; p.th_exact = th_exact; p.wrap_unsure = wrap_unsure;
                 p.ux = __dadd_rn(__ddiv_rn(v.re, r), 0.0);
                 p.uy = __dadd_rn(__ddiv_rn(v.im, r), 0.0);
-                insert_phase(sets, cand, p, v);
+                insert_phase(sets, cand, p, v, prod);
             }
             tc.pre = v.re; tc.pim = v.im;
         }
@@ -463,28 +487,41 @@ __device__ __forceinline__ unsigned memo_hash(unsigned k) {   // Fibonacci hashi
     return (k * 0x9e3779b1u) >> (32 - 11);
 }
 static_assert(MEMO_SLOTS == 2048, "memo_hash yields 11 bits");
-__device__ __forceinline__ bool memo_get(const unsigned long long* memo, unsigned key, unsigned* val) {
+// returns the slot of the entry, -1 if absent
+__device__ __forceinline__ int memo_get(const unsigned long long* memo, unsigned key, unsigned* val) {
     unsigned h = memo_hash(key);
 #pragma unroll
     for (int probe = 0; probe < 4; ++probe) {
         const unsigned long long e = memo[h];
-        if (e == ~0ull) return false;
-        if ((unsigned)(e >> 32) == key) { *val = (unsigned)e; return true; }
+        if (e == ~0ull) return -1;
+        if ((unsigned)(e >> 32) == key) { *val = (unsigned)e; return (int)h; }
         h = (h + 1) & (MEMO_SLOTS - 1);
     }
-    return false;
+    return -1;
 }
-__device__ __forceinline__ void memo_put(unsigned long long* memo, unsigned key, unsigned val) {
-    if (key == MEMO_NOKEY) return;
+__device__ __forceinline__ int memo_put(unsigned long long* memo, unsigned key, unsigned val) {
+    if (key == MEMO_NOKEY) return -1;
     const unsigned long long e = ((unsigned long long)key << 32) | val;
     unsigned h = memo_hash(key);
 #pragma unroll
     for (int probe = 0; probe < 4; ++probe) {
         const unsigned long long prev = atomicCAS(&memo[h], ~0ull, e);
-        if (prev == ~0ull || (unsigned)(prev >> 32) == key) return;
+        if (prev == ~0ull || (unsigned)(prev >> 32) == key) return (int)h;
         h = (h + 1) & (MEMO_SLOTS - 1);
     }
+    return -1;
 }
+// tagged collection: which producer regions already recorded the candidates of a
+// memo entry (a hit for a new producer still takes the slow path once)
+struct MemoTags {
+    unsigned* seen;         // MEMO_SLOTS bit masks, nullptr when not tagging
+    __device__ __forceinline__ bool fresh(int slot, int prod) const {
+        return seen && !((seen[slot] >> prod) & 1u);
+    }
+    __device__ __forceinline__ void mark(int slot, int prod) const {
+        if (seen && slot >= 0) atomicOr(&seen[slot], 1u << prod);
+    }
+};
 
 __device__ __forceinline__ void load8(const uint8_t* p, uint8_t (&b)[8]) {
     const uint2 w = *reinterpret_cast<const uint2*>(p);
@@ -517,8 +554,8 @@ __device__ void load_tables(STables& t, const ByteTables* gt) {
 
 // memo miss of a 1Q pair: decode, gate, encode both outputs, remember the tuple
 __device__ __noinline__ unsigned pair_slow(const STables& t, const Emitter& em, ThreadCache& tc,
-                                           unsigned long long* memo, unsigned key, uint64_t i0, uint64_t i1,
-                                           const double* m, bool real) {
+                                           unsigned long long* memo, const MemoTags& mt, unsigned key,
+                                           uint64_t i0, uint64_t i1, const double* m, bool real, int prod) {
     const cplx a0 = decode(t, key & 255u, (key >> 8) & 255u), a1 = decode(t, (key >> 16) & 255u, key >> 24);
     cplx r0, r1;
     if (real) {   // numpy's +-0 imaginary products dropped (exact up to the sign of zero)
@@ -531,9 +568,9 @@ __device__ __noinline__ unsigned pair_slow(const STables& t, const Emitter& em, 
         r1 = row2({m[4], m[5]}, {m[6], m[7]}, a0, a1);
     }
     bool s0, s1;
-    const unsigned c0 = em.code(i0, r0, tc, &s0), c1 = em.code(i1, r1, tc, &s1);
+    const unsigned c0 = em.code(i0, r0, tc, &s0, prod), c1 = em.code(i1, r1, tc, &s1, prod);
     const unsigned cc = c0 | (c1 << 16);
-    if (s0 && s1) memo_put(memo, key, cc);
+    if (s0 && s1) mt.mark(memo_put(memo, key, cc), prod);
     return cc;
 }
 
@@ -545,15 +582,20 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                                                   ByteCand* cand) {
     __shared__ STables t;
     __shared__ CtaSets sets;
-    extern __shared__ unsigned long long memo[];          // MEMO_SLOTS entries (dynamic)
+    extern __shared__ unsigned long long memo[];          // MEMO_SLOTS entries + MEMO_SLOTS tag masks
+    unsigned* memo_seen = reinterpret_cast<unsigned*>(memo + MEMO_SLOTS);
     load_tables(t, gtab);
     const bool collect = g.collect != 0;
-    if (collect) sets_clear(sets);
-    for (int i = threadIdx.x; i < MEMO_SLOTS; i += blockDim.x) memo[i] = ~0ull;
+    // producer == -2: every work item, candidates tagged with the item's reference producer
+    // rank (one set region per rank) -- one pass instead of one pass per rank
+    const bool tagged = g.producer == -2;
+    if (collect) sets_clear(sets, tagged ? (1 << g.rank_bits) : 1);
+    for (int i = threadIdx.x; i < MEMO_SLOTS; i += blockDim.x) { memo[i] = ~0ull; memo_seen[i] = 0u; }
     __syncthreads();
     const bool write = g.scan_only == 0;
     const Emitter em{t, g, sets, cand, mi_out, pi_out, collect, write};
-    ThreadCache tc{NAN, NAN, NAN, NAN, NAN, NAN, 0u};
+    const MemoTags mt{(tagged && collect) ? memo_seen : nullptr};
+    ThreadCache tc{NAN, NAN, NAN, NAN, NAN, NAN, 0u, 0};
     const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g.kind == SV_OP_1Q) {
@@ -580,6 +622,7 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                 if (w + step < n_chunks) fetch(w + step, nxt);
                 const uint64_t i0 = insert0(w << 4, g.qa), i1 = i0 + off;
                 if (g.producer >= 0 && producer_of(g, i0) != g.producer) continue;
+                const int prod = tagged ? producer_of(g, i0) : 0;
                 uint4 out[4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
                 auto byte_of = [](const uint4& v, int j) -> unsigned {
                     const unsigned w = j < 4 ? v.x : (j < 8 ? v.y : (j < 12 ? v.z : v.w));
@@ -601,8 +644,9 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                     const unsigned key = ((w0 >> sh) & 255u) | (((w1 >> sh) & 255u) << 8) |
                                          (((w2 >> sh) & 255u) << 16) | (((w3 >> sh) & 255u) << 24);
                     unsigned cc;
-                    if (!memo_get(memo, key, &cc))
-                        cc = pair_slow(t, em, tc, memo, key, i0 + j, i1 + j, g.m, real);
+                    const int slot = memo_get(memo, key, &cc);
+                    if (slot < 0 || mt.fresh(slot, prod))
+                        cc = pair_slow(t, em, tc, memo, mt, key, i0 + j, i1 + j, g.m, real, prod);
                     put_byte(out[0], j, cc & 255u); put_byte(out[1], j, (cc >> 8) & 255u);
                     put_byte(out[2], j, (cc >> 16) & 255u); put_byte(out[3], j, cc >> 24);
                 }
@@ -617,10 +661,12 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
         for (uint64_t w = first; w < n_items; w += step) {
             const uint64_t i0 = insert0(w, g.qa), i1 = i0 | (1ull << g.qa);
             if (g.producer >= 0 && producer_of(g, i0) != g.producer) continue;
+            const int prod = tagged ? producer_of(g, i0) : 0;
             const unsigned bm0 = mi_in[i0], bp0 = pi_in[i0], bm1 = mi_in[i1], bp1 = pi_in[i1];
             const unsigned key = bm0 | (bp0 << 8) | (bm1 << 16) | (bp1 << 24);
             unsigned cc;
-            if (!memo_get(memo, key, &cc)) {
+            const int slot = memo_get(memo, key, &cc);
+            if (slot < 0 || mt.fresh(slot, prod)) {
                 const cplx a0 = decode(t, bm0, bp0), a1 = decode(t, bm1, bp1);
                 cplx r0, r1;
                 if (real) {   // numpy's +-0 imaginary products dropped (exact up to the sign of zero)
@@ -633,9 +679,9 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                     r1 = row2(m2, m3, a0, a1);
                 }
                 bool s0, s1;
-                const unsigned c0 = em.code(i0, r0, tc, &s0), c1 = em.code(i1, r1, tc, &s1);
+                const unsigned c0 = em.code(i0, r0, tc, &s0, prod), c1 = em.code(i1, r1, tc, &s1, prod);
                 cc = c0 | (c1 << 16);
-                if (s0 && s1) memo_put(memo, key, cc);
+                if (s0 && s1) mt.mark(memo_put(memo, key, cc), prod);
             }
             if (write) {
                 mi_out[i0] = (uint8_t)(cc & 255u); pi_out[i0] = (uint8_t)((cc >> 8) & 255u);
@@ -650,20 +696,23 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
         for (uint64_t w = first; w < n_items; w += step) {
             const uint64_t e = insert0(insert0(w, lo), hi);
             if (g.producer >= 0 && producer_of(g, e) != g.producer) continue;
+            const int prod = tagged ? producer_of(g, e) : 0;
             const uint64_t idx[4] = {e, e | (1ull << g.qa), e | (1ull << g.qb), e | (1ull << g.qa) | (1ull << g.qb)};
             cplx a[4];
             for (int c = 0; c < 4; ++c) a[c] = decode(t, mi_in[idx[c]], pi_in[idx[c]]);
             cplx o[4];
             for (int r = 0; r < 4; ++r) o[r] = row4(&m[4 * r], a[0], a[1], a[2], a[3]);
-            for (int r = 0; r < 4; ++r) em.emit(idx[r], o[r], tc);
+            for (int r = 0; r < 4; ++r) em.emit(idx[r], o[r], tc, prod);
         }
     } else if (g.n_elems >= 16) {   // DIAG, 8 amplitudes per work item
         const cplx f = {g.m[0], g.m[1]};
         const uint64_t n_chunks = g.n_elems >> 3;
         for (uint64_t w = first; w < n_chunks; w += step) {
             const uint64_t i = w << 3;
-            const bool own = g.producer < 0 || (int)(i >> g.n_local) == g.producer;
-            if (!own) continue;
+            // the 8 amplitudes of a chunk share their producer (bits >= 3 decide it)
+            const int pr = (g.producer >= 0 || tagged) ? producer_of(g, i) : 0;
+            if (g.producer >= 0 && pr != g.producer) continue;
+            const int prod = tagged ? pr : 0;
             if (((i | 7ull) & g.mask) != g.mask) {           // no amplitude of the chunk is active
                 if (write) {
                     *reinterpret_cast<uint2*>(mi_out + i) = *reinterpret_cast<const uint2*>(mi_in + i);
@@ -679,10 +728,11 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                 if (((i + j) & g.mask) != g.mask) continue;
                 const unsigned key = bm[j] | ((unsigned)bp[j] << 8);
                 unsigned c;
-                if (!memo_get(memo, key, &c)) {
+                const int slot = memo_get(memo, key, &c);
+                if (slot < 0 || mt.fresh(slot, prod)) {
                     bool sure;
-                    c = em.code(i + j, cmul(decode(t, bm[j], bp[j]), f), tc, &sure);
-                    if (sure) memo_put(memo, key, c);
+                    c = em.code(i + j, cmul(decode(t, bm[j], bp[j]), f), tc, &sure, prod);
+                    if (sure) mt.mark(memo_put(memo, key, c), prod);
                 }
                 bm[j] = c & 255;
                 bp[j] = c >> 8;
@@ -695,10 +745,11 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
     } else {   // DIAG: masked amplitudes re-encoded, the rest copied
         const cplx f = {g.m[0], g.m[1]};
         for (uint64_t i = first; i < g.n_elems; i += step) {
+            const int pr = (g.producer >= 0 || tagged) ? producer_of(g, i) : 0;
             if ((i & g.mask) == g.mask) {
-                if (g.producer >= 0 && producer_of(g, i) != g.producer) continue;
-                em.emit(i, cmul(decode(t, mi_in[i], pi_in[i]), f), tc);
-            } else if (write && (g.producer < 0 || (int)(i >> g.n_local) == g.producer)) {
+                if (g.producer >= 0 && pr != g.producer) continue;
+                em.emit(i, cmul(decode(t, mi_in[i], pi_in[i]), f), tc, tagged ? pr : 0);
+            } else if (write && (g.producer < 0 || pr == g.producer)) {
                 mi_out[i] = mi_in[i];
                 pi_out[i] = pi_in[i];
             }
@@ -732,10 +783,10 @@ __global__ void __launch_bounds__(NT) k_byte_encode(const double* __restrict__ v
     __shared__ CtaSets sets;
     load_tables(t, gtab);
     const bool collect = g.collect != 0;
-    if (collect) sets_clear(sets);
+    if (collect) sets_clear(sets, 1);
     __syncthreads();
     const Emitter em{t, g, sets, cand, mi, pi, collect, true};
-    ThreadCache tc{NAN, NAN, NAN, NAN, NAN, NAN, 0u};
+    ThreadCache tc{NAN, NAN, NAN, NAN, NAN, NAN, 0u, 0};
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         em.emit(i, {vals[2 * i], vals[2 * i + 1]}, tc);
     if (collect) {
@@ -852,7 +903,7 @@ cudaError_t launch_byte_gate(const uint8_t* mi_in, const uint8_t* pi_in, uint8_t
     static bool configured[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
-    const int memo_bytes = MEMO_SLOTS * (int)sizeof(unsigned long long);
+    const int memo_bytes = MEMO_SLOTS * (int)(sizeof(unsigned long long) + sizeof(unsigned));
     if (dev < 64 && !configured[dev]) {
         cudaError_t e = cudaFuncSetAttribute(k_byte_gate, cudaFuncAttributeMaxDynamicSharedMemorySize, memo_bytes);
         if (e != cudaSuccess) return e;

@@ -29,7 +29,8 @@ struct ByteGate {
     int xkind;                  // 0 none, 1 pairwise-1q, 2 pairwise-2q, 3 quad (reference choreography)
     uint64_t xmask_a, xmask_b;  // partner rank masks
     int qlow_top;               // pairwise-2q: the local qubit is the top local bit
-    int producer;               // -1: every work item; r: only items the reference's rank r computes
+    int producer;               // -1: every work item; r: only items the reference's rank r computes;
+                                // -2: every work item, candidates tagged with their producer rank
     uint64_t phys_base;         // this buffer's first physical global index
     int rank_bits;              // log2 of the reference rank count
     int8_t lbit[12];            // physical bit of logical bit (n_local - 2 + j)
@@ -45,6 +46,8 @@ struct ByteCand {
     unsigned long long cap_mag, cap_ph, cap_unsure;
     double* mag;                // distinct unrepresentable magnitudes
     double* ph;                 // per distinct theta: (re, im, ux, uy) of the min-(ux, uy) value
+    int* mag_tag;               // producer rank of each candidate (tagged collection, producer == -2)
+    int* ph_tag;
     unsigned long long* unsure_idx;
     double* unsure_val;         // (re, im)
     int overflow, any_mag, any_ph, pad;

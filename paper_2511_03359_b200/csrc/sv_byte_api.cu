@@ -94,6 +94,8 @@ int svb_create(int device, int n_qubits, sv_bhandle* out) {
     c.cap_mag = CAP_MAG; c.cap_ph = CAP_PH; c.cap_unsure = CAP_UNSURE;
     if ((e = cudaMalloc(&c.mag, CAP_MAG * 8)) != cudaSuccess ||
         (e = cudaMalloc(&c.ph, CAP_PH * 32)) != cudaSuccess ||
+        (e = cudaMalloc(&c.mag_tag, CAP_MAG * 4)) != cudaSuccess ||
+        (e = cudaMalloc(&c.ph_tag, CAP_PH * 4)) != cudaSuccess ||
         (e = cudaMalloc(&c.unsure_idx, CAP_UNSURE * 8)) != cudaSuccess ||
         (e = cudaMalloc(&c.unsure_val, CAP_UNSURE * 16)) != cudaSuccess ||
         (e = cudaMalloc(&h->cand, sizeof(ByteCand))) != cudaSuccess)
@@ -113,6 +115,7 @@ int svb_destroy(sv_bhandle h) {
     for (int b = 0; b < 2; ++b) for (int p = 0; p < 2; ++p) sv::slab_free(h->plane[b][p], pbytes);
     cudaFree(h->tab);
     cudaFree(h->hcand.mag); cudaFree(h->hcand.ph); cudaFree(h->hcand.unsure_idx); cudaFree(h->hcand.unsure_val);
+    cudaFree(h->hcand.mag_tag); cudaFree(h->hcand.ph_tag);
     cudaFree(h->cand);
     cudaStreamDestroy(h->stream);
     delete h;
@@ -197,6 +200,19 @@ int svb_candidates(sv_bhandle h, double* mags, uint64_t cap_m, uint64_t* n_m, do
     if (nm && mags) BTRY(cudaMemcpyAsync(mags, h->hcand.mag, 8 * std::min(nm, cap_m), cudaMemcpyDeviceToHost, h->stream), "mags");
     if (np && ph4) BTRY(cudaMemcpyAsync(ph4, h->hcand.ph, 32 * std::min(np, cap_p), cudaMemcpyDeviceToHost, h->stream), "phases");
     BTRY(cudaStreamSynchronize(h->stream), "candidate copy");
+    return SV_OK;
+}
+
+int svb_candidate_tags(sv_bhandle h, int32_t* mag_tags, uint64_t cap_m, int32_t* ph_tags, uint64_t cap_p) {
+    Guard gd(h->device);
+    ByteCand c;
+    BTRY(cudaMemcpyAsync(&c, h->cand, sizeof(c), cudaMemcpyDeviceToHost, h->stream), "candidate header");
+    BTRY(cudaStreamSynchronize(h->stream), "candidate sync");
+    const uint64_t nm = std::min<uint64_t>(std::min<uint64_t>(c.n_mag, c.cap_mag), cap_m);
+    const uint64_t np = std::min<uint64_t>(std::min<uint64_t>(c.n_ph, c.cap_ph), cap_p);
+    if (nm && mag_tags) BTRY(cudaMemcpyAsync(mag_tags, h->hcand.mag_tag, 4 * nm, cudaMemcpyDeviceToHost, h->stream), "mag tags");
+    if (np && ph_tags) BTRY(cudaMemcpyAsync(ph_tags, h->hcand.ph_tag, 4 * np, cudaMemcpyDeviceToHost, h->stream), "phase tags");
+    BTRY(cudaStreamSynchronize(h->stream), "tag copy");
     return SV_OK;
 }
 

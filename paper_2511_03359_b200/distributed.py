@@ -36,6 +36,7 @@ from .circuit import Circuit, validate_circuit
 from .device import gate_op
 from .layout import PartitionLayout, TrafficLedger, plan_exchange
 from .measure import ExpectationReport, report_from_sums
+from .byte_state import MAX_TAGGED_RANKS
 from .remap import Measure, PhysGate, RemapPlanner, Swap, SwapGroup, group_schedule
 from .state import PrecisionMode
 
@@ -318,10 +319,20 @@ class CudaByteBackend:
             scan = self.scan_first
             mine = []
             unsure = []
-            for r in range(self.layout.rank_count):
-                mags, ph, u = self._pass(d, r, True, scan)
-                mine.append((mags, ph))
+            ranks = self.layout.rank_count
+            tagged = None
+            if 1 < ranks <= MAX_TAGGED_RANKS:
+                d.scan_only = 1 if scan else 0
+                tagged = self.st.collect_tagged(d, ranks)      # one pass, candidates tagged by rank
+                self.passes += 1
+            if tagged is not None:
+                mine, u = tagged
                 unsure.append(u)
+            else:
+                for r in range(ranks):
+                    mags, ph, u = self._pass(d, r, True, scan)
+                    mine.append((mags, ph))
+                    unsure.append(u)
             every = [None] * self.world
             self.dist.all_gather_object(every, mine)
             proposals = []
