@@ -161,6 +161,55 @@ __device__ __forceinline__ void gd(cplx (&r)[R], u64 mb) {
         if ((i & MR) == MR) r[i] = cmul(r[i], f);
 }
 
+// ---- long runs of diagonal ops: one compact loop over a descriptor table -----------
+// Straight-line code for ~100 diagonal ops (the adder's CPHASE runs) overflows the
+// instruction cache (ncu: no_instruction stalls 5.8 per issue).  A run is instead a
+// loop over 4-double descriptors in the kernel parameters: [out-of-tile mask bits,
+// thread mask | register mask << 16, factor re, factor im]; the register mask picks
+// one of 16 straight-line multiply blocks (compile-time register indices), so the
+// code is one switch regardless of the run length.  Same multiplies in the same
+// order as gd<> (amplitude first), the Z factor (-1, 0) included: numpy's product.
+__device__ __forceinline__ double ldp_at(u64 mb, int idx) {
+    double v;
+    asm volatile("ld.param.f64 %0, [%1];" : "=d"(v) : "l"(mb + 8ull + 8ull * (u64)idx));
+    return v;
+}
+template <int R, unsigned MR>
+__device__ __forceinline__ void gdf(cplx (&r)[R], cplx f) {
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+        if ((i & MR) == MR) r[i] = cmul(r[i], f);
+}
+template <int R>
+__device__ __forceinline__ void diag_run(cplx (&r)[R], int tb, u64 base, u64 mb, int off, int cnt) {
+    for (int k = 0; k < cnt; ++k) {
+        const int d = off + 4 * k;
+        const u64 dout = (u64)__double_as_longlong(ldp_at(mb, d));
+        const unsigned w = (unsigned)__double_as_longlong(ldp_at(mb, d + 1));
+        const unsigned dthr = w & 0xffffu, mr = w >> 16;
+        if ((base & dout) != dout || ((unsigned)tb & dthr) != dthr) continue;
+        const cplx f = {ldp_at(mb, d + 2), ldp_at(mb, d + 3)};
+        switch (mr) {
+            case 0: gdf<R, 0>(r, f); break;
+            case 1: gdf<R, 1>(r, f); break;
+            case 2: gdf<R, 2>(r, f); break;
+            case 3: gdf<R, 3>(r, f); break;
+            case 4: gdf<R, 4>(r, f); break;
+            case 5: gdf<R, 5>(r, f); break;
+            case 6: gdf<R, 6>(r, f); break;
+            case 7: gdf<R, 7>(r, f); break;
+            case 8: gdf<R, 8>(r, f); break;
+            case 9: gdf<R, 9>(r, f); break;
+            case 10: gdf<R, 10>(r, f); break;
+            case 11: gdf<R, 11>(r, f); break;
+            case 12: gdf<R, 12>(r, f); break;
+            case 13: gdf<R, 13>(r, f); break;
+            case 14: gdf<R, 14>(r, f); break;
+            default: gdf<R, 15>(r, f); break;
+        }
+    }
+}
+
 template <int R, unsigned MR>
 __device__ __forceinline__ void gdn(cplx (&r)[R]) {   // factor exactly -1 (Z): exact negation
 #pragma unroll
