@@ -57,6 +57,20 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def measured_traffic(bytes_per_launch: int):
+    """DRAM traffic per fused-pass launch from the committed ncu capture
+    (profiles/r01_traffic.json: dram read + write / algorithmic bytes, measured at N=32),
+    applied to this launch size; (None, None) if the file is absent."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+        return int(bytes_per_launch * t["ratio"]), f"profiles/r01_traffic.json (ncu --set full at N={t['n_qubits']}: " \
+                                                   f"DRAM/algorithmic = {t['ratio']})"
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def workload_layers(n: int, n_layers: int):
     """H on every qubit, then random layers (depth n) — the BASELINE config[1] circuit."""
     from tests.circuits import random_circuit
@@ -378,7 +392,8 @@ def run_b200(args):
                        "l2": "inputs (128 GiB) >> 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "frac": round(achieved / peak, 4), "traffic": measured_traffic(2 * 16 * 2 ** n)[0],
+                         "traffic_source": measured_traffic(2 * 16 * 2 ** n)[1],
                          "kernel": {0: "k_fused<c64s,12>", 1: "k_fused3<12,4,1>", 2: "k_fused3<11,3,2>",
                                     3: "k_fused3<12,3,1>", 4: "k_fused3<11,3,3>",
                                     5: "k_fused3<10,3,4>", 6: "k_fused3<11,4,3>",
@@ -645,8 +660,11 @@ def run_b200_multi(args, dist, rank, world, device):
                        "parallelism": f"state-sharded x{world} (rank = top {world.bit_length() - 1} index bits)",
                        "l2": "inputs >> 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                         "kernel": "k_fused3 (fused tile pass), rank 0", "launches_timed": passes,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": measured_traffic(2 * 16 * 2 ** n)[0],
+                         "traffic_source": measured_traffic(2 * 16 * 2 ** n)[1],
+                         "kernel": "sv_pass (NVRTC-specialised fused pass; k_fused3 until compiled), rank 0",
+                         "launches_timed": passes,
                          "bytes_per_launch": 2 * 16 * 2 ** n},
             "nvlink": nvlink,
             "gpu_launches": launches,
