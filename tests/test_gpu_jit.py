@@ -1,0 +1,88 @@
+"""GPU parity of the run-time specialised fused passes (sv_jit.cu).
+
+The library compiles one kernel per pass structure in the background and runs
+the generic k_fused3 until it is ready, so ordinary tests exercise whichever is
+ready first.  Here the JIT is put in compile-and-wait mode (sv_jit_mode(1)) so
+every FP64 fused pass runs the specialised kernel, then the generic path
+(mode 0) for the same circuits; both must equal the oracle bit for bit.
+Circuits cover the generated code paths: generic / real / monomial 1Q ops,
+generic / monomial 2Q ops, diagonal ops with register, thread and out-of-tile
+mask bits, and a >= 96-op diagonal pass (the diag_run descriptor loop).
+"""
+import numpy as np
+import pytest
+
+import paper_2511_03359_b200 as pb
+from paper_2511_03359_b200 import _native as nat
+from paper_2511_03359_b200.device import jit_stats
+from oracle import ref_engine
+from oracle.ref_builders import OCircuit, adder
+from oracle.ref_gates import OGate
+from tests.circuits import exact_class_circuit, random_circuit, to_product
+
+pytestmark = pytest.mark.gpu
+
+
+def _diag_heavy(rng, n, count):
+    """H on every qubit, then `count` CPHASE / PHASE / Z gates with a few H between."""
+    gates = [OGate("H", (q,)) for q in range(n)]
+    for i in range(count):
+        a, b = (int(x) for x in rng.choice(n, size=2, replace=False))
+        kind = ("CPHASE", "PHASE", "Z")[i % 3]
+        if kind == "CPHASE":
+            gates.append(OGate("CPHASE", (a, b), int(rng.integers(1, 6))))
+        elif kind == "PHASE":
+            gates.append(OGate("PHASE", (a,), int(rng.integers(1, 5))))
+        else:
+            gates.append(OGate("Z", (a,)))
+        if i % 40 == 39:
+            gates.append(OGate("H", (int(rng.integers(n)),)))
+    gates.append(OGate("M"))
+    return OCircuit(n, tuple(gates))
+
+
+def _cases(rng):
+    return [("random18", random_circuit(np.random.default_rng(31), 18, 120)),
+            ("exact16", exact_class_circuit(np.random.default_rng(32), 16, 120)),
+            ("diag_heavy16", _diag_heavy(np.random.default_rng(33), 16, 260)),
+            ("adder9", adder(9, [301, 88])[0])]
+
+
+@pytest.fixture
+def jit_mode():
+    lib = nat.load()
+    prev = lib.sv_jit_mode(-1)
+
+    def set_mode(m):
+        lib.sv_jit_mode(m)
+    yield set_mode
+    lib.sv_jit_mode(prev)
+
+
+@pytest.mark.parametrize("mode", [1, 0])
+def test_specialised_and_generic_passes_bit_exact(rng, jit_mode, mode):
+    jit_mode(mode)
+    before = jit_stats()
+    for name, circ in _cases(rng):
+        want = ref_engine.run_circuit(circ, ranks=1)
+        got = pb.run_circuit(to_product(circ))
+        assert np.array_equal(got.gathered_state(), want.gathered_state()), (name, mode)
+        wx, wy, wz, _ = want.report
+        diff = max(np.max(np.abs(np.array(got.report.qx) - wx)), np.max(np.abs(np.array(got.report.qz) - wz)))
+        assert diff < 1e-12, name
+    after = jit_stats()
+    if mode == 1:
+        assert after["jit_launches"] > before["jit_launches"] and after["failed"] == before["failed"]
+    else:
+        assert after["jit_launches"] == before["jit_launches"]
+
+
+def test_specialised_multi_rank_emulation(rng, jit_mode):
+    """ranks > 1 on one GPU: the same passes over the whole buffer, ledgers exact."""
+    jit_mode(1)
+    circ = random_circuit(np.random.default_rng(34), 16, 80)
+    for ranks in (2, 4):
+        want = ref_engine.run_circuit(circ, ranks=ranks)
+        got = pb.run_circuit(to_product(circ), ranks=ranks)
+        assert np.array_equal(got.gathered_state(), want.gathered_state()), ranks
+        assert [led.snapshot() for led in got.ledgers] == want.ledgers
