@@ -229,10 +229,13 @@ int sv_cached_bytes(uint64_t* out);
  * Returns the previous mode.  Both kernels are bit-identical. */
 int sv_jit_mode(int mode);
 int sv_jit_wait(void);                        /* block until queued compiles finish */
+int sv_jit_shutdown(void);                    /* drop queued compiles, wait for running ones (call
+                                               * before process teardown; registered with atexit) */
 /* plan the fused passes sv_apply_fused would run for ops on 2^n_qubits FP64
  * amplitudes and queue their specialised kernels (no launch, no device needed);
  * returns the number of new kernels queued */
 int sv_jit_prepare(int n_qubits, const sv_op* ops, int n_ops, int tile_bits);
+int sv_jit_prepare_mode(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits);  /* FP64 / FP32 */
 int sv_jit_stats(double* out6);               /* compiled, failed, jit launches, fallbacks, compile ms, cached */
 int sv_jit_available(void);                   /* 1 when NVRTC and the driver entry points resolved */
 /* CPU-side check: plan the first fused pass of ops on 2^n_qubits amplitudes, write

@@ -6,6 +6,7 @@ the B200 or not at all.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
 import threading
@@ -88,7 +89,9 @@ _SIGNATURES = {
     "sv_cached_bytes": ([ctypes.POINTER(_U64)], _I),
     "sv_jit_mode": ([_I], _I),
     "sv_jit_wait": ([], _I),
+    "sv_jit_shutdown": ([], _I),
     "sv_jit_prepare": ([_I, _P, _I, _I], _I),
+    "sv_jit_prepare_mode": ([_I, _I, _P, _I, _I], _I),
     "sv_jit_stats": ([_D], _I),
     "sv_jit_available": ([], _I),
     "sv_jit_probe": ([_P, _I, _I, ctypes.c_char_p, ctypes.c_size_t, _D], _I),
@@ -140,6 +143,9 @@ def load(require_device: bool = True):
                 fn.argtypes = args
                 fn.restype = res
             _lib = lib
+            # background NVRTC compiles must not outlive the interpreter: stop them
+            # before Python and the CUDA runtime tear down (sv_jit.cu)
+            atexit.register(lib.sv_jit_shutdown)
     if require_device:
         n = ctypes.c_int(0)
         if _lib.sv_device_count(ctypes.byref(n)) != SV_OK or n.value < 1:

@@ -368,7 +368,9 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
     if (tile_bits <= 0) tile_bits = 12;
     const int kv3 = (g_fused_v2 == 2 || g_fused_v2 == 4 || g_fused_v2 == 6) ? 11
                     : ((g_fused_v2 == 5 || g_fused_v2 == 7) ? 10 : 12);
-    const bool use_v3 = g_fused_v2 != 0 && mode == SV_FP64 && n >= kv3 && tile_bits >= kv3;
+    // FP32 storage takes the v3 planning only when the specialised kernel can run it
+    const bool use_v3 = g_fused_v2 != 0 && (mode == SV_FP64 || (mode == SV_FP32 && jit_enabled())) &&
+                        n >= kv3 && tile_bits >= kv3;
     const int k = use_v3 ? kv3 : (tile_bits < n ? tile_bits : n);
     if (k < 1 || k > kMaxTileBits) return fail(SV_EVALUE, "tile bits %d out of range", tile_bits);
     const int bmin = k >= 5 ? 5 : k;
@@ -393,8 +395,10 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
         if (prepare) {
             static thread_local Fused2Params Pp;
             if (use_v3 && build_params2(ops, cur, n, g_fused_v2, Pp) == 0 &&
-                (g_seg_limit <= 0 || Pp.n_segs <= g_seg_limit))
+                (g_seg_limit <= 0 || Pp.n_segs <= g_seg_limit)) {
+                Pp.storage = mode;
                 *prepare += jit_prepare_fused(Pp);
+            }
             cur = PassPlan();
             return SV_OK;
         }
@@ -406,11 +410,22 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
         }
         cudaError_t e;
         static thread_local Fused2Params P2;
+        auto v1 = [&]() {
+            static thread_local FusedParams P;
+            build_params(ops, cur, n, k, P);
+            count_h2d(sizeof(FusedParams));
+            return launch_fused(psi, mode, P, st);
+        };
         if (use_v3 && build_params2(ops, cur, n, g_fused_v2, P2) == 0 &&
             (g_seg_limit <= 0 || P2.n_segs <= g_seg_limit)) {
+            P2.storage = mode;
             const int jr = jit_launch_fused(psi, P2, st);
-            e = jr < 0 ? cudaErrorLaunchFailure : (jr == 0 ? cudaSuccess : launch_fused2(psi, mode, P2, st));
             count_h2d(sizeof(Fused2Params));
+            if (jr < 0) e = cudaErrorLaunchFailure;
+            else if (jr == 0) e = cudaSuccess;
+            else e = mode == SV_FP64 ? launch_fused2(psi, mode, P2, st) : v1();   // not compiled yet
+        } else if (mode == SV_FP32 && use_v3) {
+            e = v1();
         } else {
             static thread_local FusedParams P;
             build_params(ops, cur, n, k, P);
@@ -935,9 +950,14 @@ int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_
 }
 
 int sv_jit_prepare(int n_qubits, const sv_op* ops, int n_ops, int tile_bits) {
+    return sv_jit_prepare_mode(n_qubits, SV_FP64, ops, n_ops, tile_bits);
+}
+
+int sv_jit_prepare_mode(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits) {
     if (n_qubits < 1 || n_qubits > 62) return fail(SV_EVALUE, "qubit count %d out of range", n_qubits);
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "specialised passes exist for FP64 / FP32 storage");
     int queued = 0;
-    if (int rc = fused_impl(nullptr, 1ull << n_qubits, SV_FP64, ops, n_ops, tile_bits, nullptr, &queued)) return rc;
+    if (int rc = fused_impl(nullptr, 1ull << n_qubits, mode, ops, n_ops, tile_bits, nullptr, &queued)) return rc;
     return queued;
 }
 

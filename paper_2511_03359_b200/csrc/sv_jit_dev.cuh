@@ -23,6 +23,25 @@ using sv::row4;
 typedef unsigned long long u64;
 
 struct __align__(16) c64s { double re, im; };
+struct __align__(8) c32s { float re, im; };
+
+// ---- FP32 storage: the reference stores every gate's result into complex64
+// (kernels.py:36-40), i.e. one round-to-nearest-even to float after each gate:
+// F2F there and back (exact widening).  F2F runs at ~16/clk/SM on B200
+// (tools/f2f_probe.cu: 2.2 T FP64->FP32->FP64 round trips/s), the cost floor of FP32
+// passes with many gates.
+__device__ __forceinline__ double r32(double x) { return (double)__double2float_rn(x); }
+template <int R>
+__device__ __forceinline__ void rnd_all(cplx (&r)[R]) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) r[i] = {r32(r[i].re), r32(r[i].im)};
+}
+template <int R, unsigned MR>
+__device__ __forceinline__ void rnd_mask(cplx (&r)[R]) {
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+        if ((i & MR) == MR) r[i] = {r32(r[i].re), r32(r[i].im)};
+}
 
 // shared-memory swizzle of k_fused3 (linear in the element index)
 __device__ __forceinline__ int swz(int e) {
@@ -50,6 +69,10 @@ __device__ __forceinline__ T* at(T* p, u64 off) {
 
 __device__ __forceinline__ void stg(c64s* p, cplx v) {
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.re), "d"(v.im) : "memory");
+}
+// value already float-representable (rounded after its last gate): the narrowing is exact
+__device__ __forceinline__ void stg(c32s* p, cplx v) {
+    asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"((float)v.re), "f"((float)v.im) : "memory");
 }
 
 template <int U>
@@ -180,7 +203,12 @@ __device__ __forceinline__ void gdf(cplx (&r)[R], cplx f) {
     for (int i = 0; i < R; ++i)
         if ((i & MR) == MR) r[i] = cmul(r[i], f);
 }
-template <int R>
+template <int R, unsigned MR, bool F32>
+__device__ __forceinline__ void gdf_r(cplx (&r)[R], cplx f) {
+    gdf<R, MR>(r, f);
+    if constexpr (F32) rnd_mask<R, MR>(r);
+}
+template <int R, bool F32 = false>
 __device__ __forceinline__ void diag_run(cplx (&r)[R], int tb, u64 base, u64 mb, int off, int cnt) {
     for (int k = 0; k < cnt; ++k) {
         const int d = off + 4 * k;
@@ -190,22 +218,22 @@ __device__ __forceinline__ void diag_run(cplx (&r)[R], int tb, u64 base, u64 mb,
         if ((base & dout) != dout || ((unsigned)tb & dthr) != dthr) continue;
         const cplx f = {ldp_at(mb, d + 2), ldp_at(mb, d + 3)};
         switch (mr) {
-            case 0: gdf<R, 0>(r, f); break;
-            case 1: gdf<R, 1>(r, f); break;
-            case 2: gdf<R, 2>(r, f); break;
-            case 3: gdf<R, 3>(r, f); break;
-            case 4: gdf<R, 4>(r, f); break;
-            case 5: gdf<R, 5>(r, f); break;
-            case 6: gdf<R, 6>(r, f); break;
-            case 7: gdf<R, 7>(r, f); break;
-            case 8: gdf<R, 8>(r, f); break;
-            case 9: gdf<R, 9>(r, f); break;
-            case 10: gdf<R, 10>(r, f); break;
-            case 11: gdf<R, 11>(r, f); break;
-            case 12: gdf<R, 12>(r, f); break;
-            case 13: gdf<R, 13>(r, f); break;
-            case 14: gdf<R, 14>(r, f); break;
-            default: gdf<R, 15>(r, f); break;
+            case 0: gdf_r<R, 0, F32>(r, f); break;
+            case 1: gdf_r<R, 1, F32>(r, f); break;
+            case 2: gdf_r<R, 2, F32>(r, f); break;
+            case 3: gdf_r<R, 3, F32>(r, f); break;
+            case 4: gdf_r<R, 4, F32>(r, f); break;
+            case 5: gdf_r<R, 5, F32>(r, f); break;
+            case 6: gdf_r<R, 6, F32>(r, f); break;
+            case 7: gdf_r<R, 7, F32>(r, f); break;
+            case 8: gdf_r<R, 8, F32>(r, f); break;
+            case 9: gdf_r<R, 9, F32>(r, f); break;
+            case 10: gdf_r<R, 10, F32>(r, f); break;
+            case 11: gdf_r<R, 11, F32>(r, f); break;
+            case 12: gdf_r<R, 12, F32>(r, f); break;
+            case 13: gdf_r<R, 13, F32>(r, f); break;
+            case 14: gdf_r<R, 14, F32>(r, f); break;
+            default: gdf_r<R, 15, F32>(r, f); break;
         }
     }
 }

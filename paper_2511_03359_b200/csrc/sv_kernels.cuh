@@ -45,6 +45,7 @@ struct Fused2Params {
     int n, b, n_ops, n_segs;
     int direct_in, direct_out;
     int cfg, kbits, rbits;              // kernel configuration (tile bits, register bits)
+    int storage;                        // SV_FP64 / SV_FP32 (FP32 only through the specialised kernel)
     int8_t tq[12];
     uint8_t seg_reg[kMaxSegs][4];       // register bit j -> tile position
     uint8_t seg_thr[kMaxSegs][9];       // thread-id bit j -> tile position
@@ -66,6 +67,7 @@ cudaError_t launch_fused2(void* psi, int mode, const Fused2Params& p, cudaStream
 // run-time specialised form of the same pass (sv_jit.cu): 0 launched, 1 not ready, < 0 error
 int jit_launch_fused(void* psi, const Fused2Params& p, cudaStream_t st);
 int jit_prepare_fused(const Fused2Params& p);   // queue the compile; 1 if a new kernel was queued
+bool jit_enabled();                             // JIT mode != 0 and NVRTC present
 }  // namespace sv
 #include <string>
 namespace sv {

@@ -31,12 +31,13 @@ def ops_array(ops) -> ctypes.Array:
     return arr
 
 
-def jit_prepare(n_qubits: int, ops, tile_bits: int = 12) -> int:
+def jit_prepare(n_qubits: int, ops, tile_bits: int = 12, mode_code: int = nat.SV_FP64) -> int:
     """Queue the specialised kernels (sv_jit.cu) of the fused passes `ops` will run on
-    2**n_qubits FP64 amplitudes; returns how many new kernels were queued."""
+    2**n_qubits amplitudes (FP64 or FP32 storage); returns how many new kernels were queued."""
     if not ops:
         return 0
-    rc = nat.load(require_device=False).sv_jit_prepare(n_qubits, ops_array(ops), len(ops), tile_bits)
+    rc = nat.load(require_device=False).sv_jit_prepare_mode(n_qubits, mode_code, ops_array(ops), len(ops),
+                                                           tile_bits)
     nat.check(min(rc, 0))
     return rc
 

@@ -232,12 +232,12 @@ class _Engine:
         self.report = report_from_sums(norm, ones, cross)
 
     def run(self):
-        if self.fuse and self.mode is PrecisionMode.FP64:
+        if self.fuse and self.mode in (PrecisionMode.FP64, PrecisionMode.FP32):
             # queue the specialised pass kernels of the whole circuit (compiled in the
             # background; passes whose kernel is not ready yet run the generic one)
             from .device import jit_prepare
             jit_prepare(self.circuit.n_qubits, [gate_to_op(g) for g in self.circuit.gates if g.kind != "M"],
-                        self.tile_bits)
+                        self.tile_bits, self.dev.mode_code)
         for ordinal, gate in enumerate(self.circuit.gates):
             plan = plan_exchange(self.layout, gate, self.mode)
             try:

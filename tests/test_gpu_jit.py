@@ -77,6 +77,20 @@ def test_specialised_and_generic_passes_bit_exact(rng, jit_mode, mode):
         assert after["jit_launches"] == before["jit_launches"]
 
 
+@pytest.mark.parametrize("mode", [1, 0])
+def test_specialised_fp32_passes_bit_exact(rng, jit_mode, mode):
+    """FP32 storage: widened FP64 arithmetic, one rounding to float after every gate
+    (kernels.py:36-40) -- the specialised kernel rounds after each op."""
+    jit_mode(mode)
+    before = jit_stats()
+    for name, circ in _cases(rng):
+        want = ref_engine.run_circuit(circ, ranks=1, mode="fp32")
+        got = pb.run_circuit(to_product(circ), mode=pb.PrecisionMode.FP32)
+        assert np.array_equal(got.gathered_state(), want.gathered_state()), (name, mode)
+    if mode == 1:
+        assert jit_stats()["jit_launches"] > before["jit_launches"]
+
+
 def test_specialised_multi_rank_emulation(rng, jit_mode):
     """ranks > 1 on one GPU: the same passes over the whole buffer, ledgers exact."""
     jit_mode(1)

@@ -58,6 +58,7 @@ if len(sys.argv) > 3 and sys.argv[3] == "adder":
     layers_p = [tuple(g for g in circ.gates if g.kind != "M")]
 else:
     layers_p = [to_product(OCircuit(n, tuple(lo))).gates for lo in bench.workload_layers(n, 4)]
+nat.check(nat.load().sv_fused_variant(int(os.environ.get("SVB200_FUSED_CFG", "6"))))
 dev = DeviceState(n, pb.PrecisionMode.FP64)
 dev.zero(0)
 for li, gates in enumerate(layers_p):
