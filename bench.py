@@ -302,6 +302,39 @@ def run_b200(args):
     dev.free()
     del dev
 
+    # FP32 storage: same layers, complex64 at rest, FP64 arithmetic, one
+    # rounding per gate -- timed like the FP64 steps
+    fp32 = None
+    if args.fp32:
+        for o in ops:
+            jit_prepare(n, o, args.tile_bits, nat.SV_FP32)
+        jit_wait()
+        dev32 = DeviceState(n, pb.PrecisionMode.FP32, device=device)
+        dev32.zero(0)
+        for i in step_layers[:args.warmup]:
+            dev32.apply_fused(ops[i], args.tile_bits)
+        dev32.synchronize()
+        nat.pass_timing(True)
+        nat.pass_timing_read()
+        f0, f1 = nat.Event(), nat.Event()
+        f0.record(dev32.stream)
+        for i in step_layers[args.warmup:]:
+            dev32.apply_fused(ops[i], args.tile_bits)
+        f1.record(dev32.stream)
+        dev32.synchronize()
+        nat.pass_timing(False)
+        p32, ms32, by32 = nat.pass_timing_read()
+        t32 = f0.elapsed_ms(f1)
+        fp32 = {"ms_per_step": round(t32 / args.steps, 3),
+                "value": round(sum(layer_bytes(layers_o[i], n, 8) for i in step_layers[args.warmup:]) /
+                               (t32 / 1e3) / 1e9, 2),
+                "unit": "GB/s", "pass_GBps": round(by32 / (ms32 / 1e3) / 1e9, 1) if ms32 > 0 else None,
+                "passes_per_step": round(p32 / args.steps, 2),
+                "what": "same C2 steps with complex64 storage (8 B/amplitude), FP64 arithmetic, one rounding "
+                        "to float per gate (kernels.py:36-40); bound by the F2F conversions (~16/clk/SM)"}
+        dev32.free()
+        del dev32
+
     # end to end through the public API (host-built circuit in, report out)
     e2e = None
     if args.e2e_steps > 0:
@@ -408,6 +441,8 @@ def run_b200(args):
         }
         if single:
             line["single_gate_h"] = single
+        if fp32:
+            line["fp32"] = fp32
         if e2e:
             line["e2e"] = e2e
         if cpu:
@@ -705,6 +740,7 @@ def main():
                     help="BYTE benchmark amplitudes per GPU (2^n) for N>1 lines: N = n + log2(P), "
                          "38 qubits on 8 GPUs = BASELINE config 5 (0: skip)")
     ap.add_argument("--single-gate", action="store_true", default=True)
+    ap.add_argument("--fp32", type=int, default=1, help="1 GPU line: time the same steps in FP32 storage")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
