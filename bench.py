@@ -659,6 +659,31 @@ def run_b200_multi(args, dist, rank, world, device):
                  "swaps": stats.get("swaps"), "swap_groups": stats.get("swap_groups"),
                  "scaling": "strong (fixed N=32 over the GPUs)",
                  "what": "run_circuit_distributed wall clock, max over ranks (second run: compiled kernels)"}
+    # traffic optimizer A/B (BASELINE config 4 circuit): the remap planner vs the reference's
+    # per-gate exchange choreography (exchange-fused P2P pair updates), same circuit
+    planner_ab = None
+    if args.planner_ab:
+        from paper_2511_03359_b200.distributed import run_circuit_distributed
+        bc = pb.build_benchmark(N)
+        planner_ab = {"circuit": f"build_benchmark({N}) FP64"}
+        for remap in (True, False):
+            times = []
+            for rep in range(3):     # first run compiles the pass kernels; best of the next two
+                dist.barrier()
+                t0 = time.perf_counter()
+                res = run_circuit_distributed(bc, dist, device=device, remap=remap, tile_bits=args.tile_bits)
+                _ = res.report.qz[0]
+                dist.barrier()
+                times.append(max_over_ranks(dist, time.perf_counter() - t0))
+                st = res.device_stats
+                res.backend.close()
+                res.backend.dev.free()
+                del res
+                jit_wait()
+            t = min(times[1:])
+            planner_ab["remap" if remap else "reference_choreography"] = {
+                "seconds": round(t, 4), "physical_link_bytes_rank0": st.get("physical_link_bytes"),
+                "swaps": st.get("swaps"), "swap_groups": st.get("swap_groups")}
     byte = None
     if args.byte_n_multi > 0:
         from paper_2511_03359_b200.distributed import run_circuit_distributed
@@ -710,6 +735,8 @@ def run_b200_multi(args, dist, rank, world, device):
             line["e2e"] = e2e
         if adder:
             line["adder"] = adder
+        if planner_ab:
+            line["planner_ab"] = planner_ab
         if byte:
             line["byte_mode"] = byte
         print(json.dumps(line), flush=True)
@@ -740,6 +767,8 @@ def main():
                     help="BYTE benchmark amplitudes per GPU (2^n) for N>1 lines: N = n + log2(P), "
                          "38 qubits on 8 GPUs = BASELINE config 5 (0: skip)")
     ap.add_argument("--single-gate", action="store_true", default=True)
+    ap.add_argument("--planner-ab", type=int, default=1,
+                    help="N>1: benchmark(N) with the remap planner vs the reference choreography")
     ap.add_argument("--fp32", type=int, default=1, help="1 GPU line: time the same steps in FP32 storage")
     args = ap.parse_args()
     if args.impl == "reference":
