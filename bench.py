@@ -71,6 +71,32 @@ def measured_traffic(bytes_per_launch: int):
         return None, None
 
 
+def benchmark_kat(report, n: int, tol_z: float = 1e-12, tol_x: float = 1e-12):
+    """build_benchmark(n) known answers at full size (test_builders.py:21-33): qubits hit
+    twice read Qz=0, Qx=0.5, the others Qx=0, Qz=0.5.  Returns (ok, max deviation)."""
+    twice = {n - 5, n - 6, n - 1, 0, n - 2, 1}
+    dev = 0.0
+    for q in range(n):
+        if q in twice:
+            dz, dx = abs(report.qz[q]), abs(report.qx[q] - 0.5)
+        else:
+            dz, dx = abs(report.qz[q] - 0.5), abs(report.qx[q])
+        dev = max(dev, dz, dx)
+        if dz > tol_z or dx > tol_x:
+            return False, dev
+    return True, dev
+
+
+def benchmark_codebook_kat(codebook, n: int) -> bool:
+    """BYTE benchmark codebook known answer: N+2 magnitudes m_0 = 0, m_1 = 1,
+    m_k = fl(sqrt(1/2) * m_(k-1)); phases {0}."""
+    from paper_2511_03359_b200 import gates as pg
+    want = [0.0, 1.0]
+    while len(want) < n + 2:
+        want.append(pg.SQRT_HALF * want[-1])
+    return list(codebook.mags) == want and list(codebook.thetas) == [0.0]
+
+
 def workload_layers(n: int, n_layers: int):
     """H on every qubit, then random layers (depth n) — the BASELINE config[1] circuit."""
     from tests.circuits import random_circuit
@@ -393,13 +419,17 @@ def run_b200(args):
         bst.synchronize()
         t_gates = time.perf_counter() - t0
         t0 = time.perf_counter()
-        norm, _, _ = bst.measure_sums()
+        norm, ones_b, cross_b = bst.measure_sums()
         t_meas = time.perf_counter() - t0
+        from paper_2511_03359_b200.measure import report_from_sums
+        kat_b = benchmark_kat(report_from_sums(norm, ones_b, cross_b), args.byte_n, 1e-3, 0.05)
+        kat_cb = benchmark_codebook_kat(bst.codebook, args.byte_n)
         ng = len(bc.gates) - 1
         byte = {"circuit": f"build_benchmark({args.byte_n}) BYTE", "gates": ng,
                 "sec_per_gate": round(t_gates / ng, 5),
                 "effective_GBps": round(ng * 4 * 2 ** args.byte_n / t_gates / 1e9, 1),
                 "measure_s": round(t_meas, 4), "norm": norm, "passes": bst.passes,
+                "kat_parity_pattern": kat_b[0], "kat_max_dev": kat_b[1], "kat_codebook": kat_cb,
                 "codebook": [len(bst.codebook.mags), len(bst.codebook.thetas)],
                 "what": "apply_gate wall clock (passes + per-gate codebook barrier), 4 B/amplitude/gate"}
         bst.free()
@@ -676,6 +706,7 @@ def run_b200_multi(args, dist, rank, world, device):
                 dist.barrier()
                 times.append(max_over_ranks(dist, time.perf_counter() - t0))
                 st = res.device_stats
+                kat = benchmark_kat(res.report, N)
                 res.backend.close()
                 res.backend.dev.free()
                 del res
@@ -683,7 +714,8 @@ def run_b200_multi(args, dist, rank, world, device):
             t = min(times[1:])
             planner_ab["remap" if remap else "reference_choreography"] = {
                 "seconds": round(t, 4), "physical_link_bytes_rank0": st.get("physical_link_bytes"),
-                "swaps": st.get("swaps"), "swap_groups": st.get("swap_groups")}
+                "swaps": st.get("swaps"), "swap_groups": st.get("swap_groups"),
+                "kat_parity_pattern": kat[0], "kat_max_dev": kat[1]}
     byte = None
     if args.byte_n_multi > 0:
         from paper_2511_03359_b200.distributed import run_circuit_distributed
@@ -693,6 +725,8 @@ def run_b200_multi(args, dist, rank, world, device):
         t0 = time.perf_counter()
         res = run_circuit_distributed(bc, dist, mode=pb.PrecisionMode.BYTE, device=device)
         norm_dev = res.report.norm_deviation
+        kat_b = benchmark_kat(res.report, NB, 1e-3, 0.05)
+        kat_cb = benchmark_codebook_kat(res.codebook, NB)
         dist.barrier()
         t_b = max_over_ranks(dist, time.perf_counter() - t0)
         st_b = res.device_stats
@@ -704,7 +738,8 @@ def run_b200_multi(args, dist, rank, world, device):
         byte = {"circuit": f"build_benchmark({NB}) BYTE", "n_qubits": NB, "gates": ng,
                 "seconds": round(t_b, 3), "sec_per_gate": round(t_b / ng, 5),
                 "effective_GBps_per_gpu": round(ng * 4 * 2 ** args.byte_n_multi / t_b / 1e9, 1),
-                "codebook": cb, "norm_deviation": norm_dev, "swaps": st_b.get("swaps"), "swap_groups": st_b.get("swap_groups"),
+                "codebook": cb, "norm_deviation": norm_dev,
+                "kat_parity_pattern": kat_b[0], "kat_max_dev": kat_b[1], "kat_codebook": kat_cb, "swaps": st_b.get("swaps"), "swap_groups": st_b.get("swap_groups"),
                 "byte_passes": st_b.get("byte_passes"),
                 "what": "run_circuit_distributed(mode=BYTE) wall clock incl. allocation, per-gate codebook "
                         "barrier across ranks, remapped byte-plane swaps, measure-all; max over ranks"}
