@@ -460,7 +460,8 @@ def run_b200(args):
                          "kernel": {0: "k_fused<c64s,12>", 1: "k_fused3<12,4,1>", 2: "k_fused3<11,3,2>",
                                     3: "k_fused3<12,3,1>", 4: "k_fused3<11,3,3>",
                                     5: "k_fused3<10,3,4>", 6: "k_fused3<11,4,3>",
-                                    7: "k_fused3<10,4,6>"}[args.fused] + (
+                                    7: "k_fused3<10,4,6>", 8: "k_fused3<12,4,2> single buffer",
+                                    9: "auto: k_fused3<11,4,3> / <12,4,2> per op list"}[args.fused] + (
                              " as sv_pass (NVRTC-specialised per pass structure)" if jit["jit_launches"] else ""),
                          "launches_timed": passes,
                          "bytes_per_launch": 2 * 16 * 2 ** n},
@@ -788,7 +789,7 @@ def main():
     ap.add_argument("--n", type=int, default=33, help="qubits per GPU")
     ap.add_argument("--layers", type=int, default=9, help="H layer + random layers in the workload")
     ap.add_argument("--tile-bits", type=int, default=12, help="v1 tile bits / upper bound")
-    ap.add_argument("--fused", type=int, default=6, choices=[0, 1, 2, 3, 4, 5, 6, 7],
+    ap.add_argument("--fused", type=int, default=9, choices=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9],
                     help="fused-pass kernel: 0 smem-per-gate v1, 1-3 register-resident v3 configs")
     ap.add_argument("--seg-limit", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
