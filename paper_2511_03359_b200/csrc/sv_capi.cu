@@ -947,7 +947,9 @@ int sv_apply_diag(sv_handle h, uint64_t mask, const double* f2) {
 int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_t cap, double* compile_ms) {
     // plan the FIRST fused pass of `ops` on 2^n_qubits amplitudes exactly as fused_impl
     // does, print its specialised source, optionally compile it (CPU only)
-    const int K = 11;
+    const char* pc = std::getenv("SVB200_PROBE_CFG");      // debugging: another tile configuration
+    const int pcfg = pc ? std::atoi(pc) : 6;
+    const int K = (pcfg == 1 || pcfg == 3 || pcfg == 8) ? 12 : 11;
     if (n_qubits < K || n_qubits > 62 || n_ops <= 0) return fail(SV_EVALUE, "probe needs n >= 11 and ops");
     const uint64_t lowfix = 31ull;
     PassPlan cur;
@@ -964,7 +966,7 @@ int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_
         cur.mdata += op_mdata(o.kind);
     }
     static thread_local Fused2Params P2;
-    if (build_params2(ops, cur, n_qubits, 6, P2) != 0) return fail(SV_EVALUE, "pass does not fit the v3 kernel");
+    if (build_params2(ops, cur, n_qubits, pcfg, P2) != 0) return fail(SV_EVALUE, "pass does not fit the v3 kernel");
     std::string src, log;
     double ms = 0.0;
     const int rc = sv::jit_probe(P2, &src, compile_ms != nullptr, &ms, &log);

@@ -59,9 +59,23 @@ def jit_mode():
     lib.sv_jit_mode(prev)
 
 
+@pytest.fixture
+def tile_cfg():
+    lib = nat.load()
+
+    def set_cfg(c):
+        nat.check(lib.sv_fused_variant(c))
+    yield set_cfg
+    nat.check(lib.sv_fused_variant(9))
+
+
+@pytest.mark.parametrize("cfg", [6, 8])
 @pytest.mark.parametrize("mode", [1, 0])
-def test_specialised_and_generic_passes_bit_exact(rng, jit_mode, mode):
+def test_specialised_and_generic_passes_bit_exact(rng, jit_mode, tile_cfg, mode, cfg):
+    """cfg 6: 2^11 double-buffered tiles; cfg 8: 2^12 single-buffered tiles (next tile
+    requested once the last segment holds the tile in registers)."""
     jit_mode(mode)
+    tile_cfg(cfg)
     before = jit_stats()
     for name, circ in _cases(rng):
         want = ref_engine.run_circuit(circ, ranks=1)
@@ -77,11 +91,13 @@ def test_specialised_and_generic_passes_bit_exact(rng, jit_mode, mode):
         assert after["jit_launches"] == before["jit_launches"]
 
 
+@pytest.mark.parametrize("cfg", [6, 8])
 @pytest.mark.parametrize("mode", [1, 0])
-def test_specialised_fp32_passes_bit_exact(rng, jit_mode, mode):
+def test_specialised_fp32_passes_bit_exact(rng, jit_mode, tile_cfg, mode, cfg):
     """FP32 storage: widened FP64 arithmetic, one rounding to float after every gate
     (kernels.py:36-40) -- the specialised kernel rounds after each op."""
     jit_mode(mode)
+    tile_cfg(cfg)
     before = jit_stats()
     for name, circ in _cases(rng):
         want = ref_engine.run_circuit(circ, ranks=1, mode="fp32")
