@@ -461,7 +461,8 @@ def run_b200(args):
                                     3: "k_fused3<12,3,1>", 4: "k_fused3<11,3,3>",
                                     5: "k_fused3<10,3,4>", 6: "k_fused3<11,4,3>",
                                     7: "k_fused3<10,4,6>", 8: "k_fused3<12,4,2> single buffer",
-                                    9: "auto: k_fused3<11,4,3> / <12,4,2> per op list"}[args.fused] + (
+                                    9: "auto: k_fused3<11,4,3> / <12,4,2> per op list",
+                                    10: "<13,4,1> single buffer (specialised only)"}[args.fused] + (
                              " as sv_pass (NVRTC-specialised per pass structure)" if jit["jit_launches"] else ""),
                          "launches_timed": passes,
                          "bytes_per_launch": 2 * 16 * 2 ** n},

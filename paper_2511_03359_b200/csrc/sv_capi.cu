@@ -215,8 +215,8 @@ int classify(const double* m, int dim, uint32_t* mono) {
 
 int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Params& P) {
     std::memset(&P, 0, sizeof(P));
-    const int K = (cfg == 2 || cfg == 4 || cfg == 6) ? 11 : ((cfg == 5 || cfg == 7) ? 10 : 12);
-    const int RB = (cfg == 1 || cfg == 6 || cfg == 7 || cfg == 8) ? 4 : 3;
+    const int K = (cfg == 2 || cfg == 4 || cfg == 6) ? 11 : ((cfg == 5 || cfg == 7) ? 10 : (cfg == 10 ? 13 : 12));
+    const int RB = (cfg == 1 || cfg == 6 || cfg == 7 || cfg == 8 || cfg == 10) ? 4 : 3;
     const int NTH = 1 << (K - RB);
     P.cfg = cfg;
     P.kbits = K;
@@ -259,7 +259,7 @@ int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Pa
     std::vector<int> seg_of(nops);
     for (int sgi = 0, i = 0; sgi < P.n_segs; ++sgi)
         for (; i < seg_end[sgi]; ++i) seg_of[i] = sgi;
-    int regbit_of[kMaxSegs][12];
+    int regbit_of[kMaxSegs][13];
     for (int sgi = 0; sgi < P.n_segs; ++sgi) {
         uint32_t set = seg_sets[sgi];
         for (int pos = K - 1; pos >= 0 && __builtin_popcount(set) < RB; --pos)   // fill from the top
@@ -395,12 +395,12 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
     const int n = log2u(n_elems);
     if (tile_bits <= 0) tile_bits = 12;
     const int cfg = g_fused_v2 == 9 ? choose_cfg(ops, n_ops, n) : g_fused_v2;
-    const int kv3 = (cfg == 2 || cfg == 4 || cfg == 6) ? 11 : ((cfg == 5 || cfg == 7) ? 10 : 12);
+    const int kv3 = (cfg == 2 || cfg == 4 || cfg == 6) ? 11 : ((cfg == 5 || cfg == 7) ? 10 : (cfg == 10 ? 13 : 12));
     // FP32 storage takes the v3 planning only when the specialised kernel can run it
     const bool use_v3 = cfg != 0 && (mode == SV_FP64 || (mode == SV_FP32 && jit_enabled())) &&
                         n >= kv3 && tile_bits >= kv3;
     const int k = use_v3 ? kv3 : (tile_bits < n ? tile_bits : n);
-    if (k < 1 || k > kMaxTileBits) return fail(SV_EVALUE, "tile bits %d out of range", tile_bits);
+    if (k < 1 || k > (use_v3 ? 13 : kMaxTileBits)) return fail(SV_EVALUE, "tile bits %d out of range", tile_bits);
     const int bmin = k >= 5 ? 5 : k;
     const uint64_t lowfix = (1ull << bmin) - 1ull;
     for (int i = 0; i < n_ops; ++i) {
@@ -949,7 +949,7 @@ int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_
     // does, print its specialised source, optionally compile it (CPU only)
     const char* pc = std::getenv("SVB200_PROBE_CFG");      // debugging: another tile configuration
     const int pcfg = pc ? std::atoi(pc) : 6;
-    const int K = (pcfg == 1 || pcfg == 3 || pcfg == 8) ? 12 : 11;
+    const int K = (pcfg == 1 || pcfg == 3 || pcfg == 8) ? 12 : (pcfg == 10 ? 13 : 11);
     if (n_qubits < K || n_qubits > 62 || n_ops <= 0) return fail(SV_EVALUE, "probe needs n >= 11 and ops");
     const uint64_t lowfix = 31ull;
     PassPlan cur;
@@ -1043,7 +1043,7 @@ int sv_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
 }
 
 int sv_fused_variant(int v2) {
-    if (v2 < 0 || v2 > 9) return fail(SV_EVALUE, "fused variant %d not in 0..9", v2);
+    if (v2 < 0 || v2 > 9) return fail(SV_EVALUE, "fused variant %d not in 0..9", v2);   // 10 (2^13 tiles) measured slower
     g_fused_v2 = v2;
     return SV_OK;
 }

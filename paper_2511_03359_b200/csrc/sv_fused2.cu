@@ -300,6 +300,7 @@ cudaError_t launch_fused2(void* psi, int mode, const Fused2Params& p, cudaStream
         case 6: return fused3_cfg<11, 4, 3>(psi, p, st);
         case 7: return fused3_cfg<10, 4, 6>(psi, p, st);
         case 8: return fused3_cfg<12, 4, 1>(psi, p, st);   // generic stand-in for the JIT-only config 8
+        case 10: return cudaErrorNotSupported;               // 2^13 tiles: specialised kernel only
         default: return fused3_cfg<12, 4, 1>(psi, p, st);
     }
 }

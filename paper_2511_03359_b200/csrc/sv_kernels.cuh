@@ -46,7 +46,7 @@ struct Fused2Params {
     int direct_in, direct_out;
     int cfg, kbits, rbits;              // kernel configuration (tile bits, register bits)
     int storage;                        // SV_FP64 / SV_FP32 (FP32 only through the specialised kernel)
-    int8_t tq[12];
+    int8_t tq[13];                      // tile position -> qubit (2^13 tiles: config 10)
     uint8_t seg_reg[kMaxSegs][4];       // register bit j -> tile position
     uint8_t seg_thr[kMaxSegs][9];       // thread-id bit j -> tile position
     uint16_t seg_end[kMaxSegs];         // one past the segment's last op
