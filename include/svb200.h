@@ -98,6 +98,10 @@ int sv_apply_1q(sv_handle h, int q, const double* m8);
 int sv_apply_2q(sv_handle h, int qa, int qb, const double* m32);
 int sv_apply_diag(sv_handle h, uint64_t mask, const double* f2);
 int sv_apply_fused(sv_handle h, const sv_op* ops, int n_ops, int tile_bits);
+/* fused passes of ops restricted to the local indices whose bits under chunk_mask equal
+ * chunk_pattern (chunk bits must lie outside every pass's tile) */
+int sv_apply_fused_chunk(sv_handle h, const sv_op* ops, int n_ops, int tile_bits, uint64_t chunk_mask,
+                         uint64_t chunk_pattern);
 int sv_measure(sv_handle h, double* norm, double* ones, double* cross);
 /* raw storage elements [first, first+count) <-> host memory */
 int sv_export(sv_handle h, void* host, uint64_t first, uint64_t count);
@@ -184,6 +188,15 @@ int svk_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l
  * the remaining-bit indices [t_begin, t_begin + t_count). */
 int svk_swap_group(void* own, void* peer, uint64_t n_local_elems, int mode, uint64_t victim_mask,
                    uint64_t own_pattern, uint64_t peer_pattern, uint64_t t_begin, uint64_t t_count, void* stream);
+/* the same restricted to the amplitudes whose bits under chunk_mask equal chunk_pattern
+ * (t runs over the bits outside victim_mask and chunk_mask): one chunk of a swap that
+ * overlaps the following fused pass (sv_apply_fused_chunk) */
+/* grid cap (blocks) of the group-swap kernels, 0 = one wave of 8 blocks per SM; returns the
+ * previous value (a negative argument only queries) */
+int sv_swap_blocks(int blocks);
+int svk_swap_group_chunk(void* own, void* peer, uint64_t n_local_elems, int mode, uint64_t victim_mask,
+                         uint64_t own_pattern, uint64_t peer_pattern, uint64_t chunk_mask, uint64_t chunk_pattern,
+                         uint64_t t_begin, uint64_t t_count, void* stream);
 /* sum conj(a0[i]) * a1[i] over count elements (a1 may be a peer pointer):
  * measure.py:83-101 cross term of a global qubit; out2 = (re, im) */
 int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, double* out2, void* stream);
@@ -257,6 +270,10 @@ int sv_pass_timing_read(uint64_t* passes, double* ms, double* bytes);
 /* ---- device timing (CUDA events on the handle's / given stream) ------ */
 int sv_event_create(void** ev);
 int sv_event_destroy(void* ev);
+/* inter-process events (cross-GPU ordering of chunked swaps and passes) */
+int sv_event_create_ipc(void** ev, void* handle_out64);
+int sv_event_open_ipc(const void* handle64, void** ev);
+int sv_stream_wait_event(void* stream, void* ev);
 int sv_event_record(void* ev, void* stream);
 int sv_event_elapsed_ms(void* start, void* stop, float* ms);
 int sv_stream_synchronize(void* stream);

@@ -387,7 +387,7 @@ int choose_cfg(const sv_op* ops, int n_ops, int n) {
 // prepare != nullptr: plan only and queue the specialised kernels of the v3 passes for
 // compilation (sv_jit_prepare); *prepare counts them.  Nothing is launched.
 int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_ops, int tile_bits,
-               cudaStream_t st, int* prepare = nullptr) {
+               cudaStream_t st, int* prepare = nullptr, uint64_t chunk_mask = 0, uint64_t chunk_pat = 0) {
     if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "fused passes need FP64 or FP32 storage");
     if (!is_pow2(n_elems)) return fail(SV_EVALUE, "fused pass needs a power-of-two buffer");
     if (!prepare && (reinterpret_cast<uintptr_t>(psi) & 31) != 0)
@@ -438,6 +438,32 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
         }
         cudaError_t e;
         static thread_local Fused2Params P2;
+        if (chunk_mask) {   // chunked pass: only the specialised / register-resident kernels take it
+            if (!use_v3 || build_params2(ops, cur, n, cfg, P2) != 0 || (P2.tile_mask & chunk_mask))
+                return fail(SV_EVALUE, "chunked pass needs the v3 kernel and chunk bits outside its tile");
+            // chunk bits in tile-index space: tile index bit j <-> j-th out-of-tile qubit
+            uint64_t cm = 0, cp = 0;
+            int j = 0;
+            for (int q = 0; q < n; ++q) {
+                if ((P2.tile_mask >> q) & 1) continue;
+                if ((chunk_mask >> q) & 1) {
+                    cm |= 1ull << j;
+                    if ((chunk_pat >> q) & 1) cp |= 1ull << j;
+                }
+                ++j;
+            }
+            P2.cmask_t = cm;
+            P2.cpat_t = cp;
+            P2.n_tiles >>= __builtin_popcountll(cm);
+            P2.storage = mode;
+            const int jr = jit_launch_fused(psi, P2, st);
+            e = jr < 0 ? cudaErrorLaunchFailure
+                       : (jr == 0 ? cudaSuccess : (mode == SV_FP64 ? launch_fused2(psi, mode, P2, st)
+                                                                     : cudaErrorNotSupported));
+            if (e != cudaSuccess) return cuda_fail(e, "chunked fused pass launch");
+            cur = PassPlan();
+            return SV_OK;
+        }
         auto v1 = [&]() {
             static thread_local FusedParams P;
             build_params(ops, cur, n, k, P);
@@ -991,6 +1017,15 @@ int sv_jit_prepare_mode(int n_qubits, int mode, const sv_op* ops, int n_ops, int
     return queued;
 }
 
+int sv_apply_fused_chunk(sv_handle h, const sv_op* ops, int n_ops, int tile_bits, uint64_t chunk_mask,
+                         uint64_t chunk_pattern) {
+    DeviceGuard g(h->device);
+    if (n_ops <= 0) return SV_OK;
+    if ((chunk_pattern & ~chunk_mask) || (chunk_mask >> h->n)) return fail(SV_EINDEX, "chunk mask outside the state");
+    return fused_impl(h->ptr, 1ull << h->n, h->mode, ops, n_ops, tile_bits, h->stream, nullptr, chunk_mask,
+                      chunk_pattern);
+}
+
 int sv_apply_fused(sv_handle h, const sv_op* ops, int n_ops, int tile_bits) {
     DeviceGuard g(h->device);
     return svk_apply_fused(h->ptr, 1ull << h->n, h->mode, ops, n_ops, tile_bits, h->stream);
@@ -1113,15 +1148,30 @@ int svk_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l
 
 int svk_swap_group(void* own, void* peer, uint64_t n_local_elems, int mode, uint64_t victim_mask,
                    uint64_t own_pattern, uint64_t peer_pattern, uint64_t t_begin, uint64_t t_count, void* stream) {
+    return svk_swap_group_chunk(own, peer, n_local_elems, mode, victim_mask, own_pattern, peer_pattern, 0, 0, t_begin,
+                                t_count, stream);
+}
+
+namespace sv { extern int g_swap_blocks; }
+int sv_swap_blocks(int blocks) {
+    const int prev = sv::g_swap_blocks;
+    if (blocks >= 0) sv::g_swap_blocks = blocks;
+    return prev;
+}
+
+int svk_swap_group_chunk(void* own, void* peer, uint64_t n_local_elems, int mode, uint64_t victim_mask,
+                         uint64_t own_pattern, uint64_t peer_pattern, uint64_t chunk_mask, uint64_t chunk_pattern,
+                         uint64_t t_begin, uint64_t t_count, void* stream) {
     if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "swap needs FP64 or FP32 storage");
     if (!is_pow2(n_local_elems)) return fail(SV_EVALUE, "swap needs a power-of-two slice");
-    if ((victim_mask & ~(n_local_elems - 1)) || ((own_pattern | peer_pattern) & ~victim_mask))
-        return fail(SV_EINDEX, "victim mask / patterns outside the slice");
-    const uint64_t rest = n_local_elems >> __builtin_popcountll(victim_mask);
+    if (((victim_mask | chunk_mask) & ~(n_local_elems - 1)) || ((own_pattern | peer_pattern) & ~victim_mask) ||
+        (victim_mask & chunk_mask) || (chunk_pattern & ~chunk_mask))
+        return fail(SV_EINDEX, "victim / chunk masks or patterns outside the slice or overlapping");
+    const uint64_t rest = n_local_elems >> __builtin_popcountll(victim_mask | chunk_mask);
     if (t_begin > rest || t_count > rest - t_begin) return fail(SV_EINDEX, "rest range outside the slice");
     if (t_count == 0) return SV_OK;
     cudaError_t e = launch_swap_group(own, peer, t_begin, t_count, mode, victim_mask, own_pattern, peer_pattern,
-                                      as_stream(stream));
+                                      chunk_mask, chunk_pattern, as_stream(stream));
     return e == cudaSuccess ? SV_OK : cuda_fail(e, "group swap launch");
 }
 
@@ -1187,6 +1237,32 @@ int sv_event_create(void** ev) {
 }
 int sv_event_destroy(void* ev) {
     cudaEventDestroy(reinterpret_cast<cudaEvent_t>(ev));
+    return SV_OK;
+}
+int sv_event_create_ipc(void** ev, void* handle_out64) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventInterprocess), "IPC event create");
+    cudaIpcEventHandle_t hnd;
+    static_assert(sizeof(hnd) == 64, "IPC event handle size");
+    cudaError_t r = cudaIpcGetEventHandle(&hnd, e);
+    if (r != cudaSuccess) {
+        cudaEventDestroy(e);
+        return cuda_fail(r, "cudaIpcGetEventHandle");
+    }
+    std::memcpy(handle_out64, &hnd, 64);
+    *ev = reinterpret_cast<void*>(e);
+    return SV_OK;
+}
+int sv_event_open_ipc(const void* handle64, void** ev) {
+    cudaIpcEventHandle_t hnd;
+    std::memcpy(&hnd, handle64, 64);
+    cudaEvent_t e;
+    CUDA_TRY(cudaIpcOpenEventHandle(&e, hnd), "cudaIpcOpenEventHandle");
+    *ev = reinterpret_cast<void*>(e);
+    return SV_OK;
+}
+int sv_stream_wait_event(void* stream, void* ev) {
+    CUDA_TRY(cudaStreamWaitEvent(as_stream(stream), reinterpret_cast<cudaEvent_t>(ev), 0), "stream wait event");
     return SV_OK;
 }
 int sv_event_record(void* ev, void* stream) {

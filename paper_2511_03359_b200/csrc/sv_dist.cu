@@ -78,9 +78,9 @@ __global__ void __launch_bounds__(256) k_swap_peer_scalar(S* own, S* peer, uint6
 template <typename S>
 __global__ void __launch_bounds__(256) k_swap_group(S* __restrict__ own, S* __restrict__ peer, uint64_t t0,
                                                     uint64_t n, uint64_t vmask, uint64_t own_pat,
-                                                    uint64_t peer_pat) {
+                                                    uint64_t peer_pat, uint64_t cmask, uint64_t cpat) {
     for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n; w += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t base = insert_zeros(t0 + w, vmask);
+        const uint64_t base = insert_zeros(t0 + w, vmask | cmask) | cpat;
         const uint64_t x = base | own_pat, y = base | peer_pat;
         const S a = own[x];
         own[x] = peer[y];
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(256) k_swap_group(S* __restrict__ own, S* __re
 template <typename S, int U>
 __global__ void __launch_bounds__(256) k_swap_group_vec(S* __restrict__ own, S* __restrict__ peer, uint64_t t0,
                                                         uint64_t n_vec, uint64_t vmask, uint64_t own_pat,
-                                                        uint64_t peer_pat) {
+                                                        uint64_t peer_pat, uint64_t cmask, uint64_t cpat) {
     constexpr int V = Store<S>::V;
     const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t w0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w0 < n_vec; w0 += U * step) {
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256) k_swap_group_vec(S* __restrict__ own, S* 
         for (int u = 0; u < U; ++u) {
             const uint64_t w = w0 + u * step;
             if (w < n_vec) {
-                const uint64_t base = insert_zeros(t0 + w * V, vmask);
+                const uint64_t base = insert_zeros(t0 + w * V, vmask | cmask) | cpat;
                 x[u] = base | own_pat;
                 y[u] = base | peer_pat;
                 a[u] = vload(own + x[u]);
@@ -119,31 +119,34 @@ __global__ void __launch_bounds__(256) k_swap_group_vec(S* __restrict__ own, S* 
     }
 }
 
+int g_swap_blocks = 0;   // > 0: grid cap of the group-swap kernel (overlapped swaps leave SMs to the pass)
+
 template <typename S>
 static cudaError_t swap_group_t(S* own, S* peer, uint64_t t0, uint64_t n, uint64_t vmask, uint64_t op, uint64_t pp,
-                                cudaStream_t st) {
+                                uint64_t cmask, uint64_t cpat, cudaStream_t st) {
     constexpr int V = Store<S>::V;
     int dev = 0;
     cudaGetDevice(&dev);
-    const uint64_t cap = (uint64_t)sm_count(dev) * 8;
-    const bool vec = (vmask & (uint64_t)(V - 1)) == 0 && (t0 % V) == 0 && (n % V) == 0;
+    const uint64_t cap = g_swap_blocks > 0 ? (uint64_t)g_swap_blocks : (uint64_t)sm_count(dev) * 8;
+    const bool vec = ((vmask | cmask) & (uint64_t)(V - 1)) == 0 && (t0 % V) == 0 && (n % V) == 0;
     if (vec) {
         const uint64_t nv = n / V;
         const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nv + 1023) / 1024, cap));
-        k_swap_group_vec<S, 4><<<g, 256, 0, st>>>(own, peer, t0, nv, vmask, op, pp);
+        k_swap_group_vec<S, 4><<<g, 256, 0, st>>>(own, peer, t0, nv, vmask, op, pp, cmask, cpat);
     } else {
         const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, cap));
-        k_swap_group<S><<<g, 256, 0, st>>>(own, peer, t0, n, vmask, op, pp);
+        k_swap_group<S><<<g, 256, 0, st>>>(own, peer, t0, n, vmask, op, pp, cmask, cpat);
     }
     count_launch();
     return cudaGetLastError();
 }
 
 cudaError_t launch_swap_group(void* own, void* peer, uint64_t t0, uint64_t n, int mode, uint64_t vmask,
-                              uint64_t own_pat, uint64_t peer_pat, cudaStream_t st) {
-    return mode == SV_FP32
-               ? swap_group_t(static_cast<c32s*>(own), static_cast<c32s*>(peer), t0, n, vmask, own_pat, peer_pat, st)
-               : swap_group_t(static_cast<c64s*>(own), static_cast<c64s*>(peer), t0, n, vmask, own_pat, peer_pat, st);
+                              uint64_t own_pat, uint64_t peer_pat, uint64_t cmask, uint64_t cpat, cudaStream_t st) {
+    return mode == SV_FP32 ? swap_group_t(static_cast<c32s*>(own), static_cast<c32s*>(peer), t0, n, vmask, own_pat,
+                                          peer_pat, cmask, cpat, st)
+                           : swap_group_t(static_cast<c64s*>(own), static_cast<c64s*>(peer), t0, n, vmask, own_pat,
+                                          peer_pat, cmask, cpat, st);
 }
 
 template <typename S>

@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(1 << (KB - RB), MINB)
     __syncthreads();
 
     auto tile_base = [&](uint64_t t) {
+        t = insert_zeros(t, p.cmask_t) | p.cpat_t;       // chunked pass (remap overlap): fixed tile bits
         return p.base_tab[0][t & 255] | p.base_tab[1][(t >> 8) & 255] | p.base_tab[2][(t >> 16) & 255] |
                p.base_tab[3][(t >> 24) & 255];
     };

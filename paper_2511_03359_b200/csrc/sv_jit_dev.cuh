@@ -91,6 +91,19 @@ __device__ __forceinline__ cplx rmul(double m, cplx a) { return {__dmul_rn(m, a.
 // constant loads ptxas hoists every matrix of the pass out of the tile loop, the
 // uniform registers overflow into ~130 regular registers for a few U4 gates and the
 // kernel spills; a per-use LDC costs one instruction per entry per tile.
+constexpr int kArgsM = 24;   // byte offset of Args::m (after n_tiles, cmask, cpat)
+
+// tile index t of a chunked launch -> full tile index: zeros inserted at the bits of cm,
+// then the chunk pattern
+__device__ __forceinline__ u64 chunk_tile(u64 t, u64 cm, u64 cp) {
+    while (cm) {
+        const int q = __ffsll((long long)cm) - 1;
+        t = ((t >> q) << (q + 1)) | (t & ((1ull << q) - 1ull));
+        cm &= cm - 1ull;
+    }
+    return t | cp;
+}
+
 __device__ __forceinline__ u64 mbase(u64 tile) {
     u64 b;
     asm("mov.u64 %0, sv_pass_param_1;" : "=l"(b));
@@ -99,7 +112,7 @@ __device__ __forceinline__ u64 mbase(u64 tile) {
 template <int OFF>
 __device__ __forceinline__ double ldm(u64 mb) {
     double v;
-    asm volatile("ld.param.f64 %0, [%1+%2];" : "=d"(v) : "l"(mb), "n"(8 + 8 * OFF));
+    asm volatile("ld.param.f64 %0, [%1+%2];" : "=d"(v) : "l"(mb), "n"(kArgsM + 8 * OFF));
     return v;
 }
 template <int OFF>
@@ -194,7 +207,7 @@ __device__ __forceinline__ void gd(cplx (&r)[R], u64 mb) {
 // order as gd<> (amplitude first), the Z factor (-1, 0) included: numpy's product.
 __device__ __forceinline__ double ldp_at(u64 mb, int idx) {
     double v;
-    asm volatile("ld.param.f64 %0, [%1];" : "=d"(v) : "l"(mb + 8ull + 8ull * (u64)idx));
+    asm volatile("ld.param.f64 %0, [%1];" : "=d"(v) : "l"(mb + (u64)kArgsM + 8ull * (u64)idx));
     return v;
 }
 template <int R, unsigned MR>

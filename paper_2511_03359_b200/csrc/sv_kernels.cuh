@@ -46,6 +46,8 @@ struct Fused2Params {
     int direct_in, direct_out;
     int cfg, kbits, rbits;              // kernel configuration (tile bits, register bits)
     int storage;                        // SV_FP64 / SV_FP32 (FP32 only through the specialised kernel)
+    uint64_t cmask_t, cpat_t;           // chunked pass: tile-index bits fixed to cpat_t (n_tiles counts
+                                        // the remaining tiles); 0, 0 = every tile
     int8_t tq[13];                      // tile position -> qubit (2^13 tiles: config 10)
     uint8_t seg_reg[kMaxSegs][4];       // register bit j -> tile position
     uint8_t seg_thr[kMaxSegs][9];       // thread-id bit j -> tile position
@@ -131,7 +133,7 @@ cudaError_t slab_alloc(void** p, size_t bytes);
 void slab_free(void* p, size_t bytes);
 cudaError_t launch_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l, int c, cudaStream_t st);
 cudaError_t launch_swap_group(void* own, void* peer, uint64_t t0, uint64_t n, int mode, uint64_t vmask,
-                              uint64_t own_pat, uint64_t peer_pat, cudaStream_t st);
+                              uint64_t own_pat, uint64_t peer_pat, uint64_t cmask, uint64_t cpat, cudaStream_t st);
 cudaError_t launch_pair_dot(const void* a0, const void* a1, uint64_t n, int mode, double* partials, int grid,
                             cudaStream_t st);
 void count_launch(uint64_t n = 1);

@@ -116,3 +116,32 @@ def test_specialised_multi_rank_emulation(rng, jit_mode):
         got = pb.run_circuit(to_product(circ), ranks=ranks)
         assert np.array_equal(got.gathered_state(), want.gathered_state()), ranks
         assert [led.snapshot() for led in got.ledgers] == want.ledgers
+
+
+@pytest.mark.parametrize("mode", [1, 0])
+def test_chunked_passes_equal_whole_passes(rng, jit_mode, mode):
+    """sv_apply_fused_chunk over every chunk pattern == one sv_apply_fused (the chunked
+    form runs a pass under a remap swap, tile by tile as the swap chunks land)."""
+    from paper_2511_03359_b200.device import DeviceState, ops_array
+    from paper_2511_03359_b200.engine import gate_to_op
+    jit_mode(mode)
+    n = 16
+    circ = random_circuit(np.random.default_rng(41), 11, 60, measured=False)   # qubits 0..10 only
+    ops = [gate_to_op(gt) for gt in to_product(circ).gates]
+    psi0 = (rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)).astype(np.complex128)
+    lib = nat.load()
+    whole = DeviceState(n, pb.PrecisionMode.FP64)
+    whole.import_(psi0)
+    whole.apply_fused(ops)
+    want = whole.export()
+    chunked = DeviceState(n, pb.PrecisionMode.FP64)
+    chunked.import_(psi0)
+    cmask = (1 << 15) | (1 << 13)
+    arr = ops_array(ops)
+    for pat in (0, 1 << 13, 1 << 15, cmask):
+        nat.check(lib.sv_apply_fused_chunk(chunked.handle, arr, len(ops), 12, cmask, pat))
+    assert np.array_equal(chunked.export(), want)
+    with pytest.raises(ValueError):      # chunk bit inside a pass tile
+        nat.check(lib.sv_apply_fused_chunk(chunked.handle, arr, len(ops), 12, 1 << 3, 0))
+    whole.free()
+    chunked.free()
