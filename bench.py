@@ -553,41 +553,54 @@ def run_b200_multi(args, dist, rank, world, device):
             k = owner[st.ordinal]
             per_step[k] += pending_swaps + [st]
             pending_swaps = []
-    # each step as launch batches: ("swap", Swap) / ("group", SwapGroup) / ("ops", [sv_op])
+    # each step as launch batches: ("ops", [sv_op]) or ("swapops", pairs, [sv_op]): a remap
+    # swap and the ops after it, the swap overlapped with their first pass
     batches = []
     for k in range(len(seq)):
-        out, pend = [], []
+        out, pend, swap = [], [], None
+
+        def close():
+            if swap is not None:
+                out.append(("swapops", swap, pend))
+            elif pend:
+                out.append(("ops", pend))
         for st in per_step[k]:
             if isinstance(st, (Swap, SwapGroup)):
-                if pend:
-                    out.append(("ops", pend))
-                    pend = []
-                out.append(("swap" if isinstance(st, Swap) else "group", st))
+                close()
+                pend = []
+                swap = ((st.global_pos, st.local_pos),) if isinstance(st, Swap) else st.pairs
             else:
                 op = phys_op(st.gate, st.qubits, n, rank)
                 if op is not None:
                     pend.append(op)
-        if pend:
-            out.append(("ops", pend))
+        close()
         batches.append(out)
     from paper_2511_03359_b200.device import jit_prepare, jit_stats, jit_wait
     t_jit = time.perf_counter()
     for out in batches:
-        for kind, item in out:
-            if kind == "ops":
-                jit_prepare(n, item, args.tile_bits)
+        for b in out:
+            if b[0] == "ops":
+                jit_prepare(n, b[1], args.tile_bits)
+            else:            # the overlapped first pass and the rest are planned separately
+                first, rest = CudaBackend._first_pass(b[2])
+                jit_prepare(n, first, args.tile_bits)
+                jit_prepare(n, rest, args.tile_bits)
     jit_wait()
     t_jit = time.perf_counter() - t_jit
     be = CudaBackend(dist, n, pb.PrecisionMode.FP64, device, args.tile_bits)
 
     def run_step(k):
-        for kind, item in batches[k]:
-            if kind == "ops":
-                be.apply_local(item)
-            elif kind == "swap":
-                be.swap(item.global_pos, item.local_pos)
+        for b in batches[k]:
+            if b[0] == "ops":
+                be.apply_local(b[1])
+            elif args.overlap:
+                be.swap_then_apply(b[1], b[2])
             else:
-                be.swap_group(item.pairs)
+                if len(b[1]) == 1:
+                    be.swap(*b[1][0])
+                else:
+                    be.swap_group(b[1])
+                be.apply_local(b[2])
 
     for k in range(args.warmup):
         run_step(k)
@@ -804,6 +817,8 @@ def main():
                     help="BYTE benchmark amplitudes per GPU (2^n) for N>1 lines: N = n + log2(P), "
                          "38 qubits on 8 GPUs = BASELINE config 5 (0: skip)")
     ap.add_argument("--single-gate", action="store_true", default=True)
+    ap.add_argument("--overlap", type=int, default=1,
+                    help="N>1: overlap each remap swap with the first pass after it (chunked, IPC events)")
     ap.add_argument("--planner-ab", type=int, default=1,
                     help="N>1: benchmark(N) with the remap planner vs the reference choreography")
     ap.add_argument("--fp32", type=int, default=1, help="1 GPU line: time the same steps in FP32 storage")

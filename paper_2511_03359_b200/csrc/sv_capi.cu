@@ -1152,7 +1152,6 @@ int svk_swap_group(void* own, void* peer, uint64_t n_local_elems, int mode, uint
                                 t_count, stream);
 }
 
-namespace sv { extern int g_swap_blocks; }
 int sv_swap_blocks(int blocks) {
     const int prev = sv::g_swap_blocks;
     if (blocks >= 0) sv::g_swap_blocks = blocks;

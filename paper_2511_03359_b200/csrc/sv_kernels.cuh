@@ -128,6 +128,7 @@ cudaError_t launch_measure(const void* psi, int mode, const MeasureParams& p, do
 int measure_grid(int device);
 
 int sm_count(int device);
+extern int g_swap_blocks;               // grid cap of the group-swap kernels (sv_dist.cu), 0 = default
 // caching state-slab allocator (sv_slab.cu): same-size reuse per device
 cudaError_t slab_alloc(void** p, size_t bytes);
 void slab_free(void* p, size_t bytes);

@@ -33,11 +33,11 @@ import numpy as np
 from . import _native as nat
 from . import gates as g
 from .circuit import Circuit, validate_circuit
-from .device import gate_op
+from .device import gate_op, ops_array
 from .layout import PartitionLayout, TrafficLedger, plan_exchange
 from .measure import ExpectationReport, report_from_sums
 from .byte_state import MAX_TAGGED_RANKS
-from .remap import Measure, PhysGate, RemapPlanner, Swap, SwapGroup, group_schedule
+from .remap import Measure, PhysGate, RemapPlanner, Swap, SwapGroup, deposit, group_schedule
 from .state import PrecisionMode
 
 
@@ -88,10 +88,132 @@ class CudaBackend:
         self.link_bytes = 0
         self.swap_timing = False
         self.swap_events = []
+        self._overlap = None          # chunk events / swap stream, created on first overlapped swap
         dist.barrier()
 
     def apply_local(self, ops):
         self.dev.apply_fused(ops, self.tile_bits)
+
+    # -- remap swap overlapped with the following pass ------------------------------------
+    OVERLAP_CHUNK_BITS = 3           # 8 chunks
+    OVERLAP_SWAP_BLOCKS = 256        # swap kernel grid while a pass runs beside it
+
+    def _overlap_setup(self):
+        """Second stream for the swap chunks and one inter-process event per chunk, the
+        handles exchanged once; peers' events opened for cross-GPU ordering."""
+        lib = nat.load()
+        C = 1 << self.OVERLAP_CHUNK_BITS
+        stream = nat.Stream(self.dev.device)
+        own, handles = [], bytearray()
+        for _ in range(C):
+            ev = ctypes.c_void_p()
+            h = (ctypes.c_char * 64)()
+            nat.check(lib.sv_event_create_ipc(ctypes.byref(ev), h))
+            own.append(ev)
+            handles += bytes(h)
+        every = [None] * self.world
+        self.dist.all_gather_object(every, bytes(handles))
+        peers = {}
+        for r, hb in enumerate(every):
+            if r == self.rank:
+                continue
+            evs = []
+            for i in range(C):
+                ev = ctypes.c_void_p()
+                buf = (ctypes.c_char * 64).from_buffer_copy(hb[64 * i:64 * (i + 1)])
+                nat.check(lib.sv_event_open_ipc(buf, ctypes.byref(ev)))
+                evs.append(ev)
+            peers[r] = evs
+        self._overlap = (stream, own, peers)
+
+    def _chunk_bits(self, pairs, ops):
+        """Chunk positions for an overlapped swap: the highest local positions >= 12 that no
+        non-diagonal op of the overlapped pass touches and that are not swap victims (the
+        same on every rank: only diagonal ops differ between ranks)."""
+        victims = {lp for _, lp in pairs}
+        used = set()
+        for op in ops:
+            if op.kind == nat.SV_OP_1Q:
+                used.add(op.qa)
+            elif op.kind == nat.SV_OP_2Q:
+                used.update((op.qa, op.qb))
+        bits = [q for q in range(self.n_local - 1, 11, -1) if q not in used and q not in victims]
+        return bits[:self.OVERLAP_CHUNK_BITS] if len(bits) >= self.OVERLAP_CHUNK_BITS else []
+
+    @staticmethod
+    def _first_pass(ops, K: int = 11):
+        """Longest prefix of ops whose non-diagonal qubits fit one 2^K tile with the five
+        lowest qubits (the pass that runs chunk by chunk under the swap)."""
+        need = 0x1F
+        for i, op in enumerate(ops):
+            m = 0
+            if op.kind == nat.SV_OP_1Q:
+                m = 1 << op.qa
+            elif op.kind == nat.SV_OP_2Q:
+                m = (1 << op.qa) | (1 << op.qb)
+            if bin(need | m).count("1") > K or i >= 128:
+                return ops[:i], ops[i:]
+            need |= m
+        return ops, []
+
+    def swap_then_apply(self, pairs, ops) -> None:
+        """A remap swap (one or k global qubits) followed by the fused passes of `ops`, with
+        the swap's transfer overlapping the first pass: the swap runs on a second stream in
+        chunks (fixed values of three high local bits outside the pass tile); the pass runs
+        chunk by chunk on the main stream, each chunk waiting for this rank's and the
+        partners' swap of that chunk (inter-process events).  Same amplitudes, same
+        arithmetic as swap + apply_local."""
+        first, rest = self._first_pass(ops)
+        bits = self._chunk_bits(pairs, first) if first and self.mode is PrecisionMode.FP64 else []
+        if not bits:
+            if len(pairs) == 1:
+                self.swap(*pairs[0])
+            else:
+                self.swap_group(pairs)
+            if ops:
+                self.apply_local(ops)
+            return
+        if self._overlap is None:
+            self._overlap = ()
+            self._overlap_setup()
+        stream, own_ev, peer_ev = self._overlap
+        lib = nat.load()
+        L = self.dev.size
+        k = len(pairs)
+        sched = group_schedule(self.rank, pairs, self.n_local, L)
+        cmask = sum(1 << b for b in bits)
+        half = (L >> (k + len(bits))) // 2
+        C = 1 << len(bits)
+        prev_blocks = lib.sv_swap_blocks(self.OVERLAP_SWAP_BLOCKS)
+        self._sync_all()
+        if self.swap_timing:
+            e0 = nat.Event()
+            e0.record(self.dev.stream)
+        for i in range(C):
+            cpat = deposit(i, bits)
+            for member, vmask, own_pat, peer_pat, t0, cnt in sched:
+                nat.check(lib.svk_swap_group_chunk(self.dev.ptr, self.peers[member], L, self.dev.mode_code, vmask,
+                                                   own_pat, peer_pat, cmask, cpat, 0 if t0 == 0 else half, half,
+                                                   stream.ptr))
+                self.link_bytes += 2 * half * self.bpe
+            nat.check(lib.sv_event_record(own_ev[i], stream.ptr))
+        lib.sv_swap_blocks(prev_blocks)
+        self.dist.barrier()          # every rank's chunk events are recorded (enqueued)
+        members = [m for m, *_ in sched]
+        arr = ops_array(first)
+        for i in range(C):
+            nat.check(lib.sv_stream_wait_event(self.dev.stream, own_ev[i]))
+            for m in members:
+                nat.check(lib.sv_stream_wait_event(self.dev.stream, peer_ev[m][i]))
+            nat.check(lib.sv_apply_fused_chunk(self.dev.handle, arr, len(first), self.tile_bits, cmask,
+                                               deposit(i, bits)))
+        if self.swap_timing:
+            e1 = nat.Event()
+            e1.record(self.dev.stream)
+            self.swap_events.append((e0, e1))
+        self.dev._touch()
+        if rest:
+            self.apply_local(rest)
 
     def _sync_all(self):
         self.dev.synchronize()
@@ -465,7 +587,7 @@ def _charge_reference(layout, ledgers, gate, mode):
 
 def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = PrecisionMode.FP64,
                             remap: bool = True, device: int | None = None, backend_factory=None,
-                            tile_bits: int = 12, fuse_limit: int = 1024) -> DistRunResult:
+                            tile_bits: int = 12, fuse_limit: int = 1024, overlap: bool = True) -> DistRunResult:
     """Run `circuit` with one rank per process of the torch.distributed group `dist`."""
     validate_circuit(circuit)
     P = dist.get_world_size()
@@ -492,23 +614,30 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
     pending = []
     report = None
     swaps = groups = 0
+    pending_swap = None          # FP backends: a swap waits for the ops after it (overlapped)
+    overlap = overlap and not byte and hasattr(be, "swap_then_apply")
 
     def flush():
-        nonlocal pending
-        if pending:
+        nonlocal pending, pending_swap
+        if pending_swap is not None:
+            be.swap_then_apply(pending_swap, pending)
+            pending_swap = None
+        elif pending:
             be.apply_local(pending)
-            pending = []
+        pending = []
 
     for step in steps:
-        if isinstance(step, Swap):
+        if isinstance(step, (Swap, SwapGroup)):
             flush()
-            be.swap(step.global_pos, step.local_pos)
+            pairs = ((step.global_pos, step.local_pos),) if isinstance(step, Swap) else step.pairs
+            if overlap:
+                pending_swap = pairs
+            elif isinstance(step, Swap):
+                be.swap(step.global_pos, step.local_pos)
+            else:
+                be.swap_group(step.pairs)
             swaps += 1
-        elif isinstance(step, SwapGroup):
-            flush()
-            be.swap_group(step.pairs)
-            swaps += 1
-            groups += 1
+            groups += isinstance(step, SwapGroup)
         elif isinstance(step, PhysGate):
             _charge_reference(layout, ledgers, step.gate, mode)
             if byte:

@@ -28,7 +28,10 @@ def main():
     cases = [("random14", random_circuit(np.random.default_rng(11), 14, 80)),
              ("random18", random_circuit(np.random.default_rng(12), 18, 60)),
              ("bench20", benchmark(20)),
-             ("adder8", adder(8, [172, 83])[0])]
+             ("adder8", adder(8, [172, 83])[0]),
+             # large enough for overlapped swaps (chunk bits >= 12 outside the first pass)
+             ("random22", random_circuit(np.random.default_rng(13), 22, 90)),
+             ("bench23", benchmark(23))]
     ok = True
     for name, circ in cases:
         res = run_circuit_distributed(to_product(circ), dist)

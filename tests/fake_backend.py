@@ -60,6 +60,12 @@ class NumpyBackend:
         for gp, lp in pairs:
             self.swap(gp, lp)
 
+    def swap_then_apply(self, pairs, ops):
+        for gp, lp in pairs:
+            self.swap(gp, lp)
+        if ops:
+            self.apply_local(ops)
+
     def measure_local(self):
         n = self.n_local
         norm = float(np.real(np.vdot(self.psi, self.psi)))
