@@ -641,6 +641,8 @@ def run_b200_multi(args, dist, rank, world, device):
     probe_ms = [a.elapsed_ms(b) for a, b in be.swap_events]
     probe_ms_max = max_over_ranks(dist, max(probe_ms))
     nvlink = {"swaps_in_timed_steps": n_swaps, "swap_ms_in_timed_steps": round(swap_ms, 3),
+              "overlapped_swaps": be.overlapped,
+              "swap_ms_note": "with overlap, a swap's time includes the first pass after it",
               "probe_swaps": len(probe_ms), "probe_ms_per_swap_max": round(probe_ms_max, 3),
               "bytes_per_direction_per_swap": per_dir,
               "achieved_GBps_per_direction": round(per_dir / (probe_ms_max / 1e3) / 1e9, 1),

@@ -89,14 +89,15 @@ class CudaBackend:
         self.swap_timing = False
         self.swap_events = []
         self._overlap = None          # chunk events / swap stream, created on first overlapped swap
+        self.overlapped = 0
         dist.barrier()
 
     def apply_local(self, ops):
         self.dev.apply_fused(ops, self.tile_bits)
 
     # -- remap swap overlapped with the following pass ------------------------------------
-    OVERLAP_CHUNK_BITS = 3           # 8 chunks
-    OVERLAP_SWAP_BLOCKS = 256        # swap kernel grid while a pass runs beside it
+    OVERLAP_CHUNK_BITS = int(__import__("os").environ.get("SVB200_OVERLAP_CHUNK_BITS", "4"))   # 16 chunks
+    OVERLAP_SWAP_BLOCKS = int(__import__("os").environ.get("SVB200_OVERLAP_BLOCKS", "128"))   # swap grid (4 GPUs: 128 best of 64-1184)
 
     def _overlap_setup(self):
         """Second stream for the swap chunks and one inter-process event per chunk, the
@@ -177,6 +178,7 @@ class CudaBackend:
             self._overlap = ()
             self._overlap_setup()
         stream, own_ev, peer_ev = self._overlap
+        self.overlapped += 1
         lib = nat.load()
         L = self.dev.size
         k = len(pairs)
@@ -660,7 +662,8 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
                 led.gate_operations += 1
     flush()
     stats = {"swaps": swaps, "swap_groups": groups, "physical_link_bytes": be.link_bytes,
-             "planner": "remap" if remap else "reference"}
+             "planner": "remap" if remap else "reference",
+             "overlapped_swaps": getattr(be, "overlapped", 0)}
     if byte:
         stats.update(byte_passes=be.passes, byte_host_fixes=be.host_fixes)
     res = DistRunResult(circuit, layout, mode, rank, ledgers, report, tuple(planner.pos),
