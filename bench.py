@@ -553,38 +553,42 @@ def run_b200_multi(args, dist, rank, world, device):
             k = owner[st.ordinal]
             per_step[k] += pending_swaps + [st]
             pending_swaps = []
-    # each step as launch batches: ("ops", [sv_op]) or ("swapops", pairs, [sv_op]): a remap
-    # swap and the ops after it, the swap overlapped with their first pass
+    # each step as launch batches: ("ops", [sv_op]) or ("swapops", pairs, after, before): a remap
+    # swap with the ops before and after it -- the swap overlaps the last pass before it and
+    # the first pass after it (chunked, inter-process events)
     batches = []
     for k in range(len(seq)):
-        out, pend, swap = [], [], None
-
-        def close():
-            if swap is not None:
-                out.append(("swapops", swap, pend))
-            elif pend:
-                out.append(("ops", pend))
+        out, pend, swap, before = [], [], None, []
         for st in per_step[k]:
             if isinstance(st, (Swap, SwapGroup)):
-                close()
+                if swap is not None:
+                    out.append(("swapops", swap, pend, before))
+                    before = []
+                else:
+                    before = pend
                 pend = []
                 swap = ((st.global_pos, st.local_pos),) if isinstance(st, Swap) else st.pairs
             else:
                 op = phys_op(st.gate, st.qubits, n, rank)
                 if op is not None:
                     pend.append(op)
-        close()
+        if swap is not None:
+            out.append(("swapops", swap, pend, before))
+        elif pend:
+            out.append(("ops", pend))
         batches.append(out)
     from paper_2511_03359_b200.device import jit_prepare, jit_stats, jit_wait
+    from paper_2511_03359_b200.distributed import split_last_pass
     t_jit = time.perf_counter()
     for out in batches:
         for b in out:
             if b[0] == "ops":
                 jit_prepare(n, b[1], args.tile_bits)
-            else:            # the overlapped first pass and the rest are planned separately
+            else:            # the overlapped passes are planned on their own op ranges
                 first, rest = CudaBackend._first_pass(b[2])
-                jit_prepare(n, first, args.tile_bits)
-                jit_prepare(n, rest, args.tile_bits)
+                head, last = split_last_pass(n, nat.SV_FP64, b[3], args.tile_bits)
+                for part in (first, rest, head, last, b[2], b[3]):
+                    jit_prepare(n, part, args.tile_bits)
     jit_wait()
     t_jit = time.perf_counter() - t_jit
     be = CudaBackend(dist, n, pb.PrecisionMode.FP64, device, args.tile_bits)
@@ -594,13 +598,16 @@ def run_b200_multi(args, dist, rank, world, device):
             if b[0] == "ops":
                 be.apply_local(b[1])
             elif args.overlap:
-                be.swap_then_apply(b[1], b[2])
+                be.swap_then_apply(b[1], b[2], before=b[3])
             else:
+                if b[3]:
+                    be.apply_local(b[3])
                 if len(b[1]) == 1:
                     be.swap(*b[1][0])
                 else:
                     be.swap_group(b[1])
-                be.apply_local(b[2])
+                if b[2]:
+                    be.apply_local(b[2])
 
     for k in range(args.warmup):
         run_step(k)

@@ -249,6 +249,9 @@ int sv_jit_shutdown(void);                    /* drop queued compiles, wait for 
  * returns the number of new kernels queued */
 int sv_jit_prepare(int n_qubits, const sv_op* ops, int n_ops, int tile_bits);
 int sv_jit_prepare_mode(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits);  /* FP64 / FP32 */
+/* the pass split sv_apply_fused uses for ops: ends[p] = one past the last op of pass p;
+ * returns the number of passes (also queues their specialised kernels) */
+int sv_plan_passes(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int* ends, int cap);
 int sv_jit_stats(double* out6);               /* compiled, failed, jit launches, fallbacks, compile ms, cached */
 int sv_jit_available(void);                   /* 1 when NVRTC and the driver entry points resolved */
 /* CPU-side check: plan the first fused pass of ops on 2^n_qubits amplitudes, write

@@ -387,7 +387,8 @@ int choose_cfg(const sv_op* ops, int n_ops, int n) {
 // prepare != nullptr: plan only and queue the specialised kernels of the v3 passes for
 // compilation (sv_jit_prepare); *prepare counts them.  Nothing is launched.
 int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_ops, int tile_bits,
-               cudaStream_t st, int* prepare = nullptr, uint64_t chunk_mask = 0, uint64_t chunk_pat = 0) {
+               cudaStream_t st, int* prepare = nullptr, uint64_t chunk_mask = 0, uint64_t chunk_pat = 0,
+               std::vector<int>* pass_ends = nullptr) {
     if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "fused passes need FP64 or FP32 storage");
     if (!is_pow2(n_elems)) return fail(SV_EVALUE, "fused pass needs a power-of-two buffer");
     if (!prepare && (reinterpret_cast<uintptr_t>(psi) & 31) != 0)
@@ -420,6 +421,7 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
     PassPlan cur;
     auto flush = [&]() -> int {
         if (cur.ops.empty()) return SV_OK;
+        if (pass_ends) pass_ends->push_back(cur.ops.back() + 1);
         if (prepare) {
             static thread_local Fused2Params Pp;
             if (use_v3 && build_params2(ops, cur, n, cfg, Pp) == 0 &&
@@ -1003,6 +1005,18 @@ int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_
     }
     if (rc) return fail(SV_EVALUE, "NVRTC compile failed: %s", log.c_str());
     return (int)cur.ops.size();
+}
+
+int sv_plan_passes(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int* ends, int cap) {
+    if (n_qubits < 1 || n_qubits > 62) return fail(SV_EVALUE, "qubit count %d out of range", n_qubits);
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "passes are planned for FP64 / FP32 storage");
+    if (n_ops <= 0) return 0;
+    int queued = 0;
+    std::vector<int> e;
+    if (int rc = fused_impl(nullptr, 1ull << n_qubits, mode, ops, n_ops, tile_bits, nullptr, &queued, 0, 0, &e))
+        return rc;
+    for (size_t i = 0; i < e.size() && (int)i < cap; ++i) ends[i] = e[i];
+    return (int)e.size();
 }
 
 int sv_jit_prepare(int n_qubits, const sv_op* ops, int n_ops, int tile_bits) {

@@ -59,6 +59,19 @@ def phys_op(gate, phys: tuple, n_local: int, rank: int):
     return gate_op(nat.SV_OP_2Q, qa=phys[0], qb=phys[1], data=m)
 
 
+def split_last_pass(n_local: int, mode_code: int, ops, tile_bits: int = 12):
+    """(head, last): ops split before the last fused pass sv_apply_fused would run."""
+    ops = list(ops)
+    if not ops:
+        return [], []
+    ends = (ctypes.c_int * len(ops))()
+    n = nat.load(require_device=False).sv_plan_passes(n_local, mode_code, ops_array(ops), len(ops), tile_bits,
+                                                      ends, len(ops))
+    nat.check(min(n, 0))
+    start = ends[n - 2] if n > 1 else 0
+    return ops[:start], ops[start:]
+
+
 class CudaBackend:
     """This rank's slice in HBM plus IPC-mapped slices of every other rank."""
 
@@ -106,7 +119,7 @@ class CudaBackend:
         C = 1 << self.OVERLAP_CHUNK_BITS
         stream = nat.Stream(self.dev.device)
         own, handles = [], bytearray()
-        for _ in range(C):
+        for _ in range(2 * C):       # [0, C): swap chunk done; [C, 2C): pass-before chunk done
             ev = ctypes.c_void_p()
             h = (ctypes.c_char * 64)()
             nat.check(lib.sv_event_create_ipc(ctypes.byref(ev), h))
@@ -119,7 +132,7 @@ class CudaBackend:
             if r == self.rank:
                 continue
             evs = []
-            for i in range(C):
+            for i in range(2 * C):
                 ev = ctypes.c_void_p()
                 buf = (ctypes.c_char * 64).from_buffer_copy(hb[64 * i:64 * (i + 1)])
                 nat.check(lib.sv_event_open_ipc(buf, ctypes.byref(ev)))
@@ -157,7 +170,10 @@ class CudaBackend:
             need |= m
         return ops, []
 
-    def swap_then_apply(self, pairs, ops) -> None:
+    def _last_pass(self, ops):
+        return split_last_pass(self.n_local, self.dev.mode_code, ops, self.tile_bits)
+
+    def swap_then_apply(self, pairs, ops, before=()) -> None:
         """A remap swap (one or k global qubits) followed by the fused passes of `ops`, with
         the swap's transfer overlapping the first pass: the swap runs on a second stream in
         chunks (fixed values of three high local bits outside the pass tile); the pass runs
@@ -165,8 +181,11 @@ class CudaBackend:
         partners' swap of that chunk (inter-process events).  Same amplitudes, same
         arithmetic as swap + apply_local."""
         first, rest = self._first_pass(ops)
-        bits = self._chunk_bits(pairs, first) if first and self.mode is PrecisionMode.FP64 else []
+        head, last = self._last_pass(list(before)) if before else ([], [])
+        bits = self._chunk_bits(pairs, list(first) + list(last)) if first and self.mode is PrecisionMode.FP64 else []
         if not bits:
+            if before:
+                self.apply_local(list(before))
             if len(pairs) == 1:
                 self.swap(*pairs[0])
             else:
@@ -186,13 +205,33 @@ class CudaBackend:
         cmask = sum(1 << b for b in bits)
         half = (L >> (k + len(bits))) // 2
         C = 1 << len(bits)
+        members = [m for m, *_ in sched]
         prev_blocks = lib.sv_swap_blocks(self.OVERLAP_SWAP_BLOCKS)
-        self._sync_all()
-        if self.swap_timing:
-            e0 = nat.Event()
-            e0.record(self.dev.stream)
+        if last:
+            # three stages: the last pass before the swap runs chunk by chunk too, and each
+            # swap chunk waits for that chunk of the pass on this rank and every partner
+            if head:
+                self.apply_local(head)
+            if self.swap_timing:
+                e0 = nat.Event()
+                e0.record(self.dev.stream)
+            arr_l = ops_array(last)
+            for i in range(C):
+                nat.check(lib.sv_apply_fused_chunk(self.dev.handle, arr_l, len(last), self.tile_bits, cmask,
+                                                   deposit(i, bits)))
+                nat.check(lib.sv_event_record(own_ev[C + i], self.dev.stream))
+            self.dist.barrier()      # every rank's pass-chunk events are recorded
+        else:
+            self._sync_all()
+            if self.swap_timing:
+                e0 = nat.Event()
+                e0.record(self.dev.stream)
         for i in range(C):
             cpat = deposit(i, bits)
+            if last:
+                nat.check(lib.sv_stream_wait_event(stream.ptr, own_ev[C + i]))
+                for m in members:
+                    nat.check(lib.sv_stream_wait_event(stream.ptr, peer_ev[m][C + i]))
             for member, vmask, own_pat, peer_pat, t0, cnt in sched:
                 nat.check(lib.svk_swap_group_chunk(self.dev.ptr, self.peers[member], L, self.dev.mode_code, vmask,
                                                    own_pat, peer_pat, cmask, cpat, 0 if t0 == 0 else half, half,
@@ -201,7 +240,6 @@ class CudaBackend:
             nat.check(lib.sv_event_record(own_ev[i], stream.ptr))
         lib.sv_swap_blocks(prev_blocks)
         self.dist.barrier()          # every rank's chunk events are recorded (enqueued)
-        members = [m for m, *_ in sched]
         arr = ops_array(first)
         for i in range(C):
             nat.check(lib.sv_stream_wait_event(self.dev.stream, own_ev[i]))
@@ -617,27 +655,32 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
     report = None
     swaps = groups = 0
     pending_swap = None          # FP backends: a swap waits for the ops after it (overlapped)
+    pending_before = []          # ... and keeps the ops before it (the last pass overlaps too)
     overlap = overlap and not byte and hasattr(be, "swap_then_apply")
 
     def flush():
-        nonlocal pending, pending_swap
+        nonlocal pending, pending_swap, pending_before
         if pending_swap is not None:
-            be.swap_then_apply(pending_swap, pending)
-            pending_swap = None
+            be.swap_then_apply(pending_swap, pending, before=pending_before)
+            pending_swap, pending_before = None, []
         elif pending:
             be.apply_local(pending)
         pending = []
 
     for step in steps:
         if isinstance(step, (Swap, SwapGroup)):
-            flush()
             pairs = ((step.global_pos, step.local_pos),) if isinstance(step, Swap) else step.pairs
             if overlap:
+                if pending_swap is not None:     # two swaps back to back: run the first
+                    flush()
+                pending_before, pending = pending, []
                 pending_swap = pairs
-            elif isinstance(step, Swap):
-                be.swap(step.global_pos, step.local_pos)
             else:
-                be.swap_group(step.pairs)
+                flush()
+                if isinstance(step, Swap):
+                    be.swap(step.global_pos, step.local_pos)
+                else:
+                    be.swap_group(step.pairs)
             swaps += 1
             groups += isinstance(step, SwapGroup)
         elif isinstance(step, PhysGate):

@@ -60,7 +60,9 @@ class NumpyBackend:
         for gp, lp in pairs:
             self.swap(gp, lp)
 
-    def swap_then_apply(self, pairs, ops):
+    def swap_then_apply(self, pairs, ops, before=()):
+        if before:
+            self.apply_local(list(before))
         for gp, lp in pairs:
             self.swap(gp, lp)
         if ops:
