@@ -341,6 +341,37 @@ class CudaBackend:
         self.link_bytes += half * self.bpe
         return complex(out[0], out[1])
 
+    def pair_dots(self, positions):
+        """pair_dot of several global qubits on the second stream with no host barrier in
+        between (the caller synchronised all ranks): runs on a worker thread while the local
+        measurement passes stream HBM on the main stream -- NVLink-bound next to HBM-bound."""
+        if self._overlap is None:
+            self._overlap = ()
+            self._overlap_setup()
+        stream = self._overlap[0]
+        lib = nat.load()
+        nat.check(lib.sv_set_device(self.dev.device))
+        prev = lib.sv_swap_blocks(self.OVERLAP_SWAP_BLOCKS)
+        half = self.dev.size // 2
+        esz = np.dtype(self.dev.dtype).itemsize
+        out = {}
+        try:
+            for global_pos in positions:
+                bit = global_pos - self.n_local
+                partner = self.rank ^ (1 << bit)
+                low = ((self.rank >> bit) & 1) == 0
+                a0, a1 = (self.dev.ptr, self.peers[partner]) if low else (self.peers[partner], self.dev.ptr)
+                off = 0 if low else half
+                res = np.zeros(2)
+                nat.check(lib.svk_pair_dot(ctypes.c_void_p(a0.value + off * esz),
+                                           ctypes.c_void_p(a1.value + off * esz), half, self.dev.mode_code,
+                                           nat.dptr(res), stream.ptr))
+                self.link_bytes += half * self.bpe
+                out[global_pos] = complex(res[0], res[1])
+        finally:
+            lib.sv_swap_blocks(prev)
+        return out
+
     def export(self) -> np.ndarray:
         return self.dev.export()
 
@@ -754,13 +785,33 @@ def _measure(be, layout, ledgers, perm, rank, mode, dist):
         for r in range(layout.rank_count):
             ledgers[r].count_send(half_bytes)
             ledgers[r ^ m].count_receive(half_bytes)
-    norm, ones_l, cross_l = be.measure_local()
+    remote = {}
+    if hasattr(be, "pair_dots") and n > n_local:
+        # global-qubit cross sums (NVLink) concurrently with the local passes (HBM)
+        import threading
+        be._sync_all()
+        box = {}
+
+        def work():
+            try:
+                box["v"] = be.pair_dots(range(n_local, n))
+            except BaseException as exc:   # re-raised on the calling thread
+                box["e"] = exc
+        th = threading.Thread(target=work)
+        th.start()
+        norm, ones_l, cross_l = be.measure_local()
+        th.join()
+        if "e" in box:
+            raise box["e"]
+        remote = box["v"]
+    else:
+        norm, ones_l, cross_l = be.measure_local()
     ones_p = np.zeros(n)
     cross_p = np.zeros(n, dtype=np.complex128)
     ones_p[:n_local] = ones_l
     cross_p[:n_local] = cross_l
     for p in range(n_local, n):
-        cross_p[p] = be.pair_dot(p)
+        cross_p[p] = remote[p] if p in remote else be.pair_dot(p)
         ones_p[p] = norm if (rank >> (p - n_local)) & 1 else 0.0
     vec = torch.tensor(np.concatenate([[norm], ones_p, cross_p.real, cross_p.imag]), dtype=torch.float64)
     dist.all_reduce(vec)
