@@ -1194,8 +1194,7 @@ int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, doubl
     if (count == 0) return SV_OK;
     int dev = 0;
     cudaGetDevice(&dev);
-    const uint64_t gcap = sv::g_swap_blocks > 0 ? (uint64_t)sv::g_swap_blocks : (uint64_t)sm_count(dev) * 4;
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((count + 255) / 256, gcap));
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((count + 1023) / 1024, (uint64_t)sm_count(dev) * 2));
     double* part = nullptr;
     cudaStream_t st = as_stream(stream);
     CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), 16 * grid, st), "pair dot scratch");

@@ -149,14 +149,40 @@ cudaError_t launch_swap_group(void* own, void* peer, uint64_t t0, uint64_t n, in
                                           peer_pat, cmask, cpat, st);
 }
 
+// 4 independent 32-byte loads of each side per iteration: the remote side is an NVLink read,
+// so enough requests must be in flight per thread to cover its latency
 template <typename S>
 __global__ void __launch_bounds__(256) k_pair_dot(const S* __restrict__ a0, const S* __restrict__ a1, uint64_t n,
                                                   double* __restrict__ partials) {
+    constexpr int V = Store<S>::V, U = 4;
     double re = 0.0, im = 0.0;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const cplx x = Store<S>::get(a0[i]), y = Store<S>::get(a1[i]);
-        re += x.re * y.re + x.im * y.im;
-        im += x.re * y.im - x.im * y.re;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(a0) | reinterpret_cast<uintptr_t>(a1)) & 31) == 0;
+    const uint64_t nv = aligned ? n / V : 0, step = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w0 < nv; w0 += U * step) {
+        Vec<S> x[U], y[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t w = w0 + u * step;
+            if (w < nv) {
+                x[u] = vload(a0 + w * V);
+                y[u] = vload(a1 + w * V);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (w0 + u * step >= nv) continue;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const cplx a = Store<S>::get(x[u].a[v]), b = Store<S>::get(y[u].a[v]);
+                re += a.re * b.re + a.im * b.im;
+                im += a.re * b.im - a.im * b.re;
+            }
+        }
+    }
+    for (uint64_t i = nv * V + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += step) {   // tail
+        const cplx a = Store<S>::get(a0[i]), b = Store<S>::get(a1[i]);
+        re += a.re * b.re + a.im * b.im;
+        im += a.re * b.im - a.im * b.re;
     }
     __shared__ double sr[8], si[8];
 #pragma unroll
