@@ -93,6 +93,9 @@ int sv_create(int device, int n_qubits, int mode, sv_handle* out);
 int sv_destroy(sv_handle h);
 /* state.py:49-63 zero_state: all zeros, amplitude 1 at index `unit` (-1: none) */
 int sv_zero_state(sv_handle h, int64_t unit);
+/* the same state, recorded only: the first fused pass generates its tiles instead of reading
+ * them (no memset, one HBM read fewer); every other entry point writes the state first */
+int sv_zero_state_lazy(sv_handle h, int64_t unit);
 int sv_info(sv_handle h, int* device, int* n_qubits, int* mode, void** dev_ptr, void** stream);
 int sv_apply_1q(sv_handle h, int q, const double* m8);
 int sv_apply_2q(sv_handle h, int qa, int qb, const double* m32);

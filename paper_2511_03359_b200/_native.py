@@ -52,6 +52,7 @@ _SIGNATURES = {
     "sv_create": ([_I, _I, _I, ctypes.POINTER(_P)], _I),
     "sv_destroy": ([_P], _I),
     "sv_zero_state": ([_P, ctypes.c_int64], _I),
+    "sv_zero_state_lazy": ([_P, ctypes.c_int64], _I),
     "sv_info": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I),
                  ctypes.POINTER(_P), ctypes.POINTER(_P)], _I),
     "sv_apply_1q": ([_P, _I, _D], _I),

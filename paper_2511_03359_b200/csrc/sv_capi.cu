@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -215,6 +216,7 @@ int classify(const double* m, int dim, uint32_t* mono) {
 
 int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Params& P) {
     std::memset(&P, 0, sizeof(P));
+    P.vinit = -2;                       // read the tiles (see fused_impl for lazy basis states)
     const int K = (cfg == 2 || cfg == 4 || cfg == 6) ? 11 : ((cfg == 5 || cfg == 7) ? 10 : (cfg == 10 ? 13 : 12));
     const int RB = (cfg == 1 || cfg == 6 || cfg == 7 || cfg == 8 || cfg == 10) ? 4 : 3;
     const int NTH = 1 << (K - RB);
@@ -386,9 +388,13 @@ int choose_cfg(const sv_op* ops, int n_ops, int n) {
 
 // prepare != nullptr: plan only and queue the specialised kernels of the v3 passes for
 // compilation (sv_jit_prepare); *prepare counts them.  Nothing is launched.
+// init != nullptr (*init != -2): the buffer holds |*init> (-1: zeros) only virtually; the first
+// pass generates its tiles if its specialised kernel is ready, otherwise materialize() writes
+// the state first.  *init is set to -2 once the state is real.
 int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_ops, int tile_bits,
                cudaStream_t st, int* prepare = nullptr, uint64_t chunk_mask = 0, uint64_t chunk_pat = 0,
-               std::vector<int>* pass_ends = nullptr) {
+               std::vector<int>* pass_ends = nullptr, int64_t* init = nullptr,
+               const std::function<int()>& materialize_fn = nullptr) {
     if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "fused passes need FP64 or FP32 storage");
     if (!is_pow2(n_elems)) return fail(SV_EVALUE, "fused pass needs a power-of-two buffer");
     if (!prepare && (reinterpret_cast<uintptr_t>(psi) & 31) != 0)
@@ -475,14 +481,41 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
         if (use_v3 && build_params2(ops, cur, n, cfg, P2) == 0 &&
             (g_seg_limit <= 0 || P2.n_segs <= g_seg_limit)) {
             P2.storage = mode;
+            P2.vinit = -2;
+            if (init && *init != -2) {
+                P2.vinit = *init;
+                const int jr0 = jit_launch_fused(psi, P2, st);
+                if (jr0 < 0) return cuda_fail(cudaErrorLaunchFailure, "fused pass launch");
+                if (jr0 == 0) {          // generated its input: the state is real from here on
+                    *init = -2;
+                    if (g_timing) {
+                        cudaEventRecord(ev1, st);
+                        std::lock_guard<std::mutex> lk(g_timing_mu);
+                        g_timed.push_back({ev0, ev1, 1.0 * (double)n_elems * (mode == SV_FP32 ? 8.0 : 16.0)});
+                    }
+                    cur = PassPlan();
+                    return SV_OK;
+                }
+                if (int rc = materialize_fn ? materialize_fn() : SV_OK) return rc;   // not compiled yet
+                *init = -2;
+                P2.vinit = -2;
+            }
             const int jr = jit_launch_fused(psi, P2, st);
             count_h2d(sizeof(Fused2Params));
             if (jr < 0) e = cudaErrorLaunchFailure;
             else if (jr == 0) e = cudaSuccess;
             else e = mode == SV_FP64 ? launch_fused2(psi, mode, P2, st) : v1();   // not compiled yet
         } else if (mode == SV_FP32 && use_v3) {
+            if (init && *init != -2) {
+                if (int rc = materialize_fn ? materialize_fn() : SV_OK) return rc;
+                *init = -2;
+            }
             e = v1();
         } else {
+            if (init && *init != -2) {
+                if (int rc = materialize_fn ? materialize_fn() : SV_OK) return rc;
+                *init = -2;
+            }
             static thread_local FusedParams P;
             build_params(ops, cur, n, k, P);
             e = launch_fused(psi, mode, P, st);
@@ -766,7 +799,11 @@ struct sv_state {
     cudaStream_t stream;
     double* partials;
     size_t partial_cap;
+    int64_t lazy = -2;      // sv_zero_state_lazy: -1 all zeros / unit index not yet written, -2 none
 };
+extern "C" {
+static int materialize(sv_handle h);
+}
 
 namespace {
 struct DeviceGuard {
@@ -934,6 +971,10 @@ int sv_destroy(sv_handle h) {
 
 int sv_info(sv_handle h, int* device, int* n_qubits, int* mode, void** dev_ptr, void** stream) {
     if (!h) return fail(SV_EVALUE, "null handle");
+    if (dev_ptr) {   // the caller may touch the buffer directly
+        DeviceGuard g(h->device);
+        if (int rc = materialize(h)) return rc;
+    }
     if (device) *device = h->device;
     if (n_qubits) *n_qubits = h->n;
     if (mode) *mode = h->mode;
@@ -944,6 +985,7 @@ int sv_info(sv_handle h, int* device, int* n_qubits, int* mode, void** dev_ptr, 
 
 int sv_zero_state(sv_handle h, int64_t unit) {
     DeviceGuard g(h->device);
+    h->lazy = -2;
     const size_t eb = elem_bytes(h->mode);
     const uint64_t n = 1ull << h->n;
     CUDA_TRY(cudaMemsetAsync(h->ptr, 0, eb * n, h->stream), "zero state");
@@ -960,16 +1002,33 @@ int sv_zero_state(sv_handle h, int64_t unit) {
     return SV_OK;
 }
 
+// |unit> (or all zeros) recorded but not written: the first fused pass generates its tiles
+// instead of reading them (saves the memset and one full read); any other use writes it now
+int sv_zero_state_lazy(sv_handle h, int64_t unit) {
+    if (unit >= (int64_t)(1ull << h->n)) return fail(SV_EINDEX, "unit index %lld outside the state", (long long)unit);
+    h->lazy = unit < 0 ? -1 : unit;
+    return SV_OK;
+}
+
+static int materialize(sv_handle h) {
+    if (h->lazy == -2) return SV_OK;
+    const int64_t u = h->lazy;
+    return sv_zero_state(h, u);   // clears h->lazy
+}
+
 int sv_apply_1q(sv_handle h, int q, const double* m8) {
     DeviceGuard g(h->device);
+    if (int rc = materialize(h)) return rc;
     return svk_apply_1q(h->ptr, 1ull << h->n, h->mode, q, m8, h->stream);
 }
 int sv_apply_2q(sv_handle h, int qa, int qb, const double* m32) {
     DeviceGuard g(h->device);
+    if (int rc = materialize(h)) return rc;
     return svk_apply_2q(h->ptr, 1ull << h->n, h->mode, qa, qb, m32, h->stream);
 }
 int sv_apply_diag(sv_handle h, uint64_t mask, const double* f2) {
     DeviceGuard g(h->device);
+    if (int rc = materialize(h)) return rc;
     return svk_apply_diag(h->ptr, 1ull << h->n, h->mode, mask, f2, h->stream);
 }
 int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_t cap, double* compile_ms) {
@@ -1034,6 +1093,7 @@ int sv_jit_prepare_mode(int n_qubits, int mode, const sv_op* ops, int n_ops, int
 int sv_apply_fused_chunk(sv_handle h, const sv_op* ops, int n_ops, int tile_bits, uint64_t chunk_mask,
                          uint64_t chunk_pattern) {
     DeviceGuard g(h->device);
+    if (int rc = materialize(h)) return rc;
     if (n_ops <= 0) return SV_OK;
     if ((chunk_pattern & ~chunk_mask) || (chunk_mask >> h->n)) return fail(SV_EINDEX, "chunk mask outside the state");
     return fused_impl(h->ptr, 1ull << h->n, h->mode, ops, n_ops, tile_bits, h->stream, nullptr, chunk_mask,
@@ -1042,16 +1102,26 @@ int sv_apply_fused_chunk(sv_handle h, const sv_op* ops, int n_ops, int tile_bits
 
 int sv_apply_fused(sv_handle h, const sv_op* ops, int n_ops, int tile_bits) {
     DeviceGuard g(h->device);
+    if (n_ops <= 0) return SV_OK;
+    if (h->lazy != -2) {   // lazy |unit>: the first pass generates its input tiles
+        int64_t init = h->lazy;
+        const int rc = fused_impl(h->ptr, 1ull << h->n, h->mode, ops, n_ops, tile_bits, h->stream, nullptr, 0, 0,
+                                  nullptr, &init, [&]() { return materialize(h); });
+        if (rc == SV_OK) h->lazy = -2;
+        return rc;
+    }
     return svk_apply_fused(h->ptr, 1ull << h->n, h->mode, ops, n_ops, tile_bits, h->stream);
 }
 int sv_measure(sv_handle h, double* norm, double* ones, double* cross) {
     DeviceGuard g(h->device);
+    if (int rc = materialize(h)) return rc;
     return measure_impl(h->ptr, 1ull << h->n, h->mode, norm, ones, cross, h->partials, h->partial_cap,
                         h->stream);
 }
 
 int sv_export(sv_handle h, void* host, uint64_t first, uint64_t count) {
     DeviceGuard g(h->device);
+    if (int rc = materialize(h)) return rc;
     const uint64_t n = 1ull << h->n;
     if (first > n || count > n - first) return fail(SV_EINDEX, "export range outside the state");
     const size_t eb = elem_bytes(h->mode);
@@ -1064,6 +1134,7 @@ int sv_export(sv_handle h, void* host, uint64_t first, uint64_t count) {
 
 int sv_import(sv_handle h, const void* host, uint64_t first, uint64_t count) {
     DeviceGuard g(h->device);
+    if (int rc = materialize(h)) return rc;
     const uint64_t n = 1ull << h->n;
     if (first > n || count > n - first) return fail(SV_EINDEX, "import range outside the state");
     const size_t eb = elem_bytes(h->mode);
@@ -1076,6 +1147,7 @@ int sv_import(sv_handle h, const void* host, uint64_t first, uint64_t count) {
 
 int sv_synchronize(sv_handle h) {
     DeviceGuard g(h->device);
+    if (int rc = materialize(h)) return rc;
     CUDA_TRY(cudaStreamSynchronize(h->stream), "synchronize");
     return SV_OK;
 }
@@ -1130,6 +1202,7 @@ int sv_pass_timing_read(uint64_t* passes, double* ms, double* bytes) {
 
 int sv_ipc_handle(sv_handle h, void* out64) {
     DeviceGuard g(h->device);
+    if (int rc = materialize(h)) return rc;
     cudaIpcMemHandle_t ih;
     CUDA_TRY(cudaIpcGetMemHandle(&ih, h->ptr), "cudaIpcGetMemHandle");
     static_assert(sizeof(ih) == 64, "IPC handle size");

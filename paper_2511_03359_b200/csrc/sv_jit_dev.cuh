@@ -91,7 +91,7 @@ __device__ __forceinline__ cplx rmul(double m, cplx a) { return {__dmul_rn(m, a.
 // constant loads ptxas hoists every matrix of the pass out of the tile loop, the
 // uniform registers overflow into ~130 regular registers for a few U4 gates and the
 // kernel spills; a per-use LDC costs one instruction per entry per tile.
-constexpr int kArgsM = 24;   // byte offset of Args::m (after n_tiles, cmask, cpat)
+constexpr int kArgsM = 32;   // byte offset of Args::m (after n_tiles, cmask, cpat, vinit)
 
 // tile index t of a chunked launch -> full tile index: zeros inserted at the bits of cm,
 // then the chunk pattern

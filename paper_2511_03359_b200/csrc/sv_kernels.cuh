@@ -48,6 +48,8 @@ struct Fused2Params {
     int storage;                        // SV_FP64 / SV_FP32 (FP32 only through the specialised kernel)
     uint64_t cmask_t, cpat_t;           // chunked pass: tile-index bits fixed to cpat_t (n_tiles counts
                                         // the remaining tiles); 0, 0 = every tile
+    int64_t vinit;                      // -2: read the tiles; -1 / u: generate them (all zeros / |u>),
+                                        // specialised kernel only (lazy zero state, first pass)
     int8_t tq[13];                      // tile position -> qubit (2^13 tiles: config 10)
     uint8_t seg_reg[kMaxSegs][4];       // register bit j -> tile position
     uint8_t seg_thr[kMaxSegs][9];       // thread-id bit j -> tile position

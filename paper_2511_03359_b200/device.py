@@ -97,8 +97,11 @@ class DeviceState:
         self.launches += launches
 
     # -- initialisation / transfer ---------------------------------------------
-    def zero(self, unit_index: int | None = 0) -> None:
-        nat.check(nat.load().sv_zero_state(self.handle, -1 if unit_index is None else unit_index))
+    def zero(self, unit_index: int | None = 0, lazy: bool = False) -> None:
+        """|unit_index> (None: all zeros).  lazy=True records it only: the first fused pass
+        generates its tiles instead of reading them (sv_zero_state_lazy)."""
+        fn = nat.load().sv_zero_state_lazy if lazy else nat.load().sv_zero_state
+        nat.check(fn(self.handle, -1 if unit_index is None else unit_index))
         self._touch(0)
 
     def export(self, first: int = 0, count: int | None = None) -> np.ndarray:
@@ -120,7 +123,10 @@ class DeviceState:
         self.import_(values, first)
 
     def element_ptr(self, index: int) -> ctypes.c_void_p:
-        return ctypes.c_void_p(self.ptr.value + int(index) * np.dtype(self.dtype).itemsize)
+        # sv_info with a pointer out-argument writes a lazily recorded basis state first
+        p = ctypes.c_void_p()
+        nat.check(nat.load().sv_info(self.handle, None, None, None, ctypes.byref(p), None))
+        return ctypes.c_void_p(p.value + int(index) * np.dtype(self.dtype).itemsize)
 
     def measure_range(self, first: int, count: int):
         """(norm, ones, cross) of the sub-buffer [first, first + count), count = 2**k."""

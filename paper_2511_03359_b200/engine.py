@@ -149,7 +149,10 @@ class _Engine:
         else:
             from .device import DeviceState
             self.dev = DeviceState(circuit.n_qubits, mode, device=device)
-        self.dev.zero(0)
+        if mode is PrecisionMode.BYTE:
+            self.dev.zero(0)
+        else:   # the first fused pass generates |0..0> instead of reading a written state
+            self.dev.zero(0, lazy=fuse)
         L = layout.local_size
         self.states = [LocalState(layout.local_qubits, mode, _device_state=self.dev, _offset=r * L)
                        for r in range(n)]
