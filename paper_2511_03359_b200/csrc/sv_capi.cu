@@ -581,10 +581,6 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
         for (int f = bmin; popcount64(t) < K; ++f) t |= 1ull << f;
         passes.push_back(t);
     }
-    auto swz_h = [](int e) {
-        const int g = (((e >> 3) & 1) * 7) ^ (((e >> 4) & 1) * 3) ^ (((e >> 5) & 1) * 5) ^ (((e >> 6) & 1) * 6);
-        return e ^ g;
-    };
     uint64_t done = 0;
     int rc = SV_OK;
     static thread_local Measure3Params P;
@@ -623,12 +619,47 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
             int t = 0;
             for (int pos = 0; pos < K; ++pos)
                 if (!((regs >> pos) & 1)) P.seg_thr[sg][t++] = (uint8_t)pos;
-            for (int i = 0; i < 16; ++i) {
-                int e = 0;
-                for (int bit = 0; bit < RB; ++bit)
-                    if ((i >> bit) & 1) e |= 1 << P.seg_reg[sg][bit];
-                P.seg_rsw[sg][i] = (uint16_t)swz_h(e);
+        }
+        // swizzle columns with a conflict-free quarter-warp in every segment (as sv_jit.cu):
+        // segment 0 of the first pass has registers at positions 0..3, where the fixed
+        // columns 7,3,5,6 give 2-way conflicts
+        {
+            auto contrib = [](int pos, const int* c) { return pos < 3 ? (1 << pos) : (pos < 7 ? c[pos - 3] : 0); };
+            auto ok = [&](const int* c) {
+                for (int sg = 0; sg < P.n_segs; ++sg) {
+                    const int a = contrib(P.seg_thr[sg][0], c), b2 = contrib(P.seg_thr[sg][1], c),
+                              d = contrib(P.seg_thr[sg][2], c);
+                    if (!a || !b2 || !d || a == b2 || a == d || b2 == d || (a ^ b2) == d) return false;
+                }
+                return true;
+            };
+            int cols[4] = {7, 3, 5, 6};
+            if (!ok(cols)) {
+                bool found = false;
+                int c[4];
+                for (c[0] = 1; c[0] < 8 && !found; ++c[0])
+                    for (c[1] = 1; c[1] < 8 && !found; ++c[1])
+                        for (c[2] = 1; c[2] < 8 && !found; ++c[2])
+                            for (c[3] = 1; c[3] < 8 && !found; ++c[3])
+                                if (ok(c)) {
+                                    for (int i = 0; i < 4; ++i) cols[i] = c[i];
+                                    found = true;
+                                }
             }
+            for (int i = 0; i < 4; ++i) P.swz_cols[i] = (uint8_t)cols[i];
+            auto swz_h = [&](int e) {
+                int g = 0;
+                for (int bb = 3; bb < 7; ++bb)
+                    if ((e >> bb) & 1) g ^= cols[bb - 3];
+                return e ^ g;
+            };
+            for (int sg = 0; sg < P.n_segs; ++sg)
+                for (int i = 0; i < 16; ++i) {
+                    int e = 0;
+                    for (int bit = 0; bit < RB; ++bit)
+                        if ((i >> bit) & 1) e |= 1 << P.seg_reg[sg][bit];
+                    P.seg_rsw[sg][i] = (uint16_t)swz_h(e);
+                }
         }
         for (int jj = 0; jj < 16; ++jj) {
             uint64_t off = 0;

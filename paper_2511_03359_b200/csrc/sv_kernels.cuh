@@ -113,6 +113,7 @@ struct Measure3Params {
     uint8_t seg_thr[3][8];              // thread-id bit j -> tile position
     uint16_t seg_rsw[3][16];            // swizzled shared-memory offset of register slot i
     uint32_t cross_reg[3];              // register bits whose cross term the segment produces
+    uint8_t swz_cols[4];                // shared-memory swizzle: columns XORed in by tile bits 3..6
     uint64_t pf_go[16];                 // HBM offset of tile element j * threads (prefetch chunks)
     uint64_t base_tab[4][256];          // tile index byte -> local-index bits outside the tile
 };

@@ -24,8 +24,10 @@ namespace sv {
 
 namespace {
 
-__device__ __forceinline__ int swz3(int e) {
-    const int g = (((e >> 3) & 1) * 7) ^ (((e >> 4) & 1) * 3) ^ (((e >> 5) & 1) * 5) ^ (((e >> 6) & 1) * 6);
+// swizzle with the pass's columns (chosen on the host so that every segment's quarter-warp
+// loads are conflict-free)
+__device__ __forceinline__ int swz3(int e, const uint8_t (&c)[4]) {
+    const int g = (((e >> 3) & 1) * c[0]) ^ (((e >> 4) & 1) * c[1]) ^ (((e >> 5) & 1) * c[2]) ^ (((e >> 6) & 1) * c[3]);
     return e ^ g;
 }
 
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
 #pragma unroll
     for (int j = 0; j < TB; ++j)
         if ((tid >> j) & 1) go_tid += 1ull << p.tq[j];
-    const int sw_tid = swz3(tid);
+    const int sw_tid = swz3(tid, p.swz_cols);
     __syncthreads();
 
     auto tile_base = [&](uint64_t t) {
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
                 const unsigned mi = (wm[i >> 2] >> (8 * (i & 3))) & 255u, pi = (wp[i >> 2] >> (8 * (i & 3))) & 255u;
                 const double m = dtab[mi];
                 const cplx v = mi == 0 ? cplx{0.0, 0.0} : cplx{__dmul_rn(m, dtab[256 + pi]), __dmul_rn(m, dtab[512 + pi])};
-                S[swz3(16 * tid + i)] = v;
+                S[swz3(16 * tid + i, p.swz_cols)] = v;
             }
         } else {
             if (next < p.n_tiles) prefetch(next, bufs + ((it + 1) & 1) * TILE);
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
             int tb = 0;
 #pragma unroll
             for (int j = 0; j < TB; ++j) tb |= ((tid >> j) & 1) << p.seg_thr[s][j];
-            const int tsw = swz3(tb);
+            const int tsw = swz3(tb, p.swz_cols);
             cplx r[R];
 #pragma unroll
             for (int i = 0; i < R; ++i) r[i] = S[tsw ^ p.seg_rsw[s][i]];
