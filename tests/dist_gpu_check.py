@@ -63,6 +63,19 @@ def main():
         res.backend.close()
     from paper_2511_03359_b200 import PrecisionMode
     from tests.circuits import exact_class_circuit
+    # FP32 storage across GPUs (remap swaps move complex64 amplitudes)
+    for name, circ in [("random16_fp32", random_circuit(np.random.default_rng(21), 16, 70)),
+                       ("bench18_fp32", benchmark(18))]:
+        res = run_circuit_distributed(to_product(circ), dist, mode=PrecisionMode.FP32)
+        state = res.gathered_state(dist)
+        if rank == 0:
+            want = ref_engine.run_circuit(circ, ranks=world, mode="fp32")
+            same = np.array_equal(state, want.gathered_state())
+            led = [l.snapshot() for l in res.ledgers] == want.ledgers
+            print(f"[dist {world} GPUs] {name}: state bit-exact={same} ledgers={led} stats={res.device_stats}",
+                  flush=True)
+            ok = ok and same and led
+        res.backend.close()
     byte_cases = [("bench14_be", benchmark(14)), ("exact12_be", exact_class_circuit(np.random.default_rng(5), 12, 40)),
                   ("random12_be", random_circuit(np.random.default_rng(6), 12, 30)),
                   ("adder6_be", adder(6, [45, 18])[0])]
