@@ -59,6 +59,10 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
     double* red = ow + NW * kOutMax;                                                 // [NW][1 + 3 KB]
     constexpr int NSL = 1 + 3 * KB;
     double* dtab = red + NW * NSL;                                                   // BYTE: dmag, dux, duy
+    // BYTE: ring of NSTAGE raw tiles (magnitude bytes, phase bytes) filled by cp.async, so that
+    // NSTAGE - 1 tiles of bytes are in flight while one is decoded
+    constexpr int NSTAGE = 4;
+    unsigned char* stage = reinterpret_cast<unsigned char*>(dtab + 768);                // [NSTAGE][2][TILE]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int i = tid; i < NW * kOutMax; i += NT) ow[i] = 0.0;
     for (int i = tid; i < NW * NSL; i += NT) red[i] = 0.0;
@@ -95,16 +99,21 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
         for (int j = 0; j < KB - 4; ++j)
             if ((tid >> j) & 1) go_chunk += 1ull << p.tq[4 + j];
     }
-    uint4 nm = {0, 0, 0, 0}, np = {0, 0, 0, 0};
-    auto fetch_bytes = [&](uint64_t t) {
+    auto fetch_bytes = [&](uint64_t t, int sidx) {
         const uint64_t a = tile_base(t) + go_chunk;
-        nm = *reinterpret_cast<const uint4*>(bsrc.mi + a);
-        np = *reinterpret_cast<const uint4*>(bsrc.pi + a);
+        unsigned char* st = stage + (size_t)sidx * 2 * TILE;
+        cp_async16m(st + 16 * tid, bsrc.mi + a);
+        cp_async16m(st + TILE + 16 * tid, bsrc.pi + a);
     };
 
     uint64_t tile = blockIdx.x;
     if constexpr (BYTE) {
-        if (tile < p.n_tiles) fetch_bytes(tile);
+#pragma unroll
+        for (int k = 0; k < NSTAGE - 1; ++k) {
+            const uint64_t tk = tile + (uint64_t)k * gridDim.x;
+            if (tk < p.n_tiles) fetch_bytes(tk, k);
+            cp_commit_m();
+        }
     } else {
         if (tile < p.n_tiles) prefetch(tile, bufs);
         cp_commit_m();
@@ -113,15 +122,33 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
         cplx* S = bufs + (BYTE ? 0 : (it & 1) * TILE);
         const uint64_t next = tile + gridDim.x;
         if constexpr (BYTE) {
-            const uint4 cm = nm, cpp = np;
-            if (next < p.n_tiles) fetch_bytes(next);
+            cp_wait_m<NSTAGE - 2>();      // this tile's bytes landed (the newer ones may not)
+            __syncthreads();
+            const uint64_t ahead = tile + (uint64_t)(NSTAGE - 1) * gridDim.x;
+            if (ahead < p.n_tiles) fetch_bytes(ahead, (it + NSTAGE - 1) % NSTAGE);
+            cp_commit_m();
+            const unsigned char* st = stage + (size_t)(it % NSTAGE) * 2 * TILE;
+            const uint4 cm = *reinterpret_cast<const uint4*>(st + 16 * tid);
+            const uint4 cpp = *reinterpret_cast<const uint4*>(st + TILE + 16 * tid);
             const unsigned wm[4] = {cm.x, cm.y, cm.z, cm.w}, wp[4] = {cpp.x, cpp.y, cpp.z, cpp.w};
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const unsigned mi = (wm[i >> 2] >> (8 * (i & 3))) & 255u, pi = (wp[i >> 2] >> (8 * (i & 3))) & 255u;
+            auto uniform = [](const uint4& v) {
+                return v.x == v.y && v.x == v.z && v.x == v.w && v.x == (v.x & 255u) * 0x01010101u;
+            };
+            if (uniform(cm) && uniform(cpp)) {   // structured states: one decode for 16 amplitudes
+                const unsigned mi = cm.x & 255u, pi = cpp.x & 255u;
                 const double m = dtab[mi];
                 const cplx v = mi == 0 ? cplx{0.0, 0.0} : cplx{__dmul_rn(m, dtab[256 + pi]), __dmul_rn(m, dtab[512 + pi])};
-                S[swz3(16 * tid + i, p.swz_cols)] = v;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) S[swz3(16 * tid + i, p.swz_cols)] = v;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const unsigned mi = (wm[i >> 2] >> (8 * (i & 3))) & 255u, pi = (wp[i >> 2] >> (8 * (i & 3))) & 255u;
+                    const double m = dtab[mi];
+                    const cplx v =
+                        mi == 0 ? cplx{0.0, 0.0} : cplx{__dmul_rn(m, dtab[256 + pi]), __dmul_rn(m, dtab[512 + pi])};
+                    S[swz3(16 * tid + i, p.swz_cols)] = v;
+                }
             }
         } else {
             if (next < p.n_tiles) prefetch(next, bufs + ((it + 1) & 1) * TILE);
@@ -174,7 +201,7 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
         }
         __syncthreads();   // S is the prefetch target two tiles from now (BYTE: the next tile)
     }
-    if constexpr (!BYTE) cp_wait_m<0>();
+    cp_wait_m<0>();
 
     // ---- deterministic reduction: warp shuffles, then fixed-order sum over warps ----
     // slots: [0] norm, [1 + pos] ones of tile position pos, [1 + KB + 2 pos (+1)] cross of pos
@@ -229,7 +256,7 @@ static cudaError_t measure3_cfg(const c64s* psi, const Measure3Params& p, double
                                 cudaStream_t st, const MeasureBytes& b) {
     constexpr int TILE = 1 << KB, NW = (TILE / 16) / 32;
     const size_t smem = (BYTE ? 1 : 2) * sizeof(cplx) * TILE + sizeof(double) * NW * (kOutMax + 1 + 3 * KB) +
-                        (BYTE ? sizeof(double) * 768 : 0);
+                        (BYTE ? sizeof(double) * 768 + 4 * 2 * TILE : 0);
     static bool configured[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -244,7 +271,7 @@ static cudaError_t measure3_cfg(const c64s* psi, const Measure3Params& p, double
     return cudaGetLastError();
 }
 
-int measure3_grid(int device, int kb, bool byte) { return sm_count(device) * (byte ? 2 : (kb == 12 ? 1 : 3)); }
+int measure3_grid(int device, int kb, bool byte) { return sm_count(device) * (byte ? 1 : (kb == 12 ? 1 : 3)); }
 
 cudaError_t launch_measure3(const void* psi, const Measure3Params& p, double* partials, int grid, cudaStream_t st) {
     const MeasureBytes none{nullptr, nullptr, nullptr};
@@ -255,7 +282,7 @@ cudaError_t launch_measure3(const void* psi, const Measure3Params& p, double* pa
 
 cudaError_t launch_measure3_byte(const MeasureBytes& b, const Measure3Params& p, double* partials, int grid,
                                  cudaStream_t st) {
-    return measure3_cfg<12, 2, true>(nullptr, p, partials, grid, st, b);
+    return measure3_cfg<12, 1, true>(nullptr, p, partials, grid, st, b);   // 2 CTAs/SM spill (128 regs)
 }
 
 }  // namespace sv
