@@ -27,7 +27,8 @@ from . import gates as g
 from .codec import CAPACITY, Codebook
 
 _BIG = 1e308
-_CAP = 1 << 20
+_CAP = 1 << 22                # = CAP_UNSURE of sv_byte_api.cu (uncertain-phase list)
+_CCAP = 1 << 20               # = CAP_MAG / CAP_PH (candidate buffers)
 MAX_TAGGED_RANKS = 8          # candidate set regions per CTA (sv_byte.cu CtaSets)
 
 
@@ -131,12 +132,12 @@ class ByteDeviceState:
     # -- candidate plumbing -----------------------------------------------------------
     def read_candidates(self):
         lib = nat.load()
-        mags = np.empty(_CAP, dtype=np.float64)
-        ph = np.empty((_CAP, 4), dtype=np.float64)
+        mags = np.empty(_CCAP, dtype=np.float64)
+        ph = np.empty((_CCAP, 4), dtype=np.float64)
         nm, npp = ctypes.c_uint64(0), ctypes.c_uint64(0)
         flags = ctypes.c_int(0)
-        nat.check(lib.svb_candidates(self.handle, nat.dptr(mags), _CAP, ctypes.byref(nm),
-                                     ph.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _CAP, ctypes.byref(npp),
+        nat.check(lib.svb_candidates(self.handle, nat.dptr(mags), _CCAP, ctypes.byref(nm),
+                                     ph.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _CCAP, ctypes.byref(npp),
                                      ctypes.byref(flags)))
         ph = ph[:npp.value]
         return mags[:nm.value].copy(), (ph[:, 0] + 1j * ph[:, 1]), flags.value

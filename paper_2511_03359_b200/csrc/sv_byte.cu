@@ -372,12 +372,10 @@ struct Emitter {
 
     __device__ void unsure_push(uint64_t idx, cplx v) const {
         const unsigned long long slot = atomicAdd(&cand->n_unsure, 1ull);
-        if (slot < cand->cap_unsure) {
+        if (slot < cand->cap_unsure) {   // n_unsure > cap_unsure is reported by svb_unsure
             cand->unsure_idx[slot] = idx;
             cand->unsure_val[2 * slot] = v.re;
             cand->unsure_val[2 * slot + 1] = v.im;
-        } else {
-            cand->overflow = 1;
         }
     }
 

@@ -41,7 +41,7 @@ struct Guard {
     explicit Guard(int d) { cudaGetDevice(&prev); if (prev != d) cudaSetDevice(d); }
     ~Guard() { int c = -1; cudaGetDevice(&c); if (prev >= 0 && c != prev) cudaSetDevice(prev); }
 };
-constexpr uint64_t CAP_MAG = 1ull << 20, CAP_PH = 1ull << 20, CAP_UNSURE = 1ull << 20;
+constexpr uint64_t CAP_MAG = 1ull << 20, CAP_PH = 1ull << 20, CAP_UNSURE = 1ull << 22;
 
 ByteGate to_gate(const svb_gate_desc& d, uint64_t n_elems) {
     ByteGate g;
@@ -221,7 +221,9 @@ int svb_unsure(sv_bhandle h, uint64_t* idx, double* vals, uint64_t cap, uint64_t
     ByteCand c;
     BTRY(cudaMemcpyAsync(&c, h->cand, sizeof(c), cudaMemcpyDeviceToHost, h->stream), "unsure header");
     BTRY(cudaStreamSynchronize(h->stream), "unsure sync");
-    const uint64_t k = std::min<uint64_t>(c.n_unsure, c.cap_unsure);
+    if (c.n_unsure > c.cap_unsure)   // never silently drop an amplitude the host must re-encode
+        return capi_fail(SV_ENOMEM, "uncertain-phase list overflow: more amplitudes than the 4M-entry buffer");
+    const uint64_t k = c.n_unsure;
     *n = k;
     if (k > cap) return capi_fail(SV_EVALUE, "unsure buffer too small");
     if (k) {
