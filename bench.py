@@ -767,6 +767,32 @@ def run_b200_multi(args, dist, rank, world, device):
                 "byte_passes": st_b.get("byte_passes"),
                 "what": "run_circuit_distributed(mode=BYTE) wall clock incl. allocation, per-gate codebook "
                         "barrier across ranks, remapped byte-plane swaps, measure-all; max over ranks"}
+    # BYTE-encoded QFT adder (BASELINE config 5's second circuit: build_adder(19, [374982, 149305])
+    # at N=38 on 8 GPUs): the widest even N <= byte_n_multi + log2(P); known answer R2 = all ones
+    byte_adder = None
+    if args.byte_adder and args.byte_n_multi > 0:
+        from paper_2511_03359_b200.distributed import run_circuit_distributed
+        w = (args.byte_n_multi + (world.bit_length() - 1)) // 2
+        a_, b_ = 374982 % (1 << w), 149305 % (1 << w)
+        circ, regs = pb.build_adder(w, [a_, b_])
+        dist.barrier()
+        t0 = time.perf_counter()
+        res = run_circuit_distributed(circ, dist, mode=pb.PrecisionMode.BYTE, device=device)
+        qz = res.report.qz
+        dist.barrier()
+        t_a = max_over_ranks(dist, time.perf_counter() - t0)
+        st_a = res.device_stats
+        byte_adder = {"circuit": f"build_adder({w}, [{a_}, {b_}]) BYTE", "n_qubits": 2 * w, "gates": len(circ.gates),
+                      "seconds": round(t_a, 3), "sec_per_gate": round(t_a / len(circ.gates), 5),
+                      "kat_all_ones_R2": all(qz[q] > 0.5 for q in regs["R2"]),
+                      "norm_deviation": res.report.norm_deviation,
+                      "codebook": [len(res.codebook.mags), len(res.codebook.thetas)],
+                      "byte_passes": st_a.get("byte_passes"), "byte_host_fixes": st_a.get("byte_host_fixes"),
+                      "what": "run_circuit_distributed(mode=BYTE) wall clock, max over ranks; lossy like the "
+                              "reference encoding (norm deviation), R2 read-out by Qz > 0.5"}
+        res.backend.close()
+        res.backend.st.free()
+        del res
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
@@ -798,6 +824,8 @@ def run_b200_multi(args, dist, rank, world, device):
             line["planner_ab"] = planner_ab
         if byte:
             line["byte_mode"] = byte
+        if byte_adder:
+            line["byte_adder"] = byte_adder
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
@@ -828,6 +856,8 @@ def main():
     ap.add_argument("--single-gate", action="store_true", default=True)
     ap.add_argument("--overlap", type=int, default=1,
                     help="N>1: overlap each remap swap with the first pass after it (chunked, IPC events)")
+    ap.add_argument("--byte-adder", type=int, default=1,
+                    help="N>1: the BYTE-encoded adder at 2w <= byte_n_multi + log2(P) qubits (38 on 8 GPUs)")
     ap.add_argument("--planner-ab", type=int, default=1,
                     help="N>1: benchmark(N) with the remap planner vs the reference choreography")
     ap.add_argument("--fp32", type=int, default=1, help="1 GPU line: time the same steps in FP32 storage")
