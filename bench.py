@@ -578,7 +578,6 @@ def run_b200_multi(args, dist, rank, world, device):
             out.append(("ops", pend))
         batches.append(out)
     from paper_2511_03359_b200.device import jit_prepare, jit_stats, jit_wait
-    from paper_2511_03359_b200.distributed import split_last_pass
     t_jit = time.perf_counter()
     for out in batches:
         for b in out:
@@ -586,7 +585,7 @@ def run_b200_multi(args, dist, rank, world, device):
                 jit_prepare(n, b[1], args.tile_bits)
             else:            # the overlapped passes are planned on their own op ranges
                 first, rest = CudaBackend._first_pass(b[2])
-                head, last = split_last_pass(n, nat.SV_FP64, b[3], args.tile_bits)
+                head, last = CudaBackend._last_pass(b[3])
                 for part in (first, rest, head, last, b[2], b[3]):
                     jit_prepare(n, part, args.tile_bits)
     jit_wait()

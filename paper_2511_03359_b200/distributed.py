@@ -59,19 +59,6 @@ def phys_op(gate, phys: tuple, n_local: int, rank: int):
     return gate_op(nat.SV_OP_2Q, qa=phys[0], qb=phys[1], data=m)
 
 
-def split_last_pass(n_local: int, mode_code: int, ops, tile_bits: int = 12):
-    """(head, last): ops split before the last fused pass sv_apply_fused would run."""
-    ops = list(ops)
-    if not ops:
-        return [], []
-    ends = (ctypes.c_int * len(ops))()
-    n = nat.load(require_device=False).sv_plan_passes(n_local, mode_code, ops_array(ops), len(ops), tile_bits,
-                                                      ends, len(ops))
-    nat.check(min(n, 0))
-    start = ends[n - 2] if n > 1 else 0
-    return ops[:start], ops[start:]
-
-
 class CudaBackend:
     """This rank's slice in HBM plus IPC-mapped slices of every other rank."""
 
@@ -155,37 +142,55 @@ class CudaBackend:
         return bits[:self.OVERLAP_CHUNK_BITS] if len(bits) >= self.OVERLAP_CHUNK_BITS else []
 
     @staticmethod
-    def _first_pass(ops, K: int = 11):
-        """Longest prefix of ops whose non-diagonal qubits fit one 2^K tile with the five
-        lowest qubits (the pass that runs chunk by chunk under the swap)."""
+    def _need(op) -> int:
+        if op.kind == nat.SV_OP_1Q:
+            return 1 << op.qa
+        if op.kind == nat.SV_OP_2Q:
+            return (1 << op.qa) | (1 << op.qb)
+        return 0             # diagonal ops never need a tile position
+
+    @classmethod
+    def _first_pass(cls, ops, K: int = 11):
+        """Longest prefix of ops whose NON-DIAGONAL qubits fit one 2^K tile with the five
+        lowest qubits (it may still be several passes when it holds more than 128 ops).  Only
+        diagonal ops differ between ranks (phys_op), so the qubit set -- and the chunk bits
+        derived from it -- is the same on every rank."""
         need = 0x1F
         for i, op in enumerate(ops):
-            m = 0
-            if op.kind == nat.SV_OP_1Q:
-                m = 1 << op.qa
-            elif op.kind == nat.SV_OP_2Q:
-                m = (1 << op.qa) | (1 << op.qb)
-            if bin(need | m).count("1") > K or i >= 128:
+            m = cls._need(op)
+            if bin(need | m).count("1") > K:
                 return ops[:i], ops[i:]
             need |= m
         return ops, []
 
-    def _last_pass(self, ops):
-        return split_last_pass(self.n_local, self.dev.mode_code, ops, self.tile_bits)
+    @classmethod
+    def _last_pass(cls, ops, K: int = 11):
+        """(head, last): the longest suffix of ops whose non-diagonal qubits fit one tile."""
+        need = 0x1F
+        for i in range(len(ops) - 1, -1, -1):
+            m = cls._need(ops[i])
+            if bin(need | m).count("1") > K:
+                return ops[:i + 1], ops[i + 1:]
+            need |= m
+        return [], ops
 
     def swap_then_apply(self, pairs, ops, before=()) -> None:
-        """A remap swap (one or k global qubits) followed by the fused passes of `ops`, with
-        the swap's transfer overlapping the first pass: the swap runs on a second stream in
-        chunks (fixed values of three high local bits outside the pass tile); the pass runs
-        chunk by chunk on the main stream, each chunk waiting for this rank's and the
-        partners' swap of that chunk (inter-process events).  Same amplitudes, same
-        arithmetic as swap + apply_local."""
+        """A remap swap (one or k global qubits) with the ops before and after it, the
+        transfer overlapping both neighbouring passes: the last pass before the swap, the swap
+        (second stream) and the first pass after it run chunk by chunk over 16 chunks (fixed
+        values of four high local bits outside both passes' tiles and the victims); each swap
+        chunk waits for that chunk of the pass before on this rank and every partner, each
+        chunk of the pass after waits for that swap chunk everywhere (inter-process events).
+        The control flow (barriers, events) is identical on every rank: the chunk bits come
+        from non-diagonal ops only, and empty op ranges still record their events.  Same
+        amplitudes, same arithmetic as apply_local + swap + apply_local."""
+        before = list(before)
         first, rest = self._first_pass(ops)
-        head, last = self._last_pass(list(before)) if before else ([], [])
-        bits = self._chunk_bits(pairs, list(first) + list(last)) if first and self.mode is PrecisionMode.FP64 else []
+        head, last = self._last_pass(before)
+        bits = self._chunk_bits(pairs, list(first) + list(last)) if self.mode is PrecisionMode.FP64 else []
         if not bits:
             if before:
-                self.apply_local(list(before))
+                self.apply_local(before)
             if len(pairs) == 1:
                 self.swap(*pairs[0])
             else:
@@ -206,32 +211,24 @@ class CudaBackend:
         half = (L >> (k + len(bits))) // 2
         C = 1 << len(bits)
         members = [m for m, *_ in sched]
-        prev_blocks = lib.sv_swap_blocks(self.OVERLAP_SWAP_BLOCKS)
-        if last:
-            # three stages: the last pass before the swap runs chunk by chunk too, and each
-            # swap chunk waits for that chunk of the pass on this rank and every partner
-            if head:
-                self.apply_local(head)
-            if self.swap_timing:
-                e0 = nat.Event()
-                e0.record(self.dev.stream)
-            arr_l = ops_array(last)
-            for i in range(C):
+        if head:
+            self.apply_local(head)
+        if self.swap_timing:
+            e0 = nat.Event()
+            e0.record(self.dev.stream)
+        arr_l = ops_array(last)
+        for i in range(C):           # stage 1: the pass before, chunk by chunk
+            if last:
                 nat.check(lib.sv_apply_fused_chunk(self.dev.handle, arr_l, len(last), self.tile_bits, cmask,
                                                    deposit(i, bits)))
-                nat.check(lib.sv_event_record(own_ev[C + i], self.dev.stream))
-            self.dist.barrier()      # every rank's pass-chunk events are recorded
-        else:
-            self._sync_all()
-            if self.swap_timing:
-                e0 = nat.Event()
-                e0.record(self.dev.stream)
-        for i in range(C):
+            nat.check(lib.sv_event_record(own_ev[C + i], self.dev.stream))
+        self.dist.barrier()          # every rank's stage-1 events are recorded
+        prev_blocks = lib.sv_swap_blocks(self.OVERLAP_SWAP_BLOCKS)
+        for i in range(C):           # stage 2: the swap, chunk by chunk on the second stream
             cpat = deposit(i, bits)
-            if last:
-                nat.check(lib.sv_stream_wait_event(stream.ptr, own_ev[C + i]))
-                for m in members:
-                    nat.check(lib.sv_stream_wait_event(stream.ptr, peer_ev[m][C + i]))
+            nat.check(lib.sv_stream_wait_event(stream.ptr, own_ev[C + i]))
+            for m in members:
+                nat.check(lib.sv_stream_wait_event(stream.ptr, peer_ev[m][C + i]))
             for member, vmask, own_pat, peer_pat, t0, cnt in sched:
                 nat.check(lib.svk_swap_group_chunk(self.dev.ptr, self.peers[member], L, self.dev.mode_code, vmask,
                                                    own_pat, peer_pat, cmask, cpat, 0 if t0 == 0 else half, half,
@@ -239,14 +236,15 @@ class CudaBackend:
                 self.link_bytes += 2 * half * self.bpe
             nat.check(lib.sv_event_record(own_ev[i], stream.ptr))
         lib.sv_swap_blocks(prev_blocks)
-        self.dist.barrier()          # every rank's chunk events are recorded (enqueued)
+        self.dist.barrier()          # every rank's stage-2 events are recorded
         arr = ops_array(first)
-        for i in range(C):
+        for i in range(C):           # stage 3: the pass after, chunk by chunk
             nat.check(lib.sv_stream_wait_event(self.dev.stream, own_ev[i]))
             for m in members:
                 nat.check(lib.sv_stream_wait_event(self.dev.stream, peer_ev[m][i]))
-            nat.check(lib.sv_apply_fused_chunk(self.dev.handle, arr, len(first), self.tile_bits, cmask,
-                                               deposit(i, bits)))
+            if first:
+                nat.check(lib.sv_apply_fused_chunk(self.dev.handle, arr, len(first), self.tile_bits, cmask,
+                                                   deposit(i, bits)))
         if self.swap_timing:
             e1 = nat.Event()
             e1.record(self.dev.stream)
