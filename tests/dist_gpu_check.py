@@ -31,7 +31,10 @@ def main():
              ("adder8", adder(8, [172, 83])[0]),
              # large enough for overlapped swaps (chunk bits >= 12 outside the first pass)
              ("random22", random_circuit(np.random.default_rng(13), 22, 90)),
-             ("bench23", benchmark(23))]
+             ("bench23", benchmark(23)),
+             # CPHASE runs on global qubits: ranks hold different diagonal op lists around the
+             # overlapped swaps (the chunk choice must not depend on them)
+             ("adder11", adder(11, [1234, 813])[0])]
     ok = True
     for name, circ in cases:
         res = run_circuit_distributed(to_product(circ), dist)
