@@ -261,6 +261,8 @@ def run_b200(args):
     from oracle.ref_builders import OCircuit
 
     device = local if world > 1 else 0
+    if world > 1 and os.environ.get("SVB200_DEVICES"):     # test only: ranks share GPUs (rank % k)
+        device = local % int(os.environ["SVB200_DEVICES"])
     nat.check(nat.load().sv_set_device(device))
     nat.check(nat.load().sv_fused_variant(args.fused))
     nat.check(nat.load().sv_fused_segment_limit(args.seg_limit))
@@ -836,7 +838,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=33, help="qubits per GPU")
+    ap.add_argument("--n", "--qubits-per-gpu", dest="n", type=int, default=33, help="qubits per GPU")
     ap.add_argument("--layers", type=int, default=9, help="H layer + random layers in the workload")
     ap.add_argument("--tile-bits", type=int, default=12, help="v1 tile bits / upper bound")
     ap.add_argument("--fused", type=int, default=9, choices=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9],

@@ -21,6 +21,9 @@ sys.path.insert(0, ROOT)
 def main():
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
+    # SVB200_DEVICES=k: ranks share k GPUs (rank % k) -- 8-rank runs on a 4-GPU box
+    ndev = int(os.environ.get("SVB200_DEVICES", "0")) or world
+    dev = rank % ndev
     from paper_2511_03359_b200.distributed import run_circuit_distributed
     from oracle import ref_engine
     from oracle.ref_builders import adder, benchmark
@@ -37,7 +40,7 @@ def main():
              ("adder11", adder(11, [1234, 813])[0])]
     ok = True
     for name, circ in cases:
-        res = run_circuit_distributed(to_product(circ), dist)
+        res = run_circuit_distributed(to_product(circ), dist, device=dev)
         state = res.gathered_state(dist)
         if rank == 0:
             want = ref_engine.run_circuit(circ, ranks=world)
@@ -54,7 +57,7 @@ def main():
     # reference choreography (no remapping): exchange-fused pair updates over NVLink
     for name, circ in [("random14_ref", random_circuit(np.random.default_rng(11), 14, 80)),
                        ("bench16_ref", benchmark(16))]:
-        res = run_circuit_distributed(to_product(circ), dist, remap=False)
+        res = run_circuit_distributed(to_product(circ), dist, remap=False, device=dev)
         state = res.gathered_state(dist)
         if rank == 0:
             want = ref_engine.run_circuit(circ, ranks=world)
@@ -69,7 +72,7 @@ def main():
     # FP32 storage across GPUs (remap swaps move complex64 amplitudes)
     for name, circ in [("random16_fp32", random_circuit(np.random.default_rng(21), 16, 70)),
                        ("bench18_fp32", benchmark(18))]:
-        res = run_circuit_distributed(to_product(circ), dist, mode=PrecisionMode.FP32)
+        res = run_circuit_distributed(to_product(circ), dist, mode=PrecisionMode.FP32, device=dev)
         state = res.gathered_state(dist)
         if rank == 0:
             want = ref_engine.run_circuit(circ, ranks=world, mode="fp32")
@@ -83,7 +86,7 @@ def main():
                   ("random12_be", random_circuit(np.random.default_rng(6), 12, 30)),
                   ("adder6_be", adder(6, [45, 18])[0])]
     for name, circ in byte_cases:
-        res = run_circuit_distributed(to_product(circ), dist, mode=PrecisionMode.BYTE)
+        res = run_circuit_distributed(to_product(circ), dist, mode=PrecisionMode.BYTE, device=dev)
         planes = res.gathered_bytes(dist)
         if rank == 0:
             want = ref_engine.run_circuit(circ, ranks=world, mode="be")
