@@ -572,8 +572,84 @@ __device__ __noinline__ unsigned pair_slow(const STables& t, const Emitter& em, 
     return cc;
 }
 
+// 1Q gate on a low qubit (qa < 4): both amplitudes of every pair lie in the same
+// 32-byte block of each plane, so a work item is one block (16 pairs) read and
+// written with 16-byte accesses -- the per-pair byte path issued 8 one-byte
+// accesses per pair (H on qubits 0-3: 22.6 ms per pass at N=32, 2.8 ms for qa >= 4).
+template <int QA>
+__device__ __forceinline__ void byte_low_pairs(const uint8_t* __restrict__ mi_in, const uint8_t* __restrict__ pi_in,
+                                               uint8_t* __restrict__ mi_out, uint8_t* __restrict__ pi_out,
+                                               const ByteGate& g, const STables& t, const Emitter& em,
+                                               ThreadCache& tc, unsigned long long* memo, const MemoTags& mt,
+                                               bool real, bool tagged, bool write, uint64_t first, uint64_t step) {
+    const uint64_t n_blocks = g.n_elems >> 5;
+    for (uint64_t w = first; w < n_blocks; w += step) {
+        const uint64_t b = w << 5;
+        // all 32 amplitudes of a block share their producer (the caller checked the bits)
+        if (g.producer >= 0 && producer_of(g, b) != g.producer) continue;
+        const int prod = tagged ? producer_of(g, b) : 0;
+        unsigned m[8], p[8], om[8], op[8];
+        const uint4 m0 = *reinterpret_cast<const uint4*>(mi_in + b), m1 = *reinterpret_cast<const uint4*>(mi_in + b + 16);
+        const uint4 p0 = *reinterpret_cast<const uint4*>(pi_in + b), p1 = *reinterpret_cast<const uint4*>(pi_in + b + 16);
+        m[0] = m0.x; m[1] = m0.y; m[2] = m0.z; m[3] = m0.w; m[4] = m1.x; m[5] = m1.y; m[6] = m1.z; m[7] = m1.w;
+        p[0] = p0.x; p[1] = p0.y; p[2] = p0.z; p[3] = p0.w; p[4] = p1.x; p[5] = p1.y; p[6] = p1.z; p[7] = p1.w;
+        bool uni = m[0] == (m[0] & 255u) * 0x01010101u && p[0] == (p[0] & 255u) * 0x01010101u;
+#pragma unroll
+        for (int k = 1; k < 8; ++k) uni = uni && m[k] == m[0] && p[k] == p[0];
+        bool done = false;
+        if (uni) {   // one code tuple for all 16 pairs (structured states)
+            const unsigned bm = m[0] & 255u, bp = p[0] & 255u;
+            const unsigned key = bm | (bp << 8) | (bm << 16) | (bp << 24);
+            unsigned cc;
+            const int slot = memo_get(memo, key, &cc);
+            done = true;
+            if (slot < 0 || mt.fresh(slot, prod)) {
+                cc = pair_slow(t, em, tc, memo, mt, key, b, b + (1u << QA), g.m, real, prod);
+                done = memo_get(memo, key, &cc) >= 0;   // uncertain outputs: per pair (indices reported)
+            }
+            if (done) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) { om[k] = 0u; op[k] = 0u; }
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    const bool hi = (k >> QA) & 1;
+                    om[k >> 2] |= (hi ? (cc >> 16) & 255u : cc & 255u) << (8 * (k & 3));
+                    op[k >> 2] |= (hi ? cc >> 24 : (cc >> 8) & 255u) << (8 * (k & 3));
+                }
+            }
+        }
+        if (!done) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { om[k] = 0u; op[k] = 0u; }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int k0 = ((j >> QA) << (QA + 1)) | (j & ((1 << QA) - 1)), k1 = k0 | (1 << QA);
+                const unsigned key = ((m[k0 >> 2] >> (8 * (k0 & 3))) & 255u) |
+                                     (((p[k0 >> 2] >> (8 * (k0 & 3))) & 255u) << 8) |
+                                     (((m[k1 >> 2] >> (8 * (k1 & 3))) & 255u) << 16) |
+                                     (((p[k1 >> 2] >> (8 * (k1 & 3))) & 255u) << 24);
+                unsigned cc;
+                const int slot = memo_get(memo, key, &cc);
+                if (slot < 0 || mt.fresh(slot, prod))
+                    cc = pair_slow(t, em, tc, memo, mt, key, b + k0, b + k1, g.m, real, prod);
+                om[k0 >> 2] |= (cc & 255u) << (8 * (k0 & 3));
+                op[k0 >> 2] |= ((cc >> 8) & 255u) << (8 * (k0 & 3));
+                om[k1 >> 2] |= ((cc >> 16) & 255u) << (8 * (k1 & 3));
+                op[k1 >> 2] |= (cc >> 24) << (8 * (k1 & 3));
+            }
+        }
+        if (write) {
+            *reinterpret_cast<uint4*>(mi_out + b) = make_uint4(om[0], om[1], om[2], om[3]);
+            *reinterpret_cast<uint4*>(mi_out + b + 16) = make_uint4(om[4], om[5], om[6], om[7]);
+            *reinterpret_cast<uint4*>(pi_out + b) = make_uint4(op[0], op[1], op[2], op[3]);
+            *reinterpret_cast<uint4*>(pi_out + b + 16) = make_uint4(op[4], op[5], op[6], op[7]);
+        }
+    }
+}
+
 // One BYTE gate pass.  Work items: pairs (1Q), quadruples (2Q) or single
 // amplitudes (DIAG, and COPY for untouched amplitudes of a diagonal gate).
+template <int LOWQA>   // >= 0: a 1Q gate on low qubit LOWQA, 32-byte blocks (byte_low_pairs)
 __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__ mi_in, const uint8_t* __restrict__ pi_in,
                                                   uint8_t* __restrict__ mi_out, uint8_t* __restrict__ pi_out,
                                                   const ByteTables* __restrict__ gtab, const __grid_constant__ ByteGate g,
@@ -596,11 +672,19 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
     ThreadCache tc{NAN, NAN, NAN, NAN, NAN, NAN, 0u, 0};
     const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g.kind == SV_OP_1Q) {
+    // lowest physical bit the producer rule reads: a vector work item (a run of
+    // consecutive amplitudes) has one producer only if its index bits stay below it
+    int lmin = 64;
+    if (g.producer >= 0 || tagged)
+        for (int j = 0; j < 2 + g.rank_bits && j < 12; ++j) lmin = min(lmin, (int)g.lbit[j]);
+    if constexpr (LOWQA >= 0) {
+        const bool real = g.m[1] == 0.0 && g.m[3] == 0.0 && g.m[5] == 0.0 && g.m[7] == 0.0;
+        byte_low_pairs<LOWQA>(mi_in, pi_in, mi_out, pi_out, g, t, em, tc, memo, mt, real, tagged, write, first, step);
+    } else if (g.kind == SV_OP_1Q) {
         const cplx m0 = {g.m[0], g.m[1]}, m1 = {g.m[2], g.m[3]}, m2 = {g.m[4], g.m[5]}, m3 = {g.m[6], g.m[7]};
         const bool real = g.m[1] == 0.0 && g.m[3] == 0.0 && g.m[5] == 0.0 && g.m[7] == 0.0;
         const uint64_t n_items = g.n_elems >> 1;
-        if (g.qa >= 4 && g.n_elems >= 32) {
+        if (g.qa >= 4 && g.n_elems >= 32 && lmin >= 4) {
             // 16 consecutive pairs per work item (16-byte loads/stores of every plane); the next
             // item's bytes are loaded before the current one is computed (latency hiding)
             const uint64_t n_chunks = n_items >> 4;
@@ -728,7 +812,7 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
             for (int r = 0; r < 4; ++r) o[r] = row4(&m[4 * r], a[0], a[1], a[2], a[3]);
             for (int r = 0; r < 4; ++r) em.emit(idx[r], o[r], tc, prod);
         }
-    } else if (g.n_elems >= 16) {   // DIAG, 8 amplitudes per work item
+    } else if (g.n_elems >= 16 && lmin >= 3) {   // DIAG, 8 amplitudes per work item
         const cplx f = {g.m[0], g.m[1]};
         const uint64_t n_chunks = g.n_elems >> 3;
         for (uint64_t w = first; w < n_chunks; w += step) {
@@ -928,12 +1012,24 @@ cudaError_t launch_byte_gate(const uint8_t* mi_in, const uint8_t* pi_in, uint8_t
     int dev = 0;
     cudaGetDevice(&dev);
     const int memo_bytes = MEMO_SLOTS * (int)(sizeof(unsigned long long) + sizeof(unsigned));
+    void (*low[4])(const uint8_t*, const uint8_t*, uint8_t*, uint8_t*, const ByteTables*, const ByteGate, ByteCand*) = {
+        k_byte_gate<0>, k_byte_gate<1>, k_byte_gate<2>, k_byte_gate<3>};
     if (dev < 64 && !configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k_byte_gate, cudaFuncAttributeMaxDynamicSharedMemorySize, memo_bytes);
+        cudaError_t e = cudaFuncSetAttribute(k_byte_gate<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, memo_bytes);
+        for (int q = 0; q < 4 && e == cudaSuccess; ++q)
+            e = cudaFuncSetAttribute(low[q], cudaFuncAttributeMaxDynamicSharedMemorySize, memo_bytes);
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
-    k_byte_gate<<<byte_grid(items), NT, memo_bytes, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g, cand);
+    // low-qubit 1Q gates: 32-byte blocks, if a block has one producer (the bits the
+    // producer rule reads are all >= 5; k_byte_gate computes the same bound)
+    int lmin = 64;
+    if (g.producer >= 0 || g.producer == -2)
+        for (int j = 0; j < 2 + g.rank_bits && j < 12; ++j) lmin = std::min(lmin, (int)g.lbit[j]);
+    if (g.kind == SV_OP_1Q && g.qa < 4 && g.n_elems >= 1024 && lmin >= 5)
+        low[g.qa]<<<byte_grid(g.n_elems / 32), NT, memo_bytes, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g, cand);
+    else
+        k_byte_gate<-1><<<byte_grid(items), NT, memo_bytes, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g, cand);
     count_launch();
     return cudaGetLastError();
 }

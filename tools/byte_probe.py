@@ -30,9 +30,14 @@ for gate in circ.gates:
         tm = time.perf_counter() - t0
         continue
     t0 = time.perf_counter()
+    ne = len(st.pass_events)
     st.apply_gate(gate)
     st.synchronize()
     times.append((gate.kind, time.perf_counter() - t0))
+    if os.environ.get("BYTE_PROBE_VERBOSE"):
+        ev = [("s" if sc else "w") + f"{a.elapsed_ms(b):.2f}" for sc, a, b in st.pass_events[ne:]]
+        print(f"  {gate.kind}{tuple(gate.qubits) if hasattr(gate, 'qubits') else ''} {times[-1][1]*1e3:.2f} ms "
+              f"passes {' '.join(ev)} mags {len(st.codebook.mags)}", flush=True)
 byt = 4 * (1 << circ.n_qubits)
 ts = np.array([t for _, t in times])
 scan = [a.elapsed_ms(b) for sc, a, b in st.pass_events if sc]
