@@ -621,6 +621,8 @@ __device__ __forceinline__ void byte_low_pairs(const uint8_t* __restrict__ mi_in
         if (!done) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) { om[k] = 0u; op[k] = 0u; }
+            bool hit_prev = false;   // runs of equal tuples: as in k_byte_gate's per-pair loop
+            unsigned key_prev = 0u, cc_prev = 0u;
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 const int k0 = ((j >> QA) << (QA + 1)) | (j & ((1 << QA) - 1)), k1 = k0 | (1 << QA);
@@ -629,9 +631,15 @@ __device__ __forceinline__ void byte_low_pairs(const uint8_t* __restrict__ mi_in
                                      (((m[k1 >> 2] >> (8 * (k1 & 3))) & 255u) << 16) |
                                      (((p[k1 >> 2] >> (8 * (k1 & 3))) & 255u) << 24);
                 unsigned cc;
-                const int slot = memo_get(memo, key, &cc);
-                if (slot < 0 || mt.fresh(slot, prod))
-                    cc = pair_slow(t, em, tc, memo, mt, key, b + k0, b + k1, g.m, real, prod);
+                if (hit_prev && key == key_prev) {
+                    cc = cc_prev;
+                } else {
+                    const int slot = memo_get(memo, key, &cc);
+                    hit_prev = slot >= 0 && !mt.fresh(slot, prod);
+                    if (!hit_prev) cc = pair_slow(t, em, tc, memo, mt, key, b + k0, b + k1, g.m, real, prod);
+                    key_prev = key;
+                    cc_prev = cc;
+                }
                 om[k0 >> 2] |= (cc & 255u) << (8 * (k0 & 3));
                 op[k0 >> 2] |= ((cc >> 8) & 255u) << (8 * (k0 & 3));
                 om[k1 >> 2] |= ((cc >> 16) & 255u) << (8 * (k1 & 3));
@@ -741,6 +749,11 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                     continue;
                 }
             per_pair:
+                // runs of equal tuples (sparse / structured states) reuse the previous memo
+                // hit; a pair computed by pair_slow is looked up again (its outputs may be
+                // uncertain, reported per index)
+                bool hit_prev = false;
+                unsigned key_prev = 0u, cc_prev = 0u;
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     // key = (m0, p0, m1, p1) bytes of pair j; j is a literal after unrolling
@@ -752,9 +765,15 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                     const unsigned key = ((w0 >> sh) & 255u) | (((w1 >> sh) & 255u) << 8) |
                                          (((w2 >> sh) & 255u) << 16) | (((w3 >> sh) & 255u) << 24);
                     unsigned cc;
-                    const int slot = memo_get(memo, key, &cc);
-                    if (slot < 0 || mt.fresh(slot, prod))
-                        cc = pair_slow(t, em, tc, memo, mt, key, i0 + j, i1 + j, g.m, real, prod);
+                    if (hit_prev && key == key_prev) {
+                        cc = cc_prev;   // what the memo returns for it (entries are never evicted)
+                    } else {
+                        const int slot = memo_get(memo, key, &cc);
+                        hit_prev = slot >= 0 && !mt.fresh(slot, prod);
+                        if (!hit_prev) cc = pair_slow(t, em, tc, memo, mt, key, i0 + j, i1 + j, g.m, real, prod);
+                        key_prev = key;
+                        cc_prev = cc;
+                    }
                     put_byte(out[0], j, cc & 255u); put_byte(out[1], j, (cc >> 8) & 255u);
                     put_byte(out[2], j, (cc >> 16) & 255u); put_byte(out[3], j, cc >> 24);
                 }

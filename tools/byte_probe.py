@@ -31,8 +31,14 @@ for gate in circ.gates:
         continue
     t0 = time.perf_counter()
     ne = len(st.pass_events)
+    prof = os.environ.get("BYTE_PROBE_PROFILE_GATE") == str(len(times))   # ncu --profile-from-start off
+    if prof:
+        import torch
+        torch.cuda.cudart().cudaProfilerStart()
     st.apply_gate(gate)
     st.synchronize()
+    if prof:
+        torch.cuda.cudart().cudaProfilerStop()
     times.append((gate.kind, time.perf_counter() - t0))
     if os.environ.get("BYTE_PROBE_VERBOSE"):
         ev = [("s" if sc else "w") + f"{a.elapsed_ms(b):.2f}" for sc, a, b in st.pass_events[ne:]]
