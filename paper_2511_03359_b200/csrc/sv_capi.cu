@@ -559,7 +559,19 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
         const char* e = std::getenv("SVB200_MEASURE_K");
         kenv = (e && std::atoi(e) == 11) ? 11 : 12;
     }
-    const int K = byte ? 12 : kenv, RB = 4, NT = 1 << (K - RB), bmin = 5;
+    static int benv = -1;   // low index bits every later pass keeps in its tile (contiguous runs)
+    if (benv < 0) {
+        const char* e = std::getenv("SVB200_MEASURE_BMIN");
+        benv = e ? std::max(1, std::min(5, std::atoi(e))) : 5;
+    }
+    static int renv0 = -1, renv = -1;   // register bits per segment of FP64 pass 0 / later passes
+    if (renv < 0) {
+        const char* e0 = std::getenv("SVB200_MEASURE_RB0");
+        const char* e = std::getenv("SVB200_MEASURE_RB");
+        renv0 = (e0 && std::atoi(e0) == 3) ? 3 : 4;
+        renv = (e && std::atoi(e) == 3) ? 3 : 4;
+    }
+    const int K = byte ? 12 : kenv, bmin = benv;
     const int grid_cap = measure3_grid(dev, K, byte);
     const int slots = measure_slots(K, n);
     double* partials = dev_partials;
@@ -587,8 +599,10 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
     for (size_t pi = 0; pi < passes.size() && rc == SV_OK; ++pi) {
         std::memset(&P, 0, sizeof(P));
         const uint64_t tmask = passes[pi];
+        const int RB = (byte || K != 12) ? 4 : (pi == 0 ? renv0 : renv), NT = 1 << (K - RB);
         P.n = n;
         P.kbits = K;
+        P.rbits = RB;
         P.n_tiles = 1ull << (n - K);
         P.want_ones = pi == 0;
         int j = 0, o = 0;
@@ -603,17 +617,17 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
         std::vector<int> cpos;
         for (int i = 0; i < K; ++i)
             if (!((done >> P.tq[i]) & 1)) cpos.push_back(i);
-        P.n_segs = (int)((cpos.size() + 3) / 4);
+        P.n_segs = (int)((cpos.size() + RB - 1) / RB);
         if (P.n_segs < 1) P.n_segs = 1;
         for (int sg = 0; sg < P.n_segs; ++sg) {
             uint32_t regs = 0;
             int cnt = 0;
-            for (size_t c = 4 * sg; c < cpos.size() && cnt < 4; ++c, ++cnt) {
+            for (size_t c = (size_t)RB * sg; c < cpos.size() && cnt < RB; ++c, ++cnt) {
                 P.seg_reg[sg][cnt] = (uint8_t)cpos[c];
                 P.cross_reg[sg] |= 1u << cnt;
                 regs |= 1u << cpos[c];
             }
-            for (int pos = K - 1; pos >= 0 && cnt < 4; --pos)     // fill from the top
+            for (int pos = K - 1; pos >= 0 && cnt < RB; --pos)    // fill from the top
                 if (!((regs >> pos) & 1)) { P.seg_reg[sg][cnt++] = (uint8_t)pos; regs |= 1u << pos; }
             // registers ascending by position within the segment keep the slot order simple
             int t = 0;
@@ -654,14 +668,14 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
                 return e ^ g;
             };
             for (int sg = 0; sg < P.n_segs; ++sg)
-                for (int i = 0; i < 16; ++i) {
+                for (int i = 0; i < (1 << RB); ++i) {
                     int e = 0;
                     for (int bit = 0; bit < RB; ++bit)
                         if ((i >> bit) & 1) e |= 1 << P.seg_reg[sg][bit];
                     P.seg_rsw[sg][i] = (uint16_t)swz_h(e);
                 }
         }
-        for (int jj = 0; jj < 16; ++jj) {
+        for (int jj = 0; jj < (1 << RB); ++jj) {
             uint64_t off = 0;
             for (int pos = 0; pos < K; ++pos)
                 if (((jj * NT) >> pos) & 1) off += 1ull << P.tq[pos];
@@ -676,7 +690,8 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
                 }
                 P.base_tab[byte][v] = d;
             }
-        const int grid = (int)((P.n_tiles < (uint64_t)grid_cap) ? P.n_tiles : grid_cap);
+        const int gcap = sm_count(dev) * measure3_ctas_per_sm(K, byte, P);   // <= grid_cap
+        const int grid = (int)((P.n_tiles < (uint64_t)gcap) ? P.n_tiles : gcap);
         cudaError_t e = byte ? launch_measure3_byte(*static_cast<const MeasureBytes*>(psi), P, partials, grid, st)
                              : launch_measure3(psi, P, partials, grid, st);
         if (e != cudaSuccess) { rc = cuda_fail(e, "measure launch"); break; }

@@ -106,13 +106,13 @@ int measure_slots(int k, int n);        // doubles per CTA partial row
 // register-resident FP64 measurement pass (sv_measure3.cu); same partial-row layout
 struct Measure3Params {
     uint64_t n_tiles;
-    int n, kbits, b, want_ones, n_segs, n_out;
+    int n, kbits, b, want_ones, n_segs, n_out, rbits;   // rbits: register bits per segment (3 or 4)
     int8_t tq[12];
     int8_t oq[64];
-    uint8_t seg_reg[3][4];              // register bit j -> tile position
-    uint8_t seg_thr[3][8];              // thread-id bit j -> tile position
-    uint16_t seg_rsw[3][16];            // swizzled shared-memory offset of register slot i
-    uint32_t cross_reg[3];              // register bits whose cross term the segment produces
+    uint8_t seg_reg[4][4];              // register bit j -> tile position
+    uint8_t seg_thr[4][9];              // thread-id bit j -> tile position
+    uint16_t seg_rsw[4][16];            // swizzled shared-memory offset of register slot i
+    uint32_t cross_reg[4];              // register bits whose cross term the segment produces
     uint8_t swz_cols[4];                // shared-memory swizzle: columns XORed in by tile bits 3..6
     uint64_t pf_go[16];                 // HBM offset of tile element j * threads (prefetch chunks)
     uint64_t base_tab[4][256];          // tile index byte -> local-index bits outside the tile
@@ -125,7 +125,8 @@ struct MeasureBytes {                   // BYTE planes + decode tables (dmag, du
 cudaError_t launch_measure3(const void* psi, const Measure3Params& p, double* partials, int grid, cudaStream_t st);
 cudaError_t launch_measure3_byte(const MeasureBytes& b, const Measure3Params& p, double* partials, int grid,
                                  cudaStream_t st);
-int measure3_grid(int device, int kb, bool byte);
+int measure3_grid(int device, int kb, bool byte);                       // partial rows to allocate
+int measure3_ctas_per_sm(int kb, bool byte, const Measure3Params& p);   // the variant a pass runs
 cudaError_t launch_measure(const void* psi, int mode, const MeasureParams& p, double* partials,
                            int grid, cudaStream_t st);
 int measure_grid(int device);

@@ -47,12 +47,26 @@ constexpr int kOutMax = 52;
 // consecutive magnitude / phase bytes of the tile (tile positions 0..3 are qubits 0..3),
 // decodes them with the reference's single rounding (codec.py:203-206) into the
 // shared-memory tile, and the next tile's bytes are already in flight in registers.
-template <int KB, int MINB, bool BYTE>
-__global__ void __launch_bounds__(1 << (KB - 4), MINB)
+// NSEG: register segments per tile (3 for the first pass, whose 12 tile positions are all
+// new; later passes keep 5 done low positions for coalescing and need 2); ONES: the first
+// pass also sums |a|^2 per qubit.  The 2-segment form without ONES fits 128 registers,
+// i.e. 2 CTAs per SM (16 warps instead of 8 to hide the HBM latency).
+// RB: register bits per segment (R = 2^RB amplitudes per thread, 2^(KB-RB) threads).
+// RB = 3 keeps 8 amplitudes per thread, so 4 segments (every position of a 12-bit tile)
+// fit 128 registers with 16 warps per SM.
+template <int KB, int MINB, bool BYTE, int NSEG, bool ONES, int RB = 4>
+__global__ void __launch_bounds__(1 << (KB - RB), MINB)
     k_measure3(const c64s* __restrict__ psi, const __grid_constant__ Measure3Params p, double* __restrict__ partials,
                const MeasureBytes bsrc) {
-    constexpr int TILE = 1 << KB, R = 16, NT = TILE / R, TB = KB - 4, NW = NT / 32;
-    constexpr int NBUF = BYTE ? 1 : 2;
+    constexpr int TILE = 1 << KB, R = 1 << RB, NT = TILE / R, TB = KB - RB, NW = NT / 32;
+    static_assert(!BYTE || RB == 4, "BYTE decode: 16 bytes per thread");
+    // FP64 with 2 CTAs per SM: one tile buffer (2 x 2 x 64 KB would not fit); the next tile is
+    // requested once the last segment holds the tile in registers, the other CTA covers the gap
+    constexpr bool SINGLE = !BYTE && MINB >= 2;
+    constexpr int NBUF = (BYTE || SINGLE) ? 1 : 2;
+    // 2 CTAs per SM with 3 segments: segment 0 accumulates in registers, segments 1, 2 add
+    // their per-tile sums to thread-private shared-memory slots (16 doubles per thread)
+    constexpr bool ACC_SMEM = !BYTE && MINB >= 2 && NSEG >= 3;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     cplx* bufs = reinterpret_cast<cplx*>(smem_raw);
     double* ow = reinterpret_cast<double*>(smem_raw + NBUF * sizeof(cplx) * TILE);  // [NW][kOutMax]
@@ -63,7 +77,10 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
     // NSTAGE - 1 tiles of bytes are in flight while one is decoded
     constexpr int NSTAGE = 4;
     unsigned char* stage = reinterpret_cast<unsigned char*>(dtab + 768);                // [NSTAGE][2][TILE]
+    double* accs = red + NW * NSL;   // ACC_SMEM: slot k of thread t at accs[k * NT + t]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if constexpr (ACC_SMEM)
+        for (int i = tid; i < (NSEG - 1) * 2 * RB * NT; i += NT) accs[i] = 0.0;
     for (int i = tid; i < NW * kOutMax; i += NT) ow[i] = 0.0;
     for (int i = tid; i < NW * NSL; i += NT) red[i] = 0.0;
     if constexpr (BYTE)
@@ -85,12 +102,14 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
         for (int j = 0; j < R; ++j) cp_async16m(dst + (sw_tid + j * NT), g + p.pf_go[j]);
     };
 
-    double tw_all = 0.0, twr[4] = {0.0, 0.0, 0.0, 0.0};
-    double cr[3][4], ci[3][4];
+    double tw_all = 0.0, twr[RB];
+    double cr[NSEG][RB], ci[NSEG][RB];
 #pragma unroll
-    for (int s = 0; s < 3; ++s)
+    for (int j = 0; j < RB; ++j) twr[j] = 0.0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) cr[s][j] = ci[s][j] = 0.0;
+    for (int s = 0; s < NSEG; ++s)
+#pragma unroll
+        for (int j = 0; j < RB; ++j) cr[s][j] = ci[s][j] = 0.0;
 
     // BYTE: this thread's 16-byte chunk of the tile (elements 16 tid .. 16 tid + 15)
     uint64_t go_chunk = 0;
@@ -119,7 +138,7 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
         cp_commit_m();
     }
     for (int it = 0; tile < p.n_tiles; ++it, tile += gridDim.x) {
-        cplx* S = bufs + (BYTE ? 0 : (it & 1) * TILE);
+        cplx* S = bufs + (NBUF == 1 ? 0 : (it & 1) * TILE);
         const uint64_t next = tile + gridDim.x;
         if constexpr (BYTE) {
             cp_wait_m<NSTAGE - 2>();      // this tile's bytes landed (the newer ones may not)
@@ -150,6 +169,8 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
                     S[swz3(16 * tid + i, p.swz_cols)] = v;
                 }
             }
+        } else if constexpr (SINGLE) {
+            cp_wait_m<0>();
         } else {
             if (next < p.n_tiles) prefetch(next, bufs + ((it + 1) & 1) * TILE);
             cp_commit_m();
@@ -157,7 +178,7 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
         }
         __syncthreads();
 #pragma unroll
-        for (int s = 0; s < 3; ++s) {
+        for (int s = 0; s < NSEG; ++s) {
             if (s >= p.n_segs) break;
             int tb = 0;
 #pragma unroll
@@ -166,14 +187,21 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
             cplx r[R];
 #pragma unroll
             for (int i = 0; i < R; ++i) r[i] = S[tsw ^ p.seg_rsw[s][i]];
-            if (s == 0 && p.want_ones) {
+            if constexpr (SINGLE) {
+                if (s == p.n_segs - 1) {   // tile in registers: the buffer takes the next tile
+                    __syncthreads();
+                    if (next < p.n_tiles) prefetch(next, S);
+                    cp_commit_m();
+                }
+            }
+            if (ONES && s == 0) {
                 double tt = 0.0;
 #pragma unroll
                 for (int i = 0; i < R; ++i) {
                     const double w = r[i].re * r[i].re + r[i].im * r[i].im;
                     tt += w;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
+                    for (int j = 0; j < RB; ++j)
                         if ((i >> j) & 1) twr[j] += w;
                 }
                 tw_all += tt;
@@ -187,19 +215,39 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
                 }
             }
             const uint32_t cm = p.cross_reg[s];
+            if (ACC_SMEM && s > 0) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < RB; ++j) {
+                    if (!((cm >> j) & 1)) continue;
+                    double lr = 0.0, li = 0.0;
+#pragma unroll
+                    for (int i = 0; i < R; ++i) {
+                        if ((i >> j) & 1) continue;
+                        const cplx a0 = r[i], a1 = r[i | (1 << j)];
+                        lr = __fma_rn(a0.im, a1.im, __fma_rn(a0.re, a1.re, lr));
+                        li = __fma_rn(-a0.im, a1.re, __fma_rn(a0.re, a1.im, li));
+                    }
+                    const int k = ((s - 1) * RB + j) * 2;
+                    accs[k * NT + tid] += lr;
+                    accs[(k + 1) * NT + tid] += li;
+                }
+                continue;
+            }
+#pragma unroll
+            for (int j = 0; j < RB; ++j) {
                 if (!((cm >> j) & 1)) continue;
 #pragma unroll
                 for (int i = 0; i < R; ++i) {
                     if ((i >> j) & 1) continue;
                     const cplx a0 = r[i], a1 = r[i | (1 << j)];
-                    cr[s][j] += a0.re * a1.re + a0.im * a1.im;
-                    ci[s][j] += a0.re * a1.im - a0.im * a1.re;
+                    // conj(a0) a1 accumulated with two fused multiply-adds per part (reports
+                    // are compared within 1e-12, not bit for bit; one rounding per product)
+                    cr[s][j] = __fma_rn(a0.im, a1.im, __fma_rn(a0.re, a1.re, cr[s][j]));
+                    ci[s][j] = __fma_rn(-a0.im, a1.re, __fma_rn(a0.re, a1.im, ci[s][j]));
                 }
             }
         }
-        __syncthreads();   // S is the prefetch target two tiles from now (BYTE: the next tile)
+        if constexpr (!SINGLE) __syncthreads();   // S is the prefetch target two tiles from now (BYTE: the next tile)
     }
     cp_wait_m<0>();
 
@@ -212,9 +260,9 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
     };
     double v = wsum(tw_all);
     if (lane == 0) red[warp * NSL + 0] = v;
-    if (p.want_ones) {
+    if (ONES) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < RB; ++j) {
             v = wsum(twr[j]);
             if (lane == 0) red[warp * NSL + 1 + p.seg_reg[0][j]] = v;
         }
@@ -225,11 +273,13 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
         }
     }
 #pragma unroll
-    for (int s = 0; s < 3; ++s)
+    for (int s = 0; s < NSEG; ++s)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < RB; ++j) {
             if (s >= p.n_segs || !((p.cross_reg[s] >> j) & 1)) continue;
-            const double a = wsum(cr[s][j]), b = wsum(ci[s][j]);
+            const int k = ((s - 1) * RB + j) * 2;
+            const double a = wsum((ACC_SMEM && s > 0) ? accs[k * NT + tid] : cr[s][j]);
+            const double b = wsum((ACC_SMEM && s > 0) ? accs[(k + 1) * NT + tid] : ci[s][j]);
             if (lane == 0) {
                 red[warp * NSL + 1 + KB + 2 * p.seg_reg[s][j]] = a;
                 red[warp * NSL + 2 + KB + 2 * p.seg_reg[s][j]] = b;
@@ -251,38 +301,52 @@ __global__ void __launch_bounds__(1 << (KB - 4), MINB)
     }
 }
 
-template <int KB, int MINB, bool BYTE>
+template <int KB, int MINB, bool BYTE, int NSEG, bool ONES, int RB = 4>
 static cudaError_t measure3_cfg(const c64s* psi, const Measure3Params& p, double* partials, int grid,
                                 cudaStream_t st, const MeasureBytes& b) {
-    constexpr int TILE = 1 << KB, NW = (TILE / 16) / 32;
-    const size_t smem = (BYTE ? 1 : 2) * sizeof(cplx) * TILE + sizeof(double) * NW * (kOutMax + 1 + 3 * KB) +
+    constexpr int TILE = 1 << KB, NW = (TILE >> RB) / 32;
+    constexpr bool ACC_SMEM = !BYTE && MINB >= 2 && NSEG >= 3;
+    const size_t smem = (ACC_SMEM ? sizeof(double) * (NSEG - 1) * 2 * RB * (TILE >> RB) : 0) +
+                        ((BYTE || MINB >= 2) ? 1 : 2) * sizeof(cplx) * TILE + sizeof(double) * NW * (kOutMax + 1 + 3 * KB) +
                         (BYTE ? sizeof(double) * 768 + 4 * 2 * TILE : 0);
     static bool configured[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k_measure3<KB, MINB, BYTE>,
+        cudaError_t e = cudaFuncSetAttribute(k_measure3<KB, MINB, BYTE, NSEG, ONES, RB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
-    k_measure3<KB, MINB, BYTE><<<grid, TILE / 16, smem, st>>>(psi, p, partials, b);
+    k_measure3<KB, MINB, BYTE, NSEG, ONES, RB><<<grid, TILE >> RB, smem, st>>>(psi, p, partials, b);
     count_launch();
     return cudaGetLastError();
 }
 
-int measure3_grid(int device, int kb, bool byte) { return sm_count(device) * (byte ? 1 : (kb == 12 ? 1 : 3)); }
+// CTAs per SM of the variant a pass runs (grid = that x SMs)
+static bool light_pass(const Measure3Params& p) { return !p.want_ones && p.n_segs <= 2; }
+int measure3_ctas_per_sm(int kb, bool byte, const Measure3Params& p) {
+    if (kb != 12) return 3;
+    if (p.rbits == 3 || byte) return byte && light_pass(p) ? 2 : 1;
+    return 2;   // light passes, and the 3-segment pass with shared-memory accumulators
+}
+int measure3_grid(int device, int kb, bool byte) { return sm_count(device) * (kb == 12 ? 2 : 3); }   // max over variants
 
 cudaError_t launch_measure3(const void* psi, const Measure3Params& p, double* partials, int grid, cudaStream_t st) {
     const MeasureBytes none{nullptr, nullptr, nullptr};
     const c64s* s = static_cast<const c64s*>(psi);
-    return p.kbits == 12 ? measure3_cfg<12, 1, false>(s, p, partials, grid, st, none)
-                         : measure3_cfg<11, 3, false>(s, p, partials, grid, st, none);
+    if (p.kbits != 12) return measure3_cfg<11, 3, false, 3, true>(s, p, partials, grid, st, none);
+    if (p.rbits == 3)
+        return p.want_ones ? measure3_cfg<12, 1, false, 4, true, 3>(s, p, partials, grid, st, none)
+                           : measure3_cfg<12, 1, false, 4, false, 3>(s, p, partials, grid, st, none);
+    return light_pass(p) ? measure3_cfg<12, 2, false, 2, false>(s, p, partials, grid, st, none)
+                         : measure3_cfg<12, 2, false, 3, true>(s, p, partials, grid, st, none);
 }
 
 cudaError_t launch_measure3_byte(const MeasureBytes& b, const Measure3Params& p, double* partials, int grid,
                                  cudaStream_t st) {
-    return measure3_cfg<12, 1, true>(nullptr, p, partials, grid, st, b);   // 2 CTAs/SM spill (128 regs)
+    return light_pass(p) ? measure3_cfg<12, 2, true, 2, false>(nullptr, p, partials, grid, st, b)
+                         : measure3_cfg<12, 1, true, 3, true>(nullptr, p, partials, grid, st, b);
 }
 
 }  // namespace sv
