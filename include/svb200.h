@@ -147,6 +147,10 @@ int svb_set_tables(sv_bhandle h, const double* mags, int n_mag, const double* th
                    const double* uy, int n_ph);
 /* one pass: reads the current planes, writes the pending planes */
 int svb_gate(sv_bhandle h, const svb_gate_desc* g);
+/* diagonal gate, final write pass (tables fixed: saturated, or scanned and
+ * merged first): rewrites only the selected amplitudes of the CURRENT planes
+ * (engine.py:186-225 encode step of a diagonal gate; no commit follows) */
+int svb_gate_in_place(sv_bhandle h, const svb_gate_desc* g);
 /* candidates of the passes since the last reset: distinct magnitudes and,
  * per distinct theta, (re, im, ux, uy) of its smallest-(ux, uy) value
  * (duplicates possible).  flags: 1 = a buffer overflowed (retry with a cut),
@@ -161,6 +165,8 @@ int svb_unsure(sv_bhandle h, uint64_t* idx, double* vals, uint64_t cap, uint64_t
 int svb_reset(sv_bhandle h);
 /* overwrite bytes of the pending planes (host-resolved uncertain amplitudes) */
 int svb_patch(sv_bhandle h, const uint64_t* idx, const uint8_t* mi, const uint8_t* pi, uint64_t n);
+/* the same on the current planes (after svb_gate_in_place) */
+int svb_patch_in_place(sv_bhandle h, const uint64_t* idx, const uint8_t* mi, const uint8_t* pi, uint64_t n);
 /* pending planes become current */
 int svb_commit(sv_bhandle h);
 int svb_export(sv_bhandle h, uint8_t* mi, uint8_t* pi, uint64_t first, uint64_t count);

@@ -69,12 +69,14 @@ _SIGNATURES = {
     "svb_zero_state": ([_P, ctypes.c_int64], _I),
     "svb_set_tables": ([_P, _D, _I, _D, _D, _D, _I], _I),
     "svb_gate": ([_P, _P], _I),
+    "svb_gate_in_place": ([_P, _P], _I),
     "svb_candidate_tags": ([_P, ctypes.POINTER(ctypes.c_int32), _U64, ctypes.POINTER(ctypes.c_int32), _U64], _I),
     "svb_candidates": ([_P, _D, _U64, ctypes.POINTER(_U64), _D, _U64, ctypes.POINTER(_U64),
                         ctypes.POINTER(_I)], _I),
     "svb_unsure": ([_P, ctypes.POINTER(_U64), _D, _U64, ctypes.POINTER(_U64)], _I),
     "svb_reset": ([_P], _I),
     "svb_patch": ([_P, ctypes.POINTER(_U64), _P, _P, _U64], _I),
+    "svb_patch_in_place": ([_P, ctypes.POINTER(_U64), _P, _P, _U64], _I),
     "svb_commit": ([_P], _I),
     "svb_export": ([_P, _P, _P, _U64, _U64], _I),
     "svb_import": ([_P, _P, _P, _U64, _U64], _I),

@@ -19,6 +19,7 @@ protocol (engine.py:186-225, 365-377):
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -30,6 +31,8 @@ _BIG = 1e308
 _CAP = 1 << 22                # = CAP_UNSURE of sv_byte_api.cu (uncertain-phase list)
 _CCAP = 1 << 20               # = CAP_MAG / CAP_PH (candidate buffers)
 MAX_TAGGED_RANKS = 8          # candidate set regions per CTA (sv_byte.cu CtaSets)
+# diagonal write passes with fixed tables run in place (SVB200_BYTE_IN_PLACE=0: off)
+IN_PLACE = os.environ.get("SVB200_BYTE_IN_PLACE", "1") != "0"
 
 
 class SvbGateDesc(ctypes.Structure):
@@ -178,13 +181,16 @@ class ByteDeviceState:
     def reset(self):
         nat.check(nat.load().svb_reset(self.handle))
 
-    def patch(self, idx, mi, pi):
+    def patch(self, idx, mi, pi, in_place: bool = False):
+        """Host-encoded bytes into the pending planes (or the current ones after an
+        in-place pass)."""
         if len(idx) == 0:
             return
         idx = np.ascontiguousarray(idx, dtype=np.uint64)
         mi = np.ascontiguousarray(mi, dtype=np.uint8)
         pi = np.ascontiguousarray(pi, dtype=np.uint8)
-        nat.check(nat.load().svb_patch(self.handle, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+        fn = nat.load().svb_patch_in_place if in_place else nat.load().svb_patch
+        nat.check(fn(self.handle, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
                                        mi.ctypes.data_as(ctypes.c_void_p), pi.ctypes.data_as(ctypes.c_void_p),
                                        idx.size))
         self.launches += 1
@@ -193,16 +199,31 @@ class ByteDeviceState:
         nat.check(nat.load().svb_commit(self.handle))
         self.version += 1
 
-    def gate_pass(self, desc: SvbGateDesc):
+    def gate_pass(self, desc: SvbGateDesc, in_place: bool = False):
+        """One pass; in_place (diagonal write pass with fixed tables): only the selected
+        amplitudes of the current planes are rewritten, no commit follows."""
+        fn = nat.load().svb_gate_in_place if in_place else nat.load().svb_gate
         if getattr(self, "time_passes", False):
             e0, e1 = nat.Event(), nat.Event()
             e0.record(self.stream)
-            nat.check(nat.load().svb_gate(self.handle, ctypes.byref(desc)))
+            nat.check(fn(self.handle, ctypes.byref(desc)))
             e1.record(self.stream)
             self.pass_events.append((desc.scan_only, e0, e1))
         else:
-            nat.check(nat.load().svb_gate(self.handle, ctypes.byref(desc)))
+            nat.check(fn(self.handle, ctypes.byref(desc)))
         self.launches += 1
+
+    def finish_gate(self, ui, uv, in_place: bool) -> int:
+        """Patch the host-encoded uncertain amplitudes and publish the gate's planes."""
+        self.reset()
+        if len(ui):
+            mi, pi = self.codebook.host_encode(uv)
+            self.patch(ui, mi, pi, in_place)
+        if in_place:
+            self.version += 1
+        else:
+            self.commit()
+        return len(ui)
 
     # -- array-level codec -----------------------------------------------------------
     def encode_values(self, v: np.ndarray):
@@ -336,12 +357,12 @@ class ByteEngineState(ByteDeviceState):
             if len(um) <= k and len(ut) <= k:
                 raise RuntimeError("codebook candidate buffer overflow without a usable cut")
 
-    def _write_pass(self, d: SvbGateDesc):
+    def _write_pass(self, d: SvbGateDesc, in_place: bool = False):
         d.producer = -1
         d.collect = 0
         d.scan_only = 0
         self.reset()
-        self.gate_pass(d)
+        self.gate_pass(d, in_place)
         self.passes += 1
         return self.read_unsure()
 
@@ -361,10 +382,18 @@ class ByteEngineState(ByteDeviceState):
         d = self._desc(gate, plan)
         d.want_mag = 0 if sat_mag else 1
         d.want_ph = 0 if sat_ph else 1
+        # a diagonal gate's final write pass (tables fixed) rewrites only the amplitudes it
+        # selects, in the current planes; the speculative encode-while-collecting pass
+        # keeps its input intact (a table that grows forces a re-encode from it)
+        in_place = IN_PLACE and d.kind == nat.SV_OP_DIAG
+        final_in_place = False
         if sat_mag and sat_ph:
-            ui, uv = self._write_pass(d)
+            ui, uv = self._write_pass(d, in_place)
+            final_in_place = in_place
         else:
-            scan = self.scan_first
+            # diagonal gates always scan first: the scan reads only the selected amplitudes
+            # and the write pass then runs in place with the merged tables
+            scan = self.scan_first or in_place
             proposals, unsure = [], []
             ranks = self.layout.rank_count
             d.scan_only = 1 if scan else 0
@@ -385,15 +414,11 @@ class ByteEngineState(ByteDeviceState):
             self.scan_first = grew
             if scan or grew:
                 self.sync_tables()
-                ui, uv = self._write_pass(d)
+                ui, uv = self._write_pass(d, in_place)
+                final_in_place = in_place
                 if grew and not scan:
                     self.reencodes += 1
             else:
                 ui = np.concatenate([u[0] for u in unsure])
                 uv = np.concatenate([u[1] for u in unsure])
-        self.reset()
-        if len(ui):
-            mi, pi = cb.host_encode(uv)
-            self.patch(ui, mi, pi)
-            self.host_fixes += len(ui)
-        self.commit()
+        self.host_fixes += self.finish_gate(ui, uv, final_in_place)

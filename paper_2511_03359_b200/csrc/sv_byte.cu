@@ -27,6 +27,7 @@
 // "uncertain" and resolved on the host with numpy, so the produced bytes are
 // the reference's bytes.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "sv_byte.cuh"
@@ -833,9 +834,17 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
         }
     } else if (g.n_elems >= 16 && lmin >= 3) {   // DIAG, 8 amplitudes per work item
         const cplx f = {g.m[0], g.m[1]};
-        const uint64_t n_chunks = g.n_elems >> 3;
+        // in place: visit only the chunks whose index bits >= 3 match the mask
+        const uint64_t hmask = g.in_place ? ((g.mask & ~7ull) >> 3) : 0ull;
+        const uint64_t n_chunks = (g.in_place && (g.mask & ~(g.n_elems - 1ull))) ? 0ull   // selects nothing
+                                  : ((g.n_elems >> 3) >> __popcll(hmask));
         for (uint64_t w = first; w < n_chunks; w += step) {
-            const uint64_t i = w << 3;
+            uint64_t c = w;
+            for (uint64_t m = hmask; m; m &= m - 1) {   // insert a 1 at every mask position
+                const int b = __ffsll((long long)m) - 1;
+                c = ((c >> b) << (b + 1)) | (1ull << b) | (c & ((1ull << b) - 1ull));
+            }
+            const uint64_t i = c << 3;
             // the 8 amplitudes of a chunk share their producer (bits >= 3 decide it)
             const int pr = (g.producer >= 0 || tagged) ? producer_of(g, i) : 0;
             if (g.producer >= 0 && pr != g.producer) continue;
@@ -876,7 +885,7 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
             if ((i & g.mask) == g.mask) {
                 if (g.producer >= 0 && pr != g.producer) continue;
                 em.emit(i, cmul(decode(t, mi_in[i], pi_in[i]), f), tc, tagged ? pr : 0);
-            } else if (write && (g.producer < 0 || pr == g.producer)) {
+            } else if (write && !g.in_place && (g.producer < 0 || pr == g.producer)) {
                 mi_out[i] = mi_in[i];
                 pi_out[i] = pi_in[i];
             }
@@ -886,6 +895,153 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
         __syncthreads();
         sets_flush(sets, cand);
     }
+}
+
+// ---- diagonal write passes with fixed tables: a 65536-entry code table ---------------
+// A diagonal gate maps every amplitude by its own code alone: (m, p) -> code of
+// decode(m, p) * f.  When the pass collects no candidates (tables saturated, or
+// scanned and merged first) the whole map is evaluated once, with the same encoder
+// as the per-amplitude path, and the pass becomes a table lookup per selected
+// amplitude.  Entries whose phase decision is uncertain are flagged (bit 16): those
+// amplitudes are recomputed per index so they reach the host as before.
+__device__ CtaSets g_no_sets;   // never touched: the table passes collect nothing
+
+constexpr unsigned kDiagUnsure = 0xff00u;   // table entry: recompute per index (a code with
+                                            // magnitude index 0 always has phase index 0)
+__global__ void __launch_bounds__(NT) k_byte_diag_table(const ByteTables* __restrict__ gtab,
+                                                        const __grid_constant__ ByteGate g, uint16_t* lut) {
+    __shared__ STables t;
+    load_tables(t, gtab);
+    __syncthreads();
+    const Emitter em{t, g, g_no_sets, nullptr, nullptr, nullptr, false, false};
+    ThreadCache tc{NAN, NAN, NAN, NAN, NAN, NAN, 0u, 0};
+    const unsigned key = blockIdx.x * NT + threadIdx.x;   // m | p << 8
+    if (key >= 65536u) return;
+    const cplx f = {g.m[0], g.m[1]};
+    bool sure = true;
+    const unsigned c = em.code(0, cmul(decode(t, key & 255u, key >> 8), f), tc, &sure, 0);
+    lut[key] = (uint16_t)(sure ? c : kDiagUnsure);
+}
+
+// The pass itself: a table lookup per selected amplitude.  Collecting passes
+// (speculative encode, or scan) also record which (code, producer) pairs occur, in
+// a per-CTA bitmap merged into `seen`; k_byte_diag_collect then proposes the
+// candidates of exactly those codes (candidate sets are sets: the order in which
+// values are offered does not matter).
+// SCAN: record the occurring (code, producer) pairs only.  Otherwise: rewrite the
+// selected amplitudes through the table, staged in shared memory (128 KB, one
+// 1024-thread CTA per SM); a collecting write pass does both.
+constexpr int NTD = 1024;
+template <bool SCAN>
+__global__ void __launch_bounds__(SCAN ? NT : NTD) k_byte_diag_apply(
+    const uint8_t* mi_in, const uint8_t* pi_in, uint8_t* mi_out, uint8_t* pi_out, const ByteTables* __restrict__ gtab,
+    const __grid_constant__ ByteGate g, ByteCand* cand, const uint16_t* __restrict__ lut, uint32_t* seen, int nprod) {
+    constexpr int NTK = SCAN ? NT : NTD;
+    __shared__ STables t;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint16_t* slut = reinterpret_cast<uint16_t*>(dsm);                            // !SCAN: 65536 codes
+    uint32_t* bits = reinterpret_cast<uint32_t*>(dsm + (SCAN ? 0 : 65536 * 2));   // collect: nprod x 2048
+    const bool collect = seen != nullptr, tagged = g.producer == -2;
+    constexpr bool write = !SCAN;
+    if (collect)
+        for (int k = threadIdx.x; k < nprod * 2048; k += NTK) bits[k] = 0u;
+    if constexpr (!SCAN)
+        for (int k = threadIdx.x; k < 65536 / 8; k += NTK)
+            reinterpret_cast<uint4*>(slut)[k] = reinterpret_cast<const uint4*>(lut)[k];
+    load_tables(t, gtab);
+    __syncthreads();
+    const Emitter em{t, g, g_no_sets, cand, mi_out, pi_out, false, write};
+    ThreadCache tc{NAN, NAN, NAN, NAN, NAN, NAN, 0u, 0};
+    const cplx f = {g.m[0], g.m[1]};
+    const uint64_t step = (uint64_t)gridDim.x * NTK;
+    const uint64_t first = (uint64_t)blockIdx.x * NTK + threadIdx.x;
+    // chunks of 16 amplitudes (16-byte loads of each plane, the next chunk's loads issued
+    // before the current one is processed); in place or scanning, only the chunks whose
+    // index bits >= 4 match the mask are visited
+    const bool sparse = g.in_place || !write;
+    const uint64_t hmask = sparse ? ((g.mask & ~15ull) >> 4) : 0ull;
+    const uint64_t n_chunks = (g.mask & ~(g.n_elems - 1ull)) ? (sparse ? 0ull : (g.n_elems >> 4))
+                                                             : ((g.n_elems >> 4) >> __popcll(hmask));
+    auto chunk_at = [&](uint64_t w) {
+        uint64_t c = w;
+        for (uint64_t m = hmask; m; m &= m - 1) {   // insert a 1 at every mask position
+            const int b = __ffsll((long long)m) - 1;
+            c = ((c >> b) << (b + 1)) | (1ull << b) | (c & ((1ull << b) - 1ull));
+        }
+        return c << 4;
+    };
+    uint64_t w = first, inx = 0;
+    uint4 nm = {0, 0, 0, 0}, np = {0, 0, 0, 0};
+    if (w < n_chunks) {
+        inx = chunk_at(w);
+        nm = *reinterpret_cast<const uint4*>(mi_in + inx);
+        np = *reinterpret_cast<const uint4*>(pi_in + inx);
+    }
+    for (; w < n_chunks; w += step) {
+        const uint64_t i = inx;
+        const uint4 cm = nm, cpv = np;
+        if (w + step < n_chunks) {
+            inx = chunk_at(w + step);
+            nm = *reinterpret_cast<const uint4*>(mi_in + inx);
+            np = *reinterpret_cast<const uint4*>(pi_in + inx);
+        }
+        if (((i | 15ull) & g.mask) != g.mask) {   // out of place: untouched chunk copied
+            if (write) {
+                *reinterpret_cast<uint4*>(mi_out + i) = cm;
+                *reinterpret_cast<uint4*>(pi_out + i) = cpv;
+            }
+            continue;
+        }
+        // the 16 amplitudes of a chunk share their producer (the caller checked the bits)
+        const int prod = tagged ? producer_of(g, i) : 0;
+        unsigned mw[4] = {cm.x, cm.y, cm.z, cm.w}, pw[4] = {cpv.x, cpv.y, cpv.z, cpv.w};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (((i + j) & g.mask) != g.mask) continue;
+            const unsigned sh = 8 * (j & 3);
+            const unsigned bmj = (mw[j >> 2] >> sh) & 255u, bpj = (pw[j >> 2] >> sh) & 255u;
+            const unsigned key = bmj | (bpj << 8);
+            if (collect) {
+                uint32_t* wd = bits + prod * 2048 + (key >> 5);
+                if (!((*wd >> (key & 31)) & 1u)) atomicOr(wd, 1u << (key & 31));
+            }
+            if constexpr (!SCAN) {
+                unsigned code = slut[key];
+                if (code == kDiagUnsure) code = em.code(i + j, cmul(decode(t, bmj, bpj), f), tc);   // reports i+j
+                mw[j >> 2] = (mw[j >> 2] & ~(255u << sh)) | ((code & 255u) << sh);
+                pw[j >> 2] = (pw[j >> 2] & ~(255u << sh)) | ((code >> 8) << sh);
+            }
+        }
+        if (write) {
+            *reinterpret_cast<uint4*>(mi_out + i) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+            *reinterpret_cast<uint4*>(pi_out + i) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+        }
+    }
+    if (collect) {
+        __syncthreads();
+        for (int k = threadIdx.x; k < nprod * 2048; k += NTK)
+            if (bits[k]) atomicOr(seen + k, bits[k]);
+    }
+}
+
+// candidates of the codes a collecting table pass saw, per producer region
+__global__ void __launch_bounds__(NT) k_byte_diag_collect(const ByteTables* __restrict__ gtab,
+                                                          const __grid_constant__ ByteGate g, ByteCand* cand,
+                                                          const uint32_t* __restrict__ seen, int nprod) {
+    __shared__ STables t;
+    __shared__ CtaSets sets;
+    load_tables(t, gtab);
+    sets_clear(sets, g.producer == -2 ? nprod : 1);
+    __syncthreads();
+    const Emitter em{t, g, sets, cand, nullptr, nullptr, true, false};
+    ThreadCache tc{NAN, NAN, NAN, NAN, NAN, NAN, 0u, 0};
+    const cplx f = {g.m[0], g.m[1]};
+    for (unsigned key = blockIdx.x * NT + threadIdx.x; key < 65536u; key += gridDim.x * NT)
+        for (int pr = 0; pr < nprod; ++pr)
+            if ((seen[pr * 2048 + (key >> 5)] >> (key & 31)) & 1u)
+                em.code(0, cmul(decode(t, key & 255u, key >> 8), f), tc, nullptr, pr);
+    __syncthreads();
+    sets_flush(sets, cand);
 }
 
 // Decode into complex128 (export, host mirrors, measurement of small states).
@@ -1016,6 +1172,15 @@ __global__ void k_byte_pair_dot(const uint8_t* ami, const uint8_t* api, const ui
     }
 }
 
+static bool diag_table_enabled() {   // SVB200_BYTE_DIAG_TABLE=0: per-amplitude memo path
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("SVB200_BYTE_DIAG_TABLE");
+        v = (e && std::atoi(e) == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+
 static unsigned byte_grid(uint64_t items) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1045,6 +1210,46 @@ cudaError_t launch_byte_gate(const uint8_t* mi_in, const uint8_t* pi_in, uint8_t
     int lmin = 64;
     if (g.producer >= 0 || g.producer == -2)
         for (int j = 0; j < 2 + g.rank_bits && j < 12; ++j) lmin = std::min(lmin, (int)g.lbit[j]);
+    // diagonal gates through the 65536-entry code table (write passes, and collecting
+    // passes of the whole buffer or tagged by producer when a chunk has one producer)
+    const bool tagged = g.producer == -2;
+    if (g.kind == SV_OP_DIAG && g.n_elems >= 4096 && diag_table_enabled() &&
+        (g.producer == -1 || (tagged && lmin >= 4 && g.rank_bits <= 3)) && (g.collect || !g.scan_only)) {
+        const int nprod = tagged ? (1 << g.rank_bits) : 1;
+        unsigned char* scratch = nullptr;   // 65536 uint16 codes, then nprod x 2048 seen words
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), 65536 * 2 + 2048 * 8 * 4, st);
+        if (e != cudaSuccess) return e;
+        uint16_t* lut = reinterpret_cast<uint16_t*>(scratch);
+        uint32_t* seen = g.collect ? reinterpret_cast<uint32_t*>(scratch + 65536 * 2) : nullptr;
+        if (seen) cudaMemsetAsync(seen, 0, 2048 * nprod * sizeof(uint32_t), st);
+        const uint64_t chunks = g.n_elems >> 4;
+        const size_t bm_bytes = seen ? 2048 * nprod * sizeof(uint32_t) : 0;
+        if (g.scan_only) {
+            if (bm_bytes > 48 * 1024)
+                cudaFuncSetAttribute(k_byte_diag_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bm_bytes);
+            k_byte_diag_apply<true><<<byte_grid(chunks), NT, bm_bytes, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g,
+                                                                              cand, lut, seen, nprod);
+        } else {
+            k_byte_diag_table<<<65536 / NT, NT, 0, st>>>(tab, g, lut);
+            count_launch();
+            const size_t smem = 65536 * 2 + bm_bytes;
+            cudaFuncSetAttribute(k_byte_diag_apply<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int dev2 = 0;
+            cudaGetDevice(&dev2);
+            const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((chunks + NTD - 1) / NTD,
+                                                                                     (uint64_t)sm_count(dev2)));
+            k_byte_diag_apply<false><<<grid, NTD, smem, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g, cand, lut, seen,
+                                                              nprod);
+        }
+        count_launch();
+        if (seen) {
+            k_byte_diag_collect<<<64, NT, 0, st>>>(tab, g, cand, seen, nprod);
+            count_launch();
+        }
+        e = cudaGetLastError();
+        cudaFreeAsync(scratch, st);
+        return e;
+    }
     if (g.kind == SV_OP_1Q && g.qa < 4 && g.n_elems >= 1024 && lmin >= 5)
         low[g.qa]<<<byte_grid(g.n_elems / 32), NT, memo_bytes, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g, cand);
     else

@@ -38,6 +38,8 @@ struct ByteGate {
     int mag_room, ph_room;      // free table entries (informational)
     double mag_cut, ph_cut;     // only values below the cut are collected (overflow retry)
     int scan_only;              // 1: collect candidates, write nothing
+    int in_place;               // DIAG write pass into the input planes: untouched amplitudes
+                                // are neither read nor written
 };
 
 // Candidate / uncertain-amplitude output of a pass (device memory).

@@ -187,6 +187,21 @@ int svb_gate(sv_bhandle h, const svb_gate_desc* d) {
     return e == cudaSuccess ? SV_OK : capi_cuda_fail(e, "BYTE gate launch");
 }
 
+int svb_gate_in_place(sv_bhandle h, const svb_gate_desc* d) {
+    Guard gd(h->device);
+    if (d->kind != SV_OP_DIAG) return capi_fail(SV_EVALUE, "in-place BYTE passes are for diagonal gates");
+    if (d->scan_only || d->collect) return capi_fail(SV_EVALUE, "in-place BYTE pass: write pass only");
+    // a mask bit outside the buffer (a rank whose global qubit reads 0) selects nothing:
+    // in place, nothing is written
+    if (d->diag_mask >> h->n) return SV_OK;
+    ByteGate g = to_gate(*d, 1ull << h->n);
+    g.in_place = 1;
+    const int c = h->cur;
+    cudaError_t e = launch_byte_gate(h->plane[c][0], h->plane[c][1], h->plane[c][0], h->plane[c][1], h->tab, g,
+                                     h->cand, h->stream);
+    return e == cudaSuccess ? SV_OK : capi_cuda_fail(e, "BYTE gate launch");
+}
+
 int svb_candidates(sv_bhandle h, double* mags, uint64_t cap_m, uint64_t* n_m, double* ph4, uint64_t cap_p,
                    uint64_t* n_p, int* flags) {
     Guard gd(h->device);
@@ -241,7 +256,16 @@ int svb_reset(sv_bhandle h) {
     return SV_OK;
 }
 
+static int patch_planes(sv_bhandle h, int which, const uint64_t* idx, const uint8_t* mi, const uint8_t* pi,
+                        uint64_t n);
 int svb_patch(sv_bhandle h, const uint64_t* idx, const uint8_t* mi, const uint8_t* pi, uint64_t n) {
+    return patch_planes(h, 1 - h->cur, idx, mi, pi, n);
+}
+int svb_patch_in_place(sv_bhandle h, const uint64_t* idx, const uint8_t* mi, const uint8_t* pi, uint64_t n) {
+    return patch_planes(h, h->cur, idx, mi, pi, n);
+}
+static int patch_planes(sv_bhandle h, int which, const uint64_t* idx, const uint8_t* mi, const uint8_t* pi,
+                        uint64_t n) {
     if (n == 0) return SV_OK;
     Guard gd(h->device);
     uint64_t* d_idx = nullptr;
@@ -251,8 +275,7 @@ int svb_patch(sv_bhandle h, const uint64_t* idx, const uint8_t* mi, const uint8_
     BTRY(cudaMemcpyAsync(d_idx, idx, 8 * n, cudaMemcpyHostToDevice, h->stream), "patch idx");
     BTRY(cudaMemcpyAsync(d_b, mi, n, cudaMemcpyHostToDevice, h->stream), "patch mi");
     BTRY(cudaMemcpyAsync(d_b + n, pi, n, cudaMemcpyHostToDevice, h->stream), "patch pi");
-    const int nx = 1 - h->cur;
-    cudaError_t e = launch_byte_patch(h->plane[nx][0], h->plane[nx][1], d_idx, d_b, d_b + n, n, h->stream);
+    cudaError_t e = launch_byte_patch(h->plane[which][0], h->plane[which][1], d_idx, d_b, d_b + n, n, h->stream);
     cudaFreeAsync(d_idx, h->stream);
     cudaFreeAsync(d_b, h->stream);
     if (e != cudaSuccess) return capi_cuda_fail(e, "patch");

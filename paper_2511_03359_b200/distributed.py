@@ -36,7 +36,7 @@ from .circuit import Circuit, validate_circuit
 from .device import gate_op, ops_array
 from .layout import PartitionLayout, TrafficLedger, plan_exchange
 from .measure import ExpectationReport, report_from_sums
-from .byte_state import MAX_TAGGED_RANKS
+from .byte_state import IN_PLACE as BYTE_IN_PLACE, MAX_TAGGED_RANKS
 from .remap import Measure, PhysGate, RemapPlanner, Swap, SwapGroup, deposit, group_schedule
 from .state import PrecisionMode
 
@@ -484,12 +484,12 @@ class CudaByteBackend:
         d.mag_cut = d.ph_cut = 1e308
         return d
 
-    def _pass(self, d, producer, collect, scan):
+    def _pass(self, d, producer, collect, scan, in_place=False):
         d.producer = producer
         d.collect = 1 if collect else 0
         d.scan_only = 1 if scan else 0
         self.st.reset()
-        self.st.gate_pass(d)
+        self.st.gate_pass(d, in_place)
         self.passes += 1
         mags, ph, flags = self.st.read_candidates() if collect else (None, None, 0)
         if flags & 1:
@@ -504,10 +504,15 @@ class CudaByteBackend:
         d = self._desc(gate, phys, pos)
         d.want_mag = 0 if sat_mag else 1
         d.want_ph = 0 if sat_ph else 1
+        # as ByteEngineState.apply_gate: a diagonal gate's final write pass runs in place
+        # (the same decision on every rank: it depends on the gate and the shared codebook)
+        in_place = BYTE_IN_PLACE and d.kind == nat.SV_OP_DIAG
+        final_in_place = False
         if sat_mag and sat_ph:
-            _, _, (ui, uv) = self._pass(d, -1, False, False)
+            _, _, (ui, uv) = self._pass(d, -1, False, False, in_place)
+            final_in_place = in_place
         else:
-            scan = self.scan_first
+            scan = self.scan_first or in_place   # diagonal: scan, then write in place
             mine = []
             unsure = []
             ranks = self.layout.rank_count
@@ -537,16 +542,12 @@ class CudaByteBackend:
             self.scan_first = grew
             if scan or grew:
                 self.st.sync_tables()
-                _, _, (ui, uv) = self._pass(d, -1, False, False)
+                _, _, (ui, uv) = self._pass(d, -1, False, False, in_place)
+                final_in_place = in_place
             else:
                 ui = np.concatenate([u[0] for u in unsure])
                 uv = np.concatenate([u[1] for u in unsure])
-        self.st.reset()
-        if len(ui):
-            mi, pi = cb.host_encode(uv)
-            self.st.patch(ui, mi, pi)
-            self.host_fixes += len(ui)
-        self.st.commit()
+        self.host_fixes += self.st.finish_gate(ui, uv, final_in_place)
 
     def measure_local(self):
         return self.st.measure_sums()
