@@ -27,6 +27,8 @@
 // "uncertain" and resolved on the host with numpy, so the produced bytes are
 // the reference's bytes.
 #include <algorithm>
+#include <mutex>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 
@@ -1172,6 +1174,28 @@ __global__ void k_byte_pair_dot(const uint8_t* ami, const uint8_t* api, const ui
     }
 }
 
+// scratch of the diagonal table passes, one per stream (a stream-ordered allocation per
+// pass released its pool memory at every synchronisation: ~2 ms of host time per pass)
+static cudaError_t diag_scratch(cudaStream_t st, unsigned char** out) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, unsigned char*>& cache =
+        *new std::map<std::pair<int, cudaStream_t>, unsigned char*>;   // leaked: freed with the context
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({dev, st});
+    if (it != cache.end()) {
+        *out = it->second;
+        return cudaSuccess;
+    }
+    unsigned char* p = nullptr;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p), 65536 * 2 + 2048 * 8 * 4);
+    if (e != cudaSuccess) return e;
+    cache[{dev, st}] = p;
+    *out = p;
+    return cudaSuccess;
+}
+
 static bool diag_table_enabled() {   // SVB200_BYTE_DIAG_TABLE=0: per-amplitude memo path
     static int v = -1;
     if (v < 0) {
@@ -1217,27 +1241,29 @@ cudaError_t launch_byte_gate(const uint8_t* mi_in, const uint8_t* pi_in, uint8_t
         (g.producer == -1 || (tagged && lmin >= 4 && g.rank_bits <= 3)) && (g.collect || !g.scan_only)) {
         const int nprod = tagged ? (1 << g.rank_bits) : 1;
         unsigned char* scratch = nullptr;   // 65536 uint16 codes, then nprod x 2048 seen words
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), 65536 * 2 + 2048 * 8 * 4, st);
+        cudaError_t e = diag_scratch(st, &scratch);
         if (e != cudaSuccess) return e;
         uint16_t* lut = reinterpret_cast<uint16_t*>(scratch);
         uint32_t* seen = g.collect ? reinterpret_cast<uint32_t*>(scratch + 65536 * 2) : nullptr;
         if (seen) cudaMemsetAsync(seen, 0, 2048 * nprod * sizeof(uint32_t), st);
         const uint64_t chunks = g.n_elems >> 4;
         const size_t bm_bytes = seen ? 2048 * nprod * sizeof(uint32_t) : 0;
+        static bool diag_configured[64] = {false};
+        if (dev < 64 && !diag_configured[dev]) {
+            cudaFuncSetAttribute(k_byte_diag_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 8 * 4);
+            cudaFuncSetAttribute(k_byte_diag_apply<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 65536 * 2 + 2048 * 8 * 4);
+            diag_configured[dev] = true;
+        }
         if (g.scan_only) {
-            if (bm_bytes > 48 * 1024)
-                cudaFuncSetAttribute(k_byte_diag_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bm_bytes);
             k_byte_diag_apply<true><<<byte_grid(chunks), NT, bm_bytes, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g,
                                                                               cand, lut, seen, nprod);
         } else {
             k_byte_diag_table<<<65536 / NT, NT, 0, st>>>(tab, g, lut);
             count_launch();
             const size_t smem = 65536 * 2 + bm_bytes;
-            cudaFuncSetAttribute(k_byte_diag_apply<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            int dev2 = 0;
-            cudaGetDevice(&dev2);
             const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((chunks + NTD - 1) / NTD,
-                                                                                     (uint64_t)sm_count(dev2)));
+                                                                                     (uint64_t)sm_count(dev)));
             k_byte_diag_apply<false><<<grid, NTD, smem, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g, cand, lut, seen,
                                                               nprod);
         }
@@ -1246,9 +1272,7 @@ cudaError_t launch_byte_gate(const uint8_t* mi_in, const uint8_t* pi_in, uint8_t
             k_byte_diag_collect<<<64, NT, 0, st>>>(tab, g, cand, seen, nprod);
             count_launch();
         }
-        e = cudaGetLastError();
-        cudaFreeAsync(scratch, st);
-        return e;
+        return cudaGetLastError();
     }
     if (g.kind == SV_OP_1Q && g.qa < 4 && g.n_elems >= 1024 && lmin >= 5)
         low[g.qa]<<<byte_grid(g.n_elems / 32), NT, memo_bytes, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g, cand);

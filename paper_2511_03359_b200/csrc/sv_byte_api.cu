@@ -69,6 +69,7 @@ int svb_create(int device, int n_qubits, sv_bhandle* out) {
     *out = nullptr;
     if (n_qubits < 0 || n_qubits > 40) return capi_fail(SV_EVALUE, "n_qubits out of range");
     Guard gd(device);
+    keep_scratch_pool(device);
     sv_bstate* h = new sv_bstate();
     std::memset(h, 0, sizeof(*h));
     h->device = device;

@@ -977,6 +977,7 @@ int sv_create(int device, int n_qubits, int mode, sv_handle* out) {
     CUDA_TRY(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
     if (device < 0 || device >= ndev) return fail(SV_EVALUE, "device %d not present (%d visible)", device, ndev);
     DeviceGuard g(device);
+    keep_scratch_pool(device);
     sv_state* h = new sv_state();
     h->device = device;
     h->n = n_qubits;

@@ -135,6 +135,7 @@ int sm_count(int device);
 extern int g_swap_blocks;               // grid cap of the group-swap kernels (sv_dist.cu), 0 = default
 // caching state-slab allocator (sv_slab.cu): same-size reuse per device
 cudaError_t slab_alloc(void** p, size_t bytes);
+void keep_scratch_pool(int device);     // default pool keeps freed scratch (release threshold)
 void slab_free(void* p, size_t bytes);
 cudaError_t launch_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l, int c, cudaStream_t st);
 cudaError_t launch_swap_group(void* own, void* peer, uint64_t t0, uint64_t n, int mode, uint64_t vmask,

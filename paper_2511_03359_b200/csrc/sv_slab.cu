@@ -100,6 +100,21 @@ size_t slab_cached_bytes() {
     return t;
 }
 
+// Stream-ordered scratch (measurement partials, pair-dot rows, patch lists) comes from
+// the device's default pool; with the default release threshold of 0 the pool hands
+// its memory back at every synchronisation and the next cudaMallocAsync maps it
+// again (~1-2 ms of host time).  Keep up to 256 MB of freed scratch in the pool.
+void keep_scratch_pool(int device) {
+    static bool done[64] = {false};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = 256ull << 20;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[device] = true;
+}
+
 }  // namespace sv
 
 extern "C" {

@@ -25,6 +25,7 @@ them.
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -675,6 +676,8 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
         be = backend_factory(dist, n_local, mode)
     elif mode is PrecisionMode.BYTE:
         be = CudaByteBackend(dist, n_local, layout, dev_id)
+        if os.environ.get("SVB200_TIME_BYTE_PASSES"):   # probes: CUDA events around every pass
+            be.st.time_passes, be.st.pass_events = True, []
     else:
         be = CudaBackend(dist, n_local, mode, dev_id, tile_bits)
     byte = mode is PrecisionMode.BYTE and backend_factory is None
