@@ -60,6 +60,11 @@ def phys_op(gate, phys: tuple, n_local: int, rank: int):
     return gate_op(nat.SV_OP_2Q, qa=phys[0], qb=phys[1], data=m)
 
 
+# inter-process events of the overlapped swaps, created and exchanged once per process
+# (events live as long as the process; peers' handles stay valid)
+_OVERLAP_EVENTS: dict = {}  # (device, rank, world, chunks) -> (stream, own events, peer events)
+
+
 class CudaBackend:
     """This rank's slice in HBM plus IPC-mapped slices of every other rank."""
 
@@ -102,9 +107,17 @@ class CudaBackend:
 
     def _overlap_setup(self):
         """Second stream for the swap chunks and one inter-process event per chunk, the
-        handles exchanged once; peers' events opened for cross-GPU ordering."""
+        handles exchanged once per process (cached across runs); peers' events opened for
+        cross-GPU ordering."""
         lib = nat.load()
+        # events belong to the calling thread's current device (pair_dots calls this from
+        # a worker thread): make it this rank's device first
+        nat.check(lib.sv_set_device(self.dev.device))
         C = 1 << self.OVERLAP_CHUNK_BITS
+        key = (self.dev.device, self.rank, self.world, C)
+        if key in _OVERLAP_EVENTS:
+            self._overlap = _OVERLAP_EVENTS[key]
+            return
         stream = nat.Stream(self.dev.device)
         own, handles = [], bytearray()
         for _ in range(2 * C):       # [0, C): swap chunk done; [C, 2C): pass-before chunk done
@@ -127,6 +140,7 @@ class CudaBackend:
                 evs.append(ev)
             peers[r] = evs
         self._overlap = (stream, own, peers)
+        _OVERLAP_EVENTS[key] = self._overlap
 
     def _chunk_bits(self, pairs, ops):
         """Chunk positions for an overlapped swap: the highest local positions >= 12 that no
