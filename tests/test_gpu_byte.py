@@ -76,6 +76,21 @@ def test_byte_random_and_adder_match_oracle(rng):
         assert got.report.max_difference(pb.ExpectationReport(qx, qy, qz)) < 1e-12
 
 
+@pytest.mark.parametrize("ranks", [1, 8])
+def test_byte_diagonal_table_passes_match_oracle(ranks):
+    """Diagonal gates in BYTE mode run through the 65536-entry code table (scan of the
+    selected amplitudes, in-place write; sv_byte.cu k_byte_diag_*): the CPHASE-heavy QFT
+    adder at N=14, one rank and 8 reference ranks (tagged per-producer proposals)."""
+    from oracle.ref_builders import adder
+    circ = adder(7, [101, 77])[0]
+    want = ref_engine.run_circuit(circ, ranks=ranks, mode="be")
+    got = pb.run_circuit(to_product(circ), ranks=ranks, mode=BE)
+    mag, ph = _bytes(got)
+    assert got.codebook.dump() == want.codebook.dump()
+    assert np.array_equal(mag, want.mag) and np.array_equal(ph, want.phase)
+    assert got.report.max_difference(pb.ExpectationReport(*want.report[:3])) < 1e-12
+
+
 def test_codebook_api_matches_reference(golden):
     c = golden("codec.npz")
     cb = pb.Codebook()
