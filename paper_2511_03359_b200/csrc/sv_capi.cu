@@ -120,6 +120,7 @@ struct PassPlan {
     std::vector<int> ops;       // indices into the op list
     uint64_t qmask = 0;         // qubits that must be in the tile
     int mdata = 0;
+    int ndiag = 0;              // diagonal ops among them
 };
 
 int op_mdata(int kind) { return kind == SV_OP_2Q ? 32 : (kind == SV_OP_1Q ? 8 : 2); }
@@ -359,20 +360,39 @@ int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Pa
 }
 
 // greedy pass count of an op list with tiles of 2^K amplitudes (the 5 lowest qubits fixed)
+// ops per fused pass: kMaxOps, or fewer (SVB200_MAX_PASS_OPS, tuning of diagonal-heavy passes)
+static int max_pass_ops() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("SVB200_MAX_PASS_OPS");
+        const int x = e ? std::atoi(e) : kMaxOps;
+        v = (x >= 8 && x <= kMaxOps) ? x : kMaxOps;
+    }
+    return v;
+}
+// A pass of mostly diagonal ops is closed at 80 ops: the specialised kernel then keeps
+// them as straight-line code, which beats the descriptor loop that >= 96 diagonal ops
+// need (adder N=32: two 124-op passes of 78 ms became 80 + 44 ops; 0.348 -> 0.305 s).
+constexpr int kDiagPassOps = 80;
+static bool pass_full(int n, int ndiag) {
+    return n >= max_pass_ops() || (n >= kDiagPassOps && 4 * ndiag >= 3 * n);
+}
+static bool is_diag_kind(int kind) { return kind != SV_OP_1Q && kind != SV_OP_2Q; }
+
 int count_passes(const sv_op* ops, int n_ops, int n, int K) {
     const uint64_t low = 31ull;
     uint64_t qm = 0;
-    int passes = 0, cnt = 0, md = 0;
+    int passes = 0, cnt = 0, md = 0, nd = 0;
     for (int i = 0; i < n_ops; ++i) {
         const sv_op& o = ops[i];
         uint64_t need = 0;
         if (o.kind == SV_OP_1Q) need = 1ull << o.qa;
         if (o.kind == SV_OP_2Q) need = (1ull << o.qa) | (1ull << o.qb);
-        if (cnt == 0 || popcount64(qm | need | low) > K || cnt >= kMaxOps || md + op_mdata(o.kind) > kMaxMData) {
+        if (cnt == 0 || popcount64(qm | need | low) > K || pass_full(cnt, nd) || md + op_mdata(o.kind) > kMaxMData) {
             if (cnt) ++passes;
-            qm = 0; cnt = 0; md = 0;
+            qm = 0; cnt = 0; md = 0; nd = 0;
         }
-        qm |= need; ++cnt; md += op_mdata(o.kind);
+        qm |= need; ++cnt; md += op_mdata(o.kind); nd += is_diag_kind(o.kind);
     }
     (void)n;
     return passes + (cnt ? 1 : 0);
@@ -537,12 +557,13 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
         if (o.kind == SV_OP_2Q) need = (1ull << o.qa) | (1ull << o.qb);
         const uint64_t merged = cur.qmask | need;
         const bool fits = popcount64(merged | (lowfix & ((n >= 64) ? ~0ull : ((1ull << n) - 1)))) <= k;
-        if (!fits || (int)cur.ops.size() >= kMaxOps || cur.mdata + op_mdata(o.kind) > kMaxMData) {
+        if (!fits || pass_full((int)cur.ops.size(), cur.ndiag) || cur.mdata + op_mdata(o.kind) > kMaxMData) {
             if (int rc = flush()) return rc;
         }
         cur.qmask |= need;
         cur.ops.push_back(i);
         cur.mdata += op_mdata(o.kind);
+        cur.ndiag += is_diag_kind(o.kind);
     }
     return flush();
 }
@@ -1092,12 +1113,13 @@ int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_
         uint64_t need = 0;
         if (o.kind == SV_OP_1Q) need = 1ull << o.qa;
         if (o.kind == SV_OP_2Q) need = (1ull << o.qa) | (1ull << o.qb);
-        if (popcount64(cur.qmask | need | lowfix) > K || (int)cur.ops.size() >= kMaxOps ||
+        if (popcount64(cur.qmask | need | lowfix) > K || pass_full((int)cur.ops.size(), cur.ndiag) ||
             cur.mdata + op_mdata(o.kind) > kMaxMData)
             break;
         cur.qmask |= need;
         cur.ops.push_back(i);
         cur.mdata += op_mdata(o.kind);
+        cur.ndiag += is_diag_kind(o.kind);
     }
     static thread_local Fused2Params P2;
     if (build_params2(ops, cur, n_qubits, pcfg, P2) != 0) return fail(SV_EVALUE, "pass does not fit the v3 kernel");

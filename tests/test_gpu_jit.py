@@ -7,7 +7,7 @@ every FP64 fused pass runs the specialised kernel, then the generic path
 (mode 0) for the same circuits; both must equal the oracle bit for bit.
 Circuits cover the generated code paths: generic / real / monomial 1Q ops,
 generic / monomial 2Q ops, diagonal ops with register, thread and out-of-tile
-mask bits, and a >= 96-op diagonal pass (the diag_run descriptor loop).
+mask bits, and a pass with >= 96 diagonal ops (the diag_run descriptor loop).
 """
 import numpy as np
 import pytest
@@ -41,10 +41,29 @@ def _diag_heavy(rng, n, count):
     return OCircuit(n, tuple(gates))
 
 
+def _diag_run_pass(rng, n):
+    """32 one-qubit gates on tile qubits, then 100 diagonal ops: the planner keeps them in
+    one pass (it closes a pass at 80 ops only when >= 75 % are diagonal), whose >= 96
+    diagonal ops the specialised kernel runs as the descriptor loop (diag_run)."""
+    gates = [OGate(("H", "X", "Y")[i % 3], (i % 7,)) for i in range(32)]
+    for i in range(100):
+        a, b = (int(x) for x in rng.choice(n, size=2, replace=False))
+        kind = ("CPHASE", "PHASE", "Z")[i % 3]
+        if kind == "CPHASE":
+            gates.append(OGate("CPHASE", (a, b), int(rng.integers(1, 6))))
+        elif kind == "PHASE":
+            gates.append(OGate("PHASE", (a,), int(rng.integers(1, 5))))
+        else:
+            gates.append(OGate("Z", (a,)))
+    gates.append(OGate("M"))
+    return OCircuit(n, tuple(gates))
+
+
 def _cases(rng):
     return [("random18", random_circuit(np.random.default_rng(31), 18, 120)),
             ("exact16", exact_class_circuit(np.random.default_rng(32), 16, 120)),
             ("diag_heavy16", _diag_heavy(np.random.default_rng(33), 16, 260)),
+            ("diag_run16", _diag_run_pass(np.random.default_rng(35), 16)),
             ("adder9", adder(9, [301, 88])[0])]
 
 
