@@ -935,10 +935,10 @@ __global__ void __launch_bounds__(NT) k_byte_diag_table(const ByteTables* __rest
 // 1024-thread CTA per SM); a collecting write pass does both.
 constexpr int NTD = 1024;
 template <bool SCAN>
-__global__ void __launch_bounds__(SCAN ? NT : NTD) k_byte_diag_apply(
+__global__ void __launch_bounds__(NTD) k_byte_diag_apply(
     const uint8_t* mi_in, const uint8_t* pi_in, uint8_t* mi_out, uint8_t* pi_out, const ByteTables* __restrict__ gtab,
     const __grid_constant__ ByteGate g, ByteCand* cand, const uint16_t* __restrict__ lut, uint32_t* seen, int nprod) {
-    constexpr int NTK = SCAN ? NT : NTD;
+    constexpr int NTK = NTD;   // one CTA per SM: one bitmap flush per SM (atomics on 2048 shared words)
     __shared__ STables t;
     extern __shared__ __align__(16) unsigned char dsm[];
     uint16_t* slut = reinterpret_cast<uint16_t*>(dsm);                            // !SCAN: 65536 codes
@@ -1255,9 +1255,11 @@ cudaError_t launch_byte_gate(const uint8_t* mi_in, const uint8_t* pi_in, uint8_t
                                  65536 * 2 + 2048 * 8 * 4);
             diag_configured[dev] = true;
         }
+        const unsigned grid1 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((chunks + NTD - 1) / NTD,
+                                                                                  (uint64_t)sm_count(dev)));
         if (g.scan_only) {
-            k_byte_diag_apply<true><<<byte_grid(chunks), NT, bm_bytes, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g,
-                                                                              cand, lut, seen, nprod);
+            k_byte_diag_apply<true><<<grid1, NTD, bm_bytes, st>>>(mi_in, pi_in, mi_out, pi_out, tab, g, cand, lut,
+                                                                   seen, nprod);
         } else {
             k_byte_diag_table<<<65536 / NT, NT, 0, st>>>(tab, g, lut);
             count_launch();
