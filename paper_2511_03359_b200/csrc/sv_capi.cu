@@ -585,13 +585,6 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
         const char* e = std::getenv("SVB200_MEASURE_BMIN");
         benv = e ? std::max(1, std::min(5, std::atoi(e))) : 5;
     }
-    static int renv0 = -1, renv = -1;   // register bits per segment of FP64 pass 0 / later passes
-    if (renv < 0) {
-        const char* e0 = std::getenv("SVB200_MEASURE_RB0");
-        const char* e = std::getenv("SVB200_MEASURE_RB");
-        renv0 = (e0 && std::atoi(e0) == 3) ? 3 : 4;
-        renv = (e && std::atoi(e) == 3) ? 3 : 4;
-    }
     const int K = byte ? 12 : kenv, bmin = benv;
     const int grid_cap = measure3_grid(dev, K, byte);
     const int slots = measure_slots(K, n);
@@ -620,7 +613,7 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
     for (size_t pi = 0; pi < passes.size() && rc == SV_OK; ++pi) {
         std::memset(&P, 0, sizeof(P));
         const uint64_t tmask = passes[pi];
-        const int RB = (byte || K != 12) ? 4 : (pi == 0 ? renv0 : renv), NT = 1 << (K - RB);
+        const int RB = 4, NT = 1 << (K - RB);   // register bits per segment (RB = 3 measured slower)
         P.n = n;
         P.kbits = K;
         P.rbits = RB;

@@ -52,8 +52,8 @@ constexpr int kOutMax = 52;
 // pass also sums |a|^2 per qubit.  The 2-segment form without ONES fits 128 registers,
 // i.e. 2 CTAs per SM (16 warps instead of 8 to hide the HBM latency).
 // RB: register bits per segment (R = 2^RB amplitudes per thread, 2^(KB-RB) threads).
-// RB = 3 keeps 8 amplitudes per thread, so 4 segments (every position of a 12-bit tile)
-// fit 128 registers with 16 warps per SM.
+// RB = 3 (8 amplitudes per thread, 4 segments per 12-bit tile, 16 warps per SM) was
+// measured slower than the 2-CTA RB = 4 variants (N=33: 126 vs 108 ms) and is not launched.
 template <int KB, int MINB, bool BYTE, int NSEG, bool ONES, int RB = 4>
 __global__ void __launch_bounds__(1 << (KB - RB), MINB)
     k_measure3(const c64s* __restrict__ psi, const __grid_constant__ Measure3Params p, double* __restrict__ partials,
@@ -327,7 +327,7 @@ static cudaError_t measure3_cfg(const c64s* psi, const Measure3Params& p, double
 static bool light_pass(const Measure3Params& p) { return !p.want_ones && p.n_segs <= 2; }
 int measure3_ctas_per_sm(int kb, bool byte, const Measure3Params& p) {
     if (kb != 12) return 3;
-    if (p.rbits == 3 || byte) return byte && light_pass(p) ? 2 : 1;
+    if (byte) return light_pass(p) ? 2 : 1;
     return 2;   // light passes, and the 3-segment pass with shared-memory accumulators
 }
 int measure3_grid(int device, int kb, bool byte) { return sm_count(device) * (kb == 12 ? 2 : 3); }   // max over variants
@@ -336,9 +336,6 @@ cudaError_t launch_measure3(const void* psi, const Measure3Params& p, double* pa
     const MeasureBytes none{nullptr, nullptr, nullptr};
     const c64s* s = static_cast<const c64s*>(psi);
     if (p.kbits != 12) return measure3_cfg<11, 3, false, 3, true>(s, p, partials, grid, st, none);
-    if (p.rbits == 3)
-        return p.want_ones ? measure3_cfg<12, 1, false, 4, true, 3>(s, p, partials, grid, st, none)
-                           : measure3_cfg<12, 1, false, 4, false, 3>(s, p, partials, grid, st, none);
     return light_pass(p) ? measure3_cfg<12, 2, false, 2, false>(s, p, partials, grid, st, none)
                          : measure3_cfg<12, 2, false, 3, true>(s, p, partials, grid, st, none);
 }
