@@ -60,6 +60,44 @@ def phys_op(gate, phys: tuple, n_local: int, rank: int):
     return gate_op(nat.SV_OP_2Q, qa=phys[0], qb=phys[1], data=m)
 
 
+# IPC mappings of the peers' FP slices, kept across runs of the same shape:
+# (device, rank, world) -> {"shape": (n_local, mode), "maps": {peer: (handle bytes, ptr)}}.
+# A run of the same shape gets the same slab back from the slab cache (sv_slab.cu), hence
+# the same handle, and reuses the mapping instead of mapping 2^n_local amplitudes again.
+# A run of another shape (or a BYTE run) first closes every cached mapping and holds a
+# barrier before allocating, so no rank frees (slab-cache release) a slab a peer maps.
+_PEER_MAPS: dict = {}
+
+
+def _close_peer_maps(key) -> None:
+    ent = _PEER_MAPS.pop(key, None)
+    if ent:
+        for _, p in ent["maps"].values():
+            nat.load().sv_ipc_close(key[0], p)
+
+
+def release_peer_maps(dist=None) -> None:
+    """Close every cached peer mapping of this process (collective when `dist` is given:
+    ends with a barrier, after which peers may free their slabs)."""
+    for key in list(_PEER_MAPS):
+        _close_peer_maps(key)
+    if dist is not None:
+        dist.barrier()
+
+
+def _prepare_peer_maps(dist, device: int, shape) -> dict:
+    """Before a rank allocates its slice: keep the cached mappings when the shape matches
+    (every rank sees the same shapes, so the decision is the same everywhere), else close
+    them all and wait until every rank did."""
+    key = (device, dist.get_rank(), dist.get_world_size())
+    stale = [k for k, e in _PEER_MAPS.items() if k != key or e["shape"] != shape]
+    if stale:
+        for k in stale:
+            _close_peer_maps(k)
+        dist.barrier()
+    return _PEER_MAPS.setdefault(key, {"shape": shape, "maps": {}})["maps"]
+
+
 # inter-process events of the overlapped swaps, created and exchanged once per process
 # (events live as long as the process; peers' handles stay valid)
 _OVERLAP_EVENTS: dict = {}  # (device, rank, world, chunks) -> (stream, own events, peer events)
@@ -76,6 +114,7 @@ class CudaBackend:
         self.n_local = n_local
         self.mode = mode
         self.tile_bits = tile_bits
+        cached = _prepare_peer_maps(dist, device, (n_local, nat.mode_code(mode)))
         self.dev = DeviceState(n_local, mode, device=device)
         self.dev.zero(0 if self.rank == 0 else None)
         self.bpe = mode.bytes_per_element
@@ -84,13 +123,21 @@ class CudaBackend:
         handles = [None] * self.world
         dist.all_gather_object(handles, bytes(handle))
         self.peers = {}
+        self.maps_reused = 0
         for r, hb in enumerate(handles):
             if r == self.rank:
                 continue
+            if r in cached and cached[r][0] == hb:     # same slab as last run: mapping still valid
+                self.peers[r] = cached[r][1]
+                self.maps_reused += 1
+                continue
+            if r in cached:
+                nat.load().sv_ipc_close(device, cached.pop(r)[1])
             p = ctypes.c_void_p()
             buf = (ctypes.c_char * 64).from_buffer_copy(hb)
             nat.check(nat.load().sv_ipc_open(device, buf, ctypes.byref(p)))
             self.peers[r] = p
+            cached[r] = (hb, p)
         self.link_bytes = 0
         self.swap_timing = False
         self.swap_events = []
@@ -389,10 +436,10 @@ class CudaBackend:
         return self.dev.export()
 
     def close(self):
+        """End of the run: every rank is done with the peers' slices.  The mappings stay
+        cached for the next run of this shape (release_peer_maps closes them)."""
         self.dev.synchronize()
         self.dist.barrier()
-        for p in self.peers.values():
-            nat.load().sv_ipc_close(self.dev.device, p)
         self.peers = {}
 
 
@@ -415,6 +462,7 @@ class CudaByteBackend:
         self.n_local = n_local
         self.layout = layout
         self.mode = PrecisionMode.BYTE
+        _prepare_peer_maps(dist, device, ("byte", n_local))   # drop the FP mappings first
         self.st = ByteDeviceState(n_local, Codebook(), device)
         self.st.zero(0 if self.rank == 0 else None)
         self.dev = self.st

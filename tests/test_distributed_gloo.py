@@ -68,3 +68,45 @@ def test_distributed_control_plane_gloo(world, case):
                np.max(np.abs(np.array(qz) - wz))) < 1e-12
     assert ledgers == want.ledgers
     assert stats["swaps"] >= 0
+
+
+class _CountingDist:
+    def __init__(self, rank=0, world=2):
+        self.rank, self.world, self.barriers = rank, world, 0
+
+    def get_rank(self):
+        return self.rank
+
+    def get_world_size(self):
+        return self.world
+
+    def barrier(self):
+        self.barriers += 1
+
+
+def test_peer_map_cache_decisions(monkeypatch):
+    """Cached peer mappings (distributed.py _PEER_MAPS): same shape keeps them with no
+    barrier; another shape (or a BYTE run) closes every mapping, then holds a barrier
+    before the rank allocates."""
+    from paper_2511_03359_b200 import distributed as D
+    closed = []
+
+    class _Lib:
+        def sv_ipc_close(self, device, p):
+            closed.append((device, p))
+            return 0
+    monkeypatch.setattr(D.nat, "load", lambda *a, **k: _Lib())
+    monkeypatch.setattr(D, "_PEER_MAPS", {})
+    d = _CountingDist()
+    maps = D._prepare_peer_maps(d, 0, (30, 1))
+    assert maps == {} and d.barriers == 0
+    maps[1] = (b"h1", "p1")
+    again = D._prepare_peer_maps(d, 0, (30, 1))
+    assert again is maps and d.barriers == 0 and not closed
+    other = D._prepare_peer_maps(d, 0, (29, 1))
+    assert other == {} and d.barriers == 1 and closed == [(0, "p1")]
+    other[1] = (b"h2", "p2")
+    D._prepare_peer_maps(d, 0, ("byte", 29))
+    assert d.barriers == 2 and closed[-1] == (0, "p2")
+    D.release_peer_maps(d)
+    assert D._PEER_MAPS == {} and d.barriers == 3
