@@ -200,9 +200,13 @@ int svk_swap_group(void* own, void* peer, uint64_t n_local_elems, int mode, uint
 /* the same restricted to the amplitudes whose bits under chunk_mask equal chunk_pattern
  * (t runs over the bits outside victim_mask and chunk_mask): one chunk of a swap that
  * overlaps the following fused pass (sv_apply_fused_chunk) */
-/* grid cap (blocks) of the group-swap kernels, 0 = one wave of 8 blocks per SM; returns the
+/* grid cap (blocks) of the group-swap and pair-dot kernels, 0 = one full wave; returns the
  * previous value (a negative argument only queries) */
 int sv_swap_blocks(int blocks);
+/* measurement-pass CTA slots to leave free (at most one wave of 2 per SM is launched) so
+ * a concurrent pair dot (svk_pair_dot on another stream, grid capped by sv_swap_blocks)
+ * is resident at the same time; returns the previous value (negative: query) */
+int sv_measure_reserve(int ctas);
 int svk_swap_group_chunk(void* own, void* peer, uint64_t n_local_elems, int mode, uint64_t victim_mask,
                          uint64_t own_pattern, uint64_t peer_pattern, uint64_t chunk_mask, uint64_t chunk_pattern,
                          uint64_t t_begin, uint64_t t_count, void* stream);

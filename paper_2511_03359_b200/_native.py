@@ -100,6 +100,7 @@ _SIGNATURES = {
     "sv_jit_available": ([], _I),
     "sv_jit_probe": ([_P, _I, _I, ctypes.c_char_p, ctypes.c_size_t, _D], _I),
     "sv_swap_blocks": ([_I], _I),
+    "sv_measure_reserve": ([_I], _I),
     "svk_swap_group_chunk": ([_P, _P, _U64, _I, _U64, _U64, _U64, _U64, _U64, _U64, _U64, _P], _I),
     "sv_apply_fused_chunk": ([_P, _P, _I, _I, _U64, _U64], _I),
     "sv_event_create_ipc": ([ctypes.POINTER(_P), _P], _I),

@@ -568,6 +568,12 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
     return flush();
 }
 
+// CTA slots the measurement passes leave free (sv_measure_reserve): the distributed
+// measurement runs the global-qubit pair dots on a second stream at the same time, and a
+// measurement grid that fills every slot (2 x 128-register CTAs per SM) would run first
+// and serialise the two.
+int g_measure_reserve = 0;
+
 // FP64 measurement with the register-resident pass (sv_measure3.cu): tiles of 2^K
 // (K = 12: 1 + ceil((n - 12) / 7) passes), segments of 4 register positions cover the
 // cross terms of the pass's new tile qubits.
@@ -704,7 +710,8 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
                 }
                 P.base_tab[byte][v] = d;
             }
-        const int gcap = sm_count(dev) * measure3_ctas_per_sm(K, byte, P);   // <= grid_cap
+        // <= grid_cap; g_measure_reserve CTA slots stay free for a concurrent pair dot
+        const int gcap = std::max(sm_count(dev), sm_count(dev) * measure3_ctas_per_sm(K, byte, P) - g_measure_reserve);
         const int grid = (int)((P.n_tiles < (uint64_t)gcap) ? P.n_tiles : gcap);
         cudaError_t e = byte ? launch_measure3_byte(*static_cast<const MeasureBytes*>(psi), P, partials, grid, st)
                              : launch_measure3(psi, P, partials, grid, st);
@@ -1301,6 +1308,12 @@ int svk_swap_group(void* own, void* peer, uint64_t n_local_elems, int mode, uint
                                 t_count, stream);
 }
 
+int sv_measure_reserve(int ctas) {
+    const int prev = g_measure_reserve;
+    if (ctas >= 0) g_measure_reserve = ctas;
+    return prev;
+}
+
 int sv_swap_blocks(int blocks) {
     const int prev = sv::g_swap_blocks;
     if (blocks >= 0) sv::g_swap_blocks = blocks;
@@ -1329,7 +1342,8 @@ int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, doubl
     if (count == 0) return SV_OK;
     int dev = 0;
     cudaGetDevice(&dev);
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((count + 1023) / 1024, (uint64_t)sm_count(dev) * 2));
+    const uint64_t cap = sv::g_swap_blocks > 0 ? (uint64_t)sv::g_swap_blocks : (uint64_t)sm_count(dev) * 2;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((count + 1023) / 1024, cap));
     double* part = nullptr;
     cudaStream_t st = as_stream(stream);
     CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), 16 * grid, st), "pair dot scratch");

@@ -151,6 +151,13 @@ class CudaBackend:
     # -- remap swap overlapped with the following pass ------------------------------------
     OVERLAP_CHUNK_BITS = int(__import__("os").environ.get("SVB200_OVERLAP_CHUNK_BITS", "4"))   # 16 chunks
     OVERLAP_SWAP_BLOCKS = int(__import__("os").environ.get("SVB200_OVERLAP_BLOCKS", "128"))   # swap grid (4 GPUs: 128 best of 64-1184)
+    # measure-all: pair-dot grid (0: one full wave) and the measurement CTA slots left free
+    # for it.  Co-resident pair dots + local passes were measured SLOWER than letting the
+    # full-grid kernels run back to back (N=33, 2 GPUs: 196 ms vs 206-420 ms for grids of
+    # 32-148 / reserves 16-74, profiles/r01_dist_measure_overlap_2gpu.log): the peer's
+    # NVLink reads of this HBM starve under the passes' HBM load.  Defaults keep the full grids.
+    PAIR_DOT_BLOCKS = int(__import__("os").environ.get("SVB200_PAIR_DOT_BLOCKS", "0"))
+    MEASURE_RESERVE = int(__import__("os").environ.get("SVB200_MEASURE_RESERVE", "0"))
 
     def _overlap_setup(self):
         """Second stream for the swap chunks and one inter-process event per chunk, the
@@ -411,7 +418,7 @@ class CudaBackend:
         stream = self._overlap[0]
         lib = nat.load()
         nat.check(lib.sv_set_device(self.dev.device))
-        prev = lib.sv_swap_blocks(self.OVERLAP_SWAP_BLOCKS)
+        prev = lib.sv_swap_blocks(self.PAIR_DOT_BLOCKS)
         half = self.dev.size // 2
         esz = np.dtype(self.dev.dtype).itemsize
         out = {}
@@ -862,9 +869,15 @@ def _measure(be, layout, ledgers, perm, rank, mode, dist):
             except BaseException as exc:   # re-raised on the calling thread
                 box["e"] = exc
         th = threading.Thread(target=work)
-        th.start()
-        norm, ones_l, cross_l = be.measure_local()
-        th.join()
+        reserve = getattr(be, "MEASURE_RESERVE", 0)
+        prev = nat.load().sv_measure_reserve(reserve) if reserve else None
+        try:
+            th.start()
+            norm, ones_l, cross_l = be.measure_local()
+        finally:
+            th.join()
+            if prev is not None:
+                nat.load().sv_measure_reserve(prev)
         if "e" in box:
             raise box["e"]
         remote = box["v"]

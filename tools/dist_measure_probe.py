@@ -33,9 +33,11 @@ def timed(fn):
 def both():
     box = {}
     th = threading.Thread(target=lambda: box.update(v=be.pair_dots(gpos)))
+    prev = D.nat.load().sv_measure_reserve(be.MEASURE_RESERVE)
     th.start()
     be.measure_local()
     th.join()
+    D.nat.load().sv_measure_reserve(prev)
 
 
 for rep in range(3):
@@ -44,7 +46,7 @@ for rep in range(3):
     tb = timed(both)
     if rank == 0:
         half = (1 << n_local) // 2 * 16
-        print(f"rep {rep}: measure_local {tm * 1e3:.1f} ms  pair_dots {tp * 1e3:.1f} ms "
+        print(f"blocks {be.PAIR_DOT_BLOCKS} reserve {be.MEASURE_RESERVE} rep {rep}: measure_local {tm * 1e3:.1f} ms  pair_dots {tp * 1e3:.1f} ms "
               f"({len(gpos) * half / tp / 1e9:.0f} GB/s over the link)  concurrent {tb * 1e3:.1f} ms", flush=True)
 be.close()
 dist.destroy_process_group()
