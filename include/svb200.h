@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SV_ABI_VERSION 1
+#define SV_ABI_VERSION 2
 
 enum { SV_OK = 0, SV_EINDEX = -1, SV_EVALUE = -2, SV_ECUDA = -3, SV_ENOMEM = -4 };
 enum { SV_FP64 = 0, SV_FP32 = 1, SV_BYTE = 2 };              /* state.py:20-27 PrecisionMode */
@@ -186,6 +186,11 @@ int sv_ipc_handle(sv_handle h, void* out64);
 /* map a peer's state buffer into this process (device = this rank's GPU) */
 int sv_ipc_open(int device, const void* handle64, void** peer_ptr);
 int sv_ipc_close(int device, void* peer_ptr);
+/* every state buffer exported by sv_ipc_handle / svb_ipc_handles stays allocated
+ * (never returned to the driver by the slab cache) until this is called -- only
+ * after every peer process has closed its mappings (a collective barrier).
+ * was_exported (optional) = how many buffers were marked. */
+int sv_ipc_unexport_all(uint64_t* was_exported);
 /* global<->local qubit swap with the partner rank (the remap planner's move):
  * this rank has global bit `side`; its amplitudes with local bit l = 1-side
  * trade places with the partner's amplitudes with bit l = side.  Both ranks
@@ -200,19 +205,21 @@ int svk_swap_group(void* own, void* peer, uint64_t n_local_elems, int mode, uint
 /* the same restricted to the amplitudes whose bits under chunk_mask equal chunk_pattern
  * (t runs over the bits outside victim_mask and chunk_mask): one chunk of a swap that
  * overlaps the following fused pass (sv_apply_fused_chunk) */
-/* grid cap (blocks) of the group-swap and pair-dot kernels, 0 = one full wave; returns the
+/* grid cap (blocks) of the group-swap kernel, 0 = one full wave; returns the
  * previous value (a negative argument only queries) */
 int sv_swap_blocks(int blocks);
 /* measurement-pass CTA slots to leave free (at most one wave of 2 per SM is launched) so
- * a concurrent pair dot (svk_pair_dot on another stream, grid capped by sv_swap_blocks)
+ * a concurrent pair dot (svk_pair_dot on another stream, grid capped by its max_blocks)
  * is resident at the same time; returns the previous value (negative: query) */
 int sv_measure_reserve(int ctas);
 int svk_swap_group_chunk(void* own, void* peer, uint64_t n_local_elems, int mode, uint64_t victim_mask,
                          uint64_t own_pattern, uint64_t peer_pattern, uint64_t chunk_mask, uint64_t chunk_pattern,
                          uint64_t t_begin, uint64_t t_count, void* stream);
 /* sum conj(a0[i]) * a1[i] over count elements (a1 may be a peer pointer):
- * measure.py:83-101 cross term of a global qubit; out2 = (re, im) */
-int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, double* out2, void* stream);
+ * measure.py:83-101 cross term of a global qubit; out2 = (re, im).
+ * max_blocks caps the grid (0 = two CTAs per SM). */
+int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, int max_blocks, double* out2,
+                 void* stream);
 
 /* BYTE multi-GPU: IPC handles of the 4 planes ([buffer][magnitude, phase]),
  * mapped peer planes, byte-plane swap and decoded cross term */

@@ -369,6 +369,7 @@ int svb_ipc_handles(sv_bhandle h, void* out256) {
         for (int p = 0; p < 2; ++p) {
             cudaIpcMemHandle_t ih;
             BTRY(cudaIpcGetMemHandle(&ih, h->plane[b][p]), "cudaIpcGetMemHandle");
+            sv::slab_mark_exported(h->plane[b][p]);
             std::memcpy(static_cast<char*>(out256) + 64 * (2 * b + p), &ih, 64);
         }
     return SV_OK;

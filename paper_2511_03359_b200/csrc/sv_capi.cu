@@ -1274,6 +1274,7 @@ int sv_ipc_handle(sv_handle h, void* out64) {
     if (int rc = materialize(h)) return rc;
     cudaIpcMemHandle_t ih;
     CUDA_TRY(cudaIpcGetMemHandle(&ih, h->ptr), "cudaIpcGetMemHandle");
+    slab_mark_exported(h->ptr);
     static_assert(sizeof(ih) == 64, "IPC handle size");
     std::memcpy(out64, &ih, 64);
     return SV_OK;
@@ -1336,13 +1337,14 @@ int svk_swap_group_chunk(void* own, void* peer, uint64_t n_local_elems, int mode
     return e == cudaSuccess ? SV_OK : cuda_fail(e, "group swap launch");
 }
 
-int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, double* out2, void* stream) {
+int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, int max_blocks, double* out2,
+                 void* stream) {
     if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "pair dot needs FP64 or FP32 storage");
     out2[0] = out2[1] = 0.0;
     if (count == 0) return SV_OK;
     int dev = 0;
     cudaGetDevice(&dev);
-    const uint64_t cap = sv::g_swap_blocks > 0 ? (uint64_t)sv::g_swap_blocks : (uint64_t)sm_count(dev) * 2;
+    const uint64_t cap = max_blocks > 0 ? (uint64_t)max_blocks : (uint64_t)sm_count(dev) * 2;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((count + 1023) / 1024, cap));
     double* part = nullptr;
     cudaStream_t st = as_stream(stream);

@@ -137,6 +137,8 @@ extern int g_swap_blocks;               // grid cap of the group-swap kernels (s
 cudaError_t slab_alloc(void** p, size_t bytes);
 void keep_scratch_pool(int device);     // default pool keeps freed scratch (release threshold)
 void slab_free(void* p, size_t bytes);
+// CUDA IPC export: the slab is never returned to the driver until sv_ipc_unexport_all
+void slab_mark_exported(void* p);
 cudaError_t launch_swap_peer(void* own, void* peer, uint64_t n_local_elems, int mode, int l, int c, cudaStream_t st);
 cudaError_t launch_swap_group(void* own, void* peer, uint64_t t0, uint64_t n, int mode, uint64_t vmask,
                               uint64_t own_pat, uint64_t peer_pat, uint64_t cmask, uint64_t cpat, cudaStream_t st);

@@ -8,7 +8,18 @@
 // sv_release_cached() returns everything to the driver.  Callers synchronise
 // their stream before freeing (sv_destroy / svb_destroy), so a cached slab is
 // idle when it is reused.
+//
+// Slabs exported over CUDA IPC (sv_ipc_handle / svb_ipc_handles) may still be
+// mapped by peer processes after their owner freed them into the cache: CUDA
+// leaves freeing an exported allocation before every importer closed it
+// undefined.  Such slabs are marked and never returned to the driver -- neither
+// by the out-of-memory retry nor by sv_release_cached -- until the distributed
+// layer has closed every mapping on every rank and calls sv_ipc_unexport_all
+// (distributed.release_peer_maps, after its barrier).  They can still be reused
+// for the next same-size state of this process, which is what the peers' cached
+// mappings rely on.
 #include <mutex>
+#include <unordered_set>
 #include <vector>
 
 #include "sv_common.cuh"
@@ -31,6 +42,10 @@ std::vector<Slab>& slabs() {
     static std::vector<Slab>* v = new std::vector<Slab>;
     return *v;
 }
+std::unordered_set<void*>& exported() {
+    static std::unordered_set<void*>* s = new std::unordered_set<void*>;
+    return *s;
+}
 constexpr size_t kMinCached = 1ull << 20;
 
 void release_device(int device) {
@@ -38,8 +53,9 @@ void release_device(int device) {
     {
         std::lock_guard<std::mutex> lk(slab_mu());
         auto& v = slabs();
+        const auto& ex = exported();
         for (size_t i = 0; i < v.size();) {
-            if (device < 0 || v[i].device == device) {
+            if ((device < 0 || v[i].device == device) && !ex.count(v[i].ptr)) {
                 drop.push_back(v[i]);
                 v[i] = v.back();
                 v.pop_back();
@@ -61,7 +77,7 @@ void release_device(int device) {
 cudaError_t slab_alloc(void** p, size_t bytes) {
     int dev = 0;
     cudaGetDevice(&dev);
-    if (bytes >= kMinCached) {
+    {   // (slabs below kMinCached are only cached while exported)
         std::lock_guard<std::mutex> lk(slab_mu());
         auto& v = slabs();
         for (size_t i = 0; i < v.size(); ++i)
@@ -84,6 +100,15 @@ cudaError_t slab_alloc(void** p, size_t bytes) {
 void slab_free(void* p, size_t bytes) {
     if (!p) return;
     if (bytes < kMinCached) {
+        {
+            std::lock_guard<std::mutex> lk(slab_mu());
+            if (exported().count(p)) {      // a peer may still map it: keep it (cached) until unexported
+                int dev = 0;
+                cudaGetDevice(&dev);
+                slabs().push_back({dev, bytes, p});
+                return;
+            }
+        }
         cudaFree(p);
         return;
     }
@@ -91,6 +116,22 @@ void slab_free(void* p, size_t bytes) {
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(slab_mu());
     slabs().push_back({dev, bytes, p});
+}
+
+void slab_mark_exported(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(slab_mu());
+    exported().insert(p);
+}
+
+size_t slab_exported_count() {
+    std::lock_guard<std::mutex> lk(slab_mu());
+    return exported().size();
+}
+
+void slab_unexport_all() {
+    std::lock_guard<std::mutex> lk(slab_mu());
+    exported().clear();
 }
 
 size_t slab_cached_bytes() {
@@ -126,6 +167,12 @@ int sv_release_cached(void) {
 
 int sv_cached_bytes(uint64_t* out) {
     *out = sv::slab_cached_bytes();
+    return SV_OK;
+}
+
+int sv_ipc_unexport_all(uint64_t* was_exported) {
+    if (was_exported) *was_exported = sv::slab_exported_count();
+    sv::slab_unexport_all();
     return SV_OK;
 }
 

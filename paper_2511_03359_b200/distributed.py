@@ -64,8 +64,10 @@ def phys_op(gate, phys: tuple, n_local: int, rank: int):
 # (device, rank, world) -> {"shape": (n_local, mode), "maps": {peer: (handle bytes, ptr)}}.
 # A run of the same shape gets the same slab back from the slab cache (sv_slab.cu), hence
 # the same handle, and reuses the mapping instead of mapping 2^n_local amplitudes again.
-# A run of another shape (or a BYTE run) first closes every cached mapping and holds a
-# barrier before allocating, so no rank frees (slab-cache release) a slab a peer maps.
+# Every slab this process exported stays allocated (the slab cache never hands an exported
+# slab back to the driver, not even on an out-of-memory retry) until every rank has closed
+# its mappings: _unmap_everywhere closes them all, holds a barrier and only then releases
+# the export marks (sv_ipc_unexport_all).
 _PEER_MAPS: dict = {}
 
 
@@ -76,25 +78,39 @@ def _close_peer_maps(key) -> None:
             nat.load().sv_ipc_close(key[0], p)
 
 
-def release_peer_maps(dist=None) -> None:
-    """Close every cached peer mapping of this process (collective when `dist` is given:
-    ends with a barrier, after which peers may free their slabs)."""
+def _unmap_everywhere(dist) -> None:
+    """Collective: close every cached mapping of this process, wait for every rank to do
+    the same, then drop the export marks (the slabs may go back to the driver)."""
     for key in list(_PEER_MAPS):
         _close_peer_maps(key)
-    if dist is not None:
-        dist.barrier()
+    dist.barrier()
+    nat.check(nat.load().sv_ipc_unexport_all(None))
+
+
+def release_peer_maps(dist=None) -> None:
+    """Close every cached peer mapping of this process.  With `dist` (collective, every
+    rank calls it) the export marks are dropped afterwards, so the slab cache may return
+    the slabs to the driver; without it the slabs stay pinned in the cache."""
+    if dist is None:
+        for key in list(_PEER_MAPS):
+            _close_peer_maps(key)
+        return
+    _unmap_everywhere(dist)
 
 
 def _prepare_peer_maps(dist, device: int, shape) -> dict:
     """Before a rank allocates its slice: keep the cached mappings when the shape matches
-    (every rank sees the same shapes, so the decision is the same everywhere), else close
-    them all and wait until every rank did."""
+    on EVERY rank, else close them all everywhere.  The decision is collective (one
+    all-gather of the stale flags): a rank whose cache differs (an earlier constructor
+    raised, a partial release, another group of the same size) forces every rank through
+    the same close + barrier path instead of leaving one rank in a barrier while the
+    others enter the handle all-gather."""
     key = (device, dist.get_rank(), dist.get_world_size())
-    stale = [k for k, e in _PEER_MAPS.items() if k != key or e["shape"] != shape]
-    if stale:
-        for k in stale:
-            _close_peer_maps(k)
-        dist.barrier()
+    stale = any(k != key or e["shape"] != shape for k, e in _PEER_MAPS.items()) or key not in _PEER_MAPS
+    flags = [None] * dist.get_world_size()
+    dist.all_gather_object(flags, (bool(stale), shape))
+    if any(f[0] for f in flags) or any(f[1] != shape for f in flags):
+        _unmap_everywhere(dist)
     return _PEER_MAPS.setdefault(key, {"shape": shape, "maps": {}})["maps"]
 
 
@@ -404,7 +420,7 @@ class CudaBackend:
             off = half
         p0 = ctypes.c_void_p(a0.value + off * esz)
         p1 = ctypes.c_void_p(a1.value + off * esz)
-        nat.check(nat.load().svk_pair_dot(p0, p1, half, self.dev.mode_code, nat.dptr(out), self.dev.stream))
+        nat.check(nat.load().svk_pair_dot(p0, p1, half, self.dev.mode_code, 0, nat.dptr(out), self.dev.stream))
         self.link_bytes += half * self.bpe
         return complex(out[0], out[1])
 
@@ -418,25 +434,21 @@ class CudaBackend:
         stream = self._overlap[0]
         lib = nat.load()
         nat.check(lib.sv_set_device(self.dev.device))
-        prev = lib.sv_swap_blocks(self.PAIR_DOT_BLOCKS)
         half = self.dev.size // 2
         esz = np.dtype(self.dev.dtype).itemsize
         out = {}
-        try:
-            for global_pos in positions:
-                bit = global_pos - self.n_local
-                partner = self.rank ^ (1 << bit)
-                low = ((self.rank >> bit) & 1) == 0
-                a0, a1 = (self.dev.ptr, self.peers[partner]) if low else (self.peers[partner], self.dev.ptr)
-                off = 0 if low else half
-                res = np.zeros(2)
-                nat.check(lib.svk_pair_dot(ctypes.c_void_p(a0.value + off * esz),
-                                           ctypes.c_void_p(a1.value + off * esz), half, self.dev.mode_code,
-                                           nat.dptr(res), stream.ptr))
-                self.link_bytes += half * self.bpe
-                out[global_pos] = complex(res[0], res[1])
-        finally:
-            lib.sv_swap_blocks(prev)
+        for global_pos in positions:
+            bit = global_pos - self.n_local
+            partner = self.rank ^ (1 << bit)
+            low = ((self.rank >> bit) & 1) == 0
+            a0, a1 = (self.dev.ptr, self.peers[partner]) if low else (self.peers[partner], self.dev.ptr)
+            off = 0 if low else half
+            res = np.zeros(2)
+            nat.check(lib.svk_pair_dot(ctypes.c_void_p(a0.value + off * esz),
+                                       ctypes.c_void_p(a1.value + off * esz), half, self.dev.mode_code,
+                                       self.PAIR_DOT_BLOCKS, nat.dptr(res), stream.ptr))
+            self.link_bytes += half * self.bpe
+            out[global_pos] = complex(res[0], res[1])
         return out
 
     def export(self) -> np.ndarray:
@@ -644,6 +656,8 @@ class CudaByteBackend:
         return self.st.decode()
 
     def close(self):
+        """End of the run: unmap the peers' planes on every rank, then (after a barrier)
+        drop the export marks so the slab cache may free them again."""
         self.st.synchronize()
         self.dist.barrier()
         for planes in self.peers.values():
@@ -651,6 +665,7 @@ class CudaByteBackend:
                 for pl in range(2):
                     nat.load().sv_ipc_close(self.st.device, planes[b][pl])
         self.peers = {}
+        _unmap_everywhere(self.dist)
 
 
 @dataclass

@@ -101,10 +101,53 @@ def main():
                   f"ledgers={led} stats={res.device_stats}", flush=True)
             ok = ok and same and cbs and diff < 1e-12 and led
         res.backend.close()
+    ok = _check_exported_slabs(dist, rank, world, dev) and ok
     flag = [ok]
     dist.broadcast_object_list(flag, src=0)
     dist.destroy_process_group()
     sys.exit(0 if flag[0] else 1)
+
+
+def _check_exported_slabs(dist, rank, world, dev):
+    """A slab exported over CUDA IPC must survive the slab cache's release paths while
+    peers still map it (sv_slab.cu): run, free, release the cache on every rank, run the
+    same shape again on the cached mappings (bit-exact), then release the mappings
+    collectively and check the cache can empty."""
+    import ctypes
+    from paper_2511_03359_b200 import _native as nat
+    from paper_2511_03359_b200.device import release_cached_memory
+    from paper_2511_03359_b200.distributed import _PEER_MAPS, release_peer_maps, run_circuit_distributed
+    from oracle import ref_engine
+    from tests.circuits import random_circuit, to_product
+    circ = random_circuit(np.random.default_rng(31), 18, 40)
+    res = run_circuit_distributed(to_product(circ), dist, device=dev)
+    res.backend.close()
+    res.backend.dev.free()
+    del res
+    release_cached_memory()                 # the OOM-retry / user release path
+    cached = ctypes.c_uint64(0)
+    nat.load().sv_cached_bytes(ctypes.byref(cached))
+    kept = cached.value >= (1 << 18) * 16   # the exported 2^18-amplitude slab is still held
+    dist.barrier()
+    res = run_circuit_distributed(to_product(circ), dist, device=dev)
+    reused = res.backend.maps_reused
+    state = res.gathered_state(dist)
+    res.backend.close()
+    res.backend.dev.free()
+    del res
+    release_peer_maps(dist)                 # collective: unmapped everywhere, marks dropped
+    release_cached_memory()
+    nat.load().sv_cached_bytes(ctypes.byref(cached))
+    emptied = cached.value == 0 and not _PEER_MAPS
+    flags = [None] * world
+    dist.all_gather_object(flags, (kept, reused, emptied))
+    if rank != 0:
+        return True
+    want = ref_engine.run_circuit(circ, ranks=world)
+    same = np.array_equal(state, want.gathered_state())
+    print(f"[dist {world} GPUs] exported-slab guard: state bit-exact={same} per rank (kept, maps reused, "
+          f"emptied after release)={flags}", flush=True)
+    return same and all(k and e and (r == world - 1) for k, r, e in flags)
 
 
 if __name__ == "__main__":

@@ -71,8 +71,12 @@ def test_distributed_control_plane_gloo(world, case):
 
 
 class _CountingDist:
+    """Stand-in process group: all_gather_object reports this rank's object for every rank,
+    except the ranks listed in `peer_objs` (to simulate a peer whose cache differs)."""
+
     def __init__(self, rank=0, world=2):
         self.rank, self.world, self.barriers = rank, world, 0
+        self.peer_objs = {}
 
     def get_rank(self):
         return self.rank
@@ -83,30 +87,43 @@ class _CountingDist:
     def barrier(self):
         self.barriers += 1
 
+    def all_gather_object(self, out, obj):
+        for r in range(self.world):
+            out[r] = self.peer_objs.get(r, obj) if r != self.rank else obj
+
 
 def test_peer_map_cache_decisions(monkeypatch):
-    """Cached peer mappings (distributed.py _PEER_MAPS): same shape keeps them with no
-    barrier; another shape (or a BYTE run) closes every mapping, then holds a barrier
-    before the rank allocates."""
+    """Cached peer mappings (distributed.py _PEER_MAPS): same shape on every rank keeps
+    them with no barrier; another shape, a BYTE run, or ANY rank reporting a stale cache
+    closes every mapping on every rank, holds a barrier and drops the IPC export marks."""
     from paper_2511_03359_b200 import distributed as D
-    closed = []
+    closed, unexports = [], []
 
     class _Lib:
         def sv_ipc_close(self, device, p):
             closed.append((device, p))
             return 0
+
+        def sv_ipc_unexport_all(self, out):
+            unexports.append(1)
+            return 0
     monkeypatch.setattr(D.nat, "load", lambda *a, **k: _Lib())
     monkeypatch.setattr(D, "_PEER_MAPS", {})
     d = _CountingDist()
-    maps = D._prepare_peer_maps(d, 0, (30, 1))
-    assert maps == {} and d.barriers == 0
+    maps = D._prepare_peer_maps(d, 0, (30, 1))          # empty cache: collective close path
+    assert maps == {} and d.barriers == 1 and len(unexports) == 1
     maps[1] = (b"h1", "p1")
     again = D._prepare_peer_maps(d, 0, (30, 1))
-    assert again is maps and d.barriers == 0 and not closed
+    assert again is maps and d.barriers == 1 and not closed
+    d.peer_objs[1] = (True, (30, 1))                      # the peer's cache is stale: we follow
+    again = D._prepare_peer_maps(d, 0, (30, 1))
+    assert again == {} and d.barriers == 2 and closed == [(0, "p1")] and len(unexports) == 2
+    d.peer_objs.clear()
+    again[1] = (b"h1", "p1")
     other = D._prepare_peer_maps(d, 0, (29, 1))
-    assert other == {} and d.barriers == 1 and closed == [(0, "p1")]
+    assert other == {} and d.barriers == 3 and closed[-1] == (0, "p1")
     other[1] = (b"h2", "p2")
     D._prepare_peer_maps(d, 0, ("byte", 29))
-    assert d.barriers == 2 and closed[-1] == (0, "p2")
+    assert d.barriers == 4 and closed[-1] == (0, "p2")
     D.release_peer_maps(d)
-    assert D._PEER_MAPS == {} and d.barriers == 3
+    assert D._PEER_MAPS == {} and d.barriers == 5 and len(unexports) == 5
