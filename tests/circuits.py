@@ -123,3 +123,19 @@ def to_product(circuit):
                           None if g.matrix is None else np.asarray(g.matrix, dtype=np.complex128))
                   for g in circuit.gates)
     return Circuit(circuit.n_qubits, gates, tuple(circuit.label_permutation))
+
+
+def ladder_cases():
+    """SURVEY 8(c) parity ladder (tests/golden/ladder.json): (name, circuit, mode, ranks).
+    C1 is build_benchmark(20) FP64 at P=1 (builders.py:14-25)."""
+    from oracle.ref_builders import adder, benchmark
+    return [
+        ("C1_bench20", benchmark(20), "fp64", (1,)),
+        ("bench22", benchmark(22), "fp64", (1, 8)),
+        ("bench24", benchmark(24), "fp64", (1, 8)),
+        ("adder11", adder(11, [1234, 813])[0], "fp64", (1, 8)),
+        ("bench22_fp32", benchmark(22), "fp32", (1,)),
+        ("bench20_be", benchmark(20), "be", (8,)),
+        ("bench22_be", benchmark(22), "be", (8,)),
+        ("adder10_be", adder(10, [700, 323])[0], "be", (8,)),
+    ]

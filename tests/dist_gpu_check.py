@@ -127,7 +127,8 @@ def _check_exported_slabs(dist, rank, world, dev):
     release_cached_memory()                 # the OOM-retry / user release path
     cached = ctypes.c_uint64(0)
     nat.load().sv_cached_bytes(ctypes.byref(cached))
-    kept = cached.value >= (1 << 18) * 16   # the exported 2^18-amplitude slab is still held
+    n_local = 18 - (world.bit_length() - 1)
+    kept = cached.value >= (1 << n_local) * 16   # the exported 2^n_local-amplitude slab is still held
     dist.barrier()
     res = run_circuit_distributed(to_product(circ), dist, device=dev)
     reused = res.backend.maps_reused

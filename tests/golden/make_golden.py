@@ -17,6 +17,13 @@ this script:
                  states, storage bytes, ledgers, reports, codebooks
   planner.json — plan_exchange, memory_bytes, predicted_exchange_bytes and
                  optimize_labels at the BASELINE configs (N up to 38)
+  ladder.json  — the SURVEY 8(c) parity ladder at sizes too large for npz
+                 fixtures: C1 = build_benchmark(20) FP64 P=1, benchmark 22/24
+                 and adder(11) FP64 at P in {1, 8}, FP32 benchmark(22), BYTE
+                 benchmark 20/22 and adder(10) at P=8.  Stored as SHA-256
+                 digests of the state (complex128, -0.0 folded to +0.0) and of
+                 the BYTE planes, plus the full ledgers, report and codebook
+                 dump (`python tests/golden/make_golden.py --ladder`)
 
 The fixtures are what pins the oracle (tests/test_oracle_golden.py) and what
 the GPU parity tests compare against on the B200 box.
@@ -34,7 +41,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
-from tests.circuits import (SEED, exact_class_circuit, haar_unitary, pack,  # noqa: E402
+from tests.circuits import (SEED, exact_class_circuit, haar_unitary, ladder_cases, pack,  # noqa: E402
                             random_circuit, to_reference)
 from oracle.ref_builders import OCircuit, adder, benchmark  # noqa: E402
 from oracle.ref_gates import OGate  # noqa: E402
@@ -311,12 +318,63 @@ def make_planner(ref):
         json.dump(res, f, indent=1, default=lambda o: o.item() if hasattr(o, "item") else str(o))
 
 
+def state_digest(state) -> str:
+    """SHA-256 of a gathered state as complex128 with negative zeros folded (np.array_equal
+    semantics: X / CNOT as moves may flip the sign of an exact zero)."""
+    import hashlib
+    a = np.ascontiguousarray(np.asarray(state, dtype=np.complex128)).view(np.float64) + 0.0
+    return hashlib.sha256(a.tobytes()).hexdigest()
+
+
+def bytes_digest(*planes) -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for p in planes:
+        h.update(np.ascontiguousarray(p).view(np.uint8).tobytes())
+    return h.hexdigest()
+
+
+def make_ladder(ref):
+    import time
+    modes = {"fp64": ref.PrecisionMode.FP64, "fp32": ref.PrecisionMode.FP32, "be": ref.PrecisionMode.BYTE}
+    out = []
+    for name, circ, mode, ranks in ladder_cases():
+        rc = to_reference(circ, ref)
+        for P in ranks:
+            t0 = time.perf_counter()
+            res = ref.run_circuit(rc, ranks=P, mode=modes[mode])
+            dt = time.perf_counter() - t0
+            ent = dict(name=name, mode=mode, ranks=P, n_qubits=circ.n_qubits, gates=len(circ.gates),
+                       state_sha256=state_digest(res.gathered_state()), ref_seconds=round(dt, 2),
+                       ledgers=[l.snapshot() for l in res.ledgers])
+            rep = res.report
+            ent["report"] = [list(map(float, rep.qx)), list(map(float, rep.qy)), list(map(float, rep.qz))]
+            ent["norm_deviation"] = float(rep.norm_deviation)
+            if mode == "be":
+                mag = np.concatenate([s_.mag_idx for s_ in res.states])
+                ph = np.concatenate([s_.phase_idx for s_ in res.states])
+                ent["bytes_sha256"] = bytes_digest(mag, ph)
+                ent["codebook_dump"] = res.codebook.dump()
+                ent["codebook_flags"] = [bool(res.codebook.mag_overflow), bool(res.codebook.phase_overflow)]
+            if mode == "fp32":
+                psi = np.concatenate([s_.psi for s_ in res.states])
+                ent["psi32_sha256"] = bytes_digest(np.ascontiguousarray(psi).view(np.float32) + np.float32(0.0))
+            out.append(ent)
+            print("ladder", name, mode, P, f"{dt:.1f}s", flush=True)
+            with open(os.path.join(HERE, "ladder.json"), "w") as f:
+                json.dump(out, f, indent=0, default=lambda o: o.item() if hasattr(o, "item") else str(o))
+
+
 def main():
     ref = load_reference()
+    if "--ladder" in sys.argv:
+        make_ladder(ref)
+        return
     make_kernels(ref)
     make_codec(ref)
     make_planner(ref)
     make_runs(ref)
+    make_ladder(ref)
 
 
 if __name__ == "__main__":

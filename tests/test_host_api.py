@@ -216,3 +216,29 @@ def test_jit_prepare_queues_one_kernel_per_pass_structure():
     jit_wait()
     after = jit_stats()
     assert after["compiled"] - before["compiled"] == queued and after["failed"] == before["failed"]
+
+
+def test_product_pair_indices_match_reference_goldens(golden):
+    """kernels.pair_indices (the product's host helper) vs the reference's outputs."""
+    from paper_2511_03359_b200 import kernels
+    k = golden("kernels.npz")
+    keys = [key for key in k if key.startswith("pairs_")]
+    assert keys
+    for key in keys:
+        _, n, q = key.split("_")
+        assert np.array_equal(kernels.pair_indices(int(n), int(q)), k[key]), key
+    with pytest.raises(IndexError):
+        kernels.pair_indices(6, 6)
+
+
+def test_product_codebook_resolution_and_dump_match_reference(golden):
+    """Codebook.resolution / dump of the product (no device needed) on the reference's
+    final propose/merge tables (codec.npz seq*) and on its saturated table."""
+    c = golden("codec.npz")
+    last = int(c["n_seq"]) - 1
+    cb = pb.Codebook()
+    cb.mags, cb.thetas = c[f"seq{last}_mags"].copy(), c[f"seq{last}_thetas"].copy()
+    cb.ux, cb.uy = c[f"seq{last}_ux"].copy(), c[f"seq{last}_uy"].copy()
+    cb.mag_overflow, cb.phase_overflow = (bool(x) for x in c[f"seq{last}_flags"])
+    assert np.array_equal(np.array(cb.resolution()), c["resolution"])
+    assert cb.dump() == str(c["seq_dump"])
