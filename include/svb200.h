@@ -58,6 +58,8 @@ int sv_abi_version(void);
 const char* sv_last_error(void);
 int sv_device_count(int* count);
 int sv_sm_count(int device, int* count);
+/* free / total device memory in bytes (cudaMemGetInfo) */
+int sv_mem_info(int device, uint64_t* free_bytes, uint64_t* total_bytes);
 /* make `device` current on the calling thread (svk_* launch on the current device) */
 int sv_set_device(int device);
 
@@ -233,6 +235,29 @@ int svb_pair_dot(sv_bhandle h, const void* a_mi, const void* a_pi, const void* b
                  uint64_t count, double* out2);
 /* device pointers of the current planes (for offsets into own / peer planes) */
 int svb_planes(sv_bhandle h, void** cur_mi, void** cur_pi);
+
+/* ---- two-tier state: HBM + pinned host memory (svsim/tier.py executed) ----
+ * 2^n amplitudes in chunks of 2^chunk_qubits; chunk g stays in HBM when fast[g] != 0
+ * (TierAccount.fast_resident, tier.py:156-178), else lives in pinned host memory and is
+ * staged through `slots` HBM chunk slots (tier.py STAGING_SLOTS = 4). */
+typedef struct sv_tier* sv_thandle;
+int svt_create(int device, int n_qubits, int mode, int chunk_qubits, const uint8_t* fast, int slots,
+               sv_thandle* out);
+int svt_destroy(sv_thandle h);
+int svt_zero_state(sv_thandle h, int64_t unit);
+/* a "run" staging group (tier.py:121-129): ops on qubits < chunk_qubits or diagonal */
+int svt_apply_run(sv_thandle h, const sv_op* ops, int n_ops, int tile_bits);
+/* one non-diagonal gate with a qubit >= chunk_qubits ("mid" / "exchange" groups,
+ * tier.py:130-143): chunk groups co-staged and updated in place */
+int svt_apply_pairing(sv_thandle h, const sv_op* op);
+/* measure.py sums over the whole state (slow chunks staged in once) */
+int svt_measure(sv_thandle h, double* norm, double* ones, double* cross);
+int svt_export(sv_thandle h, void* host, uint64_t first, uint64_t count);
+int svt_import(sv_thandle h, const void* host, uint64_t first, uint64_t count);
+int svt_synchronize(sv_thandle h);
+/* physical counters: h2d bytes, d2h bytes, h2d copies, d2h copies, zero-copy bytes,
+ * slot memsets (never-written chunks), kernel passes, HBM bytes of the fast tier */
+int svt_stats(sv_thandle h, uint64_t* out8);
 
 /* ---- raw device buffers (for the array-level operator API) --------- */
 int sv_buffer_alloc(int device, uint64_t bytes, void** ptr);

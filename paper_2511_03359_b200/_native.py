@@ -38,6 +38,7 @@ _I = ctypes.c_int
 
 _SIGNATURES = {
     "sv_abi_version": ([], _I),
+    "sv_mem_info": ([_I, ctypes.POINTER(_U64), ctypes.POINTER(_U64)], _I),
     "sv_last_error": ([], ctypes.c_char_p),
     "sv_device_count": ([ctypes.POINTER(_I)], _I),
     "sv_sm_count": ([_I, ctypes.POINTER(_I)], _I),
@@ -131,6 +132,16 @@ _SIGNATURES = {
     "sv_event_record": ([_P, _P], _I),
     "sv_event_elapsed_ms": ([_P, _P, ctypes.POINTER(ctypes.c_float)], _I),
     "sv_stream_synchronize": ([_P], _I),
+    "svt_create": ([_I, _I, _I, _I, _P, _I, ctypes.POINTER(_P)], _I),
+    "svt_destroy": ([_P], _I),
+    "svt_zero_state": ([_P, ctypes.c_int64], _I),
+    "svt_apply_run": ([_P, _P, _I, _I], _I),
+    "svt_apply_pairing": ([_P, _P], _I),
+    "svt_measure": ([_P, _D, _D, _D], _I),
+    "svt_export": ([_P, _P, _U64, _U64], _I),
+    "svt_import": ([_P, _P, _U64, _U64], _I),
+    "svt_synchronize": ([_P], _I),
+    "svt_stats": ([_P, ctypes.POINTER(_U64)], _I),
 }
 
 _lib = None

@@ -909,6 +909,15 @@ int sv_set_device(int device) {
     return SV_OK;
 }
 
+int sv_mem_info(int device, uint64_t* free_bytes, uint64_t* total_bytes) {
+    DeviceGuard g(device);
+    size_t f = 0, t = 0;
+    CUDA_TRY(cudaMemGetInfo(&f, &t), "cudaMemGetInfo");
+    *free_bytes = f;
+    *total_bytes = t;
+    return SV_OK;
+}
+
 int sv_sm_count(int device, int* count) {
     *count = sm_count(device);
     return SV_OK;

@@ -212,6 +212,32 @@ __global__ void __launch_bounds__(256) k_quad(S* p0, S* p1, S* p2, S* p3, uint64
     }
 }
 
+// two buffers, a two-qubit gate whose qubits are an in-buffer bit `lo` and the
+// buffer choice (b0 / b1): the tier executor's chunk pairs (tier.py "mid" groups).
+// Basis index = bit(qa) + 2 bit(qb) (kernels.py:56-58); hi_is_b: the buffer choice
+// is qb, else qa.  Same row4 arithmetic as k_gate2 / k_quad.
+template <typename S>
+__global__ void __launch_bounds__(256) k_pair2q(S* __restrict__ b0, S* __restrict__ b1, uint64_t n_quads, int lo,
+                                                int hi_is_b, Mat4 m) {
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t bl = 1ull << lo;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_quads; t += step) {
+        const uint64_t i = insert0(t, lo);
+        S* p[4];
+        uint64_t o[4];
+        if (hi_is_b) {   // (qa = lo, qb = buffer): members (b0[i], b0[i|l], b1[i], b1[i|l])
+            p[0] = b0; o[0] = i; p[1] = b0; o[1] = i | bl; p[2] = b1; o[2] = i; p[3] = b1; o[3] = i | bl;
+        } else {         // (qa = buffer, qb = lo): members (b0[i], b1[i], b0[i|l], b1[i|l])
+            p[0] = b0; o[0] = i; p[1] = b1; o[1] = i; p[2] = b0; o[2] = i | bl; p[3] = b1; o[3] = i | bl;
+        }
+        cplx a[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a[c] = Store<S>::get(p[c][o[c]]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) p[r][o[r]] = Store<S>::put(row4(&m.m[4 * r], a[0], a[1], a[2], a[3]));
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Fused pass.  A tile is the 2^k amplitudes whose local index differs only
 // in the tile qubits T (tq[0..k-1], with tq[i] == i for i < b so that runs of
@@ -408,6 +434,19 @@ cudaError_t launch_quad(void* const* parts, uint64_t count, int mode, const doub
     else
         k_quad<c64s><<<g, 256, 0, st>>>(static_cast<c64s*>(parts[0]), static_cast<c64s*>(parts[1]),
                                         static_cast<c64s*>(parts[2]), static_cast<c64s*>(parts[3]), count, m);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pair2q(void* b0, void* b1, uint64_t count, int mode, int lo, int hi_is_b, const double* m32,
+                          cudaStream_t st) {
+    const Mat4 m = mat4_from(m32);
+    const uint64_t quads = count / 2;
+    const unsigned g = grid_for(quads, 256, 8);
+    if (mode == SV_FP32)
+        k_pair2q<c32s><<<g, 256, 0, st>>>(static_cast<c32s*>(b0), static_cast<c32s*>(b1), quads, lo, hi_is_b, m);
+    else
+        k_pair2q<c64s><<<g, 256, 0, st>>>(static_cast<c64s*>(b0), static_cast<c64s*>(b1), quads, lo, hi_is_b, m);
     count_launch();
     return cudaGetLastError();
 }

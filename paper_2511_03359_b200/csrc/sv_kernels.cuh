@@ -86,6 +86,9 @@ cudaError_t launch_diag(void* psi, uint64_t n_elems, int mode, uint64_t mask, co
                         cudaStream_t st);
 cudaError_t launch_pair(void* a0, void* a1, uint64_t count, int mode, const double* m8,
                         cudaStream_t st);
+// two buffers of `count` elements, a 4x4 over (in-buffer bit lo, buffer choice): the tier's chunk pairs
+cudaError_t launch_pair2q(void* b0, void* b1, uint64_t count, int mode, int lo, int hi_is_b, const double* m32,
+                          cudaStream_t st);
 cudaError_t launch_quad(void* const* parts, uint64_t count, int mode, const double* m32,
                         cudaStream_t st);
 cudaError_t launch_fused(void* psi, int mode, const FusedParams& p, cudaStream_t st);

@@ -101,10 +101,40 @@ def gate_to_op(gate: g.Gate):
     return gate_op(nat.SV_OP_2Q, qa=gate.qubits[0], qb=gate.qubits[1], data=m)
 
 
+def tier_ledger_plan(circuit: Circuit, layout: PartitionLayout, mode: PrecisionMode, tier_config, ledgers):
+    """The reference's staging plan of the whole circuit and one TierAccount per rank,
+    charging `ledgers` (engine.py:127-133)."""
+    from .tier import TierAccount, plan_passes
+    plan = plan_passes(circuit.gates, tier_config, layout.local_qubits, mode)
+    state_bytes = layout.local_size * mode.bytes_per_element
+    return plan, [TierAccount(state_bytes, tier_config, led) for led in ledgers]
+
+
+def _fits_in_hbm(n_bytes: int, device: int) -> bool:
+    import ctypes
+    free, total = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    nat.check(nat.load().sv_mem_info(device, ctypes.byref(free), ctypes.byref(total)))
+    return n_bytes + (1 << 30) <= free.value + nat_cached_bytes()
+
+
+def nat_cached_bytes() -> int:
+    import ctypes
+    v = ctypes.c_uint64(0)
+    nat.check(nat.load(require_device=False).sv_cached_bytes(ctypes.byref(v)))
+    return int(v.value)
+
+
 def run_circuit(circuit: Circuit, *, ranks: int = 1, local_qubits: int | None = None,
                 mode: PrecisionMode = PrecisionMode.FP64, tier_config=None,
                 rank_order_seed: int | None = None, transport_factory=Transport,
-                device: int = 0, fuse: bool = True, tile_bits: int = 12) -> RunResult:
+                device: int = 0, fuse: bool = True, tile_bits: int = 12,
+                tier_execute: bool | None = None) -> RunResult:
+    """svsim.run_circuit (engine.py:82-105) on one B200.
+
+    tier_config (svsim TierConfig or tier.TierConfig): the reference's staging plan and
+    TierAccount counters are charged exactly as svsim does.  tier_execute: also EXECUTE
+    the plan with the slow chunks in pinned host memory (csrc/sv_tier.cu); None = only
+    when the FP64/FP32 state does not fit in HBM.  Results are identical either way."""
     validate_circuit(circuit)
     if ranks < 1 or ranks & (ranks - 1):
         raise ValueError("rank count must be a power of two")
@@ -114,22 +144,48 @@ def run_circuit(circuit: Circuit, *, ranks: int = 1, local_qubits: int | None = 
     if layout.rank_count != ranks:
         raise ValueError(f"{ranks} ranks with {local_qubits} local qubits does not cover "
                          f"{circuit.n_qubits} qubits")
-    if tier_config is not None:
-        raise NotImplementedError("the two-tier staging model (tier.py) is out of scope on B200: "
-                                  "every configuration stays resident in HBM")
     start = time.perf_counter()
+    tier = None
+    if tier_config is not None:
+        tier = _TierRun(circuit, layout, mode, tier_config, tier_execute, device)
     launches0 = nat.launch_count()
-    eng = _Engine(circuit, layout, mode, rank_order_seed, transport_factory, device, fuse, tile_bits)
+    eng = _Engine(circuit, layout, mode, rank_order_seed, transport_factory, device, fuse, tile_bits, tier)
     eng.run()
     eng.launches = nat.launch_count() - launches0
     return RunResult(circuit, layout, mode, eng.states, eng.ledgers, eng.report, eng.codebook,
-                     None, time.perf_counter() - start, eng.stats())
+                     tier.accounts if tier else None, time.perf_counter() - start, eng.stats())
+
+
+class _TierRun:
+    """tier_config of one run: the plan (accounts bound to the engine's ledgers later)
+    and whether the plan is executed physically."""
+
+    def __init__(self, circuit, layout, mode, cfg, execute, device):
+        from .tier import plan_passes
+        self.cfg = cfg
+        self.plan = plan_passes(circuit.gates, cfg, layout.local_qubits, mode)   # validates first
+        self.accounts = None
+        if execute is None:
+            execute = mode is not PrecisionMode.BYTE and not _fits_in_hbm(
+                (1 << circuit.n_qubits) * mode.bytes_per_element, device)
+        if execute and mode is PrecisionMode.BYTE:
+            raise NotImplementedError("physical tier execution holds FP64 / FP32 storage; BYTE states "
+                                      "(2 B/amplitude) stay resident and are charged the plan's counters")
+        if execute and self.plan.chunk_qubits < 5:
+            raise ValueError("physical tier execution needs chunks of at least 32 amplitudes")
+        self.execute = bool(execute)
+
+    def bind(self, layout, mode, ledgers):
+        from .tier import TierAccount
+        state_bytes = layout.local_size * mode.bytes_per_element
+        self.accounts = [TierAccount(state_bytes, self.cfg, led) for led in ledgers]
 
 
 class _Engine:
     def __init__(self, circuit, layout, mode, rank_order_seed, transport_factory, device, fuse,
-                 tile_bits):
+                 tile_bits, tier=None):
         self.circuit = circuit
+        self.tier = tier
         self.layout = layout
         self.mode = mode
         self.fuse = fuse
@@ -142,10 +198,18 @@ class _Engine:
             random.Random(rank_order_seed).shuffle(self.order)
         self.report = None
         self.codebook = None
+        if tier is not None:
+            tier.bind(layout, mode, self.ledgers)
         if mode is PrecisionMode.BYTE:
             from .byte_state import ByteEngineState
             self.dev = ByteEngineState(circuit.n_qubits, layout, device=device)
             self.codebook = self.dev.codebook
+        elif tier is not None and tier.execute:
+            from .tier import TieredDeviceState, tier_layout_flags
+            t0 = time.perf_counter()
+            self.dev = TieredDeviceState(circuit.n_qubits, mode, tier.plan.chunk_qubits,
+                                         tier_layout_flags(tier.accounts), device=device)
+            tier.setup_seconds = time.perf_counter() - t0
         else:
             from .device import DeviceState
             self.dev = DeviceState(circuit.n_qubits, mode, device=device)
@@ -234,7 +298,60 @@ class _Engine:
             self.transport.collective([None] * P)
         self.report = report_from_sums(norm, ones, cross)
 
+    def _run_tiered(self):
+        """Group by group as the reference (engine.py:137-145): every rank's TierAccount is
+        charged, then the group's gates run -- physically staged when the plan executes."""
+        physical = self.tier.execute
+        gates = self.circuit.gates
+        for grp in self.tier.plan.groups:
+            for acct in self.tier.accounts:
+                acct.account(grp)
+            ops = []
+            for ordinal in grp.gate_indices:
+                gate = gates[ordinal]
+                plan = plan_exchange(self.layout, gate, self.mode)
+                try:
+                    if gate.kind == "M":
+                        if physical and ops:
+                            self.dev.apply_run(ops, self.tile_bits)
+                            ops = []
+                        self._measure(ordinal)
+                    else:
+                        if plan.kind != "none":
+                            self._exchange_messages(plan, ordinal)
+                        if not physical:
+                            self._enqueue(gate)
+                        elif grp.kind == "run":
+                            ops.append(gate_to_op(gate))
+                        else:
+                            self.dev.apply_pairing(gate_to_op(gate))
+                        if physical:
+                            self.gates_applied += 1
+                except TransportError as exc:
+                    raise RuntimeError(f"gate {ordinal} ({gate.kind}): {exc}") from exc
+                for led in self.ledgers:
+                    led.gate_operations += 1
+            if physical and ops:
+                self.dev.apply_run(ops, self.tile_bits)
+        self._flush()
+        self.dev.synchronize()
+        self.transport.assert_drained()
+
     def run(self):
+        t0 = time.perf_counter()
+        try:
+            self._run()
+        finally:
+            self.run_seconds = time.perf_counter() - t0
+
+    def _run(self):
+        if self.tier is not None:
+            if self.fuse and not self.tier.execute and self.mode in (PrecisionMode.FP64, PrecisionMode.FP32):
+                from .device import jit_prepare
+                jit_prepare(self.circuit.n_qubits, [gate_to_op(g) for g in self.circuit.gates if g.kind != "M"],
+                            self.tile_bits, self.dev.mode_code)
+            self._run_tiered()
+            return
         if self.fuse and self.mode in (PrecisionMode.FP64, PrecisionMode.FP32):
             # queue the specialised pass kernels of the whole circuit (compiled in the
             # background; passes whose kernel is not ready yet run the generic one)
@@ -265,4 +382,11 @@ class _Engine:
         if self.mode is PrecisionMode.BYTE:
             out.update(byte_passes=self.dev.passes, byte_reencodes=self.dev.reencodes,
                        byte_host_fixes=self.dev.host_fixes)
+        if self.tier is not None:
+            out["tier"] = {"executed": self.tier.execute, "groups": len(self.tier.plan.groups),
+                           "chunk_qubits": self.tier.plan.chunk_qubits}
+            if self.tier.execute:
+                out["tier"].update(self.dev.stats())
+                out["tier"]["setup_seconds"] = round(getattr(self.tier, "setup_seconds", 0.0), 3)
+                out["tier"]["run_seconds"] = round(getattr(self, "run_seconds", 0.0), 3)
         return out

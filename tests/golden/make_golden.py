@@ -17,6 +17,11 @@ this script:
                  states, storage bytes, ledgers, reports, codebooks
   planner.json — plan_exchange, memory_bytes, predicted_exchange_bytes and
                  optimize_labels at the BASELINE configs (N up to 38)
+  tier.json    — tier.py: plan_passes groups, TierAccount residency /
+                 high-water / counters, naive_staging_bytes,
+                 recommended_fast_bytes, validation errors, and
+                 run_circuit(tier_config=...) ledgers + state digests
+                 (`python tests/golden/make_golden.py --tier`)
   ladder.json  — the SURVEY 8(c) parity ladder at sizes too large for npz
                  fixtures: C1 = build_benchmark(20) FP64 P=1, benchmark 22/24
                  and adder(11) FP64 at P in {1, 8}, FP32 benchmark(22), BYTE
@@ -365,8 +370,82 @@ def make_ladder(ref):
                 json.dump(out, f, indent=0, default=lambda o: o.item() if hasattr(o, "item") else str(o))
 
 
+def tier_cases():
+    """(name, circuit, n_local, mode, TierConfig args) for the tier goldens."""
+    from tests.circuits import random_circuit as rc
+    r = lambda s: np.random.default_rng(SEED + 300 + s)  # noqa: E731
+    B = lambda n, m: (1 << n) * {"fp64": 16, "fp32": 8, "be": 2}[m]  # noqa: E731
+    return [
+        ("rand10_q4_c64", rc(r(1), 10, 24), 10, "fp64", (B(10, "fp64") // 4, B(10, "fp64") // 64, 64)),
+        ("rand10_q4_c16", rc(r(2), 10, 30), 10, "fp64", (B(10, "fp64") // 4, B(10, "fp64") // 16, 64)),
+        ("rand9_w4", rc(r(3), 9, 40), 9, "fp64", (B(9, "fp64") // 4, B(9, "fp64") // 32, 4)),
+        ("rand9_fp32", rc(r(4), 9, 30), 9, "fp32", (B(9, "fp32") // 3, B(9, "fp32") // 32, 64)),
+        ("rand9_be", rc(r(5), 9, 30), 9, "be", (B(9, "be") // 4, B(9, "be") // 16, 64)),
+        ("bench12_c8", benchmark(12), 12, "fp64", (B(12, "fp64") // 2, B(12, "fp64") // 8, 64)),
+        ("bench12_resident", benchmark(12), 12, "fp64", (B(12, "fp64"), B(12, "fp64") // 2, 64)),
+        ("adder6", adder(6, [40, 21])[0], 12, "fp64", (B(12, "fp64") // 4, B(12, "fp64") // 32, 64)),
+        ("exact9_r4", exact_class_circuit(r(6), 9, 20), 7, "fp64", (B(7, "fp64") // 4, B(7, "fp64") // 32, 64)),
+        ("rand8_r2", rc(r(7), 8, 30), 7, "fp64", (B(7, "fp64") // 4, B(7, "fp64") // 16, 64)),
+        ("bench34_cfg", benchmark(34), 34, "fp64", (160 << 30, 4 << 30, 64)),
+        ("bench34_c8", benchmark(34), 34, "fp64", (160 << 30, 8 << 30, 64)),
+        ("adder17_cfg", adder(17, [3, 5])[0], 34, "fp64", (160 << 30, 4 << 30, 64)),
+    ]
+
+
+def make_tier(ref):
+    T = ref.tier
+    modes = {"fp64": ref.PrecisionMode.FP64, "fp32": ref.PrecisionMode.FP32, "be": ref.PrecisionMode.BYTE}
+    out = {"cases": [], "errors": [], "recommended": []}
+    for name, circ, n_local, mode, (fast, chunk, window) in tier_cases():
+        cfg = T.TierConfig(fast, chunk, window)
+        rc_ = to_reference(circ, ref)
+        plan = T.plan_passes(rc_.gates, cfg, n_local, modes[mode])
+        led = ref.TrafficLedger()
+        state_bytes = (1 << n_local) * modes[mode].bytes_per_element
+        acct = T.TierAccount(state_bytes, cfg, led)
+        for grp in plan.groups:
+            acct.account(grp)
+        ent = dict(name=name, n_local=n_local, mode=mode, config=[fast, chunk, window],
+                   chunk_qubits=plan.chunk_qubits, n_chunks=plan.n_chunks,
+                   groups=[[grp.kind, list(grp.gate_indices), [list(m) for m in grp.chunk_groups]]
+                           for grp in plan.groups],
+                   fast_resident=[bool(x) for x in acct.fast_resident],
+                   static_fast_bytes=acct.static_fast_bytes, high_water_bytes=acct.high_water_bytes,
+                   slow_bytes=acct.slow_bytes, tier_bytes=led.tier_bytes_moved,
+                   tier_transfers=led.tier_transfer_count,
+                   naive=T.naive_staging_bytes(rc_.gates, cfg, n_local, modes[mode]),
+                   n_passes=len(plan.passes()))
+        if circ.n_qubits <= 12:
+            P = 1 << (circ.n_qubits - n_local)
+            res = ref.run_circuit(rc_, ranks=P, mode=modes[mode], tier_config=cfg)
+            ent["run"] = dict(ranks=P, state_sha256=state_digest(res.gathered_state()),
+                              ledgers=[l.snapshot() for l in res.ledgers],
+                              high_water=[a.high_water_bytes for a in res.tier_accounts])
+        out["cases"].append(ent)
+        print("tier", name, flush=True)
+    for args in ((1024, 100), (1024, 1024), (4096, 256, 0)):
+        try:
+            T.TierConfig(*args)
+            out["errors"].append([list(args), None])
+        except ValueError as exc:
+            out["errors"].append([list(args), str(exc)])
+    try:
+        T.plan_passes((ref.gates.u4(2, 3, ref.gates.CNOT_MATRIX),), T.TierConfig(2 * 64, 64), 6,
+                      ref.PrecisionMode.FP64)
+        out["errors"].append(["quad_tight", None])
+    except ValueError as exc:
+        out["errors"].append(["quad_tight", str(exc)])
+    for sb, cb in ((1280 * 1024, 1024), (256 << 30, 4 << 30), (1 << 20, 1 << 12), (12345678, 4096)):
+        out["recommended"].append([sb, cb, T.recommended_fast_bytes(sb, cb)])
+    with open(os.path.join(HERE, "tier.json"), "w") as f:
+        json.dump(out, f, indent=0)
+
+
 def main():
     ref = load_reference()
+    if "--tier" in sys.argv:
+        make_tier(ref)
+        return
     if "--ladder" in sys.argv:
         make_ladder(ref)
         return
@@ -374,6 +453,7 @@ def main():
     make_codec(ref)
     make_planner(ref)
     make_runs(ref)
+    make_tier(ref)
     make_ladder(ref)
 
 

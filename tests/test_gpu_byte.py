@@ -135,3 +135,18 @@ def test_byte_rank_invariant_codebooks(rng):
     circ = to_product(exact_class_circuit(rng, 10, 30))
     dumps = {pb.run_circuit(circ, ranks=r, mode=BE).codebook.dump() for r in (1, 2, 4, 8)}
     assert len(dumps) == 1
+
+
+def test_numerics_fingerprint_on_the_box_host(golden):
+    """SURVEY App. A on the GPU box's own host: the numpy primitives the BYTE host merge
+    (codec.py finalize_proposal / host_encode) and the oracle inherit must behave as on the
+    host that wrote the goldens -- complex abs, angle (SVML atan2) and complex multiply."""
+    c = golden("codec.npz")
+    v = c["canon_in"]
+    assert np.array_equal(np.abs(v).view(np.uint64), c["abs_out"].view(np.uint64))
+    assert np.array_equal(np.angle(v).view(np.uint64), c["angle_out"].view(np.uint64))
+    a, b = v[:10000], v[10000:20000]
+    assert np.array_equal((a * b).view(np.uint64), c["mul_out"].view(np.uint64))
+    r, th, ux, uy = pb.codec.canonicalize(v)
+    for got, key in ((r, "canon_r"), (th, "canon_th"), (ux, "canon_ux"), (uy, "canon_uy")):
+        assert np.array_equal(np.asarray(got).view(np.uint64), c[key].view(np.uint64)), key
