@@ -21,7 +21,11 @@
 //     pinned host memory is device-mapped).
 // Arithmetic is the same kernels' on the same amplitudes, so results equal the
 // untiered run bit for bit.  Physical link bytes and copies are counted.
+#include <sys/mman.h>
+
+#include <atomic>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "sv_common.cuh"
@@ -46,6 +50,7 @@ struct sv_tier {
     std::vector<uint8_t> fast;      // per chunk
     std::vector<void*> ptr;         // HBM pointer (fast) or pinned host pointer (slow)
     std::vector<uint8_t> zero;      // slow chunk known to be all zeros (never staged out yet)
+    std::vector<uint8_t> registered;   // slow chunk: mmap'd + cudaHostRegister'ed (else cudaHostAlloc)
     void* fast_arena = nullptr;     // fast chunks, contiguous
     size_t fast_bytes = 0;
     void* slot_arena = nullptr;     // staging slots, contiguous
@@ -172,15 +177,51 @@ int svt_create(int device, int n_qubits, int mode, int chunk_qubits, const uint8
     }
     if ((e = cudaMalloc(&h->slot_arena, cb * (size_t)slots)) != cudaSuccess) return bail(e, "staging slots (HBM)");
     uint64_t fi = 0;
+    std::vector<uint64_t> slow;
     for (uint64_t g = 0; g < h->n_chunks; ++g) {
-        if (h->fast[g]) {
-            h->ptr[g] = static_cast<char*>(h->fast_arena) + (fi++) * cb;
-        } else {
+        if (h->fast[g]) h->ptr[g] = static_cast<char*>(h->fast_arena) + (fi++) * cb;
+        else slow.push_back(g);
+    }
+    // Slow chunks: anonymous mappings on transparent huge pages, first-touched and pinned
+    // (cudaHostRegister, device-mapped) by 8 threads -- measured 1.3 s for 16 GiB on the
+    // B200 box against 7.0 s for cudaHostAlloc, serial or threaded (tools/pin_probe.cu).
+    // Chunks below 2 MiB take cudaHostAlloc.
+    h->registered.assign(h->n_chunks, 0);
+    std::atomic<size_t> next{0};
+    std::atomic<int> err{0};
+    auto pin_worker = [&]() {
+        cudaSetDevice(device);
+        for (size_t i = next++; i < slow.size() && !err.load(); i = next++) {
+            const uint64_t g = slow[i];
             void* p = nullptr;
-            if ((e = cudaHostAlloc(&p, cb, cudaHostAllocPortable | cudaHostAllocMapped)) != cudaSuccess)
-                return bail(e, "slow tier (pinned host memory)");
+            if (cb >= (2u << 20)) {
+                p = mmap(nullptr, cb, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+                if (p == MAP_FAILED) { err = 1; return; }
+                madvise(p, cb, MADV_HUGEPAGE);
+                std::memset(p, 0, cb);
+                if (cudaHostRegister(p, cb, cudaHostRegisterPortable | cudaHostRegisterMapped) != cudaSuccess) {
+                    munmap(p, cb);
+                    err = 2;
+                    return;
+                }
+                h->registered[g] = 1;
+            } else if (cudaHostAlloc(&p, cb, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
+                err = 3;
+                return;
+            }
             h->ptr[g] = p;
         }
+    };
+    {
+        const size_t nt = std::min<size_t>(8, std::max<size_t>(1, slow.size()));
+        std::vector<std::thread> th;
+        for (size_t t = 0; t < nt; ++t) th.emplace_back(pin_worker);
+        for (auto& t : th) t.join();
+    }
+    if (err.load()) {
+        cudaGetLastError();
+        svt_destroy(h);
+        return capi_fail(SV_ENOMEM, "slow tier: pinned host memory allocation failed");
     }
     if ((e = cudaStreamCreateWithFlags(&h->comp, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking)) != cudaSuccess ||
@@ -209,8 +250,16 @@ int svt_destroy(sv_thandle h) {
     if (h->comp) cudaStreamSynchronize(h->comp);
     if (h->h2d) cudaStreamSynchronize(h->h2d);
     if (h->d2h) cudaStreamSynchronize(h->d2h);
-    for (uint64_t g = 0; g < h->n_chunks; ++g)
-        if (!h->fast[g] && h->ptr[g]) cudaFreeHost(h->ptr[g]);
+    const size_t cb = chunk_bytes(h);
+    for (uint64_t g = 0; g < h->n_chunks; ++g) {
+        if (h->fast[g] || !h->ptr[g]) continue;
+        if (!h->registered.empty() && h->registered[g]) {
+            cudaHostUnregister(h->ptr[g]);
+            munmap(h->ptr[g], cb);
+        } else {
+            cudaFreeHost(h->ptr[g]);
+        }
+    }
     if (h->fast_arena) cudaFree(h->fast_arena);
     if (h->slot_arena) cudaFree(h->slot_arena);
     for (auto* v : {&h->ev_in, &h->ev_done, &h->ev_free, &h->ev_host})
