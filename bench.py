@@ -212,11 +212,172 @@ def cpu_baseline(steps: int, n_layers: int, sample_n: int = CPU_SAMPLE_N):
     secs = sum(r[0] for r in res)
     byts = sum(r[1] for r in res)
     gates = sum(r[2] for r in res)
+    # the reference itself runs numpy on ONE core -- the same port on one
+    # thread at three sizes, and sec/gate extrapolated to the bench size (x 2 per qubit, the
+    # per-gate work is 2^N; fitted on the measured sizes)
+    import math
+    single = []
+    for ns in (sample_n - 4, sample_n - 3, sample_n - 2):
+        r1, _ = time_layers([workload_layers(ns, 2)[1]], ns, threads=1)
+        single.append((ns, r1[0][0] / r1[0][2], r1[0][1] / r1[0][0] / 1e9))
+    xs = [a for a, _, _ in single]
+    ys = [math.log2(b) for _, b, _ in single]
+    xm, ym = sum(xs) / len(xs), sum(ys) / len(ys)
+    slope = sum((x - xm) * (y - ym) for x, y in zip(xs, ys)) / sum((x - xm) ** 2 for x in xs)
+    extrap = lambda nn: 2 ** (ym + slope * (nn - xm))  # noqa: E731
     return {"value": byts / secs / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
             "sec_per_gate": secs / gates,
+            "single_core": {"sec_per_gate": {str(a): round(b, 5) for a, b, _ in single},
+                            "GBps": {str(a): round(c, 3) for a, _, c in single},
+                            "fit_log2_slope_per_qubit": round(slope, 3),
+                            "extrapolated_sec_per_gate_n33": round(single[-1][1] * 2 ** (33 - single[-1][0]), 2),
+                            "fit_extrapolated_sec_per_gate_n33": round(extrap(33), 2),
+                            "what": "numpy port, 1 thread (the reference's own execution model), one C2 "
+                                    "layer per size; N=33 extrapolated (not measured) as sec/gate x 2^(33-N) "
+                                    "from the largest size (per-gate work is 2^N), and by the log-linear fit"},
+            "threaded_extrapolated_sec_per_gate_n33": round(secs / gates * 2 ** (33 - sample_n), 2),
             "sample": f"{len(chosen)} layer(s) x {n_layers}-layer workload at N={sample_n} FP64 "
                       f"({gates} gates, {secs:.1f} s), numpy port of svsim/kernels.py in oracle/, "
                       f"{threads} threads"}
+
+
+def fused_parity(n_small: int, device: int, tile_bits: int) -> dict:
+    """One C2 layer at n_small through fused passes vs one kernel per gate (fuse=False), bit
+    for bit, and at N=18 against the CPU oracle (test infrastructure, outside the timed
+    region)."""
+    import numpy as np
+    import paper_2511_03359_b200 as pb
+    from oracle import ref_engine
+    from oracle.ref_builders import OCircuit
+    from tests.circuits import to_product
+    out = {}
+    lay = workload_layers(n_small, 3)[2]
+    circ = to_product(OCircuit(n_small, tuple(lay)))
+    a = pb.run_circuit(circ, device=device, tile_bits=tile_bits).gathered_state()
+    b = pb.run_circuit(circ, device=device, fuse=False).gathered_state()
+    out[f"fused_vs_per_gate_n{n_small}_bit_exact"] = bool(np.array_equal(a, b))
+    del a, b
+    lay = workload_layers(18, 3)[2]
+    oc = OCircuit(18, tuple(lay))
+    got = pb.run_circuit(to_product(oc), device=device, tile_bits=tile_bits).gathered_state()
+    out["oracle_n18_bit_exact"] = bool(np.array_equal(got, ref_engine.run_circuit(oc, ranks=1).gathered_state()))
+    return out
+
+
+_COLD = r"""
+import json, os, sys, time
+t_start = time.perf_counter()
+sys.path.insert(0, sys.argv[1])
+import paper_2511_03359_b200 as pb
+from paper_2511_03359_b200 import _native as nat
+from paper_2511_03359_b200.device import jit_stats
+from oracle.ref_builders import OCircuit
+from tests.circuits import to_product
+n, layers, device, tile_bits = (int(x) for x in sys.argv[2:6])
+sys.path.insert(0, sys.argv[1])
+import bench
+lay = bench.workload_layers(n, layers)[1]
+circ = pb.Circuit(n, tuple(to_product(OCircuit(n, tuple(lay))).gates) + (pb.gates.measure_all(),))
+t_imp = time.perf_counter()
+import ctypes
+c = ctypes.c_int(0)
+nat.check(nat.load().sv_device_count(ctypes.byref(c)))
+nat.check(nat.load().sv_set_device(device))
+t_ctx0 = time.perf_counter()
+free = ctypes.c_uint64(0); tot = ctypes.c_uint64(0)
+nat.check(nat.load().sv_mem_info(device, ctypes.byref(free), ctypes.byref(tot)))   # creates the context
+t_ctx = time.perf_counter() - t_ctx0
+t0 = time.perf_counter()
+res = pb.run_circuit(circ, device=device, tile_bits=tile_bits)
+q = res.report.qz[0]
+t_first = time.perf_counter() - t0
+t0 = time.perf_counter()
+res2 = pb.run_circuit(circ, device=device, tile_bits=tile_bits)
+q = res2.report.qz[0]
+t_second = time.perf_counter() - t0
+print(json.dumps({"first_call_s": t_first, "second_call_s": t_second, "context_s": t_ctx,
+                  "import_s": t_imp - t_start, "jit": jit_stats()}))
+"""
+
+
+def cold_e2e(n: int, layers: int, device: int, tile_bits: int) -> dict:
+    """e2e of a FRESH process (run_circuit(layer + M), the same call as the warm e2e):
+    context creation, 2^N allocation, the pass kernels loaded from the persistent cubin
+    cache this process filled (sv_jit.cu) -- no NVRTC -- and the measure-all."""
+    import subprocess
+    root = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-c", _COLD, root, str(n), str(layers), str(device), str(tile_bits)],
+                       capture_output=True, text=True, timeout=600)
+    if r.returncode != 0:
+        return {"error": (r.stderr or r.stdout)[-400:]}
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    gb = layer_bytes(workload_layers(n, layers)[1], n)
+    return {"value": round(gb / d["first_call_s"] / 1e9, 2), "unit": "GB/s",
+            "first_call_s": round(d["first_call_s"], 4), "warm_second_call_s": round(d["second_call_s"], 4),
+            "context_init_s": round(d["context_s"], 3), "import_s": round(d["import_s"], 2),
+            "jit_disk_hits": d["jit"]["disk_hits"], "nvrtc_compiles": d["jit"]["compiled"],
+            "what": "first run_circuit(layer + M) in a new process after CUDA context creation: 2^N "
+                    "allocation, pass kernels from the on-disk cubin cache, measure-all, report to host"}
+
+
+def tier_run(n: int, fast_gib: float, chunk_gib: float, device: int) -> dict:
+    """build_benchmark(n) FP64 larger than HBM, the reference's staging plan
+    executed with the slow chunks in pinned host memory (tier.py / csrc/sv_tier.cu)."""
+    import ctypes
+    import paper_2511_03359_b200 as pb
+    from paper_2511_03359_b200 import _native as nat
+    from paper_2511_03359_b200.tier import TierConfig
+    free, tot = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    nat.check(nat.load().sv_mem_info(device, ctypes.byref(free), ctypes.byref(tot)))
+    if free.value < (fast_gib + 4) * 2 ** 30:
+        return {"skipped": f"needs {fast_gib + 4:.0f} GiB free HBM, {free.value / 2**30:.0f} GiB free"}
+    cfg = TierConfig(int(fast_gib * 2 ** 30), int(chunk_gib * 2 ** 30))
+    circ = pb.build_benchmark(n)
+    t0 = time.perf_counter()
+    res = pb.run_circuit(circ, tier_config=cfg, tier_execute=True, device=device)
+    wall = time.perf_counter() - t0
+    st = res.device_stats["tier"]
+    kat = benchmark_kat(res.report, n)
+    link = st["h2d_bytes"] + st["d2h_bytes"] + st["zero_copy_bytes"]
+    hl = host_link_peak()
+    out = {"circuit": f"build_benchmark({n}) FP64, {2 ** n * 16 / 2 ** 30:.0f} GiB state on 1 B200",
+           "config": {"fast_capacity_GiB": fast_gib, "chunk_GiB": chunk_gib},
+           "hbm_fast_GiB": st["hbm_fast_bytes"] / 2 ** 30, "slow_GiB": res.tier_accounts[0].slow_bytes / 2 ** 30,
+           "gates": len(circ.gates), "staging_groups": st["groups"], "wall_s": round(wall, 2),
+           "setup_s": st["setup_seconds"], "run_s": st["run_seconds"],
+           "sec_per_gate": round(st["run_seconds"] / len(circ.gates), 4),
+           "model_tier_bytes": res.total_tier_bytes, "physical_link_bytes": link,
+           "link_GBps": round(link / st["run_seconds"] / 1e9, 2),
+           "link_peak_GBps": hl, "link_frac": round(link / st["run_seconds"] / 1e9 / hl, 3) if hl else None,
+           "kat_parity_pattern": kat[0], "kat_max_dev": kat[1],
+           "what": "run_circuit(tier_config=TierConfig(fast, chunk), tier_execute=True): reference staging "
+                   "plan executed, slow chunks in pinned host memory, copy engines overlapped with passes"}
+    del res
+    return out
+
+
+def host_link_peak() -> float | None:
+    """Concurrent H2D + D2H copy bandwidth of 1 GiB pinned buffers (the tier's link)."""
+    try:
+        import torch
+        h = torch.empty(2 << 30, dtype=torch.uint8, pin_memory=True)
+        d = torch.empty(2 << 30, dtype=torch.uint8, device="cuda")
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        best = 0.0
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            with torch.cuda.stream(s1):
+                d[: 1 << 30].copy_(h[: 1 << 30], non_blocking=True)
+            with torch.cuda.stream(s2):
+                h[1 << 30:].copy_(d[1 << 30:], non_blocking=True)
+            torch.cuda.synchronize()
+            best = max(best, (2 << 30) / (time.perf_counter() - t) / 1e9)
+        del h, d
+        torch.cuda.empty_cache()
+        return round(best, 1)
+    except Exception:
+        return None
 
 
 def run_reference_arm(args):
@@ -304,6 +465,11 @@ def run_b200(args):
     launches = nat.launch_count() - launches0
     jit = jit_stats()
     ms = ev0.elapsed_ms(ev1)
+    # parity of the timed region (outside it): the 128 GiB state after warm-up + timed steps is
+    # still normalised (unitary layers), every Qz in [0, 1]
+    norm_t, ones_t, _ = dev.measure()
+    parity = {"norm_deviation_after_timed": abs(norm_t - 1.0),
+              "qz_in_range": bool(all(-1e-12 <= z <= norm_t + 1e-12 for z in ones_t))}
     if dist is not None:
         dist.barrier()
     ms_max = max_over_ranks(dist, ms)
@@ -329,6 +495,8 @@ def run_b200(args):
             single[f"q{q}"] = {"ms": round(t, 3), "GB/s": round(2 * 16 * dev.size / (t / 1e3) / 1e9, 1)}
     dev.free()
     del dev
+    if args.parity:
+        parity.update(fused_parity(n_small=args.parity_n, device=device, tile_bits=args.tile_bits))
 
     # FP32 storage: same layers, complex64 at rest, FP64 arithmetic, one
     # rounding per gate -- timed like the FP64 steps
@@ -439,6 +607,17 @@ def run_b200(args):
         bst.free()
         del bst
 
+    if e2e and args.cold_e2e:
+        from paper_2511_03359_b200.device import release_cached_memory
+        release_cached_memory()              # the child process allocates its own 2^N state
+        e2e["cold_process"] = cold_e2e(n, args.layers, device, args.tile_bits)
+
+    tier = None
+    if args.tier_n > 0 and world == 1:
+        from paper_2511_03359_b200.device import release_cached_memory
+        release_cached_memory()
+        tier = tier_run(args.tier_n, args.tier_fast_gib, args.tier_chunk_gib, device)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(max(1, args.cpu_layers), args.layers)
@@ -487,6 +666,9 @@ def run_b200(args):
             line["adder"] = adder
         if byte:
             line["byte_mode"] = byte
+        line["parity"] = parity
+        if tier:
+            line["host_tier"] = tier
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
@@ -864,6 +1046,12 @@ def main():
     ap.add_argument("--planner-ab", type=int, default=1,
                     help="N>1: benchmark(N) with the remap planner vs the reference choreography")
     ap.add_argument("--fp32", type=int, default=1, help="1 GPU line: time the same steps in FP32 storage")
+    ap.add_argument("--parity", type=int, default=1, help="1 GPU line: fused vs per-gate and oracle checks")
+    ap.add_argument("--parity-n", type=int, default=26)
+    ap.add_argument("--cold-e2e", type=int, default=1, help="1 GPU line: e2e of a fresh process")
+    ap.add_argument("--tier-n", type=int, default=34, help="1 GPU line: host-memory tier run size (0: skip)")
+    ap.add_argument("--tier-fast-gib", type=float, default=168.0)
+    ap.add_argument("--tier-chunk-gib", type=float, default=4.0)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -297,7 +297,8 @@ int sv_jit_prepare_mode(int n_qubits, int mode, const sv_op* ops, int n_ops, int
 /* the pass split sv_apply_fused uses for ops: ends[p] = one past the last op of pass p;
  * returns the number of passes (also queues their specialised kernels) */
 int sv_plan_passes(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int* ends, int cap);
-int sv_jit_stats(double* out6);               /* compiled, failed, jit launches, fallbacks, compile ms, cached */
+int sv_jit_stats(double* out8);               /* compiled, failed, jit launches, fallbacks, compile ms, cached,
+                                                 disk-cache hits, disk-cache writes ($SVB200_JIT_CACHE) */
 int sv_jit_available(void);                   /* 1 when NVRTC and the driver entry points resolved */
 /* CPU-side check: plan the first fused pass of ops on 2^n_qubits amplitudes, write
  * its specialised source to src_out and, when compile_ms is non-NULL, compile it

@@ -56,10 +56,11 @@ def jit_wait() -> None:
 
 
 def jit_stats() -> dict:
-    out = np.zeros(6)
+    out = np.zeros(8)
     nat.check(nat.load(require_device=False).sv_jit_stats(nat.dptr(out)))
     return {"compiled": int(out[0]), "failed": int(out[1]), "jit_launches": int(out[2]),
-            "generic_fallbacks": int(out[3]), "compile_ms": round(float(out[4]), 1), "cached": int(out[5])}
+            "generic_fallbacks": int(out[3]), "compile_ms": round(float(out[4]), 1), "cached": int(out[5]),
+            "disk_hits": int(out[6]), "disk_writes": int(out[7])}
 
 
 class DeviceState:

@@ -242,3 +242,47 @@ def test_product_codebook_resolution_and_dump_match_reference(golden):
     cb.mag_overflow, cb.phase_overflow = (bool(x) for x in c[f"seq{last}_flags"])
     assert np.array_equal(np.array(cb.resolution()), c["resolution"])
     assert cb.dump() == str(c["seq_dump"])
+
+
+_CACHE_PROBE = r"""
+import ctypes, sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2511_03359_b200 import _native
+from paper_2511_03359_b200.device import ops_array, jit_stats
+from paper_2511_03359_b200.engine import gate_to_op
+from tests.circuits import random_circuit, to_product
+lib = _native.load(require_device=False)
+ops = [gate_to_op(g) for g in to_product(random_circuit(np.random.default_rng(5), 14, 30, measured=False)).gates]
+buf = ctypes.create_string_buffer(1 << 20)
+ms = np.zeros(1)
+assert lib.sv_jit_probe(ops_array(ops), len(ops), 14, buf, len(buf), _native.dptr(ms)) >= 1
+st = jit_stats()
+print(st["disk_hits"], st["disk_writes"], ms[0])
+"""
+
+
+@pytest.mark.skipif(not _nvrtc_present(), reason="libnvrtc not in this image")
+def test_jit_disk_cache_serves_a_new_process(tmp_path):
+    """The persistent cubin cache (sv_jit.cu, $SVB200_JIT_CACHE): the first process compiles
+    and stores the pass, a second process loads it from disk instead of running NVRTC; a
+    corrupted entry is ignored (source compared byte for byte) and recompiled."""
+    import subprocess
+    import sys
+    env = dict(os.environ, SVB200_JIT_CACHE=str(tmp_path))
+    run = lambda: subprocess.run([sys.executable, "-c", _CACHE_PROBE, ROOT], env=env, capture_output=True,  # noqa: E731
+                                 text=True, timeout=300)
+    r1 = run()
+    assert r1.returncode == 0, r1.stderr
+    hits, writes, _ = r1.stdout.split()
+    assert (int(hits), int(writes)) == (0, 1)
+    files = list(tmp_path.glob("*.svjit"))
+    assert len(files) == 1
+    r2 = run()
+    hits, writes, ms2 = r2.stdout.split()
+    assert (int(hits), int(writes)) == (1, 0) and float(ms2) < 100.0
+    data = bytearray(files[0].read_bytes())
+    data[20] ^= 0xFF                    # corrupt the stored source
+    files[0].write_bytes(bytes(data))
+    r3 = run()
+    hits, writes, _ = r3.stdout.split()
+    assert (int(hits), int(writes)) == (0, 1)
