@@ -309,7 +309,11 @@ def cold_e2e(n: int, layers: int, device: int, tile_bits: int) -> dict:
     r = subprocess.run([sys.executable, "-c", _COLD, root, str(n), str(layers), str(device), str(tile_bits)],
                        capture_output=True, text=True, timeout=600)
     if r.returncode != 0:
-        return {"error": (r.stderr or r.stdout)[-400:]}
+        import ctypes
+        from paper_2511_03359_b200 import _native as nat
+        free, tot = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        nat.load().sv_mem_info(device, ctypes.byref(free), ctypes.byref(tot))
+        return {"error": (r.stderr or r.stdout)[-400:], "parent_free_GiB": round(free.value / 2 ** 30, 1)}
     d = json.loads(r.stdout.strip().splitlines()[-1])
     gb = layer_bytes(workload_layers(n, layers)[1], n)
     return {"value": round(gb / d["first_call_s"] / 1e9, 2), "unit": "GB/s",
@@ -608,13 +612,17 @@ def run_b200(args):
         del bst
 
     if e2e and args.cold_e2e:
+        import gc
         from paper_2511_03359_b200.device import release_cached_memory
+        gc.collect()                         # RunResult <-> state cycles still holding slabs
         release_cached_memory()              # the child process allocates its own 2^N state
         e2e["cold_process"] = cold_e2e(n, args.layers, device, args.tile_bits)
 
     tier = None
     if args.tier_n > 0 and world == 1:
+        import gc
         from paper_2511_03359_b200.device import release_cached_memory
+        gc.collect()
         release_cached_memory()
         tier = tier_run(args.tier_n, args.tier_fast_gib, args.tier_chunk_gib, device)
 

@@ -75,6 +75,13 @@ __device__ __forceinline__ void stg(c32s* p, cplx v) {
     asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"((float)v.re), "f"((float)v.im) : "memory");
 }
 
+// direct tile input (no shared-memory staging): 16-byte load, not kept in L1 (read once)
+__device__ __forceinline__ cplx ldg(const c64s* p) {
+    double re, im;
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(re), "=d"(im) : "l"(p));
+    return {re, im};
+}
+
 template <int U>
 __device__ __forceinline__ cplx mu(cplx a) {   // U: 0 -> 1, 1 -> i, 2 -> -1, 3 -> -i
     if constexpr (U == 0) return a;
