@@ -444,13 +444,20 @@ def run_b200(args):
     ops = [[gate_to_op(g) for g in layer] for layer in layers]
     # compile the specialised pass kernels of every layer before the warm-up (sv_jit.cu)
     from paper_2511_03359_b200.device import jit_prepare, jit_stats, jit_wait
+    # --fuse-steps 1: the timed steps are submitted as ONE op list (the circuit they form),
+    # so fused passes span layer boundaries as in run_circuit; 0: one apply per step
+    warm_seq = [ops[i] for i in step_layers[:args.warmup]]
+    timed_seq = [ops[i] for i in step_layers[args.warmup:]]
+    if args.fuse_steps:
+        warm_seq = [[o for lst in warm_seq for o in lst]]
+        timed_seq = [[o for lst in timed_seq for o in lst]]
     t_jit = time.perf_counter()
-    for o in ops:
+    for o in warm_seq + timed_seq:
         jit_prepare(n, o, args.tile_bits)
     jit_wait()
     t_jit = time.perf_counter() - t_jit
-    for i in step_layers[:args.warmup]:
-        dev.apply_fused(ops[i], args.tile_bits)
+    for o in warm_seq:
+        dev.apply_fused(o, args.tile_bits)
     dev.synchronize()
     if dist is not None:
         dist.barrier()
@@ -460,8 +467,8 @@ def run_b200(args):
     nat.pass_timing_read()
     with ClockSampler(device) as clk:
         ev0.record(dev.stream)
-        for i in step_layers[args.warmup:]:
-            dev.apply_fused(ops[i], args.tile_bits)
+        for o in timed_seq:
+            dev.apply_fused(o, args.tile_bits)
         ev1.record(dev.stream)
         dev.synchronize()
     nat.pass_timing(False)
@@ -506,20 +513,20 @@ def run_b200(args):
     # rounding per gate -- timed like the FP64 steps
     fp32 = None
     if args.fp32:
-        for o in ops:
+        for o in warm_seq + timed_seq:
             jit_prepare(n, o, args.tile_bits, nat.SV_FP32)
         jit_wait()
         dev32 = DeviceState(n, pb.PrecisionMode.FP32, device=device)
         dev32.zero(0)
-        for i in step_layers[:args.warmup]:
-            dev32.apply_fused(ops[i], args.tile_bits)
+        for o in warm_seq:
+            dev32.apply_fused(o, args.tile_bits)
         dev32.synchronize()
         nat.pass_timing(True)
         nat.pass_timing_read()
         f0, f1 = nat.Event(), nat.Event()
         f0.record(dev32.stream)
-        for i in step_layers[args.warmup:]:
-            dev32.apply_fused(ops[i], args.tile_bits)
+        for o in timed_seq:
+            dev32.apply_fused(o, args.tile_bits)
         f1.record(dev32.stream)
         dev32.synchronize()
         nat.pass_timing(False)
@@ -642,6 +649,7 @@ def run_b200(args):
                                    f"per GPU, {2 ** n * 16 / 2 ** 30:.0f} GiB state",
                        "n_qubits_per_gpu": n, "n_qubits_total": n + (world.bit_length() - 1),
                        "gates_per_step": n, "layers": args.layers, "tile_bits": args.tile_bits,
+                       "steps_fused": bool(args.fuse_steps),
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "inputs (128 GiB) >> 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
@@ -1054,6 +1062,8 @@ def main():
     ap.add_argument("--planner-ab", type=int, default=1,
                     help="N>1: benchmark(N) with the remap planner vs the reference choreography")
     ap.add_argument("--fp32", type=int, default=1, help="1 GPU line: time the same steps in FP32 storage")
+    ap.add_argument("--fuse-steps", type=int, default=1,
+                    help="submit the timed steps as one op list (passes span layer boundaries)")
     ap.add_argument("--parity", type=int, default=1, help="1 GPU line: fused vs per-gate and oracle checks")
     ap.add_argument("--parity-n", type=int, default=26)
     ap.add_argument("--cold-e2e", type=int, default=1, help="1 GPU line: e2e of a fresh process")

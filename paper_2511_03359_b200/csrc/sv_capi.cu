@@ -123,6 +123,20 @@ struct PassPlan {
     int ndiag = 0;              // diagonal ops among them
 };
 
+// low qubits every fused-pass tile keeps (contiguous HBM runs of 2^b amplitudes):
+// SVB200_LOW_BITS, default 4 (256-byte runs in FP64, full 32-byte sectors).  One more free
+// tile qubit per pass: the C2 layers at N=33 plan 3.35 instead of 3.55 passes per layer and
+// run 1553 instead of 1639 ms per 9 layers (per-pass efficiency 0.823 vs 0.832).
+int low_bits() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("SVB200_LOW_BITS");
+        const int x = e ? std::atoi(e) : 4;
+        v = (x >= 2 && x <= 5) ? x : 4;
+    }
+    return v;
+}
+
 int op_mdata(int kind) { return kind == SV_OP_2Q ? 32 : (kind == SV_OP_1Q ? 8 : 2); }
 
 int popcount64(uint64_t x) { return __builtin_popcountll(x); }
@@ -276,7 +290,9 @@ int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Pa
         P.seg_end[sgi] = (uint16_t)seg_end[sgi];
     }
     auto lanes_contiguous = [&](int sgi) {
-        return b >= 5 && P.seg_reg[sgi][0] >= 5;   // lanes = the 5 lowest (contiguous) positions
+        // lanes = tile positions 0..4, the low_bits() lowest of them contiguous qubits: every
+        // warp access covers whole runs of >= 2^low_bits amplitudes (full 32-byte sectors)
+        return b >= low_bits() && P.seg_reg[sgi][0] >= 5;
     };
     // linear helpers: shared-memory swizzle and HBM offset of a set of tile positions
     auto swz_h = [](int e) {
@@ -314,8 +330,26 @@ int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Pa
                 P.base_tab[byte][v] = d;
             }
     }
-    P.direct_in = lanes_contiguous(0);
-    P.direct_out = lanes_contiguous(P.n_segs - 1);
+    // direct stores of the last segment from registers: coalesced when the lanes are the
+    // contiguous low positions.  Single-buffered tiles (configs 8, 10) store directly for
+    // any other lane layout too (a warp's 16-byte stores then cover 32-byte sectors in
+    // halves that the write-back L2 merges; DRAM bytes unchanged): it saves the tile's
+    // round trip through shared memory and lets the next tile's loads start as soon as the
+    // last segment holds the tile in registers.  Measured on the C2 layers at N=33: passes
+    // whose last segment keeps a low qubit in registers 62-71 -> 48-59 ms; double-buffered
+    // tiles lose ~2 ms with scattered stores and keep the shared-memory path.
+    // SVB200_DIRECT_OUT: 0 contiguous only, 1 (default) single-buffered too, 2 always.
+    static const int dout_all = [] {
+        const char* e = std::getenv("SVB200_DIRECT_OUT");
+        return e ? std::atoi(e) : 1;
+    }();
+    static const int din_all = [] {
+        const char* e = std::getenv("SVB200_DIRECT_IN");
+        return e ? std::atoi(e) : 0;
+    }();
+    P.direct_in = din_all >= 2 ? 1 : lanes_contiguous(0);
+    const bool single_buf = cfg == 8 || cfg == 10;
+    P.direct_out = (dout_all >= 2 || (dout_all == 1 && single_buf)) ? 1 : lanes_contiguous(P.n_segs - 1);
     int md = 0;
     for (int i = 0; i < nops; ++i) {
         const sv_op& o = ops[pp.ops[i]];
@@ -380,7 +414,7 @@ static bool pass_full(int n, int ndiag) {
 static bool is_diag_kind(int kind) { return kind != SV_OP_1Q && kind != SV_OP_2Q; }
 
 int count_passes(const sv_op* ops, int n_ops, int n, int K) {
-    const uint64_t low = 31ull;
+    const uint64_t low = (1ull << low_bits()) - 1ull;
     uint64_t qm = 0;
     int passes = 0, cnt = 0, md = 0, nd = 0;
     for (int i = 0; i < n_ops; ++i) {
@@ -428,7 +462,7 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
                         n >= kv3 && tile_bits >= kv3;
     const int k = use_v3 ? kv3 : (tile_bits < n ? tile_bits : n);
     if (k < 1 || k > (use_v3 ? 13 : kMaxTileBits)) return fail(SV_EVALUE, "tile bits %d out of range", tile_bits);
-    const int bmin = k >= 5 ? 5 : k;
+    const int bmin = k >= low_bits() ? low_bits() : k;
     const uint64_t lowfix = (1ull << bmin) - 1ull;
     for (int i = 0; i < n_ops; ++i) {
         const sv_op& o = ops[i];
@@ -1115,7 +1149,7 @@ int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_
     const int pcfg = pc ? std::atoi(pc) : 6;
     const int K = (pcfg == 1 || pcfg == 3 || pcfg == 8) ? 12 : (pcfg == 10 ? 13 : 11);
     if (n_qubits < K || n_qubits > 62 || n_ops <= 0) return fail(SV_EVALUE, "probe needs n >= 11 and ops");
-    const uint64_t lowfix = 31ull;
+    const uint64_t lowfix = (1ull << low_bits()) - 1ull;
     PassPlan cur;
     for (int i = 0; i < n_ops; ++i) {
         const sv_op& o = ops[i];
