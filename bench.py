@@ -287,16 +287,18 @@ t_ctx0 = time.perf_counter()
 free = ctypes.c_uint64(0); tot = ctypes.c_uint64(0)
 nat.check(nat.load().sv_mem_info(device, ctypes.byref(free), ctypes.byref(tot)))   # creates the context
 t_ctx = time.perf_counter() - t_ctx0
+sys.stderr.write(f"cold child: free {free.value / 2**30:.1f} GiB of {tot.value / 2**30:.1f}\n")
 t0 = time.perf_counter()
 res = pb.run_circuit(circ, device=device, tile_bits=tile_bits)
 q = res.report.qz[0]
 t_first = time.perf_counter() - t0
+del res
 t0 = time.perf_counter()
 res2 = pb.run_circuit(circ, device=device, tile_bits=tile_bits)
 q = res2.report.qz[0]
 t_second = time.perf_counter() - t0
 print(json.dumps({"first_call_s": t_first, "second_call_s": t_second, "context_s": t_ctx,
-                  "import_s": t_imp - t_start, "jit": jit_stats()}))
+                  "import_s": t_imp - t_start, "jit": jit_stats(), "free_GiB_at_start": free.value / 2**30}))
 """
 
 
@@ -313,7 +315,9 @@ def cold_e2e(n: int, layers: int, device: int, tile_bits: int) -> dict:
         from paper_2511_03359_b200 import _native as nat
         free, tot = ctypes.c_uint64(0), ctypes.c_uint64(0)
         nat.load().sv_mem_info(device, ctypes.byref(free), ctypes.byref(tot))
-        return {"error": (r.stderr or r.stdout)[-400:], "parent_free_GiB": round(free.value / 2 ** 30, 1)}
+        child = [ln for ln in r.stderr.splitlines() if ln.startswith("cold child")]
+        return {"error": (r.stderr or r.stdout)[-400:], "parent_free_GiB": round(free.value / 2 ** 30, 1),
+                "child": child[-1] if child else None}
     d = json.loads(r.stdout.strip().splitlines()[-1])
     gb = layer_bytes(workload_layers(n, layers)[1], n)
     return {"value": round(gb / d["first_call_s"] / 1e9, 2), "unit": "GB/s",

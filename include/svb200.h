@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SV_ABI_VERSION 2
+#define SV_ABI_VERSION 3
 
 enum { SV_OK = 0, SV_EINDEX = -1, SV_EVALUE = -2, SV_ECUDA = -3, SV_ENOMEM = -4 };
 enum { SV_FP64 = 0, SV_FP32 = 1, SV_BYTE = 2 };              /* state.py:20-27 PrecisionMode */
@@ -136,12 +136,18 @@ typedef struct {
     uint64_t phys_base;          /* physical global index of this buffer's element 0 */
     int8_t lbit[16];             /* physical bit of logical bit n_local - 2 + j (j = 0, 1: offset
                                   * top bits; j >= 2: rank bits); identity when not remapped */
+    int32_t ph_zero_in;          /* 1: every phase index of the input planes is 0 (the phase table
+                                  * held one entry whenever a plane was written): not read */
+    int32_t ph_zero_out;         /* 1: this pass's phase table has one entry, every output phase
+                                  * index is 0 and the output phase plane already holds zeros:
+                                  * not written */
 } svb_gate_desc;
 
 int svb_create(int device, int n_qubits, sv_bhandle* out);
 int svb_destroy(sv_bhandle h);
 int svb_info(sv_bhandle h, int* device, int* n_qubits, void** stream);
-/* state.py:49-63: all zero bytes, magnitude index 1 (= 1.0) at `unit` */
+/* state.py:49-63: all zero bytes, magnitude index 1 (= 1.0) at `unit`; both buffers'
+ * phase planes are zeroed (ph_zero_out passes rely on it) */
 int svb_zero_state(sv_bhandle h, int64_t unit);
 /* upload the codebook (append order, codec.py:100-106); sorted copies are
  * built here with a stable argsort (codec.py:112-120) */

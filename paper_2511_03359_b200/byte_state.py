@@ -28,6 +28,8 @@ from . import gates as g
 from .codec import CAPACITY, Codebook
 
 _BIG = 1e308
+# SVB200_BYTE_PHASE_SKIP=0: always read and write the phase plane
+PHASE_PLANE_SKIP = os.environ.get("SVB200_BYTE_PHASE_SKIP", "1") != "0"
 _CAP = 1 << 22                # = CAP_UNSURE of sv_byte_api.cu (uncertain-phase list)
 _CCAP = 1 << 20               # = CAP_MAG / CAP_PH (candidate buffers)
 MAX_TAGGED_RANKS = 8          # candidate set regions per CTA (sv_byte.cu CtaSets)
@@ -44,7 +46,8 @@ class SvbGateDesc(ctypes.Structure):
                 ("want_mag", ctypes.c_int32), ("want_ph", ctypes.c_int32),
                 ("mag_cut", ctypes.c_double), ("ph_cut", ctypes.c_double),
                 ("scan_only", ctypes.c_int32), ("rank_bits", ctypes.c_int32),
-                ("phys_base", ctypes.c_uint64), ("lbit", ctypes.c_int8 * 16)]
+                ("phys_base", ctypes.c_uint64), ("lbit", ctypes.c_int8 * 16),
+                ("ph_zero_in", ctypes.c_int32), ("ph_zero_out", ctypes.c_int32)]
 
 
 class ByteDeviceState:
@@ -66,6 +69,9 @@ class ByteDeviceState:
         self._tables_version = None
         self.version = 0
         self.launches = 0
+        # every phase index of both plane buffers is 0 (the phase table has held one entry
+        # whenever a pass wrote them): passes then neither read nor write the phase plane
+        self.ph_zero = False
 
     @property
     def size(self) -> int:
@@ -87,6 +93,7 @@ class ByteDeviceState:
     def zero(self, unit_index: int | None = 0) -> None:
         nat.check(nat.load().svb_zero_state(self.handle, -1 if unit_index is None else unit_index))
         self.version += 1
+        self.ph_zero = PHASE_PLANE_SKIP and len(self.codebook.thetas) == 1
 
     def export_storage(self, first: int, count: int):
         mi = np.empty(count, dtype=np.uint8)
@@ -101,6 +108,7 @@ class ByteDeviceState:
         nat.check(nat.load().svb_import(self.handle, mi.ctypes.data_as(ctypes.c_void_p),
                                         pi.ctypes.data_as(ctypes.c_void_p), first, mi.size))
         self.version += 1
+        self.ph_zero = False
 
     def decode(self, first: int = 0, count: int | None = None) -> np.ndarray:
         self.sync_tables()
@@ -203,6 +211,13 @@ class ByteDeviceState:
         """One pass; in_place (diagonal write pass with fixed tables): only the selected
         amplitudes of the current planes are rewritten, no commit follows."""
         fn = nat.load().svb_gate_in_place if in_place else nat.load().svb_gate
+        # all-zero phase planes: skip reading them, and writing them while the uploaded
+        # phase table (the one this pass encodes with) still has one entry
+        desc.ph_zero_in = 1 if self.ph_zero else 0
+        desc.ph_zero_out = 1 if (self.ph_zero and self._tables_version is not None
+                                 and self._tables_version[2] == 1) else 0
+        if self.ph_zero and not desc.ph_zero_out and not desc.scan_only:
+            self.ph_zero = False         # this pass writes real phase indices
         if getattr(self, "time_passes", False):
             e0, e1 = nat.Event(), nat.Event()
             e0.record(self.stream)

@@ -384,7 +384,10 @@ struct Emitter {
 
     __device__ __forceinline__ void emit(uint64_t idx, cplx v, ThreadCache& tc, int prod = 0) const {
         const unsigned c = code(idx, v, tc, nullptr, prod);
-        if (write) { mo[idx] = (uint8_t)(c & 255); po[idx] = (uint8_t)(c >> 8); }
+        if (write) {
+            mo[idx] = (uint8_t)(c & 255);
+            if (po) po[idx] = (uint8_t)(c >> 8);   // null: phase plane stays all zero (see svb_gate)
+        }
     }
 
     // (magnitude index | phase index << 8) of a produced value; candidate and
@@ -575,6 +578,12 @@ __device__ __noinline__ unsigned pair_slow(const STables& t, const Emitter& em, 
     return cc;
 }
 
+// phase plane access: a null plane is known all zero (svb_gate: a one-entry phase table
+// throughout the state's history) -- reads return zeros, writes are skipped
+__device__ __forceinline__ uint4 ld16z(const uint8_t* p, uint64_t off) {
+    return p ? *reinterpret_cast<const uint4*>(p + off) : make_uint4(0u, 0u, 0u, 0u);
+}
+
 // 1Q gate on a low qubit (qa < 4): both amplitudes of every pair lie in the same
 // 32-byte block of each plane, so a work item is one block (16 pairs) read and
 // written with 16-byte accesses -- the per-pair byte path issued 8 one-byte
@@ -593,7 +602,7 @@ __device__ __forceinline__ void byte_low_pairs(const uint8_t* __restrict__ mi_in
         const int prod = tagged ? producer_of(g, b) : 0;
         unsigned m[8], p[8], om[8], op[8];
         const uint4 m0 = *reinterpret_cast<const uint4*>(mi_in + b), m1 = *reinterpret_cast<const uint4*>(mi_in + b + 16);
-        const uint4 p0 = *reinterpret_cast<const uint4*>(pi_in + b), p1 = *reinterpret_cast<const uint4*>(pi_in + b + 16);
+        const uint4 p0 = ld16z(pi_in, b), p1 = ld16z(pi_in, b + 16);
         m[0] = m0.x; m[1] = m0.y; m[2] = m0.z; m[3] = m0.w; m[4] = m1.x; m[5] = m1.y; m[6] = m1.z; m[7] = m1.w;
         p[0] = p0.x; p[1] = p0.y; p[2] = p0.z; p[3] = p0.w; p[4] = p1.x; p[5] = p1.y; p[6] = p1.z; p[7] = p1.w;
         bool uni = m[0] == (m[0] & 255u) * 0x01010101u && p[0] == (p[0] & 255u) * 0x01010101u;
@@ -652,8 +661,10 @@ __device__ __forceinline__ void byte_low_pairs(const uint8_t* __restrict__ mi_in
         if (write) {
             *reinterpret_cast<uint4*>(mi_out + b) = make_uint4(om[0], om[1], om[2], om[3]);
             *reinterpret_cast<uint4*>(mi_out + b + 16) = make_uint4(om[4], om[5], om[6], om[7]);
-            *reinterpret_cast<uint4*>(pi_out + b) = make_uint4(op[0], op[1], op[2], op[3]);
-            *reinterpret_cast<uint4*>(pi_out + b + 16) = make_uint4(op[4], op[5], op[6], op[7]);
+            if (pi_out) {
+                *reinterpret_cast<uint4*>(pi_out + b) = make_uint4(op[0], op[1], op[2], op[3]);
+                *reinterpret_cast<uint4*>(pi_out + b + 16) = make_uint4(op[4], op[5], op[6], op[7]);
+            }
         }
     }
 }
@@ -704,9 +715,9 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
             auto fetch = [&](uint64_t w, uint4 (&b)[4]) {
                 const uint64_t i0 = insert0(w << 4, g.qa);
                 b[0] = *reinterpret_cast<const uint4*>(mi_in + i0);
-                b[1] = *reinterpret_cast<const uint4*>(pi_in + i0);
+                b[1] = ld16z(pi_in, i0);
                 b[2] = *reinterpret_cast<const uint4*>(mi_in + i0 + off);
-                b[3] = *reinterpret_cast<const uint4*>(pi_in + i0 + off);
+                b[3] = ld16z(pi_in, i0 + off);
             };
             uint64_t w = first;
             if (w < n_chunks) fetch(w, nxt);
@@ -745,9 +756,9 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                         const unsigned b0 = (cc & 255u) * 0x01010101u, b1 = ((cc >> 8) & 255u) * 0x01010101u;
                         const unsigned b2 = ((cc >> 16) & 255u) * 0x01010101u, b3 = (cc >> 24) * 0x01010101u;
                         *reinterpret_cast<uint4*>(mi_out + i0) = make_uint4(b0, b0, b0, b0);
-                        *reinterpret_cast<uint4*>(pi_out + i0) = make_uint4(b1, b1, b1, b1);
+                        if (pi_out) *reinterpret_cast<uint4*>(pi_out + i0) = make_uint4(b1, b1, b1, b1);
                         *reinterpret_cast<uint4*>(mi_out + i1) = make_uint4(b2, b2, b2, b2);
-                        *reinterpret_cast<uint4*>(pi_out + i1) = make_uint4(b3, b3, b3, b3);
+                        if (pi_out) *reinterpret_cast<uint4*>(pi_out + i1) = make_uint4(b3, b3, b3, b3);
                     }
                     continue;
                 }
@@ -782,9 +793,9 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                 }
                 if (write) {
                     *reinterpret_cast<uint4*>(mi_out + i0) = out[0];
-                    *reinterpret_cast<uint4*>(pi_out + i0) = out[1];
+                    if (pi_out) *reinterpret_cast<uint4*>(pi_out + i0) = out[1];
                     *reinterpret_cast<uint4*>(mi_out + i1) = out[2];
-                    *reinterpret_cast<uint4*>(pi_out + i1) = out[3];
+                    if (pi_out) *reinterpret_cast<uint4*>(pi_out + i1) = out[3];
                 }
             }
         } else
@@ -792,7 +803,7 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
             const uint64_t i0 = insert0(w, g.qa), i1 = i0 | (1ull << g.qa);
             if (g.producer >= 0 && producer_of(g, i0) != g.producer) continue;
             const int prod = tagged ? producer_of(g, i0) : 0;
-            const unsigned bm0 = mi_in[i0], bp0 = pi_in[i0], bm1 = mi_in[i1], bp1 = pi_in[i1];
+            const unsigned bm0 = mi_in[i0], bp0 = pi_in ? pi_in[i0] : 0u, bm1 = mi_in[i1], bp1 = pi_in ? pi_in[i1] : 0u;
             const unsigned key = bm0 | (bp0 << 8) | (bm1 << 16) | (bp1 << 24);
             unsigned cc;
             const int slot = memo_get(memo, key, &cc);
@@ -814,8 +825,9 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                 if (s0 && s1) mt.mark(memo_put(memo, key, cc), prod);
             }
             if (write) {
-                mi_out[i0] = (uint8_t)(cc & 255u); pi_out[i0] = (uint8_t)((cc >> 8) & 255u);
-                mi_out[i1] = (uint8_t)((cc >> 16) & 255u); pi_out[i1] = (uint8_t)(cc >> 24);
+                mi_out[i0] = (uint8_t)(cc & 255u);
+                mi_out[i1] = (uint8_t)((cc >> 16) & 255u);
+                if (pi_out) { pi_out[i0] = (uint8_t)((cc >> 8) & 255u); pi_out[i1] = (uint8_t)(cc >> 24); }
             }
         }
     } else if (g.kind == SV_OP_2Q) {
@@ -829,7 +841,7 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
             const int prod = tagged ? producer_of(g, e) : 0;
             const uint64_t idx[4] = {e, e | (1ull << g.qa), e | (1ull << g.qb), e | (1ull << g.qa) | (1ull << g.qb)};
             cplx a[4];
-            for (int c = 0; c < 4; ++c) a[c] = decode(t, mi_in[idx[c]], pi_in[idx[c]]);
+            for (int c = 0; c < 4; ++c) a[c] = decode(t, mi_in[idx[c]], pi_in ? pi_in[idx[c]] : 0u);
             cplx o[4];
             for (int r = 0; r < 4; ++r) o[r] = row4(&m[4 * r], a[0], a[1], a[2], a[3]);
             for (int r = 0; r < 4; ++r) em.emit(idx[r], o[r], tc, prod);
@@ -854,13 +866,17 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
             if (((i | 7ull) & g.mask) != g.mask) {           // no amplitude of the chunk is active
                 if (write) {
                     *reinterpret_cast<uint2*>(mi_out + i) = *reinterpret_cast<const uint2*>(mi_in + i);
-                    *reinterpret_cast<uint2*>(pi_out + i) = *reinterpret_cast<const uint2*>(pi_in + i);
+                    if (pi_out) *reinterpret_cast<uint2*>(pi_out + i) = pi_in ? *reinterpret_cast<const uint2*>(pi_in + i)
+                                                                             : make_uint2(0u, 0u);
                 }
                 continue;
             }
             uint8_t bm[8], bp[8];
             load8(mi_in + i, bm);
-            load8(pi_in + i, bp);
+            if (pi_in) load8(pi_in + i, bp);
+            else
+#pragma unroll
+                for (int j = 0; j < 8; ++j) bp[j] = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 if (((i + j) & g.mask) != g.mask) continue;
@@ -877,7 +893,7 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
             }
             if (write) {
                 store8(mi_out + i, bm);
-                store8(pi_out + i, bp);
+                if (pi_out) store8(pi_out + i, bp);
             }
         }
     } else {   // DIAG: masked amplitudes re-encoded, the rest copied
@@ -886,10 +902,10 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
             const int pr = (g.producer >= 0 || tagged) ? producer_of(g, i) : 0;
             if ((i & g.mask) == g.mask) {
                 if (g.producer >= 0 && pr != g.producer) continue;
-                em.emit(i, cmul(decode(t, mi_in[i], pi_in[i]), f), tc, tagged ? pr : 0);
+                em.emit(i, cmul(decode(t, mi_in[i], pi_in ? pi_in[i] : 0u), f), tc, tagged ? pr : 0);
             } else if (write && !g.in_place && (g.producer < 0 || pr == g.producer)) {
                 mi_out[i] = mi_in[i];
-                pi_out[i] = pi_in[i];
+                if (pi_out) pi_out[i] = pi_in ? pi_in[i] : 0u;
             }
         }
     }
@@ -977,7 +993,7 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
     if (w < n_chunks) {
         inx = chunk_at(w);
         nm = *reinterpret_cast<const uint4*>(mi_in + inx);
-        np = *reinterpret_cast<const uint4*>(pi_in + inx);
+        np = ld16z(pi_in, inx);
     }
     for (; w < n_chunks; w += step) {
         const uint64_t i = inx;
@@ -985,12 +1001,12 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
         if (w + step < n_chunks) {
             inx = chunk_at(w + step);
             nm = *reinterpret_cast<const uint4*>(mi_in + inx);
-            np = *reinterpret_cast<const uint4*>(pi_in + inx);
+            np = ld16z(pi_in, inx);
         }
         if (((i | 15ull) & g.mask) != g.mask) {   // out of place: untouched chunk copied
             if (write) {
                 *reinterpret_cast<uint4*>(mi_out + i) = cm;
-                *reinterpret_cast<uint4*>(pi_out + i) = cpv;
+                if (pi_out) *reinterpret_cast<uint4*>(pi_out + i) = cpv;
             }
             continue;
         }
@@ -1016,7 +1032,7 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
         }
         if (write) {
             *reinterpret_cast<uint4*>(mi_out + i) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
-            *reinterpret_cast<uint4*>(pi_out + i) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+            if (pi_out) *reinterpret_cast<uint4*>(pi_out + i) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
         }
     }
     if (collect) {

@@ -134,6 +134,7 @@ int svb_zero_state(sv_bhandle h, int64_t unit) {
     Guard gd(h->device);
     const uint64_t n = 1ull << h->n;
     for (int p = 0; p < 2; ++p) BTRY(cudaMemsetAsync(h->plane[h->cur][p], 0, n, h->stream), "zero planes");
+    BTRY(cudaMemsetAsync(h->plane[1 - h->cur][1], 0, n, h->stream), "zero pending phase plane");
     if (unit >= 0) {
         if ((uint64_t)unit >= n) return capi_fail(SV_EINDEX, "unit index outside the state");
         static const uint8_t one = 1;
@@ -183,8 +184,8 @@ int svb_gate(sv_bhandle h, const svb_gate_desc* d) {
         return capi_fail(SV_EVALUE, "bad two-qubit operands");
     const ByteGate g = to_gate(*d, n);
     const int c = h->cur, nx = 1 - h->cur;
-    cudaError_t e = launch_byte_gate(h->plane[c][0], h->plane[c][1], h->plane[nx][0], h->plane[nx][1], h->tab, g,
-                                     h->cand, h->stream);
+    cudaError_t e = launch_byte_gate(h->plane[c][0], d->ph_zero_in ? nullptr : h->plane[c][1], h->plane[nx][0],
+                                     d->ph_zero_out ? nullptr : h->plane[nx][1], h->tab, g, h->cand, h->stream);
     return e == cudaSuccess ? SV_OK : capi_cuda_fail(e, "BYTE gate launch");
 }
 
@@ -198,8 +199,8 @@ int svb_gate_in_place(sv_bhandle h, const svb_gate_desc* d) {
     ByteGate g = to_gate(*d, 1ull << h->n);
     g.in_place = 1;
     const int c = h->cur;
-    cudaError_t e = launch_byte_gate(h->plane[c][0], h->plane[c][1], h->plane[c][0], h->plane[c][1], h->tab, g,
-                                     h->cand, h->stream);
+    cudaError_t e = launch_byte_gate(h->plane[c][0], d->ph_zero_in ? nullptr : h->plane[c][1], h->plane[c][0],
+                                     d->ph_zero_out ? nullptr : h->plane[c][1], h->tab, g, h->cand, h->stream);
     return e == cudaSuccess ? SV_OK : capi_cuda_fail(e, "BYTE gate launch");
 }
 

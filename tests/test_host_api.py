@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_native.exported_symbols())
-    assert lib.sv_abi_version() == 2
+    assert lib.sv_abi_version() == 3
 
 
 def test_gate_constants_bit_exact(golden):
