@@ -265,6 +265,10 @@ int svt_synchronize(sv_thandle h);
  * slot memsets (never-written chunks), kernel passes, HBM bytes of the fast tier */
 int svt_stats(sv_thandle h, uint64_t* out8);
 
+/* FP32-storage rounding check: host values rounded on the device to float precision by
+ * the Veltkamp split of the specialised passes (mode 1) or by F2F (mode 0), as doubles */
+int svk_f32_round(const double* host_in, double* host_out, uint64_t n, int mode);
+
 /* ---- raw device buffers (for the array-level operator API) --------- */
 int sv_buffer_alloc(int device, uint64_t bytes, void** ptr);
 int sv_buffer_free(int device, void* ptr);

@@ -132,6 +132,7 @@ _SIGNATURES = {
     "sv_event_record": ([_P, _P], _I),
     "sv_event_elapsed_ms": ([_P, _P, ctypes.POINTER(ctypes.c_float)], _I),
     "sv_stream_synchronize": ([_P], _I),
+    "svk_f32_round": ([_D, _D, _U64, _I], _I),
     "svt_create": ([_I, _I, _I, _I, _P, _I, ctypes.POINTER(_P)], _I),
     "svt_destroy": ([_P], _I),
     "svt_zero_state": ([_P, ctypes.c_int64], _I),

@@ -30,17 +30,50 @@ struct __align__(8) c32s { float re, im; };
 // F2F there and back (exact widening).  F2F runs at ~16/clk/SM on B200
 // (tools/f2f_probe.cu: 2.2 T FP64->FP32->FP64 round trips/s), the cost floor of FP32
 // passes with many gates.
-__device__ __forceinline__ double r32(double x) { return (double)__double2float_rn(x); }
+// SVJ_F32_ROUND (set by the generated source): 0 = F2F there and back for every value,
+// 1 = Veltkamp split on the FP64 pipe for every value, 2 = real parts Veltkamp, imaginary
+// parts F2F (both pipes busy).  Veltkamp with C = 2^29 + 1 in round-to-nearest-even
+// FP64: g = C x, hi = g + (x - g) is x rounded to 24 significant bits, ties to even --
+// identical to the float rounding for 2^-126 <= |x| < 2^127 (tests/test_fp32_round.py:
+// every tie / carry / exponent-edge pattern, random values; tools/f32_round_check.cu on
+// the device).  Outside that range (float subnormals, overflow, NaN / Inf, double
+// subnormals) the F2F path runs; +-0 is returned as is (the split would drop the sign).
+#ifndef SVJ_F32_ROUND
+#define SVJ_F32_ROUND 0
+#endif
+__device__ __forceinline__ double r32_f2f(double x) { return (double)__double2float_rn(x); }
+__device__ __forceinline__ double r32_split(double x) {
+    const double g = __dmul_rn(536870913.0, x);             // 2^29 + 1
+    const double v = __dadd_rn(g, __dadd_rn(x, -g));
+    const unsigned e = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
+    if (e - 897u < 253u) return v;                          // 2^-126 <= |x| < 2^127
+    if (x == 0.0) return x;
+    return r32_f2f(x);
+}
+__device__ __forceinline__ double r32(double x) {
+#if SVJ_F32_ROUND == 1
+    return r32_split(x);
+#else
+    return r32_f2f(x);
+#endif
+}
+__device__ __forceinline__ double r32_re(double x) {
+#if SVJ_F32_ROUND >= 1
+    return r32_split(x);
+#else
+    return r32_f2f(x);
+#endif
+}
 template <int R>
 __device__ __forceinline__ void rnd_all(cplx (&r)[R]) {
 #pragma unroll
-    for (int i = 0; i < R; ++i) r[i] = {r32(r[i].re), r32(r[i].im)};
+    for (int i = 0; i < R; ++i) r[i] = {r32_re(r[i].re), r32(r[i].im)};
 }
 template <int R, unsigned MR>
 __device__ __forceinline__ void rnd_mask(cplx (&r)[R]) {
 #pragma unroll
     for (int i = 0; i < R; ++i)
-        if ((i & MR) == MR) r[i] = {r32(r[i].re), r32(r[i].im)};
+        if ((i & MR) == MR) r[i] = {r32_re(r[i].re), r32(r[i].im)};
 }
 
 // shared-memory swizzle of k_fused3 (linear in the element index)
