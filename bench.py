@@ -241,6 +241,62 @@ def cpu_baseline(steps: int, n_layers: int, sample_n: int = CPU_SAMPLE_N):
                       f"{threads} threads"}
 
 
+def fp64_ops_per_amplitude(op) -> float:
+    """FP64 instructions per amplitude of one gate in the numpy-exact arithmetic of the
+    passes (sv_arith.cuh / sv_jit_dev.cuh): generic 1Q 10 (4 DMUL + 4 DFMA + 2 DADD), real
+    1Q 6, monomial 0, generic 2Q 22, real 2Q 14, diagonal 4 on the selected 2^-k, Z 0."""
+    import numpy as np
+    from paper_2511_03359_b200 import _native as nat
+    m = np.array(op.m[:32])
+    if op.kind == nat.SV_OP_1Q:
+        mm = m[:8]
+        if np.count_nonzero(mm) == 2 and all(np.count_nonzero(mm.reshape(4, 2), axis=1) <= 1):
+            return 0.0
+        return 6.0 if not np.any(mm[1::2]) else 10.0
+    if op.kind == nat.SV_OP_2Q:
+        if np.count_nonzero(m) == 4:
+            return 0.0
+        return 14.0 if not np.any(m[1::2]) else 22.0
+    if op.m[0] == -1.0 and op.m[1] == 0.0:
+        return 0.0
+    return 4.0 / (1 << bin(op.diag_mask).count("1"))
+
+
+def fp64_aware_roofline(n: int, seq, tile_bits: int, pass_ms: float, hbm_peak: float, sm_mhz: float) -> dict:
+    """Per launch the fused pass has two floors: its HBM bytes at the copy peak and its
+    FP64 instructions at 64 lanes/clk/SM x 148 SMs x the SM clock measured under load.
+    Returns the sum of max(floors) over the timed launches (the library's own pass
+    split) against their measured time."""
+    import ctypes
+    from paper_2511_03359_b200 import _native as nat
+    from paper_2511_03359_b200.device import ops_array
+    lib = nat.load()
+    sms = ctypes.c_int(0)
+    lib.sv_sm_count(0, ctypes.byref(sms))
+    fp64_peak = 64.0 * sms.value * sm_mhz * 1e6
+    hbm_ms = 2 * 16 * 2 ** n / (hbm_peak * 1e9) * 1e3
+    floor = f64_total = hbm_total = 0.0
+    n_pass = 0
+    for ops in seq:
+        ends = (ctypes.c_int * 4096)()
+        k = lib.sv_plan_passes(n, nat.SV_FP64, ops_array(ops), len(ops), tile_bits, ends, 4096)
+        a = 0
+        for i in range(k):
+            f = sum(fp64_ops_per_amplitude(o) for o in ops[a:ends[i]]) * 2 ** n / fp64_peak * 1e3
+            a = ends[i]
+            floor += max(hbm_ms, f)
+            f64_total += f
+            hbm_total += hbm_ms
+            n_pass += 1
+    return {"fp64_peak_Tops": round(fp64_peak / 1e12, 2), "passes": n_pass,
+            "hbm_floor_ms": round(hbm_total, 1), "fp64_floor_ms": round(f64_total, 1),
+            "max_floor_ms": round(floor, 1), "measured_ms": round(pass_ms, 1),
+            "frac": round(floor / pass_ms, 4) if pass_ms else None,
+            "what": "sum over the timed launches of max(HBM bytes / copy peak, FP64 instructions / "
+                    "(64 x SMs x measured SM clock)) vs their event-timed sum: passes carrying many "
+                    "generic U2/U4 gates are FP64-bound, not HBM-bound"}
+
+
 def fused_parity(n_small: int, device: int, tile_bits: int) -> dict:
     """One C2 layer at n_small through fused passes vs one kernel per gate (fuse=False), bit
     for bit, and at N=18 against the CPU oracle (test infrastructure, outside the timed
@@ -668,7 +724,9 @@ def run_b200(args):
                                     10: "<13,4,1> single buffer (specialised only)"}[args.fused] + (
                              " as sv_pass (NVRTC-specialised per pass structure)" if jit["jit_launches"] else ""),
                          "launches_timed": passes,
-                         "bytes_per_launch": 2 * 16 * 2 ** n},
+                         "bytes_per_launch": 2 * 16 * 2 ** n,
+                         "fp64_aware": fp64_aware_roofline(n, timed_seq, args.tile_bits, pass_ms, peak,
+                                                           clocks.get("sm_mhz") or 1965.0)},
             "gpu_launches": launches,
             "fused_passes_per_step": round(passes / args.steps, 2),
             "jit": dict(jit, prepare_seconds=round(t_jit, 2)),
@@ -1058,7 +1116,7 @@ def main():
     ap.add_argument("--byte-n-multi", type=int, default=35,
                     help="BYTE benchmark amplitudes per GPU (2^n) for N>1 lines: N = n + log2(P), "
                          "38 qubits on 8 GPUs = BASELINE config 5 (0: skip)")
-    ap.add_argument("--single-gate", action="store_true", default=True)
+    ap.add_argument("--single-gate", type=int, default=1)
     ap.add_argument("--overlap", type=int, default=1,
                     help="N>1: overlap each remap swap with the first pass after it (chunked, IPC events)")
     ap.add_argument("--byte-adder", type=int, default=1,

@@ -266,7 +266,8 @@ int svt_synchronize(sv_thandle h);
 int svt_stats(sv_thandle h, uint64_t* out8);
 
 /* FP32-storage rounding check: host values rounded on the device to float precision by
- * the Veltkamp split of the specialised passes (mode 1) or by F2F (mode 0), as doubles */
+ * the specialised passes' methods -- F2F (mode 0), Veltkamp split on the FP64 pipe (1),
+ * integer add-and-mask of the double's bits (2) -- returned as doubles */
 int svk_f32_round(const double* host_in, double* host_out, uint64_t n, int mode);
 
 /* ---- raw device buffers (for the array-level operator API) --------- */

@@ -595,30 +595,29 @@ __device__ __forceinline__ void byte_low_pairs(const uint8_t* __restrict__ mi_in
                                                ThreadCache& tc, unsigned long long* memo, const MemoTags& mt,
                                                bool real, bool tagged, bool write, uint64_t first, uint64_t step) {
     const uint64_t n_blocks = g.n_elems >> 5;
-    // blocks are taken KB at a time with every load of the batch issued first (latency)
-    constexpr int KB = 2;
-    for (uint64_t w0 = first; w0 < n_blocks; w0 += KB * step) {
-    uint4 bm0[KB], bm1[KB], bp0[KB], bp1[KB];
-#pragma unroll
-    for (int kb = 0; kb < KB; ++kb) {
-        const uint64_t b = (w0 + kb * step) << 5;
-        if (w0 + kb * step >= n_blocks) break;
-        bm0[kb] = *reinterpret_cast<const uint4*>(mi_in + b);
-        bm1[kb] = *reinterpret_cast<const uint4*>(mi_in + b + 16);
-        bp0[kb] = ld16z(pi_in, b);
-        bp1[kb] = ld16z(pi_in, b + 16);
+    // the next block's bytes are loaded before the current one is computed (latency)
+    uint4 nm0 = {0, 0, 0, 0}, nm1 = nm0, np0 = nm0, np1 = nm0;
+    if (first < n_blocks) {
+        const uint64_t b = first << 5;
+        nm0 = *reinterpret_cast<const uint4*>(mi_in + b);
+        nm1 = *reinterpret_cast<const uint4*>(mi_in + b + 16);
+        np0 = ld16z(pi_in, b);
+        np1 = ld16z(pi_in, b + 16);
     }
-#pragma unroll
-    for (int kb = 0; kb < KB; ++kb) {
-        const uint64_t w = w0 + kb * step;
-        if (w >= n_blocks) break;
+    for (uint64_t w = first; w < n_blocks; w += step) {
         const uint64_t b = w << 5;
+        const uint4 m0 = nm0, m1 = nm1, p0 = np0, p1 = np1;
+        if (w + step < n_blocks) {
+            const uint64_t bn = (w + step) << 5;
+            nm0 = *reinterpret_cast<const uint4*>(mi_in + bn);
+            nm1 = *reinterpret_cast<const uint4*>(mi_in + bn + 16);
+            np0 = ld16z(pi_in, bn);
+            np1 = ld16z(pi_in, bn + 16);
+        }
         // all 32 amplitudes of a block share their producer (the caller checked the bits)
         if (g.producer >= 0 && producer_of(g, b) != g.producer) continue;
         const int prod = tagged ? producer_of(g, b) : 0;
         unsigned m[8], p[8], om[8], op[8];
-        const uint4 m0 = bm0[kb], m1 = bm1[kb];
-        const uint4 p0 = bp0[kb], p1 = bp1[kb];
         m[0] = m0.x; m[1] = m0.y; m[2] = m0.z; m[3] = m0.w; m[4] = m1.x; m[5] = m1.y; m[6] = m1.z; m[7] = m1.w;
         p[0] = p0.x; p[1] = p0.y; p[2] = p0.z; p[3] = p0.w; p[4] = p1.x; p[5] = p1.y; p[6] = p1.z; p[7] = p1.w;
         bool uni = m[0] == (m[0] & 255u) * 0x01010101u && p[0] == (p[0] & 255u) * 0x01010101u;
@@ -683,7 +682,6 @@ __device__ __forceinline__ void byte_low_pairs(const uint8_t* __restrict__ mi_in
             }
         }
     }
-    }
 }
 
 // One BYTE gate pass.  Work items: pairs (1Q), quadruples (2Q) or single
@@ -724,13 +722,11 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
         const bool real = g.m[1] == 0.0 && g.m[3] == 0.0 && g.m[5] == 0.0 && g.m[7] == 0.0;
         const uint64_t n_items = g.n_elems >> 1;
         if (g.qa >= 4 && g.n_elems >= 32 && lmin >= 4) {
-            // 16 consecutive pairs per work item (16-byte loads/stores of every plane).  Items
-            // are taken KB at a time, every load of the batch issued before the first item is
-            // computed: KB x 64 bytes in flight per thread (one item ahead left the scan and
-            // write passes latency-bound at ~2 TB/s)
-            constexpr int KB = 2;
+            // 16 consecutive pairs per work item (16-byte loads/stores of every plane); the next
+            // item's bytes are loaded before the current one is computed (latency hiding)
             const uint64_t n_chunks = n_items >> 4;
             const uint64_t off = 1ull << g.qa;
+            uint4 nxt[4];
             auto fetch = [&](uint64_t w, uint4 (&b)[4]) {
                 const uint64_t i0 = insert0(w << 4, g.qa);
                 b[0] = *reinterpret_cast<const uint4*>(mi_in + i0);
@@ -738,58 +734,65 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                 b[2] = *reinterpret_cast<const uint4*>(mi_in + i0 + off);
                 b[3] = ld16z(pi_in, i0 + off);
             };
-            auto byte_of = [](const uint4& v, int j) -> unsigned {
-                const unsigned w = j < 4 ? v.x : (j < 8 ? v.y : (j < 12 ? v.z : v.w));
-                return (w >> (8 * (j & 3))) & 255u;
-            };
-            auto put_byte = [](uint4& v, int j, unsigned b) {
-                const unsigned sh = 8 * (j & 3);
-                if (j < 4) v.x |= b << sh; else if (j < 8) v.y |= b << sh;
-                else if (j < 12) v.z |= b << sh; else v.w |= b << sh;
-            };
-            // uniform run: all 16 pairs carry the same code tuple (structured states, e.g. the
-            // Hadamard benchmark) -> one lookup, replicated output bytes
-            auto uniform = [](const uint4& v) {
-                return v.x == v.y && v.x == v.z && v.x == v.w && v.x == (v.x & 255u) * 0x01010101u;
-            };
-            auto process = [&](uint64_t w, const uint4 (&cur)[4]) {
+            uint64_t w = first;
+            if (w < n_chunks) fetch(w, nxt);
+            for (; w < n_chunks; w += step) {
+                uint4 cur[4] = {nxt[0], nxt[1], nxt[2], nxt[3]};
+                if (w + step < n_chunks) fetch(w + step, nxt);
                 const uint64_t i0 = insert0(w << 4, g.qa), i1 = i0 + off;
-                if (g.producer >= 0 && producer_of(g, i0) != g.producer) return;
+                if (g.producer >= 0 && producer_of(g, i0) != g.producer) continue;
                 const int prod = tagged ? producer_of(g, i0) : 0;
+                uint4 out[4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
+                auto byte_of = [](const uint4& v, int j) -> unsigned {
+                    const unsigned w = j < 4 ? v.x : (j < 8 ? v.y : (j < 12 ? v.z : v.w));
+                    return (w >> (8 * (j & 3))) & 255u;
+                };
+                auto put_byte = [](uint4& v, int j, unsigned b) {
+                    const unsigned sh = 8 * (j & 3);
+                    if (j < 4) v.x |= b << sh; else if (j < 8) v.y |= b << sh;
+                    else if (j < 12) v.z |= b << sh; else v.w |= b << sh;
+                };
+                // uniform run: all 16 pairs carry the same code tuple (structured states, e.g. the
+                // Hadamard benchmark) -> one lookup, replicated output bytes
+                auto uniform = [](const uint4& v) {
+                    return v.x == v.y && v.x == v.z && v.x == v.w && v.x == (v.x & 255u) * 0x01010101u;
+                };
                 if (uniform(cur[0]) && uniform(cur[1]) && uniform(cur[2]) && uniform(cur[3])) {
                     const unsigned key = (cur[0].x & 255u) | ((cur[1].x & 255u) << 8) | ((cur[2].x & 255u) << 16) |
                                          ((cur[3].x & 255u) << 24);
                     unsigned cc;
                     const int slot = memo_get(memo, key, &cc);
-                    bool ok = true;
                     if (slot < 0 || mt.fresh(slot, prod)) {
                         cc = pair_slow(t, em, tc, memo, mt, key, i0, i1, g.m, real, prod);
                         // uncertain amplitudes are reported per index: take the per-pair path
-                        ok = memo_get(memo, key, &cc) >= 0;
+                        if (memo_get(memo, key, &cc) < 0) goto per_pair;
                     }
-                    if (ok) {
-                        if (write) {
-                            const unsigned b0 = (cc & 255u) * 0x01010101u, b1 = ((cc >> 8) & 255u) * 0x01010101u;
-                            const unsigned b2 = ((cc >> 16) & 255u) * 0x01010101u, b3 = (cc >> 24) * 0x01010101u;
-                            *reinterpret_cast<uint4*>(mi_out + i0) = make_uint4(b0, b0, b0, b0);
-                            if (pi_out) *reinterpret_cast<uint4*>(pi_out + i0) = make_uint4(b1, b1, b1, b1);
-                            *reinterpret_cast<uint4*>(mi_out + i1) = make_uint4(b2, b2, b2, b2);
-                            if (pi_out) *reinterpret_cast<uint4*>(pi_out + i1) = make_uint4(b3, b3, b3, b3);
-                        }
-                        return;
+                    if (write) {
+                        const unsigned b0 = (cc & 255u) * 0x01010101u, b1 = ((cc >> 8) & 255u) * 0x01010101u;
+                        const unsigned b2 = ((cc >> 16) & 255u) * 0x01010101u, b3 = (cc >> 24) * 0x01010101u;
+                        *reinterpret_cast<uint4*>(mi_out + i0) = make_uint4(b0, b0, b0, b0);
+                        if (pi_out) *reinterpret_cast<uint4*>(pi_out + i0) = make_uint4(b1, b1, b1, b1);
+                        *reinterpret_cast<uint4*>(mi_out + i1) = make_uint4(b2, b2, b2, b2);
+                        if (pi_out) *reinterpret_cast<uint4*>(pi_out + i1) = make_uint4(b3, b3, b3, b3);
                     }
+                    continue;
                 }
+            per_pair:
                 // runs of equal tuples (sparse / structured states) reuse the previous memo
                 // hit; a pair computed by pair_slow is looked up again (its outputs may be
                 // uncertain, reported per index)
-                uint4 out[4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
                 bool hit_prev = false;
                 unsigned key_prev = 0u, cc_prev = 0u;
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     // key = (m0, p0, m1, p1) bytes of pair j; j is a literal after unrolling
-                    const unsigned key = byte_of(cur[0], j) | (byte_of(cur[1], j) << 8) | (byte_of(cur[2], j) << 16) |
-                                         (byte_of(cur[3], j) << 24);
+                    const unsigned sh = 8 * (j & 3);
+                    const unsigned w0 = j < 4 ? cur[0].x : (j < 8 ? cur[0].y : (j < 12 ? cur[0].z : cur[0].w));
+                    const unsigned w1 = j < 4 ? cur[1].x : (j < 8 ? cur[1].y : (j < 12 ? cur[1].z : cur[1].w));
+                    const unsigned w2 = j < 4 ? cur[2].x : (j < 8 ? cur[2].y : (j < 12 ? cur[2].z : cur[2].w));
+                    const unsigned w3 = j < 4 ? cur[3].x : (j < 8 ? cur[3].y : (j < 12 ? cur[3].z : cur[3].w));
+                    const unsigned key = ((w0 >> sh) & 255u) | (((w1 >> sh) & 255u) << 8) |
+                                         (((w2 >> sh) & 255u) << 16) | (((w3 >> sh) & 255u) << 24);
                     unsigned cc;
                     if (hit_prev && key == key_prev) {
                         cc = cc_prev;   // what the memo returns for it (entries are never evicted)
@@ -809,15 +812,6 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                     *reinterpret_cast<uint4*>(mi_out + i1) = out[2];
                     if (pi_out) *reinterpret_cast<uint4*>(pi_out + i1) = out[3];
                 }
-            };
-            for (uint64_t w = first; w < n_chunks; w += KB * step) {
-                uint4 cur[KB][4];
-#pragma unroll
-                for (int k = 0; k < KB; ++k)
-                    if (w + k * step < n_chunks) fetch(w + k * step, cur[k]);
-#pragma unroll
-                for (int k = 0; k < KB; ++k)
-                    if (w + k * step < n_chunks) process(w + k * step, cur[k]);
             }
         } else
         for (uint64_t w = first; w < n_items; w += step) {
@@ -1009,24 +1003,21 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
         }
         return c << 4;
     };
-    // chunks taken KB at a time, every load of the batch issued before the first chunk is
-    // processed (one chunk ahead left these passes latency-bound)
-    constexpr int KB = 2;
-    for (uint64_t w0 = first; w0 < n_chunks; w0 += KB * step) {
-        uint64_t ix[KB];
-        uint4 cmv[KB], cpw[KB];
-#pragma unroll
-        for (int kb = 0; kb < KB; ++kb) {
-            if (w0 + kb * step >= n_chunks) break;
-            ix[kb] = chunk_at(w0 + kb * step);
-            cmv[kb] = *reinterpret_cast<const uint4*>(mi_in + ix[kb]);
-            cpw[kb] = ld16z(pi_in, ix[kb]);
+    uint64_t w = first, inx = 0;
+    uint4 nm = {0, 0, 0, 0}, np = {0, 0, 0, 0};
+    if (w < n_chunks) {
+        inx = chunk_at(w);
+        nm = *reinterpret_cast<const uint4*>(mi_in + inx);
+        np = ld16z(pi_in, inx);
+    }
+    for (; w < n_chunks; w += step) {
+        const uint64_t i = inx;
+        const uint4 cm = nm, cpv = np;
+        if (w + step < n_chunks) {
+            inx = chunk_at(w + step);
+            nm = *reinterpret_cast<const uint4*>(mi_in + inx);
+            np = ld16z(pi_in, inx);
         }
-#pragma unroll
-        for (int kb = 0; kb < KB; ++kb) {
-        if (w0 + kb * step >= n_chunks) break;
-        const uint64_t i = ix[kb];
-        const uint4 cm = cmv[kb], cpv = cpw[kb];
         if (((i | 15ull) & g.mask) != g.mask) {   // out of place: untouched chunk copied
             if (write) {
                 *reinterpret_cast<uint4*>(mi_out + i) = cm;
@@ -1057,7 +1048,6 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
         if (write) {
             *reinterpret_cast<uint4*>(mi_out + i) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
             if (pi_out) *reinterpret_cast<uint4*>(pi_out + i) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
-        }
         }
     }
     if (collect) {

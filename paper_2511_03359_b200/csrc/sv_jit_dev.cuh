@@ -50,16 +50,31 @@ __device__ __forceinline__ double r32_split(double x) {
     if (x == 0.0) return x;
     return r32_f2f(x);
 }
+// integer pipe: add half an ulp of the float mantissa (ties to even) to the double's bits
+// and clear the 29 dropped bits -- the same rounding, no FP64 or conversion instruction
+__device__ __forceinline__ double r32_int(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    const unsigned e = (unsigned)(b >> 52) & 0x7ffu;
+    if (e - 897u < 253u)
+        return __longlong_as_double((long long)((b + 0x0FFFFFFFull + ((b >> 29) & 1ull)) & ~0x1FFFFFFFull));
+    if ((b << 1) == 0ull) return x;
+    return r32_f2f(x);
+}
+// SVJ_F32_ROUND: 0 F2F, 1 split, 2 re split / im F2F, 3 re integer / im F2F, 4 integer
 __device__ __forceinline__ double r32(double x) {
 #if SVJ_F32_ROUND == 1
     return r32_split(x);
+#elif SVJ_F32_ROUND == 4
+    return r32_int(x);
 #else
     return r32_f2f(x);
 #endif
 }
 __device__ __forceinline__ double r32_re(double x) {
-#if SVJ_F32_ROUND >= 1
+#if SVJ_F32_ROUND == 1 || SVJ_F32_ROUND == 2
     return r32_split(x);
+#elif SVJ_F32_ROUND == 3 || SVJ_F32_ROUND == 4
+    return r32_int(x);
 #else
     return r32_f2f(x);
 #endif

@@ -14,13 +14,13 @@ int capi_cuda_fail(cudaError_t e, const char* what);
 namespace {
 __global__ void k_f32_round(const double* in, double* out, uint64_t n, int mode) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        out[i] = mode == 1 ? svj::r32_split(in[i]) : svj::r32_f2f(in[i]);
+        out[i] = mode == 1 ? svj::r32_split(in[i]) : (mode == 2 ? svj::r32_int(in[i]) : svj::r32_f2f(in[i]));
 }
 }  // namespace
 }  // namespace sv
 
 extern "C" int svk_f32_round(const double* host_in, double* host_out, uint64_t n, int mode) {
-    if (mode != 0 && mode != 1) return sv::capi_fail(SV_EVALUE, "rounding mode must be 0 (F2F) or 1 (split)");
+    if (mode < 0 || mode > 2) return sv::capi_fail(SV_EVALUE, "rounding mode must be 0 (F2F), 1 (split) or 2 (integer)");
     if (n == 0) return SV_OK;
     double *d_in = nullptr, *d_out = nullptr;
     cudaError_t e = cudaMalloc(&d_in, 8 * n);

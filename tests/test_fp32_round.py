@@ -49,6 +49,17 @@ def split_numpy(x: np.ndarray) -> np.ndarray:
     return np.where(fast, v, np.where(x == 0.0, x, conv))
 
 
+def int_numpy(x: np.ndarray) -> np.ndarray:
+    """r32_int restated: add half a float ulp (ties to even) to the bits, clear 29 bits."""
+    b = x.view(np.uint64)
+    e = (b >> np.uint64(52)) & np.uint64(0x7FF)
+    r = ((b + np.uint64(0x0FFFFFFF) + ((b >> np.uint64(29)) & np.uint64(1))) & ~np.uint64(0x1FFFFFFF)).view(np.float64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        conv = x.astype(np.float32).astype(np.float64)
+    fast = (e >= 897) & (e <= 1149)
+    return np.where(fast, r, np.where(x == 0.0, x, conv))
+
+
 def _same(a, b):
     return np.array_equal(a.view(np.uint64), b.view(np.uint64)) or np.array_equal(a, b, equal_nan=True)
 
@@ -57,9 +68,9 @@ def test_split_equals_float_rounding_cpu():
     for x in (edge_patterns(), random_values(2_000_000)):
         with np.errstate(over="ignore"):
             want = x.astype(np.float32).astype(np.float64)
-        got = split_numpy(x)
-        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), \
-            np.nonzero(got.view(np.uint64) != want.view(np.uint64))[0][:5]
+        for got in (split_numpy(x), int_numpy(x)):
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), \
+                np.nonzero(got.view(np.uint64) != want.view(np.uint64))[0][:5]
 
 
 @pytest.mark.gpu
@@ -70,7 +81,7 @@ def test_split_equals_float_rounding_on_device():
         x = np.ascontiguousarray(x)
         with np.errstate(over="ignore"):
             want = x.astype(np.float32).astype(np.float64)
-        for mode in (0, 1):
+        for mode in (0, 1, 2):
             out = np.empty_like(x)
             nat.check(lib.svk_f32_round(nat.dptr(x), nat.dptr(out), x.size, mode))
             # NaN payloads are not compared (the GPU returns its canonical NaN)
