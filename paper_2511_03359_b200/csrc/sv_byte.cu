@@ -583,6 +583,14 @@ __device__ __noinline__ unsigned pair_slow(const STables& t, const Emitter& em, 
 __device__ __forceinline__ uint4 ld16z(const uint8_t* p, uint64_t off) {
     return p ? *reinterpret_cast<const uint4*>(p + off) : make_uint4(0u, 0u, 0u, 0u);
 }
+// L2 prefetch of a work item several grid strides ahead: the passes hold one item per
+// thread in registers (one ahead), too few bytes in flight to cover the HBM latency on
+// their own (scan passes read 32 bytes per item); the prefetched lines turn the
+// register loads into L2 hits.  No registers, no shared memory.
+constexpr int kL2Ahead = 4;
+__device__ __forceinline__ void l2_prefetch(const uint8_t* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 // 1Q gate on a low qubit (qa < 4): both amplitudes of every pair lie in the same
 // 32-byte block of each plane, so a work item is one block (16 pairs) read and
@@ -607,6 +615,11 @@ __device__ __forceinline__ void byte_low_pairs(const uint8_t* __restrict__ mi_in
     for (uint64_t w = first; w < n_blocks; w += step) {
         const uint64_t b = w << 5;
         const uint4 m0 = nm0, m1 = nm1, p0 = np0, p1 = np1;
+        if (w + kL2Ahead * step < n_blocks) {
+            const uint64_t bp = (w + kL2Ahead * step) << 5;
+            l2_prefetch(mi_in + bp);
+            if (pi_in) l2_prefetch(pi_in + bp);
+        }
         if (w + step < n_blocks) {
             const uint64_t bn = (w + step) << 5;
             nm0 = *reinterpret_cast<const uint4*>(mi_in + bn);
@@ -739,6 +752,12 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
             for (; w < n_chunks; w += step) {
                 uint4 cur[4] = {nxt[0], nxt[1], nxt[2], nxt[3]};
                 if (w + step < n_chunks) fetch(w + step, nxt);
+                if (w + kL2Ahead * step < n_chunks) {
+                    const uint64_t ip = insert0((w + kL2Ahead * step) << 4, g.qa);
+                    l2_prefetch(mi_in + ip);
+                    l2_prefetch(mi_in + ip + off);
+                    if (pi_in) { l2_prefetch(pi_in + ip); l2_prefetch(pi_in + ip + off); }
+                }
                 const uint64_t i0 = insert0(w << 4, g.qa), i1 = i0 + off;
                 if (g.producer >= 0 && producer_of(g, i0) != g.producer) continue;
                 const int prod = tagged ? producer_of(g, i0) : 0;
@@ -1017,6 +1036,11 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
             inx = chunk_at(w + step);
             nm = *reinterpret_cast<const uint4*>(mi_in + inx);
             np = ld16z(pi_in, inx);
+        }
+        if (w + kL2Ahead * step < n_chunks) {
+            const uint64_t ipf = chunk_at(w + kL2Ahead * step);
+            l2_prefetch(mi_in + ipf);
+            if (pi_in) l2_prefetch(pi_in + ipf);
         }
         if (((i | 15ull) & g.mask) != g.mask) {   // out of place: untouched chunk copied
             if (write) {
