@@ -1037,11 +1037,7 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
             nm = *reinterpret_cast<const uint4*>(mi_in + inx);
             np = ld16z(pi_in, inx);
         }
-        if (w + kL2Ahead * step < n_chunks) {
-            const uint64_t ipf = chunk_at(w + kL2Ahead * step);
-            l2_prefetch(mi_in + ipf);
-            if (pi_in) l2_prefetch(pi_in + ipf);
-        }
+
         if (((i | 15ull) & g.mask) != g.mask) {   // out of place: untouched chunk copied
             if (write) {
                 *reinterpret_cast<uint4*>(mi_out + i) = cm;
