@@ -279,8 +279,23 @@ int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Pa
     int regbit_of[kMaxSegs][13];
     for (int sgi = 0; sgi < P.n_segs; ++sgi) {
         uint32_t set = seg_sets[sgi];
-        for (int pos = K - 1; pos >= 0 && __builtin_popcount(set) < RB; --pos)   // fill from the top
-            if (!((set >> pos) & 1)) set |= 1u << pos;
+        // free register slots take the tile positions the segment's diagonal masks use most:
+        // a diagonal op on register bits multiplies an exact subset of the registers, on a
+        // lane bit it runs on every register with part of the warp masked off (the adder's
+        // CPHASE passes).  Ties (and segments without diagonal ops): from the top, as before.
+        int use[16] = {0};
+        for (int i = (sgi ? seg_end[sgi - 1] : 0); i < seg_end[sgi]; ++i) {
+            const sv_op& o = ops[pp.ops[i]];
+            if (o.kind == SV_OP_1Q || o.kind == SV_OP_2Q) continue;
+            for (int q = 0; q < n; ++q)
+                if (((o.diag_mask >> q) & 1) && pos_of[q] >= 0) ++use[pos_of[q]];
+        }
+        while (__builtin_popcount(set) < RB) {
+            int best = -1;
+            for (int pos = K - 1; pos >= 0; --pos)
+                if (!((set >> pos) & 1) && (best < 0 || use[pos] > use[best])) best = pos;
+            set |= 1u << best;
+        }
         int r = 0, t = 0;
         for (int pos = 0; pos < K; ++pos) {
             regbit_of[sgi][pos] = -1;
