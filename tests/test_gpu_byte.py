@@ -150,3 +150,34 @@ def test_numerics_fingerprint_on_the_box_host(golden):
     r, th, ux, uy = pb.codec.canonicalize(v)
     for got, key in ((r, "canon_r"), (th, "canon_th"), (ux, "canon_ux"), (uy, "canon_uy")):
         assert np.array_equal(np.asarray(got).view(np.uint64), c[key].view(np.uint64)), key
+
+
+def test_phase_candidate_grouping_with_clustered_angles():
+    """The device keeps one phase candidate per distinct GPU theta (sv_byte.cu CtaSets);
+    the reference proposes per distinct numpy theta (codec.py:137-152).  Values whose
+    angles differ by a few ulps -- where CUDA and numpy atan2 may round apart -- must
+    still give the reference's proposals and encodings: clusters of 1-3 ulp angle steps
+    around 200 angles (including the axes and 2 pi wrap), several magnitudes each."""
+    rng = np.random.default_rng(77)
+    base = np.concatenate([rng.uniform(-np.pi, np.pi, 200), [0.0, np.pi / 2, np.pi, -np.pi / 2, 1e-13, -1e-13]])
+    vals = []
+    for th in base:
+        t = th
+        for _ in range(6):
+            t = np.nextafter(t, 10.0) if rng.integers(2) else np.nextafter(np.nextafter(t, 10.0), 10.0)
+            r = rng.uniform(0.05, 1.0)
+            vals.append(r * np.exp(1j * t))
+    vals = np.array(vals)
+    cb = pb.Codebook()
+    ref = ref_codec.RefCodebook()
+    p = cb.propose(vals)
+    q = ref.propose(vals)
+    for got, want in zip((p.mags, p.thetas, p.ux, p.uy), q):
+        assert np.array_equal(got, want)
+    cb.merge([p])
+    ref.merge([q])
+    assert cb.dump() == ref.dump()
+    probe = vals[rng.permutation(vals.size)] * np.exp(1j * 1e-15)
+    mi, pi = cb.encode(probe)
+    rmi, rpi = ref.encode(probe)
+    assert np.array_equal(mi, rmi) and np.array_equal(pi, rpi)
