@@ -59,13 +59,13 @@ def peaks():
 
 def measured_traffic(bytes_per_launch: int):
     """DRAM traffic per fused-pass launch from the committed ncu capture
-    (profiles/r01_traffic.json: dram read + write / algorithmic bytes, measured at N=32),
+    (profiles/r02_traffic.json: dram read + write / algorithmic bytes, measured at N=32),
     applied to this launch size; (None, None) if the file is absent."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic.json")
     try:
         with open(path) as fh:
             t = json.load(fh)
-        return int(bytes_per_launch * t["ratio"]), f"profiles/r01_traffic.json (ncu --set full at N={t['n_qubits']}: " \
+        return int(bytes_per_launch * t["ratio"]), f"profiles/r02_traffic.json (ncu --set full at N={t['n_qubits']}: " \
                                                    f"DRAM/algorithmic = {t['ratio']})"
     except (OSError, KeyError, ValueError):
         return None, None
@@ -608,9 +608,19 @@ def run_b200(args):
         h2d0, d2h0 = nat.transfer_bytes()
         t_e2e = 0.0
         e2e_bytes = 0
+        # warm e2e = a repeated call: every circuit runs once untimed first (its pass kernels
+        # compiled then, as a second call in production finds them); the first call of a
+        # fresh process is `cold_process` below
+        e2e_circs = []
         for j in range(args.e2e_steps):
             li = 1 + j % (len(layers) - 1) if len(layers) > 1 else 0
-            circ = pb.Circuit(n, tuple(layers[li]) + (pb.gates.measure_all(),))
+            e2e_circs.append((li, pb.Circuit(n, tuple(layers[li]) + (pb.gates.measure_all(),))))
+        for li, circ in {li: c for li, c in e2e_circs}.items():
+            warm = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
+            del warm
+            jit_wait()
+        h2d0, d2h0 = nat.transfer_bytes()
+        for j, (li, circ) in enumerate(e2e_circs):
             t0 = time.perf_counter()
             res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
             _ = res.report.qz[0]
