@@ -233,28 +233,67 @@ __device__ __forceinline__ bool lex_less(double ax, double ay, double bx, double
     return ax < bx || (ax == bx && ay < by);
 }
 
+// Phase candidates.  codec.py:137-152 keeps, per exact numpy theta, the value of smallest
+// (ux, uy).  Only on the axes is the device's theta bit-identical to numpy's: there values
+// are grouped by theta and the smallest (ux, uy) kept.  Any other angle comes from CUDA
+// atan2, which can round two angles numpy keeps apart (a few ulps) to the same double, so
+// grouping by it could drop a proposal (tests/test_gpu_byte.py clustered-angle test): such
+// values are kept per distinct VALUE (re, im), deduplicated exactly, and the host groups
+// them by numpy's theta (codec.finalize_proposal).  Keys: theta bits (top bit 0, theta is
+// in [0, 2 pi)) or a hash of the value bits with the top bit set; a value key is confirmed
+// by comparing the stored (re, im) under the slot lock (hash collisions keep probing).
+__device__ __forceinline__ unsigned long long value_key(cplx v) {
+    const unsigned long long a = (unsigned long long)__double_as_longlong(v.re);
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v.im);
+    unsigned long long k = a * 0x9e3779b97f4a7c15ull ^ (b + 0x632be59bd9b4e019ull + (a << 6) + (a >> 2));
+    k ^= k >> 31;
+    return k | (1ull << 63);
+}
+
 __device__ void insert_phase(CtaSets& s, ByteCand* out, const Polar& p, cplx v, int prod) {
-    const unsigned long long key = (unsigned long long)__double_as_longlong(p.th);
+    const bool by_value = !p.th_exact;
+    const unsigned long long key = by_value ? value_key(v) : (unsigned long long)__double_as_longlong(p.th);
     const unsigned rs = (unsigned)s.ph_rs, base = (unsigned)prod * rs;
     unsigned h0 = hash64(key ^ 0x9e3779b97f4a7c15ull) & (rs - 1);
     for (int probe = 0; probe < 64; ++probe) {
         const unsigned h = base + h0;
         unsigned long long cur = s.ph_key[h];
+        bool mine = false;
         if (cur == EMPTY) {
             cur = atomicCAS(&s.ph_key[h], EMPTY, key);
-            if (cur == EMPTY) { atomicAdd(&s.ph_count, 1); cur = key; }
+            if (cur == EMPTY) { atomicAdd(&s.ph_count, 1); cur = key; mine = true; }
         }
         if (cur == key) {
-            // keep the lexicographically smallest (ux, uy) per exact theta (codec.py:144-148);
-            // the stored ux only decreases, so a strictly larger ux can never win
-            if (p.ux > *(volatile double*)&s.ph_ux[h]) return;
-            while (atomicCAS(&s.ph_lock[h], 0, 1) != 0) {}
-            if (lex_less(p.ux, p.uy, s.ph_ux[h], s.ph_uy[h])) {
-                s.ph_ux[h] = p.ux; s.ph_uy[h] = p.uy; s.ph_re[h] = v.re; s.ph_im[h] = v.im;
+            if (by_value) {
+                for (;;) {
+                    while (atomicCAS(&s.ph_lock[h], 0, 1) != 0) {}
+                    const double sre = *(volatile double*)&s.ph_re[h], sim = *(volatile double*)&s.ph_im[h];
+                    int verdict;   // 1: this value, 0: another value (collision), -1: owner not done
+                    if (mine) {
+                        s.ph_ux[h] = p.ux; s.ph_uy[h] = p.uy; s.ph_re[h] = v.re; s.ph_im[h] = v.im;
+                        verdict = 1;
+                    } else if (sre != sre) {
+                        verdict = -1;
+                    } else {
+                        verdict = (sre == v.re && sim == v.im) ? 1 : 0;
+                    }
+                    __threadfence_block();
+                    atomicExch(&s.ph_lock[h], 0);
+                    if (verdict == 1) return;
+                    if (verdict == 0) break;
+                }
+            } else {
+                // keep the lexicographically smallest (ux, uy) per exact theta (codec.py:144-148);
+                // the stored ux only decreases, so a strictly larger ux can never win
+                if (p.ux > *(volatile double*)&s.ph_ux[h]) return;
+                while (atomicCAS(&s.ph_lock[h], 0, 1) != 0) {}
+                if (lex_less(p.ux, p.uy, s.ph_ux[h], s.ph_uy[h])) {
+                    s.ph_ux[h] = p.ux; s.ph_uy[h] = p.uy; s.ph_re[h] = v.re; s.ph_im[h] = v.im;
+                }
+                __threadfence_block();
+                atomicExch(&s.ph_lock[h], 0);
+                return;
             }
-            __threadfence_block();
-            atomicExch(&s.ph_lock[h], 0);
-            return;
         }
         h0 = (h0 + 1) & (rs - 1);
     }
@@ -265,6 +304,8 @@ __device__ void sets_clear(CtaSets& s, int regions) {
     for (int i = threadIdx.x; i < MAG_SLOTS; i += blockDim.x) s.mag_key[i] = EMPTY;
     for (int i = threadIdx.x; i < PH_SLOTS; i += blockDim.x) {
         s.ph_key[i] = EMPTY; s.ph_ux[i] = 1e300; s.ph_uy[i] = 1e300; s.ph_lock[i] = 0;
+        s.ph_re[i] = __longlong_as_double(0x7ff8000000000000ll);   // NaN: value slot not written yet
+        s.ph_im[i] = 0.0;
     }
     if (threadIdx.x == 0) {
         s.mag_count = 0; s.ph_count = 0; s.full = 0;
