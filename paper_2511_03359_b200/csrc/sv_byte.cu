@@ -738,49 +738,6 @@ __device__ __forceinline__ void byte_low_pairs(const uint8_t* __restrict__ mi_in
     }
 }
 
-// The 16 pairs of a 1Q work item one by one (non-uniform items): runs of equal code
-// tuples reuse the previous memo hit (entries are never evicted); a pair computed by
-// pair_slow is looked up again (its outputs may be uncertain, reported per index).
-__device__ __noinline__ void pairs16_slow(uint4 c0, uint4 c1, uint4 c2, uint4 c3, uint64_t i0, uint64_t i1, int prod,
-                                          const STables& t, const Emitter& em, ThreadCache& tc,
-                                          unsigned long long* memo, const MemoTags& mt, const double* m, bool real,
-                                          bool write, uint8_t* mi_out, uint8_t* pi_out) {
-    auto byte_of = [](const uint4& v, int j) -> unsigned {
-        const unsigned w = j < 4 ? v.x : (j < 8 ? v.y : (j < 12 ? v.z : v.w));
-        return (w >> (8 * (j & 3))) & 255u;
-    };
-    auto put_byte = [](uint4& v, int j, unsigned b) {
-        const unsigned sh = 8 * (j & 3);
-        if (j < 4) v.x |= b << sh; else if (j < 8) v.y |= b << sh;
-        else if (j < 12) v.z |= b << sh; else v.w |= b << sh;
-    };
-    uint4 out[4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
-    bool hit_prev = false;
-    unsigned key_prev = 0u, cc_prev = 0u;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const unsigned key = byte_of(c0, j) | (byte_of(c1, j) << 8) | (byte_of(c2, j) << 16) | (byte_of(c3, j) << 24);
-        unsigned cc;
-        if (hit_prev && key == key_prev) {
-            cc = cc_prev;
-        } else {
-            const int slot = memo_get(memo, key, &cc);
-            hit_prev = slot >= 0 && !mt.fresh(slot, prod);
-            if (!hit_prev) cc = pair_slow(t, em, tc, memo, mt, key, i0 + j, i1 + j, m, real, prod);
-            key_prev = key;
-            cc_prev = cc;
-        }
-        put_byte(out[0], j, cc & 255u); put_byte(out[1], j, (cc >> 8) & 255u);
-        put_byte(out[2], j, (cc >> 16) & 255u); put_byte(out[3], j, cc >> 24);
-    }
-    if (write) {
-        *reinterpret_cast<uint4*>(mi_out + i0) = out[0];
-        if (pi_out) *reinterpret_cast<uint4*>(pi_out + i0) = out[1];
-        *reinterpret_cast<uint4*>(mi_out + i1) = out[2];
-        if (pi_out) *reinterpret_cast<uint4*>(pi_out + i1) = out[3];
-    }
-}
-
 // One BYTE gate pass.  Work items: pairs (1Q), quadruples (2Q) or single
 // amplitudes (DIAG, and COPY for untouched amplitudes of a diagonal gate).
 template <int LOWQA>   // >= 0: a 1Q gate on low qubit LOWQA, 32-byte blocks (byte_low_pairs)
@@ -819,71 +776,102 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
         const bool real = g.m[1] == 0.0 && g.m[3] == 0.0 && g.m[5] == 0.0 && g.m[7] == 0.0;
         const uint64_t n_items = g.n_elems >> 1;
         if (g.qa >= 4 && g.n_elems >= 32 && lmin >= 4) {
-            // 16 consecutive pairs per work item (16-byte loads/stores of every plane).  Two
-            // items ping-pong between register sets A and B: each set is refilled right after
-            // it was consumed, so the next item's loads are always in flight (no register
-            // copies per item), and the uniform-run fast path stays inline while the per-pair
-            // path is one out-of-line call (code size).
+            // 16 consecutive pairs per work item (16-byte loads/stores of every plane); the next
+            // item's bytes are loaded before the current one is computed (latency hiding)
             const uint64_t n_chunks = n_items >> 4;
             const uint64_t off = 1ull << g.qa;
+            uint4 nxt[4];
             auto fetch = [&](uint64_t w, uint4 (&b)[4]) {
                 const uint64_t i0 = insert0(w << 4, g.qa);
                 b[0] = *reinterpret_cast<const uint4*>(mi_in + i0);
                 b[1] = ld16z(pi_in, i0);
                 b[2] = *reinterpret_cast<const uint4*>(mi_in + i0 + off);
                 b[3] = ld16z(pi_in, i0 + off);
+            };
+            uint64_t w = first;
+            if (w < n_chunks) fetch(w, nxt);
+            for (; w < n_chunks; w += step) {
+                uint4 cur[4] = {nxt[0], nxt[1], nxt[2], nxt[3]};
+                if (w + step < n_chunks) fetch(w + step, nxt);
                 if (w + kL2Ahead * step < n_chunks) {
                     const uint64_t ip = insert0((w + kL2Ahead * step) << 4, g.qa);
                     l2_prefetch(mi_in + ip);
                     l2_prefetch(mi_in + ip + off);
                     if (pi_in) { l2_prefetch(pi_in + ip); l2_prefetch(pi_in + ip + off); }
                 }
-            };
-            // uniform run: all 16 pairs carry the same code tuple (structured states, e.g. the
-            // Hadamard benchmark) -> one lookup, replicated output bytes
-            auto uniform = [](const uint4& v) {
-                return v.x == v.y && v.x == v.z && v.x == v.w && v.x == (v.x & 255u) * 0x01010101u;
-            };
-            auto process = [&](uint64_t w, const uint4 (&cur)[4]) {
                 const uint64_t i0 = insert0(w << 4, g.qa), i1 = i0 + off;
-                if (g.producer >= 0 && producer_of(g, i0) != g.producer) return;
+                if (g.producer >= 0 && producer_of(g, i0) != g.producer) continue;
                 const int prod = tagged ? producer_of(g, i0) : 0;
+                uint4 out[4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
+                auto byte_of = [](const uint4& v, int j) -> unsigned {
+                    const unsigned w = j < 4 ? v.x : (j < 8 ? v.y : (j < 12 ? v.z : v.w));
+                    return (w >> (8 * (j & 3))) & 255u;
+                };
+                auto put_byte = [](uint4& v, int j, unsigned b) {
+                    const unsigned sh = 8 * (j & 3);
+                    if (j < 4) v.x |= b << sh; else if (j < 8) v.y |= b << sh;
+                    else if (j < 12) v.z |= b << sh; else v.w |= b << sh;
+                };
+                // uniform run: all 16 pairs carry the same code tuple (structured states, e.g. the
+                // Hadamard benchmark) -> one lookup, replicated output bytes
+                auto uniform = [](const uint4& v) {
+                    return v.x == v.y && v.x == v.z && v.x == v.w && v.x == (v.x & 255u) * 0x01010101u;
+                };
                 if (uniform(cur[0]) && uniform(cur[1]) && uniform(cur[2]) && uniform(cur[3])) {
                     const unsigned key = (cur[0].x & 255u) | ((cur[1].x & 255u) << 8) | ((cur[2].x & 255u) << 16) |
                                          ((cur[3].x & 255u) << 24);
                     unsigned cc;
                     const int slot = memo_get(memo, key, &cc);
-                    bool ok = true;
                     if (slot < 0 || mt.fresh(slot, prod)) {
                         cc = pair_slow(t, em, tc, memo, mt, key, i0, i1, g.m, real, prod);
                         // uncertain amplitudes are reported per index: take the per-pair path
-                        ok = memo_get(memo, key, &cc) >= 0;
+                        if (memo_get(memo, key, &cc) < 0) goto per_pair;
                     }
-                    if (ok) {
-                        if (write) {
-                            const unsigned b0 = (cc & 255u) * 0x01010101u, b1 = ((cc >> 8) & 255u) * 0x01010101u;
-                            const unsigned b2 = ((cc >> 16) & 255u) * 0x01010101u, b3 = (cc >> 24) * 0x01010101u;
-                            *reinterpret_cast<uint4*>(mi_out + i0) = make_uint4(b0, b0, b0, b0);
-                            if (pi_out) *reinterpret_cast<uint4*>(pi_out + i0) = make_uint4(b1, b1, b1, b1);
-                            *reinterpret_cast<uint4*>(mi_out + i1) = make_uint4(b2, b2, b2, b2);
-                            if (pi_out) *reinterpret_cast<uint4*>(pi_out + i1) = make_uint4(b3, b3, b3, b3);
-                        }
-                        return;
+                    if (write) {
+                        const unsigned b0 = (cc & 255u) * 0x01010101u, b1 = ((cc >> 8) & 255u) * 0x01010101u;
+                        const unsigned b2 = ((cc >> 16) & 255u) * 0x01010101u, b3 = (cc >> 24) * 0x01010101u;
+                        *reinterpret_cast<uint4*>(mi_out + i0) = make_uint4(b0, b0, b0, b0);
+                        if (pi_out) *reinterpret_cast<uint4*>(pi_out + i0) = make_uint4(b1, b1, b1, b1);
+                        *reinterpret_cast<uint4*>(mi_out + i1) = make_uint4(b2, b2, b2, b2);
+                        if (pi_out) *reinterpret_cast<uint4*>(pi_out + i1) = make_uint4(b3, b3, b3, b3);
                     }
+                    continue;
                 }
-                pairs16_slow(cur[0], cur[1], cur[2], cur[3], i0, i1, prod, t, em, tc, memo, mt, g.m, real, write,
-                             mi_out, pi_out);
-            };
-            uint4 A[4], B[4];
-            uint64_t w = first;
-            if (w < n_chunks) fetch(w, A);
-            if (w + step < n_chunks) fetch(w + step, B);
-            for (; w < n_chunks; w += 2 * step) {
-                process(w, A);
-                if (w + 2 * step < n_chunks) fetch(w + 2 * step, A);
-                if (w + step >= n_chunks) break;
-                process(w + step, B);
-                if (w + 3 * step < n_chunks) fetch(w + 3 * step, B);
+            per_pair:
+                // runs of equal tuples (sparse / structured states) reuse the previous memo
+                // hit; a pair computed by pair_slow is looked up again (its outputs may be
+                // uncertain, reported per index)
+                bool hit_prev = false;
+                unsigned key_prev = 0u, cc_prev = 0u;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    // key = (m0, p0, m1, p1) bytes of pair j; j is a literal after unrolling
+                    const unsigned sh = 8 * (j & 3);
+                    const unsigned w0 = j < 4 ? cur[0].x : (j < 8 ? cur[0].y : (j < 12 ? cur[0].z : cur[0].w));
+                    const unsigned w1 = j < 4 ? cur[1].x : (j < 8 ? cur[1].y : (j < 12 ? cur[1].z : cur[1].w));
+                    const unsigned w2 = j < 4 ? cur[2].x : (j < 8 ? cur[2].y : (j < 12 ? cur[2].z : cur[2].w));
+                    const unsigned w3 = j < 4 ? cur[3].x : (j < 8 ? cur[3].y : (j < 12 ? cur[3].z : cur[3].w));
+                    const unsigned key = ((w0 >> sh) & 255u) | (((w1 >> sh) & 255u) << 8) |
+                                         (((w2 >> sh) & 255u) << 16) | (((w3 >> sh) & 255u) << 24);
+                    unsigned cc;
+                    if (hit_prev && key == key_prev) {
+                        cc = cc_prev;   // what the memo returns for it (entries are never evicted)
+                    } else {
+                        const int slot = memo_get(memo, key, &cc);
+                        hit_prev = slot >= 0 && !mt.fresh(slot, prod);
+                        if (!hit_prev) cc = pair_slow(t, em, tc, memo, mt, key, i0 + j, i1 + j, g.m, real, prod);
+                        key_prev = key;
+                        cc_prev = cc;
+                    }
+                    put_byte(out[0], j, cc & 255u); put_byte(out[1], j, (cc >> 8) & 255u);
+                    put_byte(out[2], j, (cc >> 16) & 255u); put_byte(out[3], j, cc >> 24);
+                }
+                if (write) {
+                    *reinterpret_cast<uint4*>(mi_out + i0) = out[0];
+                    if (pi_out) *reinterpret_cast<uint4*>(pi_out + i0) = out[1];
+                    *reinterpret_cast<uint4*>(mi_out + i1) = out[2];
+                    if (pi_out) *reinterpret_cast<uint4*>(pi_out + i1) = out[3];
+                }
             }
         } else
         for (uint64_t w = first; w < n_items; w += step) {
@@ -1075,29 +1063,20 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
         }
         return c << 4;
     };
-    // two chunks ahead in registers (one ahead left ~32 KB per SM in flight: latency-bound)
-    uint64_t w = first, inx = 0, inx2 = 0;
-    uint4 nm = {0, 0, 0, 0}, np = {0, 0, 0, 0}, nm2 = nm, np2 = nm;
+    uint64_t w = first, inx = 0;
+    uint4 nm = {0, 0, 0, 0}, np = {0, 0, 0, 0};
     if (w < n_chunks) {
         inx = chunk_at(w);
         nm = *reinterpret_cast<const uint4*>(mi_in + inx);
         np = ld16z(pi_in, inx);
     }
-    if (w + step < n_chunks) {
-        inx2 = chunk_at(w + step);
-        nm2 = *reinterpret_cast<const uint4*>(mi_in + inx2);
-        np2 = ld16z(pi_in, inx2);
-    }
     for (; w < n_chunks; w += step) {
         const uint64_t i = inx;
         const uint4 cm = nm, cpv = np;
-        inx = inx2;
-        nm = nm2;
-        np = np2;
-        if (w + 2 * step < n_chunks) {
-            inx2 = chunk_at(w + 2 * step);
-            nm2 = *reinterpret_cast<const uint4*>(mi_in + inx2);
-            np2 = ld16z(pi_in, inx2);
+        if (w + step < n_chunks) {
+            inx = chunk_at(w + step);
+            nm = *reinterpret_cast<const uint4*>(mi_in + inx);
+            np = ld16z(pi_in, inx);
         }
 
         if (((i | 15ull) & g.mask) != g.mask) {   // out of place: untouched chunk copied
