@@ -25,20 +25,24 @@ MODES = {"fp64": pb.PrecisionMode.FP64, "fp32": pb.PrecisionMode.FP32, "be": pb.
 
 
 def _golden_runs():
+    """(case, circuit, execute): every golden run resident; executed physically too where
+    the executor applies (FP storage, chunks of at least 32 amplitudes)."""
     from tests.golden.make_golden import tier_cases
     circs = {name: circ for name, circ, *_ in tier_cases()}
     with open(os.path.join(HERE, "golden", "tier.json")) as f:
         cases = [c for c in json.load(f)["cases"] if "run" in c]
-    return [pytest.param(c, circs[c["name"]], id=c["name"]) for c in cases]
+    out = []
+    for c in cases:
+        out.append(pytest.param(c, circs[c["name"]], False, id=c["name"] + "-resident"))
+        if c["mode"] != "be" and c["chunk_qubits"] >= 5:
+            out.append(pytest.param(c, circs[c["name"]], True, id=c["name"] + "-executed"))
+    return out
 
 
-@pytest.mark.parametrize("case,circ", _golden_runs())
-@pytest.mark.parametrize("execute", [False, True])
+@pytest.mark.parametrize("case,circ,execute", _golden_runs())
 def test_tiered_run_matches_reference(case, circ, execute):
     mode = MODES[case["mode"]]
     cfg = TierConfig(*case["config"])
-    if execute and (mode is pb.PrecisionMode.BYTE or case["chunk_qubits"] < 5):
-        pytest.skip("physical execution: FP storage, chunks >= 32 amplitudes")
     res = pb.run_circuit(to_product(circ), ranks=case["run"]["ranks"], mode=mode, tier_config=cfg,
                          tier_execute=execute)
     assert state_digest(res.gathered_state()) == case["run"]["state_sha256"]
