@@ -620,18 +620,23 @@ def run_b200(args):
             del warm
             jit_wait()
         h2d0, d2h0 = nat.transfer_bytes()
+        calls = []
         for j, (li, circ) in enumerate(e2e_circs):
             t0 = time.perf_counter()
             res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
             _ = res.report.qz[0]
-            t_e2e += time.perf_counter() - t0
+            dt = time.perf_counter() - t0
+            t_e2e += dt
             e2e_bytes += lbytes[li]
+            calls.append({"layer": li, "s": round(dt, 4), "gates": len(circ.gates) - 1,
+                          "launches": res.device_stats.get("kernel_launches")})
             del res
         h2d1, d2h1 = nat.transfer_bytes()
         t_e2e = max_over_ranks(dist, t_e2e)
         e2e = {"value": round(sum_over_ranks(dist, e2e_bytes) / t_e2e / 1e9, 2), "unit": "GB/s",
                "h2d_bytes_per_step": (h2d1 - h2d0) // args.e2e_steps,
                "d2h_bytes_per_step": (d2h1 - d2h0) // args.e2e_steps,
+               "calls": calls,
                "what": "run_circuit(layer + M): allocate + zero 2^N state, fused layer, measure-all, "
                        "report to host; wall clock per call"}
 
