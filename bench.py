@@ -244,7 +244,8 @@ def cpu_baseline(steps: int, n_layers: int, sample_n: int = CPU_SAMPLE_N):
 def fp64_ops_per_amplitude(op) -> float:
     """FP64 instructions per amplitude of one gate in the numpy-exact arithmetic of the
     passes (sv_arith.cuh / sv_jit_dev.cuh): generic 1Q 10 (4 DMUL + 4 DFMA + 2 DADD), real
-    1Q 6, monomial 0, generic 2Q 22, real 2Q 14, diagonal 4 on the selected 2^-k, Z 0."""
+    1Q 6, monomial 0, any non-monomial 2Q 22, diagonal 4 on the selected 2^-k, Z 0 (fallback
+    model for passes the generic kernel runs; sv_plan_pass_costs counts the others)."""
     import numpy as np
     from paper_2511_03359_b200 import _native as nat
     m = np.array(op.m[:32])
@@ -256,7 +257,7 @@ def fp64_ops_per_amplitude(op) -> float:
     if op.kind == nat.SV_OP_2Q:
         if np.count_nonzero(m) == 4:
             return 0.0
-        return 14.0 if not np.any(m[1::2]) else 22.0
+        return 22.0                       # real 4x4 matrices run the generic row4 too
     if op.m[0] == -1.0 and op.m[1] == 0.0:
         return 0.0
     return 4.0 / (1 << bin(op.diag_mask).count("1"))
@@ -265,9 +266,12 @@ def fp64_ops_per_amplitude(op) -> float:
 def fp64_aware_roofline(n: int, seq, tile_bits: int, pass_ms: float, hbm_peak: float, sm_mhz: float) -> dict:
     """Per launch the fused pass has two floors: its HBM bytes at the copy peak and its
     FP64 instructions at 64 lanes/clk/SM x 148 SMs x the SM clock measured under load.
-    Returns the sum of max(floors) over the timed launches (the library's own pass
-    split) against their measured time."""
+    The FP64 count per pass is the library's own (sv_plan_pass_costs: warp instructions
+    of the specialised kernel per amplitude -- a diagonal op selecting lanes still issues
+    for the whole warp).  Returns the sum of max(floors) over the timed launches (the
+    library's own pass split) against their measured time."""
     import ctypes
+    import numpy as np
     from paper_2511_03359_b200 import _native as nat
     from paper_2511_03359_b200.device import ops_array
     lib = nat.load()
@@ -277,18 +281,25 @@ def fp64_aware_roofline(n: int, seq, tile_bits: int, pass_ms: float, hbm_peak: f
     hbm_ms = 2 * 16 * 2 ** n / (hbm_peak * 1e9) * 1e3
     floor = f64_total = hbm_total = 0.0
     n_pass = 0
+    per_amp = []
     for ops in seq:
         ends = (ctypes.c_int * 4096)()
-        k = lib.sv_plan_passes(n, nat.SV_FP64, ops_array(ops), len(ops), tile_bits, ends, 4096)
+        cost = np.zeros(4096)
+        k = lib.sv_plan_pass_costs(n, nat.SV_FP64, ops_array(ops), len(ops), tile_bits, ends, nat.dptr(cost), 4096)
+        nat.check(min(k, 0))
         a = 0
         for i in range(k):
-            f = sum(fp64_ops_per_amplitude(o) for o in ops[a:ends[i]]) * 2 ** n / fp64_peak * 1e3
+            c = cost[i] if cost[i] >= 0 else sum(fp64_ops_per_amplitude(o) for o in ops[a:ends[i]])
+            per_amp.append(float(c))
+            f = c * 2 ** n / fp64_peak * 1e3
             a = ends[i]
             floor += max(hbm_ms, f)
             f64_total += f
             hbm_total += hbm_ms
             n_pass += 1
     return {"fp64_peak_Tops": round(fp64_peak / 1e12, 2), "passes": n_pass,
+            "fp64_per_amplitude": {"min": min(per_amp), "mean": round(sum(per_amp) / len(per_amp), 1),
+                                   "max": max(per_amp)} if per_amp else None,
             "hbm_floor_ms": round(hbm_total, 1), "fp64_floor_ms": round(f64_total, 1),
             "max_floor_ms": round(floor, 1), "measured_ms": round(pass_ms, 1),
             "frac": round(floor / pass_ms, 4) if pass_ms else None,

@@ -308,6 +308,11 @@ int sv_jit_prepare_mode(int n_qubits, int mode, const sv_op* ops, int n_ops, int
 /* the pass split sv_apply_fused uses for ops: ends[p] = one past the last op of pass p;
  * returns the number of passes (also queues their specialised kernels) */
 int sv_plan_passes(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int* ends, int cap);
+/* the same split without queueing kernels, plus each pass's FP64 warp instructions per
+ * amplitude in its specialised kernel (fp64_per_amp[p] = -1: generic kernel); the
+ * FP64 floor of a pass is that x 2^n / (64 lanes x SMs x SM clock) -- bench.py roofline */
+int sv_plan_pass_costs(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int* ends,
+                       double* fp64_per_amp, int cap);
 int sv_jit_stats(double* out8);               /* compiled, failed, jit launches, fallbacks, compile ms, cached,
                                                  disk-cache hits, disk-cache writes ($SVB200_JIT_CACHE) */
 int sv_jit_available(void);                   /* 1 when NVRTC and the driver entry points resolved */

@@ -460,6 +460,9 @@ int choose_cfg(const sv_op* ops, int n_ops, int n) {
 // init != nullptr (*init != -2): the buffer holds |*init> (-1: zeros) only virtually; the first
 // pass generates its tiles if its specialised kernel is ready, otherwise materialize() writes
 // the state first.  *init is set to -2 once the state is real.
+// sv_plan_pass_costs: the planning walk also records each pass's FP64 instructions per amplitude
+static thread_local std::vector<double>* g_plan_costs = nullptr;
+
 int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_ops, int tile_bits,
                cudaStream_t st, int* prepare = nullptr, uint64_t chunk_mask = 0, uint64_t chunk_pat = 0,
                std::vector<int>* pass_ends = nullptr, int64_t* init = nullptr,
@@ -502,7 +505,10 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
             if (use_v3 && build_params2(ops, cur, n, cfg, Pp) == 0 &&
                 (g_seg_limit <= 0 || Pp.n_segs <= g_seg_limit)) {
                 Pp.storage = mode;
-                *prepare += jit_prepare_fused(Pp);
+                if (g_plan_costs) g_plan_costs->push_back(jit_fp64_per_amp(Pp));
+                else *prepare += jit_prepare_fused(Pp);
+            } else if (g_plan_costs) {
+                g_plan_costs->push_back(-1.0);   // generic kernel (no specialised pass)
             }
             cur = PassPlan();
             return SV_OK;
@@ -1191,6 +1197,25 @@ int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_
     }
     if (rc) return fail(SV_EVALUE, "NVRTC compile failed: %s", log.c_str());
     return (int)cur.ops.size();
+}
+
+int sv_plan_pass_costs(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int* ends,
+                       double* fp64_per_amp, int cap) {
+    if (n_qubits < 1 || n_qubits > 62) return fail(SV_EVALUE, "qubit count %d out of range", n_qubits);
+    if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "passes are planned for FP64 / FP32 storage");
+    if (n_ops <= 0) return 0;
+    int queued = 0;
+    std::vector<int> e;
+    std::vector<double> c;
+    g_plan_costs = &c;
+    const int rc = fused_impl(nullptr, 1ull << n_qubits, mode, ops, n_ops, tile_bits, nullptr, &queued, 0, 0, &e);
+    g_plan_costs = nullptr;
+    if (rc) return rc;
+    for (size_t i = 0; i < e.size() && (int)i < cap; ++i) {
+        ends[i] = e[i];
+        fp64_per_amp[i] = i < c.size() ? c[i] : -1.0;
+    }
+    return (int)e.size();
 }
 
 int sv_plan_passes(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int* ends, int cap) {

@@ -105,6 +105,40 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// ---- bulk tile loads (FP64 passes): one cp.async.bulk (TMA engine, SASS UBLKCP) per
+// 256-byte run of 16 contiguous amplitudes (tile positions 0..3 = qubits 0..3), completion
+// counted in bytes on an mbarrier, instead of 16 cp.async (LDGSTS) per thread.  A bulk
+// copy cannot permute inside a run, so bank conflicts are avoided by PADDING between runs
+// instead of the XOR swizzle: slot(e) = e + D0 (e >> 4) + D1 (e >> 7) + D2 (e >> 10)
+// (additive over disjoint bit sets, so a thread's slot + a register's slot is the element's
+// slot); sv_jit.cu picks D0..D2 and the thread-bit order per pass.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "SVJ_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SVJ_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// generic-proxy reads of the buffer (earlier tile) ordered before the async-proxy writes
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, u64* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // p + off amplitudes, computed where it is used: the 16 prefetch / store addresses of
 // a tile are loop-invariant offsets from the tile base, and hoisting them out of the
 // tile loop (32 live 64-bit pointers) is what made the compiler spill

@@ -76,6 +76,9 @@ bool jit_enabled();                             // JIT mode != 0 and NVRTC prese
 #include <string>
 namespace sv {
 int jit_probe(const Fused2Params& P, std::string* src, bool compile, double* ms, std::string* log);
+// FP64 warp instructions per amplitude the specialised pass issues (a warp instruction
+// occupies the FP64 pipe for all 32 lanes, whichever lanes a diagonal mask selects)
+double jit_fp64_per_amp(const Fused2Params& P);
 
 // mode: SV_FP64 / SV_FP32 storage
 cudaError_t launch_gate1(void* psi, uint64_t n_elems, int mode, int q, const double* m8,

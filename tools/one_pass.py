@@ -23,8 +23,12 @@ n, li, pi = (int(x) for x in sys.argv[1:4])
 cfg = int(sys.argv[4]) if len(sys.argv) > 4 else 9
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 1
 lib = nat.load()
-lay = bench.workload_layers(n, 9)[li]
-ops = [gate_to_op(g) for g in to_product(OCircuit(n, tuple(lay))).gates]
+if li < 0:     # LAYER -1: build_adder(N // 2, ...) (BASELINE config 3 at N=32)
+    circ = pb.build_adder(n // 2, [47302 % (1 << (n // 2)), 18233 % (1 << (n // 2))])[0]
+    ops = [gate_to_op(g) for g in circ.gates if g.kind != "M"]
+else:
+    lay = bench.workload_layers(n, 9)[li]
+    ops = [gate_to_op(g) for g in to_product(OCircuit(n, tuple(lay))).gates]
 
 
 def plan(c):
