@@ -1305,22 +1305,38 @@ static unsigned byte_grid(uint64_t items) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
 }
 
+// Kernel attributes of the gate passes, once per device.  The attribute call also loads the
+// kernels' module (CUDA lazy loading), so svb_create calls this: a state's first gate then
+// pays no module load (first BYTE pass of a process 7.7 -> 1.5 ms at N=32).
+cudaError_t byte_kernels_prepare() {
+    static bool configured[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64 || configured[dev]) return cudaSuccess;
+    const int memo_bytes = MEMO_SLOTS * (int)(sizeof(unsigned long long) + sizeof(unsigned));
+    void (*low[4])(const uint8_t*, const uint8_t*, uint8_t*, uint8_t*, const ByteTables*, const ByteGate, ByteCand*) = {
+        k_byte_gate<0>, k_byte_gate<1>, k_byte_gate<2>, k_byte_gate<3>};
+    cudaError_t e = cudaFuncSetAttribute(k_byte_gate<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, memo_bytes);
+    for (int q = 0; q < 4 && e == cudaSuccess; ++q)
+        e = cudaFuncSetAttribute(low[q], cudaFuncAttributeMaxDynamicSharedMemorySize, memo_bytes);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_byte_diag_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 8 * 4);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_byte_diag_apply<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 65536 * 2 + 2048 * 8 * 4);
+    if (e == cudaSuccess) configured[dev] = true;
+    return e;
+}
+
 cudaError_t launch_byte_gate(const uint8_t* mi_in, const uint8_t* pi_in, uint8_t* mi_out, uint8_t* pi_out,
                              const ByteTables* tab, const ByteGate& g, ByteCand* cand, cudaStream_t st) {
     const uint64_t items = g.kind == SV_OP_1Q ? g.n_elems / 2 : (g.kind == SV_OP_2Q ? g.n_elems / 4 : g.n_elems);
-    static bool configured[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     const int memo_bytes = MEMO_SLOTS * (int)(sizeof(unsigned long long) + sizeof(unsigned));
     void (*low[4])(const uint8_t*, const uint8_t*, uint8_t*, uint8_t*, const ByteTables*, const ByteGate, ByteCand*) = {
         k_byte_gate<0>, k_byte_gate<1>, k_byte_gate<2>, k_byte_gate<3>};
-    if (dev < 64 && !configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k_byte_gate<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, memo_bytes);
-        for (int q = 0; q < 4 && e == cudaSuccess; ++q)
-            e = cudaFuncSetAttribute(low[q], cudaFuncAttributeMaxDynamicSharedMemorySize, memo_bytes);
-        if (e != cudaSuccess) return e;
-        configured[dev] = true;
-    }
+    if (cudaError_t e = byte_kernels_prepare()) return e;
     // low-qubit 1Q gates: 32-byte blocks, if a block has one producer (the bits the
     // producer rule reads are all >= 5; k_byte_gate computes the same bound)
     int lmin = 64;
@@ -1340,13 +1356,6 @@ cudaError_t launch_byte_gate(const uint8_t* mi_in, const uint8_t* pi_in, uint8_t
         if (seen) cudaMemsetAsync(seen, 0, 2048 * nprod * sizeof(uint32_t), st);
         const uint64_t chunks = g.n_elems >> 4;
         const size_t bm_bytes = seen ? 2048 * nprod * sizeof(uint32_t) : 0;
-        static bool diag_configured[64] = {false};
-        if (dev < 64 && !diag_configured[dev]) {
-            cudaFuncSetAttribute(k_byte_diag_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 8 * 4);
-            cudaFuncSetAttribute(k_byte_diag_apply<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 65536 * 2 + 2048 * 8 * 4);
-            diag_configured[dev] = true;
-        }
         const unsigned grid1 = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((chunks + NTD - 1) / NTD,
                                                                                   (uint64_t)sm_count(dev)));
         if (g.scan_only) {

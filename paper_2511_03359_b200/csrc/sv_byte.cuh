@@ -55,6 +55,7 @@ struct ByteCand {
     int overflow, any_mag, any_ph, pad;
 };
 
+cudaError_t byte_kernels_prepare();   // attributes + module load of the gate kernels (svb_create)
 cudaError_t launch_byte_gate(const uint8_t* mi_in, const uint8_t* pi_in, uint8_t* mi_out, uint8_t* pi_out,
                              const ByteTables* tab, const ByteGate& g, ByteCand* cand, cudaStream_t st);
 cudaError_t launch_byte_decode(const uint8_t* mi, const uint8_t* pi, const ByteTables* tab, double* out, uint64_t n,

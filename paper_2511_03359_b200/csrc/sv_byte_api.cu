@@ -70,6 +70,7 @@ int svb_create(int device, int n_qubits, sv_bhandle* out) {
     if (n_qubits < 0 || n_qubits > 40) return capi_fail(SV_EVALUE, "n_qubits out of range");
     Guard gd(device);
     keep_scratch_pool(device);
+    if (cudaError_t e0 = sv::byte_kernels_prepare()) return capi_cuda_fail(e0, "BYTE kernel attributes");
     sv_bstate* h = new sv_bstate();
     std::memset(h, 0, sizeof(*h));
     h->device = device;
