@@ -562,6 +562,7 @@ def run_b200(args):
     peak, peak_src = peaks()
     achieved = pass_bytes / (pass_ms / 1e3) / 1e9 if pass_ms > 0 else 0.0
 
+    clk_mhz = clk.summary().get("sm_mhz") or 1965.0
     # single-gate streaming kernel (no fusion): the per-gate roofline the north star names
     single = {}
     if args.single_gate:
@@ -665,12 +666,27 @@ def run_b200(args):
         res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
         t_adder = time.perf_counter() - t0
         kat = all(abs(res.report.qz[q] - 1.0) < 1e-12 for q in regs["R2"])
+        del res
+        # device view of a third run: the fused passes timed with CUDA events next to their
+        # HBM and FP64 floors (the adder's CPHASE runs make most passes FP64-bound)
+        nat.pass_timing(True)
+        nat.pass_timing_read()
+        res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
+        nat.pass_timing(False)
+        a_passes, a_ms, _ = nat.pass_timing_read()
+        a_ops = [gate_to_op(gt) for gt in circ.gates if gt.kind != "M"]
+        a_roof = fp64_aware_roofline(32, [a_ops], args.tile_bits, a_ms, peak, clk_mhz)
         adder = {"circuit": "build_adder(16, [47302, 18233])", "n_qubits": 32, "gates": len(circ.gates),
                  "seconds": round(t_adder, 4), "sec_per_gate": round(t_adder / len(circ.gates), 6),
                  "first_run_seconds": round(t_first, 4),
                  "kat_all_ones_R2": kat, "kernel_launches": res.device_stats.get("kernel_launches"),
+                 "passes": {"count": a_passes, "ms": round(a_ms, 2), "hbm_floor_ms": a_roof["hbm_floor_ms"],
+                            "fp64_floor_ms": a_roof["fp64_floor_ms"], "max_floor_ms": a_roof["max_floor_ms"],
+                            "frac_of_max_floor": a_roof["frac"],
+                            "fp64_per_amplitude": a_roof["fp64_per_amplitude"]},
                  "what": "run_circuit wall clock incl. allocation, zero state, fused passes, measure-all "
-                         "(second run: specialised pass kernels compiled; first_run_seconds: cold)"}
+                         "(second run: specialised pass kernels compiled; first_run_seconds: cold); passes: "
+                         "a third run's fused passes (CUDA events) vs max(HBM, FP64) floors per pass"}
         del res
     # byte-encoded benchmark (BASELINE config 5 shape on one GPU): time per gate
     byte = None

@@ -692,6 +692,17 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
         std::vector<int> cpos;
         for (int i = 0; i < K; ++i)
             if (!((done >> P.tq[i]) & 1)) cpos.push_back(i);
+        // direct segment 0 (sv_measure3.cu DIRECT): its registers take cross positions >= 5 so
+        // that its lanes are tile positions 0..4 = qubits 0..4 (512-byte warp loads)
+        static int denv = -1;
+        if (denv < 0) {
+            const char* e = std::getenv("SVB200_MEASURE_DIRECT");
+            denv = e ? std::atoi(e) : 0;   // measured slower (N=33: 108.9 vs 99.2 ms)
+        }
+        int n_hi = 0;
+        for (int i : cpos) n_hi += i >= 5;
+        P.direct = (denv && !byte && K == 12 && b >= 5 && n_hi >= RB) ? 1 : 0;
+        if (P.direct) std::stable_partition(cpos.begin(), cpos.end(), [](int i) { return i >= 5; });
         P.n_segs = (int)((cpos.size() + RB - 1) / RB);
         if (P.n_segs < 1) P.n_segs = 1;
         for (int sg = 0; sg < P.n_segs; ++sg) {
@@ -755,6 +766,10 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
             for (int pos = 0; pos < K; ++pos)
                 if (((jj * NT) >> pos) & 1) off += 1ull << P.tq[pos];
             P.pf_go[jj] = off;
+            uint64_t o0 = 0;
+            for (int bit = 0; bit < RB; ++bit)
+                if ((jj >> bit) & 1) o0 += 1ull << P.tq[P.seg_reg[0][bit]];
+            P.seg0_go[jj] = o0;
         }
         for (int byte = 0; byte < 4; ++byte)
             for (int v = 0; v < 256; ++v) {

@@ -54,7 +54,12 @@ constexpr int kOutMax = 52;
 // RB: register bits per segment (R = 2^RB amplitudes per thread, 2^(KB-RB) threads).
 // RB = 3 (8 amplitudes per thread, 4 segments per 12-bit tile, 16 warps per SM) was
 // measured slower than the 2-CTA RB = 4 variants (N=33: 126 vs 108 ms) and is not launched.
-template <int KB, int MINB, bool BYTE, int NSEG, bool ONES, int RB = 4>
+// DIRECT (FP64): segment 0 loads its 16 registers straight from HBM -- its lanes are tile
+// positions 0..4 = qubits 0..4, so a warp load is 512 contiguous bytes -- and stores them
+// into the shared-memory tile only for the later segments: one shared-memory sweep less per
+// tile (the 3-segment first pass is shared-memory bound: cp.async write + 3 reads = 4 sweeps
+// of the tile at 128 B/clk vs its HBM read).  The next tile is prefetched into L2.
+template <int KB, int MINB, bool BYTE, int NSEG, bool ONES, int RB = 4, bool DIRECT = false>
 __global__ void __launch_bounds__(1 << (KB - RB), MINB)
     k_measure3(const c64s* __restrict__ psi, const __grid_constant__ Measure3Params p, double* __restrict__ partials,
                const MeasureBytes bsrc) {
@@ -62,8 +67,9 @@ __global__ void __launch_bounds__(1 << (KB - RB), MINB)
     static_assert(!BYTE || RB == 4, "BYTE decode: 16 bytes per thread");
     // FP64 with 2 CTAs per SM: one tile buffer (2 x 2 x 64 KB would not fit); the next tile is
     // requested once the last segment holds the tile in registers, the other CTA covers the gap
-    constexpr bool SINGLE = !BYTE && MINB >= 2;
-    constexpr int NBUF = (BYTE || SINGLE) ? 1 : 2;
+    static_assert(!(DIRECT && BYTE), "direct loads read FP64 tiles");
+    constexpr bool SINGLE = !BYTE && MINB >= 2 && !DIRECT;
+    constexpr int NBUF = (BYTE || SINGLE || DIRECT) ? 1 : 2;
     // 2 CTAs per SM with 3 segments: segment 0 accumulates in registers, segments 1, 2 add
     // their per-tile sums to thread-private shared-memory slots (16 doubles per thread)
     constexpr bool ACC_SMEM = !BYTE && MINB >= 2 && NSEG >= 3;
@@ -101,8 +107,16 @@ __global__ void __launch_bounds__(1 << (KB - RB), MINB)
 #pragma unroll
         for (int j = 0; j < R; ++j) cp_async16m(dst + (sw_tid + j * NT), g + p.pf_go[j]);
     };
+    uint64_t go0 = 0;   // DIRECT: HBM offset of this thread's segment-0 registers
+    if constexpr (DIRECT) {
+#pragma unroll
+        for (int j = 0; j < TB; ++j)
+            if ((tid >> j) & 1) go0 += 1ull << p.tq[p.seg_thr[0][j]];
+    }
 
     double tw_all = 0.0, twr[RB];
+    double out_acc0 = 0.0, out_acc1 = 0.0;   // ONES: out-of-tile qubits lane, lane + 32
+    const int oq0 = lane < p.n_out ? p.oq[lane] : 0, oq1 = lane + 32 < p.n_out ? p.oq[lane + 32] : 0;
     double cr[NSEG][RB], ci[NSEG][RB];
 #pragma unroll
     for (int j = 0; j < RB; ++j) twr[j] = 0.0;
@@ -133,7 +147,7 @@ __global__ void __launch_bounds__(1 << (KB - RB), MINB)
             if (tk < p.n_tiles) fetch_bytes(tk, k);
             cp_commit_m();
         }
-    } else {
+    } else if constexpr (!DIRECT) {
         if (tile < p.n_tiles) prefetch(tile, bufs);
         cp_commit_m();
     }
@@ -169,6 +183,13 @@ __global__ void __launch_bounds__(1 << (KB - RB), MINB)
                     S[swz3(16 * tid + i, p.swz_cols)] = v;
                 }
             }
+        } else if constexpr (DIRECT) {
+            if (next < p.n_tiles) {   // the next tile's lines into L2 while this one is reduced
+                const c64s* g = psi + tile_base(next) + go0;
+#pragma unroll
+                for (int i = 0; i < R; ++i)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(g + p.seg0_go[i]));
+            }
         } else if constexpr (SINGLE) {
             cp_wait_m<0>();
         } else {
@@ -176,7 +197,7 @@ __global__ void __launch_bounds__(1 << (KB - RB), MINB)
             cp_commit_m();
             cp_wait_m<1>();
         }
-        __syncthreads();
+        if constexpr (!DIRECT) __syncthreads();
 #pragma unroll
         for (int s = 0; s < NSEG; ++s) {
             if (s >= p.n_segs) break;
@@ -185,8 +206,25 @@ __global__ void __launch_bounds__(1 << (KB - RB), MINB)
             for (int j = 0; j < TB; ++j) tb |= ((tid >> j) & 1) << p.seg_thr[s][j];
             const int tsw = swz3(tb, p.swz_cols);
             cplx r[R];
+            if (DIRECT && s == 0) {
+                const c64s* g = psi + tile_base(tile) + go0;
 #pragma unroll
-            for (int i = 0; i < R; ++i) r[i] = S[tsw ^ p.seg_rsw[s][i]];
+                for (int i = 0; i < R; ++i) {
+                    double re, im;
+                    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                                 : "=d"(re), "=d"(im) : "l"(g + p.seg0_go[i]));
+                    r[i] = {re, im};
+                }
+                if (p.n_segs > 1) {   // the later segments read the tile from shared memory
+                    __syncthreads();  // (the previous tile's last segment has read it)
+#pragma unroll
+                    for (int i = 0; i < R; ++i) S[tsw ^ p.seg_rsw[0][i]] = r[i];
+                    __syncthreads();
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < R; ++i) r[i] = S[tsw ^ p.seg_rsw[s][i]];
+            }
             if constexpr (SINGLE) {
                 if (s == p.n_segs - 1) {   // tile in registers: the buffer takes the next tile
                     __syncthreads();
@@ -205,14 +243,14 @@ __global__ void __launch_bounds__(1 << (KB - RB), MINB)
                         if ((i >> j) & 1) twr[j] += w;
                 }
                 tw_all += tt;
-                // out-of-tile qubits: bit constant over the tile
+                // out-of-tile qubits: bit constant over the tile.  Every lane gets the warp's
+                // tile sum and lane j adds it for out-of-tile qubit j (and j + 32): no serial
+                // per-qubit loop in lane 0 (a chain of shared-memory read-modify-writes per tile)
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) tt += __shfl_down_sync(0xffffffffu, tt, o);
-                if (lane == 0) {
-                    const uint64_t base = tile_base(tile);
-                    for (int j = 0; j < p.n_out; ++j)
-                        if ((base >> p.oq[j]) & 1) ow[warp * kOutMax + j] += tt;
-                }
+                for (int o = 16; o > 0; o >>= 1) tt += __shfl_xor_sync(0xffffffffu, tt, o);
+                const uint64_t base = tile_base(tile);
+                if (lane < p.n_out && ((base >> oq0) & 1)) out_acc0 += tt;
+                if (lane + 32 < p.n_out && ((base >> oq1) & 1)) out_acc1 += tt;
             }
             const uint32_t cm = p.cross_reg[s];
             if (ACC_SMEM && s > 0) {
@@ -271,6 +309,8 @@ __global__ void __launch_bounds__(1 << (KB - RB), MINB)
             v = wsum(((tid >> j) & 1) ? tw_all : 0.0);
             if (lane == 0) red[warp * NSL + 1 + p.seg_thr[0][j]] = v;
         }
+        if (lane < p.n_out) ow[warp * kOutMax + lane] = out_acc0;
+        if (lane + 32 < p.n_out) ow[warp * kOutMax + lane + 32] = out_acc1;
     }
 #pragma unroll
     for (int s = 0; s < NSEG; ++s)
@@ -301,24 +341,24 @@ __global__ void __launch_bounds__(1 << (KB - RB), MINB)
     }
 }
 
-template <int KB, int MINB, bool BYTE, int NSEG, bool ONES, int RB = 4>
+template <int KB, int MINB, bool BYTE, int NSEG, bool ONES, int RB = 4, bool DIRECT = false>
 static cudaError_t measure3_cfg(const c64s* psi, const Measure3Params& p, double* partials, int grid,
                                 cudaStream_t st, const MeasureBytes& b) {
     constexpr int TILE = 1 << KB, NW = (TILE >> RB) / 32;
     constexpr bool ACC_SMEM = !BYTE && MINB >= 2 && NSEG >= 3;
     const size_t smem = (ACC_SMEM ? sizeof(double) * (NSEG - 1) * 2 * RB * (TILE >> RB) : 0) +
-                        ((BYTE || MINB >= 2) ? 1 : 2) * sizeof(cplx) * TILE + sizeof(double) * NW * (kOutMax + 1 + 3 * KB) +
+                        ((BYTE || MINB >= 2 || DIRECT) ? 1 : 2) * sizeof(cplx) * TILE + sizeof(double) * NW * (kOutMax + 1 + 3 * KB) +
                         (BYTE ? sizeof(double) * 768 + 4 * 2 * TILE : 0);
     static bool configured[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k_measure3<KB, MINB, BYTE, NSEG, ONES, RB>,
+        cudaError_t e = cudaFuncSetAttribute(k_measure3<KB, MINB, BYTE, NSEG, ONES, RB, DIRECT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
-    k_measure3<KB, MINB, BYTE, NSEG, ONES, RB><<<grid, TILE >> RB, smem, st>>>(psi, p, partials, b);
+    k_measure3<KB, MINB, BYTE, NSEG, ONES, RB, DIRECT><<<grid, TILE >> RB, smem, st>>>(psi, p, partials, b);
     count_launch();
     return cudaGetLastError();
 }
@@ -336,6 +376,9 @@ cudaError_t launch_measure3(const void* psi, const Measure3Params& p, double* pa
     const MeasureBytes none{nullptr, nullptr, nullptr};
     const c64s* s = static_cast<const c64s*>(psi);
     if (p.kbits != 12) return measure3_cfg<11, 3, false, 3, true>(s, p, partials, grid, st, none);
+    if (p.direct)
+        return light_pass(p) ? measure3_cfg<12, 2, false, 2, false, 4, true>(s, p, partials, grid, st, none)
+                             : measure3_cfg<12, 2, false, 3, true, 4, true>(s, p, partials, grid, st, none);
     return light_pass(p) ? measure3_cfg<12, 2, false, 2, false>(s, p, partials, grid, st, none)
                          : measure3_cfg<12, 2, false, 3, true>(s, p, partials, grid, st, none);
 }
