@@ -629,6 +629,9 @@ __device__ __forceinline__ uint4 ld16z(const uint8_t* p, uint64_t off) {
 // their own (scan passes read 32 bytes per item); the prefetched lines turn the
 // register loads into L2 hits.  No registers, no shared memory.
 constexpr int kL2Ahead = 4;
+// warp-cooperative per-pair path (k_byte_gate, 1Q on qubits >= 4) when at most this many
+// lanes of a warp hold mixed items; more, and every lane walks its own item
+constexpr int kCoopMaxItems = 12;
 __device__ __forceinline__ void l2_prefetch(const uint8_t* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -777,9 +780,16 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
         const uint64_t n_items = g.n_elems >> 1;
         if (g.qa >= 4 && g.n_elems >= 32 && lmin >= 4) {
             // 16 consecutive pairs per work item (16-byte loads/stores of every plane); the next
-            // item's bytes are loaded before the current one is computed (latency hiding)
+            // item's bytes are loaded before the current one is computed (latency hiding).
+            // The loop is warp-uniform: items whose 16 pairs are not one code tuple (or whose
+            // tuple is new to the CTA) take the per-pair path, and when a few lanes of a warp
+            // have such items the whole warp works on them together, one pair per lane
+            // (16 lanes per item).  Otherwise one mixed item kept 31 idle lanes waiting for
+            // 16 sequential pairs (Hadamard benchmark, H on qubit 9 at N=32: 1 item in 32
+            // mixed, 64 % of the warps diverged, ~470 instructions per warp-iteration).
             const uint64_t n_chunks = n_items >> 4;
             const uint64_t off = 1ull << g.qa;
+            const int lane = threadIdx.x & 31;
             uint4 nxt[4];
             auto fetch = [&](uint64_t w, uint4 (&b)[4]) {
                 const uint64_t i0 = insert0(w << 4, g.qa);
@@ -788,9 +798,24 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                 b[2] = *reinterpret_cast<const uint4*>(mi_in + i0 + off);
                 b[3] = ld16z(pi_in, i0 + off);
             };
+            auto byte_of = [](const uint4& v, int j) -> unsigned {
+                const unsigned w = j < 4 ? v.x : (j < 8 ? v.y : (j < 12 ? v.z : v.w));
+                return (w >> (8 * (j & 3))) & 255u;
+            };
+            auto put_byte = [](uint4& v, int j, unsigned b) {
+                const unsigned sh = 8 * (j & 3);
+                if (j < 4) v.x |= b << sh; else if (j < 8) v.y |= b << sh;
+                else if (j < 12) v.z |= b << sh; else v.w |= b << sh;
+            };
+            // uniform run: all 16 pairs carry the same code tuple (structured states, e.g. the
+            // Hadamard benchmark) -> one lookup, replicated output bytes
+            auto uniform = [](const uint4& v) {
+                return v.x == v.y && v.x == v.z && v.x == v.w && v.x == (v.x & 255u) * 0x01010101u;
+            };
             uint64_t w = first;
             if (w < n_chunks) fetch(w, nxt);
-            for (; w < n_chunks; w += step) {
+            for (; __any_sync(0xffffffffu, w < n_chunks); w += step) {
+                const bool inb = w < n_chunks;
                 uint4 cur[4] = {nxt[0], nxt[1], nxt[2], nxt[3]};
                 if (w + step < n_chunks) fetch(w + step, nxt);
                 if (w + kL2Ahead * step < n_chunks) {
@@ -799,72 +824,107 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                     l2_prefetch(mi_in + ip + off);
                     if (pi_in) { l2_prefetch(pi_in + ip); l2_prefetch(pi_in + ip + off); }
                 }
-                const uint64_t i0 = insert0(w << 4, g.qa), i1 = i0 + off;
-                if (g.producer >= 0 && producer_of(g, i0) != g.producer) continue;
-                const int prod = tagged ? producer_of(g, i0) : 0;
-                uint4 out[4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
-                auto byte_of = [](const uint4& v, int j) -> unsigned {
-                    const unsigned w = j < 4 ? v.x : (j < 8 ? v.y : (j < 12 ? v.z : v.w));
-                    return (w >> (8 * (j & 3))) & 255u;
-                };
-                auto put_byte = [](uint4& v, int j, unsigned b) {
-                    const unsigned sh = 8 * (j & 3);
-                    if (j < 4) v.x |= b << sh; else if (j < 8) v.y |= b << sh;
-                    else if (j < 12) v.z |= b << sh; else v.w |= b << sh;
-                };
-                // uniform run: all 16 pairs carry the same code tuple (structured states, e.g. the
-                // Hadamard benchmark) -> one lookup, replicated output bytes
-                auto uniform = [](const uint4& v) {
-                    return v.x == v.y && v.x == v.z && v.x == v.w && v.x == (v.x & 255u) * 0x01010101u;
-                };
-                if (uniform(cur[0]) && uniform(cur[1]) && uniform(cur[2]) && uniform(cur[3])) {
-                    const unsigned key = (cur[0].x & 255u) | ((cur[1].x & 255u) << 8) | ((cur[2].x & 255u) << 16) |
-                                         ((cur[3].x & 255u) << 24);
-                    unsigned cc;
-                    const int slot = memo_get(memo, key, &cc);
-                    if (slot < 0 || mt.fresh(slot, prod)) {
-                        cc = pair_slow(t, em, tc, memo, mt, key, i0, i1, g.m, real, prod);
-                        // uncertain amplitudes are reported per index: take the per-pair path
-                        if (memo_get(memo, key, &cc) < 0) goto per_pair;
+                const uint64_t i0 = inb ? insert0(w << 4, g.qa) : 0ull, i1 = i0 + off;
+                const bool valid = inb && !(g.producer >= 0 && producer_of(g, i0) != g.producer);
+                const int prod = (tagged && valid) ? producer_of(g, i0) : 0;
+                bool slow = false;
+                if (valid) {
+                    if (uniform(cur[0]) && uniform(cur[1]) && uniform(cur[2]) && uniform(cur[3])) {
+                        const unsigned key = (cur[0].x & 255u) | ((cur[1].x & 255u) << 8) |
+                                             ((cur[2].x & 255u) << 16) | ((cur[3].x & 255u) << 24);
+                        unsigned cc;
+                        const int slot = memo_get(memo, key, &cc);
+                        bool have = slot >= 0 && !mt.fresh(slot, prod);
+                        if (!have) {
+                            cc = pair_slow(t, em, tc, memo, mt, key, i0, i1, g.m, real, prod);
+                            // uncertain amplitudes are reported per index: take the per-pair path
+                            have = memo_get(memo, key, &cc) >= 0;
+                        }
+                        if (have && write) {
+                            const unsigned b0 = (cc & 255u) * 0x01010101u, b1 = ((cc >> 8) & 255u) * 0x01010101u;
+                            const unsigned b2 = ((cc >> 16) & 255u) * 0x01010101u, b3 = (cc >> 24) * 0x01010101u;
+                            *reinterpret_cast<uint4*>(mi_out + i0) = make_uint4(b0, b0, b0, b0);
+                            if (pi_out) *reinterpret_cast<uint4*>(pi_out + i0) = make_uint4(b1, b1, b1, b1);
+                            *reinterpret_cast<uint4*>(mi_out + i1) = make_uint4(b2, b2, b2, b2);
+                            if (pi_out) *reinterpret_cast<uint4*>(pi_out + i1) = make_uint4(b3, b3, b3, b3);
+                        }
+                        slow = !have;
+                    } else {
+                        slow = true;
                     }
-                    if (write) {
-                        const unsigned b0 = (cc & 255u) * 0x01010101u, b1 = ((cc >> 8) & 255u) * 0x01010101u;
-                        const unsigned b2 = ((cc >> 16) & 255u) * 0x01010101u, b3 = (cc >> 24) * 0x01010101u;
-                        *reinterpret_cast<uint4*>(mi_out + i0) = make_uint4(b0, b0, b0, b0);
-                        if (pi_out) *reinterpret_cast<uint4*>(pi_out + i0) = make_uint4(b1, b1, b1, b1);
-                        *reinterpret_cast<uint4*>(mi_out + i1) = make_uint4(b2, b2, b2, b2);
-                        if (pi_out) *reinterpret_cast<uint4*>(pi_out + i1) = make_uint4(b3, b3, b3, b3);
+                }
+                unsigned mm = __ballot_sync(0xffffffffu, slow);
+                if (!mm) continue;
+                if (__popc(mm) <= kCoopMaxItems) {
+                    // cooperative: two mixed items per round, pair j of item a on lane j, of item b
+                    // on lane 16 + j; outputs as byte stores (16 lanes fill one 16-byte run)
+                    const int j = lane & 15;
+                    while (mm) {
+                        const int la = __ffs(mm) - 1;
+                        mm &= mm - 1;
+                        int lb = -1;
+                        if (mm) {
+                            lb = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                        }
+                        const int src = lane < 16 ? la : (lb >= 0 ? lb : la);
+                        const bool act = lane < 16 || lb >= 0;
+                        const uint64_t s_i0 = __shfl_sync(0xffffffffu, i0, src);
+                        const int s_prod = __shfl_sync(0xffffffffu, prod, src);
+                        unsigned wv[4];
+#pragma unroll
+                        for (int pl = 0; pl < 4; ++pl) {
+                            const unsigned x = __shfl_sync(0xffffffffu, cur[pl].x, src);
+                            const unsigned y = __shfl_sync(0xffffffffu, cur[pl].y, src);
+                            const unsigned z = __shfl_sync(0xffffffffu, cur[pl].z, src);
+                            const unsigned v = __shfl_sync(0xffffffffu, cur[pl].w, src);
+                            wv[pl] = j < 4 ? x : (j < 8 ? y : (j < 12 ? z : v));
+                        }
+                        if (act) {
+                            const unsigned sh = 8 * (j & 3);
+                            const unsigned key = ((wv[0] >> sh) & 255u) | (((wv[1] >> sh) & 255u) << 8) |
+                                                 (((wv[2] >> sh) & 255u) << 16) | (((wv[3] >> sh) & 255u) << 24);
+                            unsigned cc;
+                            const int slot = memo_get(memo, key, &cc);
+                            if (slot < 0 || mt.fresh(slot, s_prod))
+                                cc = pair_slow(t, em, tc, memo, mt, key, s_i0 + j, s_i0 + off + j, g.m, real, s_prod);
+                            if (write) {
+                                mi_out[s_i0 + j] = (uint8_t)(cc & 255u);
+                                mi_out[s_i0 + off + j] = (uint8_t)((cc >> 16) & 255u);
+                                if (pi_out) {
+                                    pi_out[s_i0 + j] = (uint8_t)((cc >> 8) & 255u);
+                                    pi_out[s_i0 + off + j] = (uint8_t)(cc >> 24);
+                                }
+                            }
+                        }
                     }
                     continue;
                 }
-            per_pair:
-                // runs of equal tuples (sparse / structured states) reuse the previous memo
-                // hit; a pair computed by pair_slow is looked up again (its outputs may be
-                // uncertain, reported per index)
+                if (!slow) continue;
+                // many mixed items in the warp: every lane walks its own 16 pairs; runs of equal
+                // tuples (sparse / structured states) reuse the previous memo hit; a pair
+                // computed by pair_slow is looked up again (its outputs may be uncertain,
+                // reported per index)
+                uint4 out[4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
                 bool hit_prev = false;
                 unsigned key_prev = 0u, cc_prev = 0u;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    // key = (m0, p0, m1, p1) bytes of pair j; j is a literal after unrolling
-                    const unsigned sh = 8 * (j & 3);
-                    const unsigned w0 = j < 4 ? cur[0].x : (j < 8 ? cur[0].y : (j < 12 ? cur[0].z : cur[0].w));
-                    const unsigned w1 = j < 4 ? cur[1].x : (j < 8 ? cur[1].y : (j < 12 ? cur[1].z : cur[1].w));
-                    const unsigned w2 = j < 4 ? cur[2].x : (j < 8 ? cur[2].y : (j < 12 ? cur[2].z : cur[2].w));
-                    const unsigned w3 = j < 4 ? cur[3].x : (j < 8 ? cur[3].y : (j < 12 ? cur[3].z : cur[3].w));
-                    const unsigned key = ((w0 >> sh) & 255u) | (((w1 >> sh) & 255u) << 8) |
-                                         (((w2 >> sh) & 255u) << 16) | (((w3 >> sh) & 255u) << 24);
+                for (int jj = 0; jj < 16; ++jj) {
+                    // key = (m0, p0, m1, p1) bytes of pair jj; jj is a literal after unrolling
+                    const unsigned key = byte_of(cur[0], jj) | (byte_of(cur[1], jj) << 8) |
+                                         (byte_of(cur[2], jj) << 16) | (byte_of(cur[3], jj) << 24);
                     unsigned cc;
                     if (hit_prev && key == key_prev) {
                         cc = cc_prev;   // what the memo returns for it (entries are never evicted)
                     } else {
                         const int slot = memo_get(memo, key, &cc);
                         hit_prev = slot >= 0 && !mt.fresh(slot, prod);
-                        if (!hit_prev) cc = pair_slow(t, em, tc, memo, mt, key, i0 + j, i1 + j, g.m, real, prod);
+                        if (!hit_prev) cc = pair_slow(t, em, tc, memo, mt, key, i0 + jj, i1 + jj, g.m, real, prod);
                         key_prev = key;
                         cc_prev = cc;
                     }
-                    put_byte(out[0], j, cc & 255u); put_byte(out[1], j, (cc >> 8) & 255u);
-                    put_byte(out[2], j, (cc >> 16) & 255u); put_byte(out[3], j, cc >> 24);
+                    put_byte(out[0], jj, cc & 255u); put_byte(out[1], jj, (cc >> 8) & 255u);
+                    put_byte(out[2], jj, (cc >> 16) & 255u); put_byte(out[3], jj, cc >> 24);
                 }
                 if (write) {
                     *reinterpret_cast<uint4*>(mi_out + i0) = out[0];
