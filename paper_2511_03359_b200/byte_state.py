@@ -141,10 +141,18 @@ class ByteDeviceState:
         nat.check(nat.load().sv_stream_synchronize(self.stream))
 
     # -- candidate plumbing -----------------------------------------------------------
+    def _host_buffers(self):
+        """Candidate / uncertain-list landing buffers, allocated once per state (136 MB of
+        host memory; a fresh np.empty of them per gate was an mmap + munmap per call)."""
+        b = getattr(self, "_hbuf", None)
+        if b is None:
+            b = self._hbuf = (np.empty(_CCAP, dtype=np.float64), np.empty((_CCAP, 4), dtype=np.float64),
+                              np.empty(_CAP, dtype=np.uint64), np.empty(2 * _CAP, dtype=np.float64))
+        return b
+
     def read_candidates(self):
         lib = nat.load()
-        mags = np.empty(_CCAP, dtype=np.float64)
-        ph = np.empty((_CCAP, 4), dtype=np.float64)
+        mags, ph = self._host_buffers()[:2]
         nm, npp = ctypes.c_uint64(0), ctypes.c_uint64(0)
         flags = ctypes.c_int(0)
         nat.check(lib.svb_candidates(self.handle, nat.dptr(mags), _CCAP, ctypes.byref(nm),
@@ -178,8 +186,7 @@ class ByteDeviceState:
         return [(mags[mt == r], ph[pt == r]) for r in range(ranks)], unsure
 
     def read_unsure(self):
-        idx = np.empty(_CAP, dtype=np.uint64)
-        vals = np.empty(2 * _CAP, dtype=np.float64)
+        idx, vals = self._host_buffers()[2:]
         n = ctypes.c_uint64(0)
         nat.check(nat.load().svb_unsure(self.handle, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
                                         nat.dptr(vals), _CAP, ctypes.byref(n)))

@@ -1125,6 +1125,8 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
     };
     uint64_t w = first, inx = 0;
     uint4 nm = {0, 0, 0, 0}, np = {0, 0, 0, 0};
+    const unsigned lowm = (unsigned)(g.mask & 15ull);   // selected chunk positions: j & lowm == lowm
+    unsigned last_tag = 0xffffffffu;                       // scan: last (key, producer) marked
     if (w < n_chunks) {
         inx = chunk_at(w);
         nm = *reinterpret_cast<const uint4*>(mi_in + inx);
@@ -1149,21 +1151,32 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
         // the 16 amplitudes of a chunk share their producer (the caller checked the bits)
         const int prod = tagged ? producer_of(g, i) : 0;
         unsigned mw[4] = {cm.x, cm.y, cm.z, cm.w}, pw[4] = {cpv.x, cpv.y, cpv.z, cpv.w};
+        // The passes are issue-bound (ncu: 84 % issue active, 28 / 41 instructions per
+        // selected amplitude for scan / write): the selection test uses the mask's low
+        // bits only (the chunk's bits >= 4 match it), a key is one byte permute of the two
+        // plane words, a code goes back with one permute, and the scan skips the bitmap
+        // for a (key, producer) it has just marked.
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            if (((i + j) & g.mask) != g.mask) continue;
-            const unsigned sh = 8 * (j & 3);
-            const unsigned bmj = (mw[j >> 2] >> sh) & 255u, bpj = (pw[j >> 2] >> sh) & 255u;
-            const unsigned key = bmj | (bpj << 8);
+            if ((j & lowm) != lowm) continue;
+            const int wj = j >> 2, bj = j & 3;
+            const unsigned key = __byte_perm(mw[wj], pw[wj], (unsigned)(bj | ((4 + bj) << 4))) & 0xffffu;
             if (collect) {
-                uint32_t* wd = bits + prod * 2048 + (key >> 5);
-                if (!((*wd >> (key & 31)) & 1u)) atomicOr(wd, 1u << (key & 31));
+                const unsigned tag = key | ((unsigned)prod << 16);
+                if (tag != last_tag) {
+                    last_tag = tag;
+                    uint32_t* wd = bits + prod * 2048 + (key >> 5);
+                    if (!((*wd >> (key & 31)) & 1u)) atomicOr(wd, 1u << (key & 31));
+                }
             }
             if constexpr (!SCAN) {
                 unsigned code = slut[key];
-                if (code == kDiagUnsure) code = em.code(i + j, cmul(decode(t, bmj, bpj), f), tc);   // reports i+j
-                mw[j >> 2] = (mw[j >> 2] & ~(255u << sh)) | ((code & 255u) << sh);
-                pw[j >> 2] = (pw[j >> 2] & ~(255u << sh)) | ((code >> 8) << sh);
+                if (code == kDiagUnsure)   // reports i + j
+                    code = em.code(i + j, cmul(decode(t, key & 255u, key >> 8), f), tc);
+                // byte bj of the word <- byte 0 of the code part (selector nibble 4 = y.byte0)
+                constexpr unsigned kIns[4] = {0x3214u, 0x3240u, 0x3410u, 0x4210u};
+                mw[wj] = __byte_perm(mw[wj], code & 255u, kIns[bj]);
+                pw[wj] = __byte_perm(pw[wj], code >> 8, kIns[bj]);
             }
         }
         if (write) {

@@ -253,9 +253,10 @@ int svb_unsure(sv_bhandle h, uint64_t* idx, double* vals, uint64_t cap, uint64_t
 }
 
 int svb_reset(sv_bhandle h) {
+    // stream-ordered: the next pass on this stream sees the cleared header; no host wait
+    // (hcand lives as long as the handle and is never written after svb_create)
     Guard gd(h->device);
     BTRY(cudaMemcpyAsync(h->cand, &h->hcand, sizeof(ByteCand), cudaMemcpyHostToDevice, h->stream), "reset");
-    BTRY(cudaStreamSynchronize(h->stream), "reset sync");
     return SV_OK;
 }
 
