@@ -1127,6 +1127,7 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
     uint4 nm = {0, 0, 0, 0}, np = {0, 0, 0, 0};
     const unsigned lowm = (unsigned)(g.mask & 15ull);   // selected chunk positions: j & lowm == lowm
     unsigned last_tag = 0xffffffffu;                       // scan: last (key, producer) marked
+    unsigned last_key = 0xffffffffu, last_code = 0u;       // write: last key and its table code
     if (w < n_chunks) {
         inx = chunk_at(w);
         nm = *reinterpret_cast<const uint4*>(mi_in + inx);
@@ -1170,9 +1171,18 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
                 }
             }
             if constexpr (!SCAN) {
-                unsigned code = slut[key];
-                if (code == kDiagUnsure)   // reports i + j
-                    code = em.code(i + j, cmul(decode(t, key & 255u, key >> 8), f), tc);
+                unsigned code;
+                if (key == last_key) {
+                    code = last_code;   // never an uncertain entry (those are not cached)
+                } else {
+                    code = slut[key];
+                    if (code == kDiagUnsure) {   // reports i + j
+                        code = em.code(i + j, cmul(decode(t, key & 255u, key >> 8), f), tc);
+                    } else {
+                        last_key = key;
+                        last_code = code;
+                    }
+                }
                 // byte bj of the word <- byte 0 of the code part (selector nibble 4 = y.byte0)
                 constexpr unsigned kIns[4] = {0x3214u, 0x3240u, 0x3410u, 0x4210u};
                 mw[wj] = __byte_perm(mw[wj], code & 255u, kIns[bj]);
