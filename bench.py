@@ -1148,7 +1148,7 @@ def main():
     ap.add_argument("--fused", type=int, default=9, choices=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9],
                     help="fused-pass kernel: 0 smem-per-gate v1, 1-3 register-resident v3 configs")
     ap.add_argument("--seg-limit", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--cpu-layers", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--adder", type=int, default=1, help="time the N=32 adder circuit (1 GPU line)")
