@@ -233,7 +233,7 @@ int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Pa
     std::memset(&P, 0, sizeof(P));
     P.vinit = -2;                       // read the tiles (see fused_impl for lazy basis states)
     const int K = (cfg == 2 || cfg == 4 || cfg == 6) ? 11 : ((cfg == 5 || cfg == 7) ? 10 : (cfg == 10 ? 13 : 12));
-    const int RB = (cfg == 1 || cfg == 6 || cfg == 7 || cfg == 8 || cfg == 10) ? 4 : 3;
+    const int RB = (cfg == 1 || cfg == 6 || cfg == 7 || cfg == 8 || cfg == 10 || cfg == 11) ? 4 : 3;
     const int NTH = 1 << (K - RB);
     P.cfg = cfg;
     P.kbits = K;
@@ -363,7 +363,7 @@ int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Pa
         return e ? std::atoi(e) : 0;
     }();
     P.direct_in = din_all >= 2 ? 1 : lanes_contiguous(0);
-    const bool single_buf = cfg == 8 || cfg == 10;
+    const bool single_buf = cfg == 8 || cfg == 10 || cfg == 11;
     P.direct_out = (dout_all >= 2 || (dout_all == 1 && single_buf)) ? 1 : lanes_contiguous(P.n_segs - 1);
     int md = 0;
     for (int i = 0; i < nops; ++i) {
@@ -452,7 +452,12 @@ int count_passes(const sv_op* ops, int n_ops, int n, int K) {
 // (77 % vs 83 % of HBM measured), otherwise config 6
 int choose_cfg(const sv_op* ops, int n_ops, int n) {
     if (n < 12 || !jit_enabled()) return 6;
-    return count_passes(ops, n_ops, n, 12) < count_passes(ops, n_ops, n, 11) ? 8 : 6;
+    static const int ring = [] {   // SVB200_RING=1: 2^12 tiles as config 11 (two warp groups, 3 buffers)
+        const char* e = std::getenv("SVB200_RING");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (count_passes(ops, n_ops, n, 12) < count_passes(ops, n_ops, n, 11)) return ring ? 11 : 8;
+    return 6;
 }
 
 // prepare != nullptr: plan only and queue the specialised kernels of the v3 passes for
@@ -473,7 +478,8 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
         return fail(SV_EVALUE, "fused pass needs a 32-byte aligned buffer");
     const int n = log2u(n_elems);
     if (tile_bits <= 0) tile_bits = 12;
-    const int cfg = g_fused_v2 == 9 ? choose_cfg(ops, n_ops, n) : g_fused_v2;
+    int cfg = g_fused_v2 == 9 ? choose_cfg(ops, n_ops, n) : g_fused_v2;
+    if (cfg == 11 && mode != SV_FP64) cfg = 8;   // the ring form exists for FP64 tiles only
     const int kv3 = (cfg == 2 || cfg == 4 || cfg == 6) ? 11 : ((cfg == 5 || cfg == 7) ? 10 : (cfg == 10 ? 13 : 12));
     // FP32 storage takes the v3 planning only when the specialised kernel can run it
     const bool use_v3 = cfg != 0 && (mode == SV_FP64 || (mode == SV_FP32 && jit_enabled())) &&
@@ -1183,7 +1189,7 @@ int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_
     // does, print its specialised source, optionally compile it (CPU only)
     const char* pc = std::getenv("SVB200_PROBE_CFG");      // debugging: another tile configuration
     const int pcfg = pc ? std::atoi(pc) : 6;
-    const int K = (pcfg == 1 || pcfg == 3 || pcfg == 8) ? 12 : (pcfg == 10 ? 13 : 11);
+    const int K = (pcfg == 1 || pcfg == 3 || pcfg == 8 || pcfg == 11) ? 12 : (pcfg == 10 ? 13 : 11);
     if (n_qubits < K || n_qubits > 62 || n_ops <= 0) return fail(SV_EVALUE, "probe needs n >= 11 and ops");
     const uint64_t lowfix = (1ull << low_bits()) - 1ull;
     PassPlan cur;
@@ -1331,7 +1337,7 @@ int sv_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
 }
 
 int sv_fused_variant(int v2) {
-    if (v2 < 0 || v2 > 9) return fail(SV_EVALUE, "fused variant %d not in 0..9", v2);   // 10 (2^13 tiles) measured slower
+    if (v2 < 0 || (v2 > 9 && v2 != 11)) return fail(SV_EVALUE, "fused variant %d not in 0..9, 11", v2);   // 10 (2^13 tiles) measured slower
     g_fused_v2 = v2;
     return SV_OK;
 }

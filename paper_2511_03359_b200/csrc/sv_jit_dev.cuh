@@ -129,6 +129,18 @@ __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// arrive on `bar` once every cp.async this thread issued so far has landed (the barrier
+// counts one arrival per issuing thread: .noinc)
+__device__ __forceinline__ void cp_async_mbar_arrive(u64* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// named barrier of one warp group (ring passes: two groups of `n` threads per CTA)
+__device__ __forceinline__ void bar_group(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 // generic-proxy reads of the buffer (earlier tile) ordered before the async-proxy writes
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, u64* bar) {
