@@ -1145,7 +1145,7 @@ def main():
     ap.add_argument("--n", "--qubits-per-gpu", dest="n", type=int, default=33, help="qubits per GPU")
     ap.add_argument("--layers", type=int, default=9, help="H layer + random layers in the workload")
     ap.add_argument("--tile-bits", type=int, default=12, help="v1 tile bits / upper bound")
-    ap.add_argument("--fused", type=int, default=9, choices=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9],
+    ap.add_argument("--fused", type=int, default=9, choices=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11],
                     help="fused-pass kernel: 0 smem-per-gate v1, 1-3 register-resident v3 configs")
     ap.add_argument("--seg-limit", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=4)

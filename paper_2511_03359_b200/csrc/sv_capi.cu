@@ -1337,7 +1337,7 @@ int sv_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
 }
 
 int sv_fused_variant(int v2) {
-    if (v2 < 0 || (v2 > 9 && v2 != 11)) return fail(SV_EVALUE, "fused variant %d not in 0..9, 11", v2);   // 10 (2^13 tiles) measured slower
+    if (v2 < 0 || v2 > 11) return fail(SV_EVALUE, "fused variant %d not in 0..11", v2);
     g_fused_v2 = v2;
     return SV_OK;
 }

@@ -52,9 +52,12 @@ def fp64_per_amp(op):
     return 4.0 / (1 << bin(op.diag_mask).count("1"))
 
 
+TB = 13 if cfg == 10 else 12   # tile-bits cap handed to the library (config 10: 2^13 tiles)
+
+
 def plan(ops):
     ends = (ctypes.c_int * 256)()
-    k = lib.sv_plan_passes(n, nat.SV_FP64, ops_array(ops), len(ops), 12, ends, 256)
+    k = lib.sv_plan_passes(n, nat.SV_FP64, ops_array(ops), len(ops), TB, ends, 256)
     nat.check(min(k, 0))
     out, a = [], 0
     for i in range(k):
@@ -85,14 +88,14 @@ with clk:
         passes = plan(ops)
         for pi, (a, b) in enumerate(passes):
             sub = ops[a:b]
-            jit_prepare(n, sub, 12)
+            jit_prepare(n, sub, TB)
             jit_wait()
-            dev.apply_fused(sub)
+            dev.apply_fused(sub, TB)
             dev.synchronize()
             nat.pass_timing(True)
             nat.pass_timing_read()
             for _ in range(3):
-                dev.apply_fused(sub)
+                dev.apply_fused(sub, TB)
             dev.synchronize()
             cnt, ms, by = nat.pass_timing_read()
             nat.pass_timing(False)
