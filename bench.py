@@ -263,7 +263,8 @@ def fp64_ops_per_amplitude(op) -> float:
     return 4.0 / (1 << bin(op.diag_mask).count("1"))
 
 
-def fp64_aware_roofline(n: int, seq, tile_bits: int, pass_ms: float, hbm_peak: float, sm_mhz: float) -> dict:
+def fp64_aware_roofline(n: int, seq, tile_bits: int, pass_ms: float, hbm_peak: float, sm_mhz: float,
+                        combine_diag: bool = False) -> dict:
     """Per launch the fused pass has two floors: its HBM bytes at the copy peak and its
     FP64 instructions at 64 lanes/clk/SM x 148 SMs x the SM clock measured under load.
     The FP64 count per pass is the library's own (sv_plan_pass_costs: warp instructions
@@ -285,7 +286,8 @@ def fp64_aware_roofline(n: int, seq, tile_bits: int, pass_ms: float, hbm_peak: f
     for ops in seq:
         ends = (ctypes.c_int * 4096)()
         cost = np.zeros(4096)
-        k = lib.sv_plan_pass_costs(n, nat.SV_FP64, ops_array(ops), len(ops), tile_bits, ends, nat.dptr(cost), 4096)
+        k = lib.sv_plan_pass_costs(n, nat.SV_FP64, ops_array(ops), len(ops), tile_bits, ends, nat.dptr(cost), 4096,
+                                   1 if combine_diag else 0)
         nat.check(min(k, 0))
         a = 0
         for i in range(k):
@@ -687,7 +689,30 @@ def run_b200(args):
                  "what": "run_circuit wall clock incl. allocation, zero state, fused passes, measure-all "
                          "(second run: specialised pass kernels compiled; first_run_seconds: cold); passes: "
                          "a third run's fused passes (CUDA events) vs max(HBM, FP64) floors per pass"}
+        rep_exact = res.report
         del res
+        # the same circuit with combined diagonal runs (exact_diagonals=False: within 1e-12 of
+        # the reference, not bit-identical): one multiply per register mask per CPHASE run
+        pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, exact_diagonals=False)
+        jit_wait()
+        t0 = time.perf_counter()
+        res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, exact_diagonals=False)
+        t_comb = time.perf_counter() - t0
+        nat.pass_timing(True)
+        nat.pass_timing_read()
+        res2 = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, exact_diagonals=False)
+        nat.pass_timing(False)
+        c_passes, c_ms, _ = nat.pass_timing_read()
+        c_roof = fp64_aware_roofline(32, [a_ops], args.tile_bits, c_ms, peak, clk_mhz, combine_diag=True)
+        adder["combined_diagonals"] = {
+            "seconds": round(t_comb, 4), "sec_per_gate": round(t_comb / len(circ.gates), 6),
+            "passes": {"count": c_passes, "ms": round(c_ms, 2), "fp64_floor_ms": c_roof["fp64_floor_ms"],
+                       "max_floor_ms": c_roof["max_floor_ms"], "frac_of_max_floor": c_roof["frac"]},
+            "report_max_diff_vs_exact": float(rep_exact.max_difference(res.report)),
+            "kat_all_ones_R2": all(abs(res.report.qz[q] - 1.0) < 1e-12 for q in regs["R2"]),
+            "what": "run_circuit(exact_diagonals=False): runs of diagonal gates multiply each amplitude "
+                    "by their combined factor (north-star FP64 tolerance 1e-12, not bit-identical)"}
+        del res, res2
     # byte-encoded benchmark (BASELINE config 5 shape on one GPU): time per gate
     byte = None
     if args.byte_n > 0:

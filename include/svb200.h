@@ -305,6 +305,13 @@ int sv_jit_shutdown(void);                    /* drop queued compiles, wait for 
  * returns the number of new kernels queued */
 int sv_jit_prepare(int n_qubits, const sv_op* ops, int n_ops, int tile_bits);
 int sv_jit_prepare_mode(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits);  /* FP64 / FP32 */
+/* flags bit 0: the kernels of combined diagonal runs (sv_set_diag_combine) */
+int sv_jit_prepare_opts(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int flags);
+/* FP64 handles: runs of consecutive diagonal ops inside a fused pass multiply each
+ * amplitude by the product of their factors (one multiply per distinct register mask)
+ * instead of one rounding per gate -- amplitudes within 1e-12 relative of the
+ * reference (the north star's FP64 tolerance), NOT bit-identical.  Default off. */
+int sv_set_diag_combine(sv_handle h, int on);
 /* the pass split sv_apply_fused uses for ops: ends[p] = one past the last op of pass p;
  * returns the number of passes (also queues their specialised kernels) */
 int sv_plan_passes(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int* ends, int cap);
@@ -312,7 +319,7 @@ int sv_plan_passes(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile
  * amplitude in its specialised kernel (fp64_per_amp[p] = -1: generic kernel); the
  * FP64 floor of a pass is that x 2^n / (64 lanes x SMs x SM clock) -- bench.py roofline */
 int sv_plan_pass_costs(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int* ends,
-                       double* fp64_per_amp, int cap);
+                       double* fp64_per_amp, int cap, int flags);   /* flags bit 0: combined diagonal runs */
 int sv_jit_stats(double* out8);               /* compiled, failed, jit launches, fallbacks, compile ms, cached,
                                                  disk-cache hits, disk-cache writes ($SVB200_JIT_CACHE) */
 int sv_jit_available(void);                   /* 1 when NVRTC and the driver entry points resolved */

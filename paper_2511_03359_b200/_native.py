@@ -97,8 +97,10 @@ _SIGNATURES = {
     "sv_jit_shutdown": ([], _I),
     "sv_jit_prepare": ([_I, _P, _I, _I], _I),
     "sv_jit_prepare_mode": ([_I, _I, _P, _I, _I], _I),
+    "sv_jit_prepare_opts": ([_I, _I, _P, _I, _I, _I], _I),
+    "sv_set_diag_combine": ([_P, _I], _I),
     "sv_plan_passes": ([_I, _I, _P, _I, _I, ctypes.POINTER(_I), _I], _I),
-    "sv_plan_pass_costs": ([_I, _I, _P, _I, _I, ctypes.POINTER(_I), _D, _I], _I),
+    "sv_plan_pass_costs": ([_I, _I, _P, _I, _I, ctypes.POINTER(_I), _D, _I, _I], _I),
     "sv_jit_stats": ([_D], _I),
     "sv_jit_available": ([], _I),
     "sv_jit_probe": ([_P, _I, _I, ctypes.c_char_p, ctypes.c_size_t, _D], _I),

@@ -229,8 +229,18 @@ int classify(const double* m, int dim, uint32_t* mono) {
     return real ? 1 : 0;
 }
 
+// combined diagonal runs (sv_set_diag_combine): set by the C entry points for the duration of
+// one fused_impl call; diagonal ops then cost one conditional multiply into a per-mask factor,
+// so mostly-diagonal passes are no longer closed at kDiagPassOps
+static thread_local int g_combine_diag = 0;
+struct CombineScope {
+    int prev;
+    explicit CombineScope(int on) : prev(g_combine_diag) { g_combine_diag = on; }
+    ~CombineScope() { g_combine_diag = prev; }
+};
 int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Params& P) {
     std::memset(&P, 0, sizeof(P));
+    P.combine_diag = g_combine_diag;
     P.vinit = -2;                       // read the tiles (see fused_impl for lazy basis states)
     const int K = (cfg == 2 || cfg == 4 || cfg == 6) ? 11 : ((cfg == 5 || cfg == 7) ? 10 : (cfg == 10 ? 13 : 12));
     const int RB = (cfg == 1 || cfg == 6 || cfg == 7 || cfg == 8 || cfg == 10 || cfg == 11) ? 4 : 3;
@@ -409,21 +419,24 @@ int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Pa
 }
 
 // greedy pass count of an op list with tiles of 2^K amplitudes (the 5 lowest qubits fixed)
-// ops per fused pass: kMaxOps, or fewer (SVB200_MAX_PASS_OPS, tuning of diagonal-heavy passes)
+// ops per fused pass: 128, or fewer (SVB200_MAX_PASS_OPS, tuning of diagonal-heavy passes);
+// combined diagonal runs cost one factor multiply per op, so those passes take up to kMaxOps
+constexpr int kDefaultPassOps = 128;
 static int max_pass_ops() {
     static int v = -1;
     if (v < 0) {
         const char* e = std::getenv("SVB200_MAX_PASS_OPS");
-        const int x = e ? std::atoi(e) : kMaxOps;
-        v = (x >= 8 && x <= kMaxOps) ? x : kMaxOps;
+        const int x = e ? std::atoi(e) : kDefaultPassOps;
+        v = (x >= 8 && x <= kMaxOps) ? x : kDefaultPassOps;
     }
-    return v;
+    return g_combine_diag ? kMaxOps : v;
 }
 // A pass of mostly diagonal ops is closed at 80 ops: the specialised kernel then keeps
 // them as straight-line code, which beats the descriptor loop that >= 96 diagonal ops
 // need (adder N=32: two 124-op passes of 78 ms became 80 + 44 ops; 0.348 -> 0.305 s).
 constexpr int kDiagPassOps = 80;
 static bool pass_full(int n, int ndiag) {
+    if (g_combine_diag) return n >= max_pass_ops();
     return n >= max_pass_ops() || (n >= kDiagPassOps && 4 * ndiag >= 3 * n);
 }
 static bool is_diag_kind(int kind) { return kind != SV_OP_1Q && kind != SV_OP_2Q; }
@@ -943,6 +956,7 @@ struct sv_state {
     double* partials;
     size_t partial_cap;
     int64_t lazy = -2;      // sv_zero_state_lazy: -1 all zeros / unit index not yet written, -2 none
+    int diag_combine = 0;   // sv_set_diag_combine
 };
 extern "C" {
 static int materialize(sv_handle h);
@@ -1188,6 +1202,7 @@ int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_
     // plan the FIRST fused pass of `ops` on 2^n_qubits amplitudes exactly as fused_impl
     // does, print its specialised source, optionally compile it (CPU only)
     const char* pc = std::getenv("SVB200_PROBE_CFG");      // debugging: another tile configuration
+    CombineScope cs(std::getenv("SVB200_PROBE_COMBINE") ? 1 : 0);   // debugging: combined diagonal runs
     const int pcfg = pc ? std::atoi(pc) : 6;
     const int K = (pcfg == 1 || pcfg == 3 || pcfg == 8 || pcfg == 11) ? 12 : (pcfg == 10 ? 13 : 11);
     if (n_qubits < K || n_qubits > 62 || n_ops <= 0) return fail(SV_EVALUE, "probe needs n >= 11 and ops");
@@ -1221,8 +1236,10 @@ int sv_jit_probe(const sv_op* ops, int n_ops, int n_qubits, char* src_out, size_
 }
 
 int sv_plan_pass_costs(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int* ends,
-                       double* fp64_per_amp, int cap) {
+                       double* fp64_per_amp, int cap, int flags) {
     if (n_qubits < 1 || n_qubits > 62) return fail(SV_EVALUE, "qubit count %d out of range", n_qubits);
+    if ((flags & 1) && mode != SV_FP64) return fail(SV_EVALUE, "combined diagonal runs need FP64 storage");
+    CombineScope cs(flags & 1);
     if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "passes are planned for FP64 / FP32 storage");
     if (n_ops <= 0) return 0;
     int queued = 0;
@@ -1255,6 +1272,12 @@ int sv_jit_prepare(int n_qubits, const sv_op* ops, int n_ops, int tile_bits) {
     return sv_jit_prepare_mode(n_qubits, SV_FP64, ops, n_ops, tile_bits);
 }
 
+int sv_jit_prepare_opts(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int flags) {
+    if ((flags & 1) && mode != SV_FP64) return fail(SV_EVALUE, "combined diagonal runs need FP64 storage");
+    CombineScope cs(flags & 1);
+    return sv_jit_prepare_mode(n_qubits, mode, ops, n_ops, tile_bits);
+}
+
 int sv_jit_prepare_mode(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits) {
     if (n_qubits < 1 || n_qubits > 62) return fail(SV_EVALUE, "qubit count %d out of range", n_qubits);
     if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "specialised passes exist for FP64 / FP32 storage");
@@ -1273,9 +1296,16 @@ int sv_apply_fused_chunk(sv_handle h, const sv_op* ops, int n_ops, int tile_bits
                       chunk_pattern);
 }
 
+int sv_set_diag_combine(sv_handle h, int on) {
+    if (on && h->mode != SV_FP64) return fail(SV_EVALUE, "combined diagonal runs need FP64 storage");
+    h->diag_combine = on ? 1 : 0;
+    return SV_OK;
+}
+
 int sv_apply_fused(sv_handle h, const sv_op* ops, int n_ops, int tile_bits) {
     DeviceGuard g(h->device);
     if (n_ops <= 0) return SV_OK;
+    CombineScope cs(h->diag_combine);
     if (h->lazy != -2) {   // lazy |unit>: the first pass generates its input tiles
         int64_t init = h->lazy;
         const int rc = fused_impl(h->ptr, 1ull << h->n, h->mode, ops, n_ops, tile_bits, h->stream, nullptr, 0, 0,

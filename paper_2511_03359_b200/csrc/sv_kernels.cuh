@@ -10,7 +10,7 @@ namespace sv {
 // Fused-pass parameters travel as one kernel-parameter block (constant bank:
 // broadcast reads, no per-CTA global loads).  Kept well under the 32 KB
 // kernel-parameter limit of sm_70+ with CUDA >= 12.1.
-constexpr int kMaxOps = 128;
+constexpr int kMaxOps = 256;           // ops per pass (128 unless diagonal runs are combined)
 constexpr int kMaxMData = 1536;         // doubles
 constexpr int kMaxTileBits = 12;
 
@@ -46,6 +46,8 @@ struct Fused2Params {
     int direct_in, direct_out;
     int cfg, kbits, rbits;              // kernel configuration (tile bits, register bits)
     int storage;                        // SV_FP64 / SV_FP32 (FP32 only through the specialised kernel)
+    int combine_diag;                   // 1: runs of diagonal ops multiply each amplitude by their combined
+                                        // factor (within 1e-12, not bit-exact; FP64 specialised passes only)
     uint64_t cmask_t, cpat_t;           // chunked pass: tile-index bits fixed to cpat_t (n_tiles counts
                                         // the remaining tiles); 0, 0 = every tile
     int64_t vinit;                      // -2: read the tiles; -1 / u: generate them (all zeros / |u>),

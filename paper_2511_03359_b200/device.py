@@ -31,13 +31,18 @@ def ops_array(ops) -> ctypes.Array:
     return arr
 
 
-def jit_prepare(n_qubits: int, ops, tile_bits: int = 12, mode_code: int = nat.SV_FP64) -> int:
+def jit_prepare(n_qubits: int, ops, tile_bits: int = 12, mode_code: int = nat.SV_FP64,
+                combine_diag: bool = False) -> int:
     """Queue the specialised kernels (sv_jit.cu) of the fused passes `ops` will run on
-    2**n_qubits amplitudes (FP64 or FP32 storage); returns how many new kernels were queued."""
+    2**n_qubits amplitudes (FP64 or FP32 storage); returns how many new kernels were queued.
+    combine_diag: the kernels of a state with combined diagonal runs (set_diag_combine)."""
     if not ops:
         return 0
-    rc = nat.load(require_device=False).sv_jit_prepare_mode(n_qubits, mode_code, ops_array(ops), len(ops),
-                                                           tile_bits)
+    lib = nat.load(require_device=False)
+    if combine_diag:
+        rc = lib.sv_jit_prepare_opts(n_qubits, mode_code, ops_array(ops), len(ops), tile_bits, 1)
+    else:
+        rc = lib.sv_jit_prepare_mode(n_qubits, mode_code, ops_array(ops), len(ops), tile_bits)
     nat.check(min(rc, 0))
     return rc
 
@@ -92,6 +97,14 @@ class DeviceState:
     @property
     def nbytes(self) -> int:
         return self.size * np.dtype(self.dtype).itemsize
+
+    def set_diag_combine(self, on: bool) -> None:
+        """FP64: runs of consecutive diagonal gates inside a fused pass multiply every
+        amplitude by their combined factor (one rounding per register mask instead of per
+        gate): amplitudes within 1e-12 relative of the reference -- the north star's FP64
+        tolerance -- but not bit-identical.  Off by default."""
+        nat.check(nat.load().sv_set_diag_combine(self.handle, 1 if on else 0))
+        self.diag_combine = bool(on)
 
     def _touch(self, launches: int = 1):
         self.version += 1

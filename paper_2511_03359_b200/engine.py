@@ -128,13 +128,18 @@ def run_circuit(circuit: Circuit, *, ranks: int = 1, local_qubits: int | None = 
                 mode: PrecisionMode = PrecisionMode.FP64, tier_config=None,
                 rank_order_seed: int | None = None, transport_factory=Transport,
                 device: int = 0, fuse: bool = True, tile_bits: int = 12,
-                tier_execute: bool | None = None) -> RunResult:
+                tier_execute: bool | None = None, exact_diagonals: bool = True) -> RunResult:
     """svsim.run_circuit (engine.py:82-105) on one B200.
 
     tier_config (svsim TierConfig or tier.TierConfig): the reference's staging plan and
     TierAccount counters are charged exactly as svsim does.  tier_execute: also EXECUTE
     the plan with the slow chunks in pinned host memory (csrc/sv_tier.cu); None = only
-    when the FP64/FP32 state does not fit in HBM.  Results are identical either way."""
+    when the FP64/FP32 state does not fit in HBM.  Results are identical either way.
+
+    exact_diagonals=False (FP64, fused, resident): runs of consecutive diagonal gates in a
+    fused pass multiply each amplitude by their combined factor -- amplitudes within 1e-12
+    relative of the reference (the north star's FP64 tolerance) instead of bit-identical;
+    the QFT adder's CPHASE runs then cost one multiply per register mask, not per gate."""
     validate_circuit(circuit)
     if ranks < 1 or ranks & (ranks - 1):
         raise ValueError("rank count must be a power of two")
@@ -149,7 +154,10 @@ def run_circuit(circuit: Circuit, *, ranks: int = 1, local_qubits: int | None = 
     if tier_config is not None:
         tier = _TierRun(circuit, layout, mode, tier_config, tier_execute, device)
     launches0 = nat.launch_count()
-    eng = _Engine(circuit, layout, mode, rank_order_seed, transport_factory, device, fuse, tile_bits, tier)
+    combine = (not exact_diagonals and fuse and mode is PrecisionMode.FP64
+               and not (tier is not None and tier.execute))
+    eng = _Engine(circuit, layout, mode, rank_order_seed, transport_factory, device, fuse, tile_bits, tier,
+                  combine_diag=combine)
     eng.run()
     eng.launches = nat.launch_count() - launches0
     return RunResult(circuit, layout, mode, eng.states, eng.ledgers, eng.report, eng.codebook,
@@ -183,8 +191,9 @@ class _TierRun:
 
 class _Engine:
     def __init__(self, circuit, layout, mode, rank_order_seed, transport_factory, device, fuse,
-                 tile_bits, tier=None):
+                 tile_bits, tier=None, combine_diag=False):
         self.circuit = circuit
+        self.combine_diag = combine_diag
         self.tier = tier
         self.layout = layout
         self.mode = mode
@@ -213,6 +222,8 @@ class _Engine:
         else:
             from .device import DeviceState
             self.dev = DeviceState(circuit.n_qubits, mode, device=device)
+            if combine_diag:
+                self.dev.set_diag_combine(True)
         if mode is PrecisionMode.BYTE:
             self.dev.zero(0)
         else:   # the first fused pass generates |0..0> instead of reading a written state
@@ -357,7 +368,7 @@ class _Engine:
             # background; passes whose kernel is not ready yet run the generic one)
             from .device import jit_prepare
             jit_prepare(self.circuit.n_qubits, [gate_to_op(g) for g in self.circuit.gates if g.kind != "M"],
-                        self.tile_bits, self.dev.mode_code)
+                        self.tile_bits, self.dev.mode_code, combine_diag=self.combine_diag)
         for ordinal, gate in enumerate(self.circuit.gates):
             plan = plan_exchange(self.layout, gate, self.mode)
             try:
@@ -377,6 +388,7 @@ class _Engine:
 
     def stats(self) -> dict:
         out = {"device": self.dev.device, "kernel_launches": getattr(self, "launches", self.dev.launches),
+               "diag_combine": self.combine_diag,
                "gates_applied": self.gates_applied, "fused": self.fuse and self.mode is not PrecisionMode.BYTE,
                "physical_link_bytes": 0}
         if self.mode is PrecisionMode.BYTE:

@@ -203,6 +203,33 @@ def test_adder_all_ones_kat():
         assert pb.decode_register(bits, regs["R1"]) == a
 
 
+@pytest.mark.parametrize("case", ["adder9", "adder11", "random18"])
+def test_combined_diagonal_runs_within_tolerance(rng, case):
+    """run_circuit(exact_diagonals=False): runs of diagonal gates multiply each amplitude by
+    their combined factor (sv_set_diag_combine) -- amplitudes within 1e-12 relative of the
+    reference oracle (the north star's FP64 tolerance), reports within 1e-12, and the
+    passes really are the combined kernels (fewer FP64 instructions than the exact ones)."""
+    from oracle import ref_engine
+    from oracle.ref_builders import adder
+    if case.startswith("adder"):
+        w = int(case[5:])
+        circ = adder(w, [(1 << w) - 1 - (0x2AAA & ((1 << w) - 1)), 0x1555 & ((1 << w) - 1)])[0]
+    else:
+        circ = random_circuit(rng, 18, 60)
+    prod = to_product(circ)
+    got = pb.run_circuit(prod, exact_diagonals=False)
+    want = ref_engine.run_circuit(circ)
+    ref = want.gathered_state()
+    dev = np.max(np.abs(got.gathered_state() - ref)) / np.max(np.abs(ref))
+    assert dev < 1e-12, dev
+    qx, qy, qz, _ = want.report
+    assert got.report.max_difference(pb.ExpectationReport(qx, qy, qz)) < 1e-12
+    assert got.device_stats["diag_combine"] is True
+    exact = pb.run_circuit(prod)
+    assert exact.device_stats["diag_combine"] is False
+    assert np.array_equal(exact.gathered_state(), ref)
+
+
 # ---- engine contracts ---------------------------------------------------------------------
 def test_scheduling_invariance(rng):
     circ = to_product(random_circuit(rng, 8, 18))
