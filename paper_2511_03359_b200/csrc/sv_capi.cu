@@ -248,7 +248,23 @@ int build_params2(const sv_op* ops, const PassPlan& pp, int n, int cfg, Fused2Pa
     P.cfg = cfg;
     P.kbits = K;
     P.rbits = RB;
-    const uint64_t tmask = tile_mask_for(pp.qmask, n, K);
+    // Tile = the pass's non-diagonal qubits + the fixed low qubits (HBM runs) + fillers.  The
+    // fillers avoid qubits the pass's diagonal ops test: a diagonal mask bit outside the tile
+    // is a tile-uniform condition (the whole tile skips the op), inside the tile it would be
+    // a thread position, where a lane condition still issues the warp's multiplies
+    // (SVB200_TILE_FILL=0: lowest qubits first, as before).
+    static const int fill_env = [] {
+        const char* e = std::getenv("SVB200_TILE_FILL");
+        return e ? std::atoi(e) : 1;
+    }();
+    uint64_t diag_used = 0;
+    for (int i : pp.ops)
+        if (ops[i].kind != SV_OP_1Q && ops[i].kind != SV_OP_2Q) diag_used |= ops[i].diag_mask;
+    uint64_t tmask = pp.qmask;
+    for (int q = 0; q < n && q < low_bits() && popcount64(tmask) < K; ++q) tmask |= 1ull << q;
+    for (int pass = fill_env ? 0 : 1; pass < 2; ++pass)
+        for (int q = 0; q < n && popcount64(tmask) < K; ++q)
+            if (pass == 1 || !((diag_used >> q) & 1)) tmask |= 1ull << q;
     P.n = n;
     P.tile_mask = tmask;
     P.n_tiles = 1ull << (n - K);
