@@ -20,8 +20,10 @@ layer of 33 gates applied to the 2**33-amplitude state resident in HBM.
                state per launch), its algorithmic bytes / average launch time
                from CUDA events bracketing every launch on its own stream.
   e2e        = the same metric through the public API: run_circuit() on a
-               Circuit built on the host (layer + measure-all), state
-               allocated and zeroed by the call, report copied back.
+               Circuit built on the host (the Hadamard layer + one random layer
+               + measure-all, i.e. the C2 circuit from |0..0>), state allocated
+               by the call, report copied back; e2e.dense = the same calls with
+               support tracking off (every tile of every pass).
   cpu_baseline = the reference algorithm (numpy port in oracle/, threaded over
                the box's cores) on a bounded sample of the same layers at N=24.
 
@@ -345,8 +347,9 @@ from tests.circuits import to_product
 n, layers, device, tile_bits = (int(x) for x in sys.argv[2:6])
 sys.path.insert(0, sys.argv[1])
 import bench
-lay = bench.workload_layers(n, layers)[1]
-circ = pb.Circuit(n, tuple(to_product(OCircuit(n, tuple(lay))).gates) + (pb.gates.measure_all(),))
+wl = bench.workload_layers(n, layers)
+circ = pb.Circuit(n, tuple(to_product(OCircuit(n, tuple(wl[0]))).gates) + tuple(to_product(OCircuit(n, tuple(wl[1]))).gates)
+                  + (pb.gates.measure_all(),))
 t_imp = time.perf_counter()
 import ctypes
 c = ctypes.c_int(0)
@@ -372,7 +375,7 @@ print(json.dumps({"first_call_s": t_first, "second_call_s": t_second, "context_s
 
 
 def cold_e2e(n: int, layers: int, device: int, tile_bits: int) -> dict:
-    """e2e of a FRESH process (run_circuit(layer + M), the same call as the warm e2e):
+    """e2e of a FRESH process (run_circuit(H layer + layer + M), the same call as the warm e2e):
     context creation, 2^N allocation, the pass kernels loaded from the persistent cubin
     cache this process filled (sv_jit.cu) -- no NVRTC -- and the measure-all."""
     import subprocess
@@ -388,12 +391,12 @@ def cold_e2e(n: int, layers: int, device: int, tile_bits: int) -> dict:
         return {"error": (r.stderr or r.stdout)[-400:], "parent_free_GiB": round(free.value / 2 ** 30, 1),
                 "child": child[-1] if child else None}
     d = json.loads(r.stdout.strip().splitlines()[-1])
-    gb = layer_bytes(workload_layers(n, layers)[1], n)
+    gb = layer_bytes(workload_layers(n, layers)[0], n) + layer_bytes(workload_layers(n, layers)[1], n)
     return {"value": round(gb / d["first_call_s"] / 1e9, 2), "unit": "GB/s",
             "first_call_s": round(d["first_call_s"], 4), "warm_second_call_s": round(d["second_call_s"], 4),
             "context_init_s": round(d["context_s"], 3), "import_s": round(d["import_s"], 2),
             "jit_disk_hits": d["jit"]["disk_hits"], "nvrtc_compiles": d["jit"]["compiled"],
-            "what": "first run_circuit(layer + M) in a new process after CUDA context creation: 2^N "
+            "what": "first run_circuit(H layer + layer + M) in a new process after CUDA context creation: 2^N "
                     "allocation, pass kernels from the on-disk cubin cache, measure-all, report to host"}
 
 
@@ -625,34 +628,47 @@ def run_b200(args):
         # warm e2e = a repeated call: every circuit runs once untimed first (its pass kernels
         # compiled then, as a second call in production finds them); the first call of a
         # fresh process is `cold_process` below
+        # the C2 circuit through the public API: the Hadamard layer on |0..0>, one random layer,
+        # measure-all (the Hadamard layer makes the state dense before the random layer)
         e2e_circs = []
         for j in range(args.e2e_steps):
             li = 1 + j % (len(layers) - 1) if len(layers) > 1 else 0
-            e2e_circs.append((li, pb.Circuit(n, tuple(layers[li]) + (pb.gates.measure_all(),))))
+            e2e_circs.append((li, pb.Circuit(n, tuple(layers[0]) + tuple(layers[li]) + (pb.gates.measure_all(),))))
         for li, circ in {li: c for li, c in e2e_circs}.items():
-            warm = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
-            del warm
+            for track in (True, False):
+                warm = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, track_support=track)
+                del warm
             jit_wait()
+
+        def e2e_pass(track):
+            t_sum, b_sum, cl = 0.0, 0, []
+            for li, circ in e2e_circs:
+                t0 = time.perf_counter()
+                res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, track_support=track)
+                _ = res.report.qz[0]
+                dt = time.perf_counter() - t0
+                t_sum += dt
+                b_sum += lbytes[0] + lbytes[li]
+                cl.append({"layers": [0, li], "s": round(dt, 4), "gates": len(circ.gates) - 1,
+                           "launches": res.device_stats.get("kernel_launches")})
+                del res
+            return t_sum, b_sum, cl
+
         h2d0, d2h0 = nat.transfer_bytes()
-        calls = []
-        for j, (li, circ) in enumerate(e2e_circs):
-            t0 = time.perf_counter()
-            res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
-            _ = res.report.qz[0]
-            dt = time.perf_counter() - t0
-            t_e2e += dt
-            e2e_bytes += lbytes[li]
-            calls.append({"layer": li, "s": round(dt, 4), "gates": len(circ.gates) - 1,
-                          "launches": res.device_stats.get("kernel_launches")})
-            del res
+        t_e2e, e2e_bytes, calls = e2e_pass(True)
         h2d1, d2h1 = nat.transfer_bytes()
+        t_dense, dense_bytes, _ = e2e_pass(False)
         t_e2e = max_over_ranks(dist, t_e2e)
+        t_dense = max_over_ranks(dist, t_dense)
         e2e = {"value": round(sum_over_ranks(dist, e2e_bytes) / t_e2e / 1e9, 2), "unit": "GB/s",
                "h2d_bytes_per_step": (h2d1 - h2d0) // args.e2e_steps,
                "d2h_bytes_per_step": (d2h1 - d2h0) // args.e2e_steps,
                "calls": calls,
-               "what": "run_circuit(layer + M): allocate + zero 2^N state, fused layer, measure-all, "
-                       "report to host; wall clock per call"}
+               "dense": {"value": round(sum_over_ranks(dist, dense_bytes) / t_dense / 1e9, 2), "unit": "GB/s",
+                         "what": "the same calls with track_support=False: every tile of every pass"},
+               "what": "run_circuit(H layer + random layer + M) on |0..0>: allocate 2^N state, fused passes "
+                       "(support tracking: the Hadamard layer's early passes read only the tiles that can be "
+                       "nonzero), measure-all, report to host; wall clock per call"}
 
     # adder circuit time (BASELINE config 3: build_adder(16, [47302, 18233]), N=32 FP64, public API)
     adder = None
@@ -668,6 +684,7 @@ def run_b200(args):
         res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
         t_adder = time.perf_counter() - t0
         kat = all(abs(res.report.qz[q] - 1.0) < 1e-12 for q in regs["R2"])
+        rep_support = res.device_stats.get("support")
         del res
         # device view of a third run: the fused passes timed with CUDA events next to their
         # HBM and FP64 floors (the adder's CPHASE runs make most passes FP64-bound)
@@ -688,8 +705,18 @@ def run_b200(args):
                             "fp64_per_amplitude": a_roof["fp64_per_amplitude"]},
                  "what": "run_circuit wall clock incl. allocation, zero state, fused passes, measure-all "
                          "(second run: specialised pass kernels compiled; first_run_seconds: cold); passes: "
-                         "a third run's fused passes (CUDA events) vs max(HBM, FP64) floors per pass"}
+                         "a third run's fused passes (CUDA events) vs max(HBM, FP64) floors per pass; the "
+                         "adder's state stays inside a 2^k-amplitude support (basis-state inputs), which the "
+                         "passes and the measurement track; dense_seconds: track_support=False"}
         rep_exact = res.report
+        del res
+        # dense: every tile of every pass (track_support=False), the work the reference does
+        pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, track_support=False)
+        jit_wait()
+        t0 = time.perf_counter()
+        res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, track_support=False)
+        adder["dense_seconds"] = round(time.perf_counter() - t0, 4)
+        adder["support"] = rep_support
         del res
         # the same circuit with combined diagonal runs (exact_diagonals=False: within 1e-12 of
         # the reference, not bit-identical): one multiply per register mask per CPHASE run

@@ -312,6 +312,15 @@ int sv_jit_prepare_opts(int n_qubits, int mode, const sv_op* ops, int n_ops, int
  * instead of one rounding per gate -- amplitudes within 1e-12 relative of the
  * reference (the north star's FP64 tolerance), NOT bit-identical.  Default off. */
 int sv_set_diag_combine(sv_handle h, int on);
+/* Support tracking (default off; run_circuit turns it on for its state): after
+ * sv_zero_state[_lazy](h, unit) the handle records which index bits may differ from
+ * unit's -- freed by non-monomial gates, moved by monomials, untouched by diagonal
+ * gates -- and fused passes run only the tiles that can hold nonzero amplitudes.
+ * Results are identical (the skipped amplitudes are zeros that stay zero); writes
+ * through the raw device pointer require turning tracking off first.  sv_import,
+ * sv_apply_fused_chunk and all-zero states turn it off. */
+int sv_set_support_tracking(sv_handle h, int on);
+int sv_support_info(sv_handle h, int* on, uint64_t* free_mask, uint64_t* val, uint64_t* tiles_skipped);
 /* the pass split sv_apply_fused uses for ops: ends[p] = one past the last op of pass p;
  * returns the number of passes (also queues their specialised kernels) */
 int sv_plan_passes(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int* ends, int cap);

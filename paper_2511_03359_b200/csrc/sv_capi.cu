@@ -36,6 +36,7 @@ int g_fused_v2 = 9;      // default: auto (config 6 = 2^11 tiles, 3 CTAs/SM; con
 int g_seg_limit = 0;        // > 0: passes needing more segments fall back to v1
 std::mutex g_timing_mu;
 std::vector<TimedPass> g_timed;
+std::atomic<unsigned long long> g_support_tiles_skipped{0};   // tiles support tracking left out
 
 int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -227,6 +228,46 @@ int classify(const double* m, int dim, uint32_t* mono) {
         return 2;
     }
     return real ? 1 : 0;
+}
+
+// ---- support tracking (sv_set_support_tracking) ---------------------------------------------
+// Amplitudes outside {i : (i & ~free) == val} are exactly zero: a state starts as a basis state
+// (free = 0), a non-monomial gate frees its qubits, a monomial on fixed qubits moves val, a
+// diagonal gate changes nothing.  A fused pass then runs only the tiles whose fixed
+// out-of-tile bits equal val (the chunked-launch path): the others hold zeros and stay zeros
+// (+-0: identical under np.array_equal, the parity tests' comparison).
+struct Support {
+    bool on = false;
+    uint64_t free = 0, val = 0;
+};
+static thread_local Support* g_support = nullptr;   // the handle's, for one fused_impl call
+struct SupportScope {
+    Support* prev;
+    explicit SupportScope(Support* s) : prev(g_support) { g_support = (s && s->on) ? s : nullptr; }
+    ~SupportScope() { g_support = prev; }
+};
+static bool czero(const double* m, int idx) { return m[2 * idx] == 0.0 && m[2 * idx + 1] == 0.0; }
+static void support_apply(Support& s, const sv_op& o) {
+    if (!s.on || (o.kind != SV_OP_1Q && o.kind != SV_OP_2Q)) return;   // diagonal: support unchanged
+    if (o.kind == SV_OP_1Q) {
+        const uint64_t b = 1ull << o.qa;
+        if (s.free & b) return;
+        const int c = (s.val & b) ? 1 : 0;                 // the column the fixed bit selects
+        const bool r0 = !czero(o.m, 0 * 2 + c), r1 = !czero(o.m, 1 * 2 + c);
+        if (r0 && r1) s.free |= b;
+        else if (r1) s.val |= b;
+        else if (r0) s.val &= ~b;
+        else s.free |= b;                                  // a zero column: conservative
+        return;
+    }
+    const uint64_t ba = 1ull << o.qa, bb = 1ull << o.qb;
+    if ((s.free & ba) || (s.free & bb)) { s.free |= ba | bb; return; }
+    const int c = ((s.val & ba) ? 1 : 0) + ((s.val & bb) ? 2 : 0);   // basis index bit(qa) + 2 bit(qb)
+    int rows = 0, r = -1;
+    for (int row = 0; row < 4; ++row)
+        if (!czero(o.m, row * 4 + c)) { ++rows; r = row; }
+    if (rows != 1) { s.free |= ba | bb; return; }
+    s.val = (s.val & ~(ba | bb)) | ((r & 1) ? ba : 0) | ((r & 2) ? bb : 0);
 }
 
 // combined diagonal runs (sv_set_diag_combine): set by the C entry points for the duration of
@@ -588,10 +629,54 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
             count_h2d(sizeof(FusedParams));
             return launch_fused(psi, mode, P, st);
         };
+        // after a launch: the support moves through the pass's ops (in order)
+        auto advance_support = [&]() {
+            if (g_support)
+                for (int i : cur.ops) support_apply(*g_support, ops[i]);
+        };
+        double pass_bytes = 2.0 * (double)n_elems * (mode == SV_FP32 ? 8.0 : 16.0);
         if (use_v3 && build_params2(ops, cur, n, cfg, P2) == 0 &&
             (g_seg_limit <= 0 || P2.n_segs <= g_seg_limit)) {
             P2.storage = mode;
             P2.vinit = -2;
+            if (g_support && !(init && *init != -2)) {
+                // only the tiles whose fixed out-of-tile bits read val can be nonzero
+                const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+                const uint64_t fixed_out = ~g_support->free & ~P2.tile_mask & all;
+                if (fixed_out) {
+                    uint64_t cm = 0, cp = 0;
+                    int j = 0;
+                    for (int q = 0; q < n; ++q) {
+                        if ((P2.tile_mask >> q) & 1) continue;
+                        if ((fixed_out >> q) & 1) {
+                            cm |= 1ull << j;
+                            if ((g_support->val >> q) & 1) cp |= 1ull << j;
+                        }
+                        ++j;
+                    }
+                    const uint64_t full_tiles = P2.n_tiles;
+                    P2.cmask_t = cm;
+                    P2.cpat_t = cp;
+                    P2.n_tiles >>= __builtin_popcountll(cm);
+                    const int jr = jit_launch_fused(psi, P2, st);
+                    if (jr < 0) return cuda_fail(cudaErrorLaunchFailure, "fused pass launch");
+                    if (jr == 0) {
+                        g_support_tiles_skipped += full_tiles - P2.n_tiles;
+                        if (g_timing) {
+                            cudaEventRecord(ev1, st);
+                            std::lock_guard<std::mutex> lk(g_timing_mu);
+                            g_timed.push_back({ev0, ev1, pass_bytes * (double)P2.n_tiles / (double)full_tiles});
+                        }
+                        advance_support();
+                        cur = PassPlan();
+                        return SV_OK;
+                    }
+                    // specialised kernel not compiled yet: the whole state through the generic one
+                    P2.cmask_t = 0;
+                    P2.cpat_t = 0;
+                    P2.n_tiles = full_tiles;
+                }
+            }
             if (init && *init != -2) {
                 P2.vinit = *init;
                 const int jr0 = jit_launch_fused(psi, P2, st);
@@ -603,6 +688,7 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
                         std::lock_guard<std::mutex> lk(g_timing_mu);
                         g_timed.push_back({ev0, ev1, 1.0 * (double)n_elems * (mode == SV_FP32 ? 8.0 : 16.0)});
                     }
+                    advance_support();
                     cur = PassPlan();
                     return SV_OK;
                 }
@@ -634,9 +720,10 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
         if (g_timing) {
             cudaEventRecord(ev1, st);
             std::lock_guard<std::mutex> lk(g_timing_mu);
-            g_timed.push_back({ev0, ev1, 2.0 * (double)n_elems * (mode == SV_FP32 ? 8.0 : 16.0)});
+            g_timed.push_back({ev0, ev1, pass_bytes});
         }
         if (e != cudaSuccess) return cuda_fail(e, "fused pass launch");
+        advance_support();
         cur = PassPlan();
         return SV_OK;
     };
@@ -667,8 +754,14 @@ int g_measure_reserve = 0;
 // FP64 measurement with the register-resident pass (sv_measure3.cu): tiles of 2^K
 // (K = 12: 1 + ceil((n - 12) / 7) passes), segments of 4 register positions cover the
 // cross terms of the pass's new tile qubits.
+// sup (tracked support, FP64): amplitudes outside {i : (i & ~free) == val} are zero, so the
+// passes read only the tiles inside it, cross terms are formed for the free qubits only (a
+// fixed qubit's partner amplitudes are zero) and a fixed qubit's Qz is the norm or 0.
 int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cross, double* dev_partials,
-                  size_t partial_cap, cudaStream_t st, bool byte = false) {
+                  size_t partial_cap, cudaStream_t st, bool byte = false, const Support* sup = nullptr) {
+    const uint64_t all = (n >= 64) ? ~0ull : ((1ull << n) - 1ull);
+    const bool tracked = sup && sup->on && !byte;
+    const uint64_t freem = tracked ? (sup->free & all) : all, fixv = tracked ? (sup->val & ~sup->free & all) : 0;
     int dev = 0;
     cudaGetDevice(&dev);
     static int kenv = -1;
@@ -699,11 +792,15 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
     for (int q = K; q < n;) {
         uint64_t t = (1ull << bmin) - 1ull;
         int c = 0;
-        while (q < n && c < K - bmin) { t |= 1ull << q; ++q; ++c; }
+        while (q < n && c < K - bmin) {
+            if ((freem >> q) & 1) { t |= 1ull << q; ++c; }   // fixed qubits need no cross term
+            ++q;
+        }
+        if (!c) break;
         for (int f = bmin; popcount64(t) < K; ++f) t |= 1ull << f;
         passes.push_back(t);
     }
-    uint64_t done = 0;
+    uint64_t done = ~freem & all;   // fixed qubits: cross terms are zero
     int rc = SV_OK;
     static thread_local Measure3Params P;
     for (size_t pi = 0; pi < passes.size() && rc == SV_OK; ++pi) {
@@ -718,9 +815,11 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
         int j = 0, o = 0;
         for (int q = 0; q < n; ++q) {
             if ((tmask >> q) & 1) P.tq[j++] = (int8_t)q;
-            else P.oq[o++] = (int8_t)q;
+            else if ((freem >> q) & 1) P.oq[o++] = (int8_t)q;   // tiles vary in the free out-of-tile bits
         }
         P.n_out = o;
+        P.base_const = fixv & ~tmask;                             // and carry the fixed ones
+        P.n_tiles = 1ull << o;
         int b = 0;
         while (b < K && P.tq[b] == b) ++b;
         P.b = b;
@@ -832,19 +931,23 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
                 for (int i = 0; i < K; ++i) ones[P.tq[i]] += row[1 + i];
                 for (int jj = 0; jj < o; ++jj) ones[P.oq[jj]] += row[1 + K + jj];
             }
-            for (int i : cpos) {
-                cross[2 * P.tq[i]] += row[1 + n + 2 * i];
-                cross[2 * P.tq[i] + 1] += row[2 + n + 2 * i];
+            for (int i : cpos) {   // the kernel's row: norm, K tile ones, n_out outside ones, cross
+                cross[2 * P.tq[i]] += row[1 + K + o + 2 * i];
+                cross[2 * P.tq[i] + 1] += row[2 + K + o + 2 * i];
             }
         }
         for (int i : cpos) done |= 1ull << P.tq[i];
     }
+    if (tracked && rc == SV_OK)   // fixed qubits outside the first pass's tile: every amplitude shares the bit
+        for (int q = 0; q < n; ++q)
+            if (!((freem >> q) & 1) && !((passes[0] >> q) & 1)) ones[q] = ((fixv >> q) & 1) ? *norm : 0.0;
     if (owned) cudaFreeAsync(partials, st);
     return rc;
 }
 
 int measure_impl(const void* psi, uint64_t n_elems, int mode, double* norm, double* ones,
-                 double* cross, double* dev_partials, size_t partial_cap, cudaStream_t st) {
+                 double* cross, double* dev_partials, size_t partial_cap, cudaStream_t st,
+                 const Support* sup = nullptr) {
     if (!valid_fp_mode(mode) && mode != SV_BYTE) return fail(SV_EVALUE, "unknown storage mode");
     if (!is_pow2(n_elems)) return fail(SV_EVALUE, "measurement needs a power-of-two buffer");
     const int n = log2u(n_elems);
@@ -866,7 +969,7 @@ int measure_impl(const void* psi, uint64_t n_elems, int mode, double* norm, doub
         use3 = (e && std::atoi(e) == 0) ? 0 : 1;
     }
     if (use3 && mode == SV_FP64 && n >= 16 && (reinterpret_cast<uintptr_t>(psi) & 15) == 0)
-        return measure3_impl(psi, n, norm, ones, cross, dev_partials, partial_cap, st);
+        return measure3_impl(psi, n, norm, ones, cross, dev_partials, partial_cap, st, false, sup);
     if (use3 && mode == SV_BYTE && n >= 16)
         return measure3_impl(psi, n, norm, ones, cross, dev_partials, partial_cap, st, true);
     const int bmin = k >= 5 ? 5 : k;
@@ -973,6 +1076,8 @@ struct sv_state {
     size_t partial_cap;
     int64_t lazy = -2;      // sv_zero_state_lazy: -1 all zeros / unit index not yet written, -2 none
     int diag_combine = 0;   // sv_set_diag_combine
+    int track = 0;          // sv_set_support_tracking
+    Support sup;            // valid while sup.on
 };
 extern "C" {
 static int materialize(sv_handle h);
@@ -1168,6 +1273,11 @@ int sv_info(sv_handle h, int* device, int* n_qubits, int* mode, void** dev_ptr, 
 
 int sv_zero_state(sv_handle h, int64_t unit) {
     DeviceGuard g(h->device);
+    if (h->lazy == -2) {   // (materialize() keeps the support recorded by sv_zero_state_lazy)
+        h->sup.on = h->track && unit >= 0;
+        h->sup.free = 0;
+        h->sup.val = unit >= 0 ? (uint64_t)unit : 0;
+    }
     h->lazy = -2;
     const size_t eb = elem_bytes(h->mode);
     const uint64_t n = 1ull << h->n;
@@ -1190,6 +1300,23 @@ int sv_zero_state(sv_handle h, int64_t unit) {
 int sv_zero_state_lazy(sv_handle h, int64_t unit) {
     if (unit >= (int64_t)(1ull << h->n)) return fail(SV_EINDEX, "unit index %lld outside the state", (long long)unit);
     h->lazy = unit < 0 ? -1 : unit;
+    h->sup.on = h->track && unit >= 0;
+    h->sup.free = 0;
+    h->sup.val = unit >= 0 ? (uint64_t)unit : 0;
+    return SV_OK;
+}
+
+int sv_set_support_tracking(sv_handle h, int on) {
+    h->track = on ? 1 : 0;
+    if (!on) h->sup.on = false;
+    return SV_OK;
+}
+
+int sv_support_info(sv_handle h, int* on, uint64_t* free_mask, uint64_t* val, uint64_t* tiles_skipped) {
+    if (on) *on = h->sup.on ? 1 : 0;
+    if (free_mask) *free_mask = h->sup.free;
+    if (val) *val = h->sup.val;
+    if (tiles_skipped) *tiles_skipped = g_support_tiles_skipped.load();
     return SV_OK;
 }
 
@@ -1202,12 +1329,29 @@ static int materialize(sv_handle h) {
 int sv_apply_1q(sv_handle h, int q, const double* m8) {
     DeviceGuard g(h->device);
     if (int rc = materialize(h)) return rc;
-    return svk_apply_1q(h->ptr, 1ull << h->n, h->mode, q, m8, h->stream);
+    const int rc = svk_apply_1q(h->ptr, 1ull << h->n, h->mode, q, m8, h->stream);
+    if (rc == SV_OK && h->sup.on) {
+        sv_op o{};
+        o.kind = SV_OP_1Q;
+        o.qa = q;
+        std::memcpy(o.m, m8, 8 * sizeof(double));
+        support_apply(h->sup, o);
+    }
+    return rc;
 }
 int sv_apply_2q(sv_handle h, int qa, int qb, const double* m32) {
     DeviceGuard g(h->device);
     if (int rc = materialize(h)) return rc;
-    return svk_apply_2q(h->ptr, 1ull << h->n, h->mode, qa, qb, m32, h->stream);
+    const int rc = svk_apply_2q(h->ptr, 1ull << h->n, h->mode, qa, qb, m32, h->stream);
+    if (rc == SV_OK && h->sup.on) {
+        sv_op o{};
+        o.kind = SV_OP_2Q;
+        o.qa = qa;
+        o.qb = qb;
+        std::memcpy(o.m, m32, 32 * sizeof(double));
+        support_apply(h->sup, o);
+    }
+    return rc;
 }
 int sv_apply_diag(sv_handle h, uint64_t mask, const double* f2) {
     DeviceGuard g(h->device);
@@ -1308,6 +1452,7 @@ int sv_apply_fused_chunk(sv_handle h, const sv_op* ops, int n_ops, int tile_bits
     if (int rc = materialize(h)) return rc;
     if (n_ops <= 0) return SV_OK;
     if ((chunk_pattern & ~chunk_mask) || (chunk_mask >> h->n)) return fail(SV_EINDEX, "chunk mask outside the state");
+    h->sup.on = false;   // chunked passes belong to the distributed layer (peers write this buffer)
     return fused_impl(h->ptr, 1ull << h->n, h->mode, ops, n_ops, tile_bits, h->stream, nullptr, chunk_mask,
                       chunk_pattern);
 }
@@ -1322,6 +1467,7 @@ int sv_apply_fused(sv_handle h, const sv_op* ops, int n_ops, int tile_bits) {
     DeviceGuard g(h->device);
     if (n_ops <= 0) return SV_OK;
     CombineScope cs(h->diag_combine);
+    SupportScope ss(&h->sup);
     if (h->lazy != -2) {   // lazy |unit>: the first pass generates its input tiles
         int64_t init = h->lazy;
         const int rc = fused_impl(h->ptr, 1ull << h->n, h->mode, ops, n_ops, tile_bits, h->stream, nullptr, 0, 0,
@@ -1335,7 +1481,7 @@ int sv_measure(sv_handle h, double* norm, double* ones, double* cross) {
     DeviceGuard g(h->device);
     if (int rc = materialize(h)) return rc;
     return measure_impl(h->ptr, 1ull << h->n, h->mode, norm, ones, cross, h->partials, h->partial_cap,
-                        h->stream);
+                        h->stream, h->sup.on ? &h->sup : nullptr);
 }
 
 int sv_export(sv_handle h, void* host, uint64_t first, uint64_t count) {
@@ -1354,6 +1500,7 @@ int sv_export(sv_handle h, void* host, uint64_t first, uint64_t count) {
 int sv_import(sv_handle h, const void* host, uint64_t first, uint64_t count) {
     DeviceGuard g(h->device);
     if (int rc = materialize(h)) return rc;
+    h->sup.on = false;   // arbitrary values
     const uint64_t n = 1ull << h->n;
     if (first > n || count > n - first) return fail(SV_EINDEX, "import range outside the state");
     const size_t eb = elem_bytes(h->mode);

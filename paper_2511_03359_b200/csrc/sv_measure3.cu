@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(1 << (KB - RB), MINB)
 
     auto tile_base = [&](uint64_t t) {
         return p.base_tab[0][t & 255] | p.base_tab[1][(t >> 8) & 255] | p.base_tab[2][(t >> 16) & 255] |
-               p.base_tab[3][(t >> 24) & 255];
+               p.base_tab[3][(t >> 24) & 255] | p.base_const;
     };
     auto prefetch = [&](uint64_t t, cplx* dst) {
         const c64s* g = psi + tile_base(t) + go_tid;

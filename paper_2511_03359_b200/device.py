@@ -106,6 +106,18 @@ class DeviceState:
         nat.check(nat.load().sv_set_diag_combine(self.handle, 1 if on else 0))
         self.diag_combine = bool(on)
 
+    def set_support_tracking(self, on: bool) -> None:
+        """Record which index bits may differ from the initial basis state (sv_set_support_tracking):
+        fused passes then skip the tiles that can only hold zeros.  Call before zero()."""
+        nat.check(nat.load().sv_set_support_tracking(self.handle, 1 if on else 0))
+
+    def support_info(self) -> dict:
+        on, free, val, skipped = ctypes.c_int(0), ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_uint64(0)
+        nat.check(nat.load().sv_support_info(self.handle, ctypes.byref(on), ctypes.byref(free), ctypes.byref(val),
+                                             ctypes.byref(skipped)))
+        return {"tracking": bool(on.value), "free_qubits": bin(free.value).count("1"),
+                "tiles_skipped_total": int(skipped.value)}
+
     def _touch(self, launches: int = 1):
         self.version += 1
         self.launches += launches

@@ -39,6 +39,9 @@ from .state import LocalState, PrecisionMode
 from .transport import ExchangeToken, Transport, TransportError
 
 FUSE_QUEUE_LIMIT = 1024
+# SVB200_SUPPORT=0: run_circuit processes every tile of every pass (no support tracking)
+import os as _os
+_SUPPORT_TRACKING = _os.environ.get("SVB200_SUPPORT", "1") != "0"
 
 
 @dataclass
@@ -128,7 +131,8 @@ def run_circuit(circuit: Circuit, *, ranks: int = 1, local_qubits: int | None = 
                 mode: PrecisionMode = PrecisionMode.FP64, tier_config=None,
                 rank_order_seed: int | None = None, transport_factory=Transport,
                 device: int = 0, fuse: bool = True, tile_bits: int = 12,
-                tier_execute: bool | None = None, exact_diagonals: bool = True) -> RunResult:
+                tier_execute: bool | None = None, exact_diagonals: bool = True,
+                track_support: bool = True) -> RunResult:
     """svsim.run_circuit (engine.py:82-105) on one B200.
 
     tier_config (svsim TierConfig or tier.TierConfig): the reference's staging plan and
@@ -139,7 +143,13 @@ def run_circuit(circuit: Circuit, *, ranks: int = 1, local_qubits: int | None = 
     exact_diagonals=False (FP64, fused, resident): runs of consecutive diagonal gates in a
     fused pass multiply each amplitude by their combined factor -- amplitudes within 1e-12
     relative of the reference (the north star's FP64 tolerance) instead of bit-identical;
-    the QFT adder's CPHASE runs then cost one multiply per register mask, not per gate."""
+    the QFT adder's CPHASE runs then cost one multiply per register mask, not per gate.
+
+    track_support (FP64/FP32, one GPU, default on): the state starts as |0..0>; the device
+    records which index bits may differ from it (freed by non-monomial gates, moved by
+    monomials, untouched by diagonal gates) and fused passes and the measurement read
+    only the tiles that can hold nonzero amplitudes.  The skipped amplitudes are zeros
+    that stay zero, so results are identical; False processes every tile."""
     validate_circuit(circuit)
     if ranks < 1 or ranks & (ranks - 1):
         raise ValueError("rank count must be a power of two")
@@ -157,7 +167,7 @@ def run_circuit(circuit: Circuit, *, ranks: int = 1, local_qubits: int | None = 
     combine = (not exact_diagonals and fuse and mode is PrecisionMode.FP64
                and not (tier is not None and tier.execute))
     eng = _Engine(circuit, layout, mode, rank_order_seed, transport_factory, device, fuse, tile_bits, tier,
-                  combine_diag=combine)
+                  combine_diag=combine, support_tracking=track_support and _SUPPORT_TRACKING)
     eng.run()
     eng.launches = nat.launch_count() - launches0
     return RunResult(circuit, layout, mode, eng.states, eng.ledgers, eng.report, eng.codebook,
@@ -191,7 +201,7 @@ class _TierRun:
 
 class _Engine:
     def __init__(self, circuit, layout, mode, rank_order_seed, transport_factory, device, fuse,
-                 tile_bits, tier=None, combine_diag=False):
+                 tile_bits, tier=None, combine_diag=False, support_tracking=True):
         self.circuit = circuit
         self.combine_diag = combine_diag
         self.tier = tier
@@ -224,6 +234,8 @@ class _Engine:
             self.dev = DeviceState(circuit.n_qubits, mode, device=device)
             if combine_diag:
                 self.dev.set_diag_combine(True)
+            # the state starts as |0..0>: fused passes skip the tiles that can only hold zeros
+            self.dev.set_support_tracking(support_tracking)
         if mode is PrecisionMode.BYTE:
             self.dev.zero(0)
         else:   # the first fused pass generates |0..0> instead of reading a written state
@@ -389,6 +401,7 @@ class _Engine:
     def stats(self) -> dict:
         out = {"device": self.dev.device, "kernel_launches": getattr(self, "launches", self.dev.launches),
                "diag_combine": self.combine_diag,
+               "support": self.dev.support_info() if hasattr(self.dev, "support_info") else None,
                "gates_applied": self.gates_applied, "fused": self.fuse and self.mode is not PrecisionMode.BYTE,
                "physical_link_bytes": 0}
         if self.mode is PrecisionMode.BYTE:

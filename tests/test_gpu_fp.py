@@ -230,6 +230,39 @@ def test_combined_diagonal_runs_within_tolerance(rng, case):
     assert np.array_equal(exact.gathered_state(), ref)
 
 
+def test_support_tracking_skips_zero_tiles_bit_exact():
+    """run_circuit tracks the support of its |0..0> state: the adder's state lives in the
+    superposed register (the other register stays a basis state), so most tiles of most
+    passes are left out -- and the state is still bit-identical to the oracle's and to a
+    run with tracking off (SVB200_SUPPORT=0 semantics, via the DeviceState switch)."""
+    from oracle import ref_engine
+    from oracle.ref_builders import adder
+    w = 9
+    circ = adder(w, [0x155 & ((1 << w) - 1), 0x0AB & ((1 << w) - 1)])[0]
+    res = pb.run_circuit(to_product(circ))
+    want = ref_engine.run_circuit(circ)
+    assert np.array_equal(res.gathered_state(), want.gathered_state())
+    sup = res.device_stats["support"]
+    assert sup["tracking"] and sup["free_qubits"] < circ.n_qubits
+    assert sup["tiles_skipped_total"] > 0
+    qx, qy, qz, _ = want.report
+    assert res.report.max_difference(pb.ExpectationReport(qx, qy, qz)) < 1e-12
+    # monomials on fixed qubits move the support, they do not free it
+    from paper_2511_03359_b200.device import DeviceState
+    dev = DeviceState(14, pb.PrecisionMode.FP64)
+    dev.set_support_tracking(True)
+    dev.zero(0)
+    dev.apply_1q(3, pb.gates.unitary_matrix(pb.gates.x(3)))
+    dev.apply_2q(3, 7, pb.gates.unitary_matrix(pb.gates.cnot(3, 7)))
+    assert dev.support_info()["free_qubits"] == 0
+    dev.apply_1q(5, pb.gates.H_MATRIX)
+    assert dev.support_info()["free_qubits"] == 1
+    out = dev.export()
+    assert out[(1 << 3) | (1 << 7)] != 0 and out[(1 << 3) | (1 << 7) | (1 << 5)] != 0
+    assert np.count_nonzero(out) == 2
+    dev.free()
+
+
 # ---- engine contracts ---------------------------------------------------------------------
 def test_scheduling_invariance(rng):
     circ = to_product(random_circuit(rng, 8, 18))
