@@ -141,6 +141,10 @@ typedef struct {
     int32_t ph_zero_out;         /* 1: this pass's phase table has one entry, every output phase
                                   * index is 0 and the output phase plane already holds zeros:
                                   * not written */
+    uint64_t sup_fixed;          /* support: bits every nonzero amplitude shares with sup_val (0 =
+                                  * dense); both plane buffers must hold zeros outside it and it
+                                  * may only grow (byte_state.py tracks it) */
+    uint64_t sup_val;
 } svb_gate_desc;
 
 int svb_create(int device, int n_qubits, sv_bhandle* out);
@@ -155,6 +159,9 @@ int svb_set_tables(sv_bhandle h, const double* mags, int n_mag, const double* th
                    const double* uy, int n_ph);
 /* one pass: reads the current planes, writes the pending planes */
 int svb_gate(sv_bhandle h, const svb_gate_desc* g);
+/* svb_measure over a tracked support (sup_fixed / sup_val as in svb_gate_desc) */
+int svb_measure_support(sv_bhandle h, uint64_t sup_fixed, uint64_t sup_val, double* norm, double* ones,
+                        double* cross);
 /* diagonal gate, final write pass (tables fixed: saturated, or scanned and
  * merged first): rewrites only the selected amplitudes of the CURRENT planes
  * (engine.py:186-225 encode step of a diagonal gate; no commit follows) */

@@ -83,6 +83,7 @@ _SIGNATURES = {
     "svb_import": ([_P, _P, _P, _U64, _U64], _I),
     "svb_decode": ([_P, _D, _U64, _U64], _I),
     "svb_measure": ([_P, _D, _D, _D], _I),
+    "svb_measure_support": ([_P, _U64, _U64, _D, _D, _D], _I),
     "svb_encode_values": ([_P, _D, _U64, _P, _P, _I], _I),
     "sv_ipc_handle": ([_P, _P], _I),
     "sv_ipc_open": ([_I, _P, ctypes.POINTER(_P)], _I),

@@ -47,7 +47,8 @@ class SvbGateDesc(ctypes.Structure):
                 ("mag_cut", ctypes.c_double), ("ph_cut", ctypes.c_double),
                 ("scan_only", ctypes.c_int32), ("rank_bits", ctypes.c_int32),
                 ("phys_base", ctypes.c_uint64), ("lbit", ctypes.c_int8 * 16),
-                ("ph_zero_in", ctypes.c_int32), ("ph_zero_out", ctypes.c_int32)]
+                ("ph_zero_in", ctypes.c_int32), ("ph_zero_out", ctypes.c_int32),
+                ("sup_fixed", ctypes.c_uint64), ("sup_val", ctypes.c_uint64)]
 
 
 class ByteDeviceState:
@@ -94,6 +95,9 @@ class ByteDeviceState:
         nat.check(nat.load().svb_zero_state(self.handle, -1 if unit_index is None else unit_index))
         self.version += 1
         self.ph_zero = PHASE_PLANE_SKIP and len(self.codebook.thetas) == 1
+        # support of a basis state: every other bit fixed (all zeros: no tracking)
+        self.sup_free = 0 if unit_index is not None else (1 << self.n_qubits) - 1
+        self.sup_val = unit_index or 0
 
     def export_storage(self, first: int, count: int):
         mi = np.empty(count, dtype=np.uint8)
@@ -109,6 +113,7 @@ class ByteDeviceState:
                                         pi.ctypes.data_as(ctypes.c_void_p), first, mi.size))
         self.version += 1
         self.ph_zero = False
+        self.sup_free = (1 << self.n_qubits) - 1   # arbitrary bytes: dense
 
     def decode(self, first: int = 0, count: int | None = None) -> np.ndarray:
         self.sync_tables()
@@ -128,7 +133,14 @@ class ByteDeviceState:
         norm = np.zeros(1)
         ones = np.zeros(max(n, 1))
         cross = np.zeros(2 * max(n, 1))
-        nat.check(nat.load().svb_measure(self.handle, nat.dptr(norm), nat.dptr(ones), nat.dptr(cross)))
+        full = (1 << self.n_qubits) - 1
+        free = getattr(self, "sup_free", full)
+        if free != full:   # tracked support: only its tiles are read
+            fixed = full & ~free
+            nat.check(nat.load().svb_measure_support(self.handle, fixed, getattr(self, "sup_val", 0) & fixed,
+                                                     nat.dptr(norm), nat.dptr(ones), nat.dptr(cross)))
+        else:
+            nat.check(nat.load().svb_measure(self.handle, nat.dptr(norm), nat.dptr(ones), nat.dptr(cross)))
         self.launches += 2
         return float(norm[0]), ones[:n].copy(), cross[0:2 * n:2] + 1j * cross[1:2 * n:2]
 
@@ -328,6 +340,8 @@ class ByteEngineState(ByteDeviceState):
         self.passes = 0
         self.reencodes = 0
         self.host_fixes = 0
+        self.sup_free = (1 << n_qubits) - 1        # dense until zero() records a basis state
+        self.sup_val = 0
         self.scan_first = False         # the previous gate grew a table: scan before encoding
 
     def _desc(self, gate, plan) -> SvbGateDesc:
@@ -351,6 +365,11 @@ class ByteEngineState(ByteDeviceState):
         set_logical_bits(d, self.layout, None, 0)
         d.producer = -1
         d.mag_cut = d.ph_cut = _BIG
+        # support before the gate (csrc sv_byte.cu: the vector passes visit only its items; both
+        # plane buffers hold zeros outside it, so it may only grow -- monomials free their qubits)
+        all_bits = (1 << self.n_qubits) - 1
+        d.sup_fixed = all_bits & ~self.sup_free
+        d.sup_val = self.sup_val & d.sup_fixed
         return d
 
     def _collect_rank(self, d: SvbGateDesc, rank: int):
@@ -444,3 +463,6 @@ class ByteEngineState(ByteDeviceState):
                 ui = np.concatenate([u[0] for u in unsure])
                 uv = np.concatenate([u[1] for u in unsure])
         self.host_fixes += self.finish_gate(ui, uv, final_in_place)
+        if not g.is_diagonal(gate):
+            for q in gate.qubits:
+                self.sup_free |= 1 << q

@@ -629,6 +629,15 @@ __device__ __forceinline__ uint4 ld16z(const uint8_t* p, uint64_t off) {
 // their own (scan passes read 32 bytes per item); the prefetched lines turn the
 // register loads into L2 hits.  No registers, no shared memory.
 constexpr int kL2Ahead = 4;
+// x with a bit inserted at every position of `holes` (ascending), valued by `vals`: maps a
+// compact work-item index to its index when the bits under `holes` are fixed (a support)
+__device__ __forceinline__ uint64_t expand_bits(uint64_t x, uint64_t holes, uint64_t vals) {
+    for (uint64_t h = holes; h; h &= h - 1) {
+        const int b = __ffsll((long long)h) - 1;
+        x = ((x >> b) << (b + 1)) | (x & ((1ull << b) - 1ull)) | (((vals >> b) & 1ull) << b);
+    }
+    return x;
+}
 // warp-cooperative per-pair path (k_byte_gate, 1Q on qubits >= 4) when at most this many
 // lanes of a warp hold mixed items; more, and every lane walks its own item
 constexpr int kCoopMaxItems = 12;
@@ -649,26 +658,29 @@ __device__ __forceinline__ void byte_low_pairs(const uint8_t* __restrict__ mi_in
                                                const ByteGate& g, const STables& t, const Emitter& em,
                                                ThreadCache& tc, unsigned long long* memo, const MemoTags& mt,
                                                bool real, bool tagged, bool write, uint64_t first, uint64_t step) {
-    const uint64_t n_blocks = g.n_elems >> 5;
+    // support: only the blocks whose fixed bits (>= 5) read sup_val
+    const uint64_t fixb = g.sup_fixed & ~31ull, valb = g.sup_val & fixb;
+    const uint64_t n_blocks = (g.n_elems >> 5) >> __popcll(fixb);
+    auto block_at = [&](uint64_t w) { return fixb ? expand_bits(w << 5, fixb, valb) : (w << 5); };
     // the next block's bytes are loaded before the current one is computed (latency)
     uint4 nm0 = {0, 0, 0, 0}, nm1 = nm0, np0 = nm0, np1 = nm0;
     if (first < n_blocks) {
-        const uint64_t b = first << 5;
+        const uint64_t b = block_at(first);
         nm0 = *reinterpret_cast<const uint4*>(mi_in + b);
         nm1 = *reinterpret_cast<const uint4*>(mi_in + b + 16);
         np0 = ld16z(pi_in, b);
         np1 = ld16z(pi_in, b + 16);
     }
     for (uint64_t w = first; w < n_blocks; w += step) {
-        const uint64_t b = w << 5;
+        const uint64_t b = block_at(w);
         const uint4 m0 = nm0, m1 = nm1, p0 = np0, p1 = np1;
         if (w + kL2Ahead * step < n_blocks) {
-            const uint64_t bp = (w + kL2Ahead * step) << 5;
+            const uint64_t bp = block_at(w + kL2Ahead * step);
             l2_prefetch(mi_in + bp);
             if (pi_in) l2_prefetch(pi_in + bp);
         }
         if (w + step < n_blocks) {
-            const uint64_t bn = (w + step) << 5;
+            const uint64_t bn = block_at(w + step);
             nm0 = *reinterpret_cast<const uint4*>(mi_in + bn);
             nm1 = *reinterpret_cast<const uint4*>(mi_in + bn + 16);
             np0 = ld16z(pi_in, bn);
@@ -790,12 +802,17 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
             // (16 lanes per item).  Otherwise one mixed item kept 31 idle lanes waiting for
             // 16 sequential pairs (Hadamard benchmark, H on qubit 9 at N=32: 1 item in 32
             // mixed, 64 % of the warps diverged, ~470 instructions per warp-iteration).
-            const uint64_t n_chunks = n_items >> 4;
+            // support: only the items whose fixed bits (>= 4, not qa) read sup_val
+            const uint64_t fixi = g.sup_fixed & ~15ull & ~(1ull << g.qa), vali = g.sup_val & fixi;
+            const uint64_t n_chunks = (n_items >> 4) >> __popcll(fixi);
+            auto item_i0 = [&](uint64_t w) {
+                return fixi ? expand_bits(w << 4, fixi | (1ull << g.qa), vali) : insert0(w << 4, g.qa);
+            };
             const uint64_t off = 1ull << g.qa;
             const int lane = threadIdx.x & 31;
             uint4 nxt[4];
             auto fetch = [&](uint64_t w, uint4 (&b)[4]) {
-                const uint64_t i0 = insert0(w << 4, g.qa);
+                const uint64_t i0 = item_i0(w);
                 b[0] = *reinterpret_cast<const uint4*>(mi_in + i0);
                 b[1] = ld16z(pi_in, i0);
                 b[2] = *reinterpret_cast<const uint4*>(mi_in + i0 + off);
@@ -879,12 +896,12 @@ __global__ void __launch_bounds__(NT, 2) k_byte_gate(const uint8_t* __restrict__
                 uint4 cur[4] = {nxt[0], nxt[1], nxt[2], nxt[3]};
                 if (w + step < n_chunks) fetch(w + step, nxt);
                 if (w + kL2Ahead * step < n_chunks) {
-                    const uint64_t ip = insert0((w + kL2Ahead * step) << 4, g.qa);
+                    const uint64_t ip = item_i0(w + kL2Ahead * step);
                     l2_prefetch(mi_in + ip);
                     l2_prefetch(mi_in + ip + off);
                     if (pi_in) { l2_prefetch(pi_in + ip); l2_prefetch(pi_in + ip + off); }
                 }
-                const uint64_t i0 = inb ? insert0(w << 4, g.qa) : 0ull, i1 = i0 + off;
+                const uint64_t i0 = inb ? item_i0(w) : 0ull, i1 = i0 + off;
                 const bool valid = inb && !(g.producer >= 0 && producer_of(g, i0) != g.producer);
                 const int prod = (tagged && valid) ? producer_of(g, i0) : 0;
                 bool slow = false;
@@ -1172,17 +1189,16 @@ __global__ void __launch_bounds__(NTD) k_byte_diag_apply(
     // before the current one is processed); in place or scanning, only the chunks whose
     // index bits >= 4 match the mask are visited
     const bool sparse = g.in_place || !write;
-    const uint64_t hmask = sparse ? ((g.mask & ~15ull) >> 4) : 0ull;
-    const uint64_t n_chunks = (g.mask & ~(g.n_elems - 1ull)) ? (sparse ? 0ull : (g.n_elems >> 4))
-                                                             : ((g.n_elems >> 4) >> __popcll(hmask));
-    auto chunk_at = [&](uint64_t w) {
-        uint64_t c = w;
-        for (uint64_t m = hmask; m; m &= m - 1) {   // insert a 1 at every mask position
-            const int b = __ffsll((long long)m) - 1;
-            c = ((c >> b) << (b + 1)) | (1ull << b) | (c & ((1ull << b) - 1ull));
-        }
-        return c << 4;
-    };
+    // chunk index bits (>= 4) that are fixed: the mask's (sparse passes: value 1) and the
+    // support's (value sup_val); a mask bit the support fixes to 0 selects nothing
+    const uint64_t hmask_i = sparse ? (g.mask & ~15ull) : 0ull;
+    const uint64_t fix_i = g.sup_fixed & ~15ull, holes = hmask_i | fix_i;
+    const uint64_t hvals = hmask_i | (g.sup_val & fix_i & ~hmask_i);
+    const bool empty = sparse && (hmask_i & fix_i & ~g.sup_val);
+    const uint64_t n_chunks = ((g.mask & ~(g.n_elems - 1ull)) && sparse) || empty
+                                  ? 0ull
+                                  : ((g.n_elems >> 4) >> __popcll(holes));
+    auto chunk_at = [&](uint64_t w) { return expand_bits(w << 4, holes, hvals); };
     uint64_t w = first, inx = 0;
     uint4 nm = {0, 0, 0, 0}, np = {0, 0, 0, 0};
     const unsigned lowm = (unsigned)(g.mask & 15ull);   // selected chunk positions: j & lowm == lowm

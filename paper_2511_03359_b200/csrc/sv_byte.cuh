@@ -40,6 +40,8 @@ struct ByteGate {
     int scan_only;              // 1: collect candidates, write nothing
     int in_place;               // DIAG write pass into the input planes: untouched amplitudes
                                 // are neither read nor written
+    uint64_t sup_fixed;         // support: index bits every nonzero amplitude has equal to sup_val
+    uint64_t sup_val;           // (0 = dense); the vector paths visit only those work items
 };
 
 // Candidate / uncertain-amplitude output of a pass (device memory).

@@ -17,6 +17,8 @@ int capi_cuda_fail(cudaError_t e, const char* what);      // sv_capi.cu
 int capi_measure(const void* psi, uint64_t n, int mode, double* norm, double* ones, double* cross,
                  cudaStream_t st);                        // sv_capi.cu
 int capi_measure_byte(const void* src, uint64_t n, double* norm, double* ones, double* cross, cudaStream_t st);
+int capi_measure_byte_sup(const void* src, uint64_t n, uint64_t sup_fixed, uint64_t sup_val, double* norm,
+                          double* ones, double* cross, cudaStream_t st);
 }
 
 #define BTRY(expr, what)                                        \
@@ -59,6 +61,8 @@ ByteGate to_gate(const svb_gate_desc& d, uint64_t n_elems) {
     g.phys_base = d.phys_base;
     g.rank_bits = d.rank_bits;
     for (int j = 0; j < 12; ++j) g.lbit[j] = d.lbit[j];
+    g.sup_fixed = d.sup_fixed & (n_elems - 1ull);
+    g.sup_val = d.sup_val & g.sup_fixed;
     return g;
 }
 }  // namespace
@@ -134,8 +138,9 @@ int svb_info(sv_bhandle h, int* device, int* n_qubits, void** stream) {
 int svb_zero_state(sv_bhandle h, int64_t unit) {
     Guard gd(h->device);
     const uint64_t n = 1ull << h->n;
-    for (int p = 0; p < 2; ++p) BTRY(cudaMemsetAsync(h->plane[h->cur][p], 0, n, h->stream), "zero planes");
-    BTRY(cudaMemsetAsync(h->plane[1 - h->cur][1], 0, n, h->stream), "zero pending phase plane");
+    // both buffers: a support-restricted pass (sup_fixed) writes only the items inside the support
+    for (int b = 0; b < 2; ++b)
+        for (int p = 0; p < 2; ++p) BTRY(cudaMemsetAsync(h->plane[b][p], 0, n, h->stream), "zero planes");
     if (unit >= 0) {
         if ((uint64_t)unit >= n) return capi_fail(SV_EINDEX, "unit index outside the state");
         static const uint8_t one = 1;
@@ -322,6 +327,16 @@ int svb_decode(sv_bhandle h, double* out, uint64_t first, uint64_t count) {
     if (e != cudaSuccess) return capi_cuda_fail(e, "decode");
     BTRY(cudaStreamSynchronize(h->stream), "decode sync");
     return SV_OK;
+}
+
+int svb_measure_support(sv_bhandle h, uint64_t sup_fixed, uint64_t sup_val, double* norm, double* ones,
+                        double* cross) {
+    Guard gd(h->device);
+    const uint64_t n = 1ull << h->n;
+    if (h->n < 16 || !sup_fixed) return svb_measure(h, norm, ones, cross);
+    struct { const uint8_t* mi; const uint8_t* pi; const double* tab; } src = {
+        h->plane[h->cur][0], h->plane[h->cur][1], reinterpret_cast<const double*>(h->tab)};
+    return capi_measure_byte_sup(&src, n, sup_fixed, sup_val, norm, ones, cross, h->stream);
 }
 
 int svb_measure(sv_bhandle h, double* norm, double* ones, double* cross) {

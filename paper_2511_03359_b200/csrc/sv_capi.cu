@@ -760,7 +760,7 @@ int g_measure_reserve = 0;
 int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cross, double* dev_partials,
                   size_t partial_cap, cudaStream_t st, bool byte = false, const Support* sup = nullptr) {
     const uint64_t all = (n >= 64) ? ~0ull : ((1ull << n) - 1ull);
-    const bool tracked = sup && sup->on && !byte;
+    const bool tracked = sup && sup->on;
     const uint64_t freem = tracked ? (sup->free & all) : all, fixv = tracked ? (sup->val & ~sup->free & all) : 0;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -971,7 +971,7 @@ int measure_impl(const void* psi, uint64_t n_elems, int mode, double* norm, doub
     if (use3 && mode == SV_FP64 && n >= 16 && (reinterpret_cast<uintptr_t>(psi) & 15) == 0)
         return measure3_impl(psi, n, norm, ones, cross, dev_partials, partial_cap, st, false, sup);
     if (use3 && mode == SV_BYTE && n >= 16)
-        return measure3_impl(psi, n, norm, ones, cross, dev_partials, partial_cap, st, true);
+        return measure3_impl(psi, n, norm, ones, cross, dev_partials, partial_cap, st, true, sup);
     const int bmin = k >= 5 ? 5 : k;
     const int grid_cap = measure_grid(dev);
     const int slots_max = measure_slots(k, n);
@@ -1061,6 +1061,15 @@ int capi_measure(const void* psi, uint64_t n, int mode, double* norm, double* on
 // psi = host pointer to {mi plane, pi plane, decode tables} (sv_measure.cu ByteSrc)
 int capi_measure_byte(const void* src, uint64_t n, double* norm, double* ones, double* cross, cudaStream_t st) {
     return measure_impl(src, n, SV_BYTE, norm, ones, cross, nullptr, 0, st);
+}
+// BYTE states with a tracked support (byte_state.py): the passes read only its tiles
+int capi_measure_byte_sup(const void* src, uint64_t n, uint64_t sup_fixed, uint64_t sup_val, double* norm,
+                          double* ones, double* cross, cudaStream_t st) {
+    Support sp;
+    sp.on = true;
+    sp.free = ~sup_fixed & (n - 1ull);
+    sp.val = sup_val & sup_fixed & (n - 1ull);
+    return measure_impl(src, n, SV_BYTE, norm, ones, cross, nullptr, 0, st, &sp);
 }
 }  // namespace sv
 
