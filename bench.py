@@ -685,61 +685,64 @@ def run_b200(args):
         t_adder = time.perf_counter() - t0
         kat = all(abs(res.report.qz[q] - 1.0) < 1e-12 for q in regs["R2"])
         rep_support = res.device_stats.get("support")
+        rep_exact = res.report
+        launches_a = res.device_stats.get("kernel_launches")
         del res
-        # device view of a third run: the fused passes timed with CUDA events next to their
-        # HBM and FP64 floors (the adder's CPHASE runs make most passes FP64-bound)
-        nat.pass_timing(True)
-        nat.pass_timing_read()
-        res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
-        nat.pass_timing(False)
-        a_passes, a_ms, _ = nat.pass_timing_read()
         a_ops = [gate_to_op(gt) for gt in circ.gates if gt.kind != "M"]
-        a_roof = fp64_aware_roofline(32, [a_ops], args.tile_bits, a_ms, peak, clk_mhz)
+
+        def timed_passes(**kw):
+            """(wall seconds of a warm run, pass count, pass ms of a further run, report)"""
+            pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, **kw)
+            jit_wait()
+            t0 = time.perf_counter()
+            r = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, **kw)
+            t = time.perf_counter() - t0
+            rep = r.report
+            del r
+            nat.pass_timing(True)
+            nat.pass_timing_read()
+            r = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, **kw)
+            nat.pass_timing(False)
+            cnt, ms, _ = nat.pass_timing_read()
+            del r
+            return t, cnt, ms, rep
+
+        # support tracking on (the default): the passes' own CUDA-event time
+        _, s_passes, s_ms, _ = timed_passes()
+        # dense (track_support=False): every tile of every pass, the amount of work the
+        # reference does; its passes against their max(HBM, FP64) floors
+        t_dense, d_passes, d_ms, _ = timed_passes(track_support=False)
+        d_roof = fp64_aware_roofline(32, [a_ops], args.tile_bits, d_ms, peak, clk_mhz)
         adder = {"circuit": "build_adder(16, [47302, 18233])", "n_qubits": 32, "gates": len(circ.gates),
                  "seconds": round(t_adder, 4), "sec_per_gate": round(t_adder / len(circ.gates), 6),
                  "first_run_seconds": round(t_first, 4),
-                 "kat_all_ones_R2": kat, "kernel_launches": res.device_stats.get("kernel_launches"),
-                 "passes": {"count": a_passes, "ms": round(a_ms, 2), "hbm_floor_ms": a_roof["hbm_floor_ms"],
-                            "fp64_floor_ms": a_roof["fp64_floor_ms"], "max_floor_ms": a_roof["max_floor_ms"],
-                            "frac_of_max_floor": a_roof["frac"],
-                            "fp64_per_amplitude": a_roof["fp64_per_amplitude"]},
-                 "what": "run_circuit wall clock incl. allocation, zero state, fused passes, measure-all "
-                         "(second run: specialised pass kernels compiled; first_run_seconds: cold); passes: "
-                         "a third run's fused passes (CUDA events) vs max(HBM, FP64) floors per pass; the "
-                         "adder's state stays inside a 2^k-amplitude support (basis-state inputs), which the "
-                         "passes and the measurement track; dense_seconds: track_support=False"}
-        rep_exact = res.report
-        del res
-        # dense: every tile of every pass (track_support=False), the work the reference does
-        pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, track_support=False)
-        jit_wait()
-        t0 = time.perf_counter()
-        res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, track_support=False)
-        adder["dense_seconds"] = round(time.perf_counter() - t0, 4)
-        adder["support"] = rep_support
-        del res
+                 "kat_all_ones_R2": kat, "kernel_launches": launches_a,
+                 "support": rep_support,
+                 "support_passes": {"count": s_passes, "ms": round(s_ms, 2)},
+                 "dense_seconds": round(t_dense, 4),
+                 "dense_passes": {"count": d_passes, "ms": round(d_ms, 2), "hbm_floor_ms": d_roof["hbm_floor_ms"],
+                                  "fp64_floor_ms": d_roof["fp64_floor_ms"], "max_floor_ms": d_roof["max_floor_ms"],
+                                  "frac_of_max_floor": d_roof["frac"],
+                                  "fp64_per_amplitude": d_roof["fp64_per_amplitude"]},
+                 "what": "run_circuit wall clock incl. allocation, |0..0>, fused passes, measure-all (second "
+                         "run: specialised pass kernels compiled; first_run_seconds: cold).  The adder's state "
+                         "stays inside a 2^k-amplitude support (basis-state inputs, only one register "
+                         "superposed), which run_circuit tracks: passes and measurement read only its tiles "
+                         "(support_passes).  dense_*: track_support=False, every tile, with the passes' "
+                         "max(HBM, FP64) floors"}
         # the same circuit with combined diagonal runs (exact_diagonals=False: within 1e-12 of
         # the reference, not bit-identical): one multiply per register mask per CPHASE run
-        pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, exact_diagonals=False)
-        jit_wait()
-        t0 = time.perf_counter()
-        res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, exact_diagonals=False)
-        t_comb = time.perf_counter() - t0
-        nat.pass_timing(True)
-        nat.pass_timing_read()
-        res2 = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, exact_diagonals=False)
-        nat.pass_timing(False)
-        c_passes, c_ms, _ = nat.pass_timing_read()
+        t_comb, _, _, rep_comb = timed_passes(exact_diagonals=False)
+        tc_dense, c_passes, c_ms, _ = timed_passes(exact_diagonals=False, track_support=False)
         c_roof = fp64_aware_roofline(32, [a_ops], args.tile_bits, c_ms, peak, clk_mhz, combine_diag=True)
         adder["combined_diagonals"] = {
-            "seconds": round(t_comb, 4), "sec_per_gate": round(t_comb / len(circ.gates), 6),
-            "passes": {"count": c_passes, "ms": round(c_ms, 2), "fp64_floor_ms": c_roof["fp64_floor_ms"],
-                       "max_floor_ms": c_roof["max_floor_ms"], "frac_of_max_floor": c_roof["frac"]},
-            "report_max_diff_vs_exact": float(rep_exact.max_difference(res.report)),
-            "kat_all_ones_R2": all(abs(res.report.qz[q] - 1.0) < 1e-12 for q in regs["R2"]),
+            "seconds": round(t_comb, 4), "dense_seconds": round(tc_dense, 4),
+            "dense_passes": {"count": c_passes, "ms": round(c_ms, 2), "fp64_floor_ms": c_roof["fp64_floor_ms"],
+                             "max_floor_ms": c_roof["max_floor_ms"], "frac_of_max_floor": c_roof["frac"]},
+            "report_max_diff_vs_exact": float(rep_exact.max_difference(rep_comb)),
+            "kat_all_ones_R2": all(abs(rep_comb.qz[q] - 1.0) < 1e-12 for q in regs["R2"]),
             "what": "run_circuit(exact_diagonals=False): runs of diagonal gates multiply each amplitude "
                     "by their combined factor (north-star FP64 tolerance 1e-12, not bit-identical)"}
-        del res, res2
     # byte-encoded benchmark (BASELINE config 5 shape on one GPU): time per gate
     byte = None
     if args.byte_n > 0:
@@ -768,7 +771,9 @@ def run_b200(args):
                 "passes": bst.passes,
                 "kat_parity_pattern": kat_b[0], "kat_max_dev": kat_b[1], "kat_codebook": kat_cb,
                 "codebook": [len(bst.codebook.mags), len(bst.codebook.thetas)],
-                "what": "apply_gate wall clock (passes + per-gate codebook barrier), 4 B/amplitude/gate"}
+                "what": "apply_gate wall clock (passes + per-gate codebook barrier), 4 B/amplitude/gate as if "
+                        "dense; the state's support is tracked (byte_state.py), so the early Hadamard stages "
+                        "visit only its items"}
         bst.free()
         del bst
 
