@@ -1282,11 +1282,10 @@ int sv_info(sv_handle h, int* device, int* n_qubits, int* mode, void** dev_ptr, 
 
 int sv_zero_state(sv_handle h, int64_t unit) {
     DeviceGuard g(h->device);
-    if (h->lazy == -2) {   // (materialize() keeps the support recorded by sv_zero_state_lazy)
-        h->sup.on = h->track && unit >= 0;
-        h->sup.free = 0;
-        h->sup.val = unit >= 0 ? (uint64_t)unit : 0;
-    }
+    // a basis state's support (materialize() writes the pending lazy |unit>, the same point)
+    h->sup.on = h->track && unit >= 0;
+    h->sup.free = 0;
+    h->sup.val = unit >= 0 ? (uint64_t)unit : 0;
     h->lazy = -2;
     const size_t eb = elem_bytes(h->mode);
     const uint64_t n = 1ull << h->n;
