@@ -56,6 +56,8 @@ class ByteDeviceState:
 
     mode_code = nat.SV_BYTE
 
+    track_support = False      # only the engine's whole-register state maintains a support
+
     def __init__(self, n_qubits: int, codebook: Codebook | None = None, device: int = 0):
         lib = nat.load()
         self.n_qubits = int(n_qubits)
@@ -95,8 +97,11 @@ class ByteDeviceState:
         nat.check(nat.load().svb_zero_state(self.handle, -1 if unit_index is None else unit_index))
         self.version += 1
         self.ph_zero = PHASE_PLANE_SKIP and len(self.codebook.thetas) == 1
-        # support of a basis state: every other bit fixed (all zeros: no tracking)
-        self.sup_free = 0 if unit_index is not None else (1 << self.n_qubits) - 1
+        # support of a basis state: every other bit fixed (all zeros, or a state whose passes do
+        # not maintain it -- the distributed slices, whose remap swaps move data between ranks --
+        # is dense)
+        tracked = unit_index is not None and self.track_support
+        self.sup_free = 0 if tracked else (1 << self.n_qubits) - 1
         self.sup_val = unit_index or 0
 
     def export_storage(self, first: int, count: int):
@@ -333,6 +338,8 @@ def _exchange_fields(desc: SvbGateDesc, gate, layout, plan) -> None:
 
 class ByteEngineState(ByteDeviceState):
     """The engine's whole-register BYTE state (all rank slices in one buffer)."""
+
+    track_support = True
 
     def __init__(self, n_qubits: int, layout, device: int = 0):
         super().__init__(n_qubits, Codebook(), device)

@@ -84,7 +84,10 @@ def main():
         res.backend.close()
     byte_cases = [("bench14_be", benchmark(14)), ("exact12_be", exact_class_circuit(np.random.default_rng(5), 12, 40)),
                   ("random12_be", random_circuit(np.random.default_rng(6), 12, 30)),
-                  ("adder6_be", adder(6, [45, 18])[0])]
+                  ("adder6_be", adder(6, [45, 18])[0]),
+                  # rank slices of >= 16 qubits: the tiled BYTE measurement (a rank slice is
+                  # dense -- remap swaps move amplitudes between ranks, no support is tracked)
+                  ("bench18_be", benchmark(18)), ("adder9_be", adder(9, [300, 77])[0])]
     for name, circ in byte_cases:
         res = run_circuit_distributed(to_product(circ), dist, mode=PrecisionMode.BYTE, device=dev)
         planes = res.gathered_bytes(dist)
