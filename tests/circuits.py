@@ -70,6 +70,38 @@ def exact_class_circuit(rng, n_qubits: int, depth: int, measured: bool = True) -
     return OCircuit(n_qubits, tuple(out))
 
 
+def sparse_circuit(rng, n_qubits: int, depth: int, n_spread: int = 4, measured: bool = True) -> OCircuit:
+    """Random circuit whose non-monomial gates (H, U2, U4) touch only ``n_spread`` random
+    qubits; X / Y / CNOT (monomials: they move a basis state) and Z / PHASE / CPHASE
+    (diagonal) act anywhere.  From |0..0> the state keeps a small support -- the case support
+    tracking (csrc/sv_capi.cu Support, byte_state.py sup_free) restricts passes to."""
+    spread = [int(q) for q in rng.choice(n_qubits, size=n_spread, replace=False)]
+    kinds = ["H", "U2", "U4", "X", "Y", "CNOT", "Z", "PHASE", "CPHASE"]
+    out = []
+    for _ in range(depth):
+        kind = kinds[rng.integers(len(kinds))]
+        q1 = int(rng.integers(n_qubits))
+        q2 = int((q1 + 1 + rng.integers(n_qubits - 1)) % n_qubits)
+        k = int(rng.integers(1, 5))
+        if kind in ("H", "U2"):
+            q = spread[rng.integers(n_spread)]
+            out.append(OGate("H", (q,)) if kind == "H" else OGate("U2", (q,), 0, haar_unitary(rng, 2)))
+        elif kind == "U4":
+            a, b = (int(x) for x in rng.choice(spread, size=2, replace=False))
+            out.append(OGate("U4", (a, b), 0, haar_unitary(rng, 4)))
+        elif kind in ("X", "Y", "Z"):
+            out.append(OGate(kind, (q1,)))
+        elif kind == "PHASE":
+            out.append(OGate("PHASE", (q1,), k if rng.integers(2) else -k))
+        elif kind == "CPHASE":
+            out.append(OGate("CPHASE", (q1, q2), k))
+        else:
+            out.append(OGate("CNOT", (q1, q2)))
+    if measured:
+        out.append(OGate("M"))
+    return OCircuit(n_qubits, tuple(out))
+
+
 # --- (de)serialisation so circuits travel inside golden .npz files ---------
 
 def pack(circuit) -> dict:

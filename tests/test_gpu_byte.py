@@ -50,6 +50,23 @@ def test_engine_byte_runs_match_reference_goldens(golden):
     assert checked >= 30
 
 
+@pytest.mark.parametrize("n,depth,spread,ranks", [(16, 80, 3, 1), (18, 100, 4, 4), (17, 60, 2, 8)])
+def test_byte_support_tracking_sparse_circuits(n, depth, spread, ranks):
+    """BYTE states keep a monotone support (byte_state.py sup_free; monomials and
+    non-monomials free their qubits): sparse circuits give byte planes, codebook and report
+    identical to the oracle, with the passes and the measurement restricted to the support."""
+    from tests.circuits import sparse_circuit
+    circ = sparse_circuit(np.random.default_rng(2000 + n + depth), n, depth, spread)
+    want = ref_engine.run_circuit(circ, ranks=ranks, mode="be")
+    got = pb.run_circuit(to_product(circ), ranks=ranks, mode=BE)
+    mag, ph = _bytes(got)
+    assert np.array_equal(mag, want.mag) and np.array_equal(ph, want.phase)
+    assert got.codebook.dump() == want.codebook.dump()
+    qx, qy, qz, _ = want.report
+    diff = np.max(np.abs(np.array([got.report.qx, got.report.qy, got.report.qz]) - np.array([qx, qy, qz])))
+    assert diff < 1e-12, diff
+
+
 @pytest.mark.parametrize("n,ranks", [(14, 1), (16, 4), (18, 8)])
 def test_byte_benchmark_matches_oracle(n, ranks):
     circ = to_product(__import__("oracle.ref_builders", fromlist=["benchmark"]).benchmark(n))

@@ -263,6 +263,29 @@ def test_support_tracking_skips_zero_tiles_bit_exact():
     dev.free()
 
 
+@pytest.mark.parametrize("n,depth,spread,ranks,mode", [
+    (16, 120, 3, 1, "fp64"), (18, 200, 4, 4, "fp64"), (20, 160, 5, 1, "fp64"),
+    (18, 150, 4, 1, "fp32"), (21, 100, 2, 8, "fp64")])
+def test_support_tracking_sparse_circuits_bit_exact(n, depth, spread, ranks, mode):
+    """Non-monomial gates on a few qubits, monomials (X, Y, CNOT) and diagonals anywhere: the
+    tracked support moves (monomials on fixed qubits) and grows (CNOT from a free control,
+    U4 across free/fixed qubits) -- state bit-identical to the oracle and to the dense run."""
+    from oracle import ref_engine
+    from tests.circuits import sparse_circuit
+    circ = sparse_circuit(np.random.default_rng(1000 + n + depth), n, depth, spread)
+    pm = {"fp64": pb.PrecisionMode.FP64, "fp32": pb.PrecisionMode.FP32}[mode]
+    res = pb.run_circuit(to_product(circ), ranks=ranks, mode=pm)
+    want = ref_engine.run_circuit(circ, ranks=ranks, mode=mode)
+    assert np.array_equal(res.gathered_state(), want.gathered_state())
+    qx, qy, qz, _ = want.report
+    assert res.report.max_difference(pb.ExpectationReport(qx, qy, qz)) < 1e-12
+    sup = res.device_stats["support"]
+    assert sup["tracking"] and sup["tiles_skipped_total"] > 0, sup
+    dense = pb.run_circuit(to_product(circ), ranks=ranks, mode=pm, track_support=False)
+    assert np.array_equal(res.gathered_state(), dense.gathered_state())
+    assert res.report == dense.report or res.report.max_difference(dense.report) < 1e-12
+
+
 # ---- engine contracts ---------------------------------------------------------------------
 def test_scheduling_invariance(rng):
     circ = to_product(random_circuit(rng, 8, 18))
