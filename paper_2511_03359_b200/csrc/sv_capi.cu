@@ -658,8 +658,14 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
                     P2.cmask_t = cm;
                     P2.cpat_t = cp;
                     P2.n_tiles >>= __builtin_popcountll(cm);
-                    const int jr = jit_launch_fused(psi, P2, st);
+                    int jr = jit_launch_fused(psi, P2, st);
                     if (jr < 0) return cuda_fail(cudaErrorLaunchFailure, "fused pass launch");
+                    if (jr != 0 && mode == SV_FP64) {   // not compiled yet: the generic kernel takes chunks too
+                        count_h2d(sizeof(Fused2Params));
+                        const cudaError_t eg = launch_fused2(psi, mode, P2, st);
+                        if (eg != cudaSuccess) return cuda_fail(eg, "fused pass launch");
+                        jr = 0;
+                    }
                     if (jr == 0) {
                         g_support_tiles_skipped += full_tiles - P2.n_tiles;
                         if (g_timing) {
@@ -671,7 +677,7 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
                         cur = PassPlan();
                         return SV_OK;
                     }
-                    // specialised kernel not compiled yet: the whole state through the generic one
+                    // FP32, specialised kernel not compiled yet: the whole state through v1
                     P2.cmask_t = 0;
                     P2.cpat_t = 0;
                     P2.n_tiles = full_tiles;

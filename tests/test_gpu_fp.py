@@ -230,6 +230,16 @@ def test_combined_diagonal_runs_within_tolerance(rng, case):
     assert np.array_equal(exact.gathered_state(), ref)
 
 
+def _tiles_skipped() -> int:
+    """Process-wide count of tiles the support-restricted passes left out (sv_support_info)."""
+    from paper_2511_03359_b200.device import DeviceState
+    dev = DeviceState(4, pb.PrecisionMode.FP64)
+    try:
+        return dev.support_info()["tiles_skipped_total"]
+    finally:
+        dev.free()
+
+
 def test_support_tracking_skips_zero_tiles_bit_exact():
     """run_circuit tracks the support of its |0..0> state: the adder's state lives in the
     superposed register (the other register stays a basis state), so most tiles of most
@@ -239,12 +249,13 @@ def test_support_tracking_skips_zero_tiles_bit_exact():
     from oracle.ref_builders import adder
     w = 9
     circ = adder(w, [0x155 & ((1 << w) - 1), 0x0AB & ((1 << w) - 1)])[0]
+    skipped0 = _tiles_skipped()
     res = pb.run_circuit(to_product(circ))
     want = ref_engine.run_circuit(circ)
     assert np.array_equal(res.gathered_state(), want.gathered_state())
     sup = res.device_stats["support"]
     assert sup["tracking"] and sup["free_qubits"] < circ.n_qubits
-    assert sup["tiles_skipped_total"] > 0
+    assert sup["tiles_skipped_total"] > skipped0   # (the generic kernel restricts too: no JIT wait)
     qx, qy, qz, _ = want.report
     assert res.report.max_difference(pb.ExpectationReport(qx, qy, qz)) < 1e-12
     # monomials on fixed qubits move the support, they do not free it
@@ -274,13 +285,19 @@ def test_support_tracking_sparse_circuits_bit_exact(n, depth, spread, ranks, mod
     from tests.circuits import sparse_circuit
     circ = sparse_circuit(np.random.default_rng(1000 + n + depth), n, depth, spread)
     pm = {"fp64": pb.PrecisionMode.FP64, "fp32": pb.PrecisionMode.FP32}[mode]
-    res = pb.run_circuit(to_product(circ), ranks=ranks, mode=pm)
+    lib = __import__("paper_2511_03359_b200._native", fromlist=["load"]).load()
+    prev = lib.sv_jit_mode(1)     # FP32 restricts only through specialised passes: compile and wait
+    try:
+        skipped0 = _tiles_skipped()
+        res = pb.run_circuit(to_product(circ), ranks=ranks, mode=pm)
+    finally:
+        lib.sv_jit_mode(prev)
     want = ref_engine.run_circuit(circ, ranks=ranks, mode=mode)
     assert np.array_equal(res.gathered_state(), want.gathered_state())
     qx, qy, qz, _ = want.report
     assert res.report.max_difference(pb.ExpectationReport(qx, qy, qz)) < 1e-12
     sup = res.device_stats["support"]
-    assert sup["tracking"] and sup["tiles_skipped_total"] > 0, sup
+    assert sup["tracking"] and sup["tiles_skipped_total"] > skipped0, sup
     dense = pb.run_circuit(to_product(circ), ranks=ranks, mode=pm, track_support=False)
     assert np.array_equal(res.gathered_state(), dense.gathered_state())
     assert res.report == dense.report or res.report.max_difference(dense.report) < 1e-12
