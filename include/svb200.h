@@ -328,6 +328,12 @@ int sv_set_diag_combine(sv_handle h, int on);
  * sv_apply_fused_chunk and all-zero states turn it off. */
 int sv_set_support_tracking(sv_handle h, int on);
 int sv_support_info(sv_handle h, int* on, uint64_t* free_mask, uint64_t* val, uint64_t* tiles_skipped);
+/* set the tracked support explicitly ({i : (i & ~free_mask) == val}; tracking on) -- the
+ * distributed layer's rank slice of the global support after a remap swap */
+int sv_set_support(sv_handle h, uint64_t free_mask, uint64_t val);
+/* host only: move a support through ops by the rule the passes apply (non-monomial 1Q/2Q
+ * ops free their qubits, monomials on fixed qubits move val, diagonal ops keep it) */
+int sv_support_advance(const sv_op* ops, int n_ops, uint64_t* free_mask, uint64_t* val);
 /* the pass split sv_apply_fused uses for ops: ends[p] = one past the last op of pass p;
  * returns the number of passes (also queues their specialised kernels) */
 int sv_plan_passes(int n_qubits, int mode, const sv_op* ops, int n_ops, int tile_bits, int* ends, int cap);

@@ -102,6 +102,8 @@ _SIGNATURES = {
     "sv_set_diag_combine": ([_P, _I], _I),
     "sv_set_support_tracking": ([_P, _I], _I),
     "sv_support_info": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_U64)], _I),
+    "sv_set_support": ([_P, _U64, _U64], _I),
+    "sv_support_advance": ([_P, _I, ctypes.POINTER(_U64), ctypes.POINTER(_U64)], _I),
     "sv_plan_passes": ([_I, _I, _P, _I, _I, ctypes.POINTER(_I), _I], _I),
     "sv_plan_pass_costs": ([_I, _I, _P, _I, _I, ctypes.POINTER(_I), _D, _I, _I], _I),
     "sv_jit_stats": ([_D], _I),

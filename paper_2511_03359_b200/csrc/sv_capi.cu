@@ -1326,6 +1326,35 @@ int sv_set_support_tracking(sv_handle h, int on) {
     return SV_OK;
 }
 
+// a support the caller derived itself (the distributed layer: its rank slice of the global
+// support, re-derived after every remap swap); the handle then tracks it from here
+int sv_set_support(sv_handle h, uint64_t free_mask, uint64_t val) {
+    const uint64_t all = h->n >= 64 ? ~0ull : ((1ull << h->n) - 1ull);
+    h->track = 1;
+    h->sup.on = true;
+    h->sup.free = free_mask & all;
+    h->sup.val = val & ~free_mask & all;
+    return SV_OK;
+}
+
+// the support rule of the fused passes and sv_apply_1q/2q, without a state: *free_mask / *val
+// move through ops in order (host-side bookkeeping of the distributed layer, and tests)
+int sv_support_advance(const sv_op* ops, int n_ops, uint64_t* free_mask, uint64_t* val) {
+    if (n_ops < 0 || (n_ops && !ops) || !free_mask || !val) return fail(SV_EVALUE, "bad support arguments");
+    Support s;
+    s.on = true;
+    s.free = *free_mask;
+    s.val = *val & ~*free_mask;
+    for (int i = 0; i < n_ops; ++i) {
+        if (ops[i].qa < 0 || ops[i].qa >= 64 || ops[i].qb < 0 || ops[i].qb >= 64)
+            return fail(SV_EINDEX, "op %d: qubit outside 0..63", i);
+        support_apply(s, ops[i]);
+    }
+    *free_mask = s.free;
+    *val = s.val & ~s.free;
+    return SV_OK;
+}
+
 int sv_support_info(sv_handle h, int* on, uint64_t* free_mask, uint64_t* val, uint64_t* tiles_skipped) {
     if (on) *on = h->sup.on ? 1 : 0;
     if (free_mask) *free_mask = h->sup.free;

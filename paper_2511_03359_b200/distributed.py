@@ -60,6 +60,10 @@ def phys_op(gate, phys: tuple, n_local: int, rank: int):
     return gate_op(nat.SV_OP_2Q, qa=phys[0], qb=phys[1], data=m)
 
 
+# SVB200_SUPPORT=0: distributed FP runs process every tile of every pass (no support tracking)
+_DIST_SUPPORT = os.environ.get("SVB200_SUPPORT", "1") != "0"
+
+
 # IPC mappings of the peers' FP slices, kept across runs of the same shape:
 # (device, rank, world) -> {"shape": (n_local, mode), "maps": {peer: (handle bytes, ptr)}}.
 # A run of the same shape gets the same slab back from the slab cache (sv_slab.cu), hence
@@ -159,10 +163,55 @@ class CudaBackend:
         self.swap_events = []
         self._overlap = None          # chunk events / swap stream, created on first overlapped swap
         self.overlapped = 0
+        # support of the global state in physical positions (csrc sv_capi.cu Support): the run
+        # starts from |0..0>, every rank moves it through the same non-diagonal ops, so every
+        # rank holds the same set.  A rank slice outside it holds zeros (passes, measurement
+        # and pair dots skipped); inside it, the handle gets the slice's restriction before
+        # each local pass, since remap swaps move bits between local and global positions.
+        self.n = n_local + (self.world.bit_length() - 1)
+        self.track = _DIST_SUPPORT
+        self.sup_free, self.sup_val = 0, 0
+        self.skipped_passes = 0
         dist.barrier()
 
+    # -- support tracking ------------------------------------------------------------------
+    def _advance(self, ops) -> None:
+        if not self.track or not ops:
+            return
+        f, v = ctypes.c_uint64(self.sup_free), ctypes.c_uint64(self.sup_val)
+        nat.check(nat.load(require_device=False).sv_support_advance(ops_array(ops), len(ops), ctypes.byref(f),
+                                                                    ctypes.byref(v)))
+        self.sup_free, self.sup_val = f.value, v.value
+
+    def _swap_bits(self, pairs) -> None:
+        for a, b in pairs:
+            for name in ("sup_free", "sup_val"):
+                x = getattr(self, name)
+                if ((x >> a) ^ (x >> b)) & 1:
+                    x ^= (1 << a) | (1 << b)
+                setattr(self, name, x)
+
+    def _slice_empty(self) -> bool:
+        """True when a fixed global bit of the support differs from this rank's bit."""
+        gmask = ((1 << self.n) - 1) & ~((1 << self.n_local) - 1)
+        return bool((self.sup_val ^ (self.rank << self.n_local)) & gmask & ~self.sup_free)
+
+    def _restrict(self) -> bool:
+        """Hand this slice's support to the handle; False when the slice can only hold zeros."""
+        if not self.track:
+            return True
+        if self._slice_empty():
+            return False
+        lm = (1 << self.n_local) - 1
+        nat.check(nat.load().sv_set_support(self.dev.handle, self.sup_free & lm, self.sup_val & lm))
+        return True
+
     def apply_local(self, ops):
-        self.dev.apply_fused(ops, self.tile_bits)
+        if self._restrict():
+            self.dev.apply_fused(ops, self.tile_bits)
+        else:
+            self.skipped_passes += 1
+        self._advance(ops)
 
     # -- remap swap overlapped with the following pass ------------------------------------
     OVERLAP_CHUNK_BITS = int(__import__("os").environ.get("SVB200_OVERLAP_CHUNK_BITS", "4"))   # 16 chunks
@@ -307,6 +356,7 @@ class CudaBackend:
                 nat.check(lib.sv_apply_fused_chunk(self.dev.handle, arr_l, len(last), self.tile_bits, cmask,
                                                    deposit(i, bits)))
             nat.check(lib.sv_event_record(own_ev[C + i], self.dev.stream))
+        self._advance(last)          # (chunked passes run dense: sv_apply_fused_chunk ends tracking)
         self.dist.barrier()          # every rank's stage-1 events are recorded
         prev_blocks = lib.sv_swap_blocks(self.OVERLAP_SWAP_BLOCKS)
         for i in range(C):           # stage 2: the swap, chunk by chunk on the second stream
@@ -321,6 +371,7 @@ class CudaBackend:
                 self.link_bytes += 2 * half * self.bpe
             nat.check(lib.sv_event_record(own_ev[i], stream.ptr))
         lib.sv_swap_blocks(prev_blocks)
+        self._swap_bits(pairs)
         self.dist.barrier()          # every rank's stage-2 events are recorded
         arr = ops_array(first)
         for i in range(C):           # stage 3: the pass after, chunk by chunk
@@ -330,6 +381,7 @@ class CudaBackend:
             if first:
                 nat.check(lib.sv_apply_fused_chunk(self.dev.handle, arr, len(first), self.tile_bits, cmask,
                                                    deposit(i, bits)))
+        self._advance(first)
         if self.swap_timing:
             e1 = nat.Event()
             e1.record(self.dev.stream)
@@ -357,6 +409,7 @@ class CudaBackend:
             self.swap_events.append((e0, e1))
         self._sync_all()
         self.dev._touch()
+        self._swap_bits(((global_pos, local_pos),))
         self.link_bytes += 2 * (self.dev.size // 4) * self.bpe      # this rank's reads + writes over NVLink
 
     def swap_group(self, pairs) -> None:
@@ -378,6 +431,7 @@ class CudaBackend:
             self.swap_events.append((e0, e1))
         self._sync_all()
         self.dev._touch()
+        self._swap_bits(pairs)
 
     def pair_gate(self, global_pos: int, matrix) -> None:
         """The reference's pairwise round for a single-qubit gate on a global qubit
@@ -399,12 +453,22 @@ class CudaBackend:
         self._sync_all()
         self.dev._touch()
         self.link_bytes += 2 * half * self.bpe
+        self._advance([gate_op(nat.SV_OP_1Q, qa=global_pos, data=m)])
 
     def measure_local(self):
+        if not self._restrict():      # zeros: sums of zeros
+            n = self.n_local
+            return 0.0, np.zeros(n), np.zeros(n, dtype=np.complex128)
         return self.dev.measure()
+
+    def _pair_is_zero(self, global_pos: int) -> bool:
+        """A fixed global qubit: one amplitude of every pair is zero, the cross sum is 0."""
+        return self.track and not (self.sup_free >> global_pos) & 1
 
     def pair_dot(self, global_pos: int) -> complex:
         """This rank's share of sum conj(a0) a1 for a global qubit (measure.py:92-99)."""
+        if self._pair_is_zero(global_pos):
+            return 0j
         bit = global_pos - self.n_local
         partner = self.rank ^ (1 << bit)
         low = ((self.rank >> bit) & 1) == 0
@@ -438,6 +502,9 @@ class CudaBackend:
         esz = np.dtype(self.dev.dtype).itemsize
         out = {}
         for global_pos in positions:
+            if self._pair_is_zero(global_pos):
+                out[global_pos] = 0j
+                continue
             bit = global_pos - self.n_local
             partner = self.rank ^ (1 << bit)
             low = ((self.rank >> bit) & 1) == 0
@@ -826,6 +893,9 @@ def run_circuit_distributed(circuit: Circuit, dist, *, mode: PrecisionMode = Pre
              "overlapped_swaps": getattr(be, "overlapped", 0)}
     if byte:
         stats.update(byte_passes=be.passes, byte_host_fixes=be.host_fixes)
+    elif hasattr(be, "skipped_passes"):
+        stats.update(support_free_qubits=bin(be.sup_free).count("1") if be.track else None,
+                     passes_skipped_empty_slice=be.skipped_passes)
     res = DistRunResult(circuit, layout, mode, rank, ledgers, report, tuple(planner.pos),
                         time.perf_counter() - start, stats, be)
     if byte:

@@ -27,7 +27,7 @@ def main():
     from paper_2511_03359_b200.distributed import run_circuit_distributed
     from oracle import ref_engine
     from oracle.ref_builders import adder, benchmark
-    from tests.circuits import random_circuit, to_product
+    from tests.circuits import random_circuit, sparse_circuit, to_product
     cases = [("random14", random_circuit(np.random.default_rng(11), 14, 80)),
              ("random18", random_circuit(np.random.default_rng(12), 18, 60)),
              ("bench20", benchmark(20)),
@@ -37,7 +37,12 @@ def main():
              ("bench23", benchmark(23)),
              # CPHASE runs on global qubits: ranks hold different diagonal op lists around the
              # overlapped swaps (the chunk choice must not depend on them)
-             ("adder11", adder(11, [1234, 813])[0])]
+             ("adder11", adder(11, [1234, 813])[0]),
+             # small supports (non-monomials on a few qubits): rank slices outside the support
+             # skip their passes, the others run support-restricted ones; pair dots of fixed
+             # global qubits are skipped
+             ("sparse18", sparse_circuit(np.random.default_rng(31), 18, 150, 3)),
+             ("sparse22", sparse_circuit(np.random.default_rng(32), 22, 120, 4))]
     ok = True
     for name, circ in cases:
         res = run_circuit_distributed(to_product(circ), dist, device=dev)
@@ -56,7 +61,8 @@ def main():
         res.backend.close()
     # reference choreography (no remapping): exchange-fused pair updates over NVLink
     for name, circ in [("random14_ref", random_circuit(np.random.default_rng(11), 14, 80)),
-                       ("bench16_ref", benchmark(16))]:
+                       ("bench16_ref", benchmark(16)),
+                       ("sparse14_ref", sparse_circuit(np.random.default_rng(33), 14, 80, 3))]:
         res = run_circuit_distributed(to_product(circ), dist, remap=False, device=dev)
         state = res.gathered_state(dist)
         if rank == 0:
@@ -71,7 +77,8 @@ def main():
     from tests.circuits import exact_class_circuit
     # FP32 storage across GPUs (remap swaps move complex64 amplitudes)
     for name, circ in [("random16_fp32", random_circuit(np.random.default_rng(21), 16, 70)),
-                       ("bench18_fp32", benchmark(18))]:
+                       ("bench18_fp32", benchmark(18)),
+                       ("sparse16_fp32", sparse_circuit(np.random.default_rng(34), 16, 80, 3))]:
         res = run_circuit_distributed(to_product(circ), dist, mode=PrecisionMode.FP32, device=dev)
         state = res.gathered_state(dist)
         if rank == 0:

@@ -325,3 +325,53 @@ def test_measured_off_variants_still_compile(env, marks):
     assert r.returncode == 0, r.stderr[-2000:]
     for m in marks:
         assert m in r.stdout, m
+
+
+def _advance(ops, free, val):
+    import ctypes
+    from paper_2511_03359_b200.device import ops_array
+    f, v = ctypes.c_uint64(free), ctypes.c_uint64(val)
+    _native.check(_native.load(require_device=False).sv_support_advance(ops_array(ops), len(ops),
+                                                                        ctypes.byref(f), ctypes.byref(v)))
+    return f.value, v.value
+
+
+def test_support_rule_host_side():
+    """sv_support_advance: the support rule of the fused passes (csrc sv_capi.cu support_apply)
+    -- monomials on fixed qubits move val, non-monomials and gates touching a free qubit free
+    their qubits, diagonal gates keep the set."""
+    from paper_2511_03359_b200.engine import gate_to_op
+    op = lambda gate: gate_to_op(gate)   # noqa: E731
+    assert _advance([op(g.x(3))], 0, 0) == (0, 1 << 3)
+    assert _advance([op(g.x(3))], 0, 1 << 3) == (0, 0)
+    assert _advance([op(g.h(5))], 0, 0) == (1 << 5, 0)
+    assert _advance([op(g.cnot(1, 4))], 0, 1 << 1) == (0, (1 << 1) | (1 << 4))     # control 1: target flips
+    assert _advance([op(g.cnot(1, 4))], 0, 0) == (0, 0)                           # control 0: nothing
+    assert _advance([op(g.cnot(1, 4))], 1 << 1, 0) == ((1 << 1) | (1 << 4), 0)    # free control: both free
+    assert _advance([op(g.z(2)), op(g.cphase(2, 6, 3)), op(g.phase(7, 2))], 0, 1 << 2) == (0, 1 << 2)
+    y = gate_to_op(g.y(0))
+    assert _advance([y], 0, 0) == (0, 1)                                          # Y: monomial with phase
+    # the same rule as the handle-side tracking of a run: a sparse circuit's free set
+    from tests.circuits import sparse_circuit
+    circ = to_product(sparse_circuit(np.random.default_rng(3), 20, 120, 3, measured=False))
+    free, val = _advance([gate_to_op(x) for x in circ.gates], 0, 0)
+    assert bin(free).count("1") < 20 and val & free == 0
+
+
+def test_distributed_support_bookkeeping():
+    """CudaBackend's support bookkeeping (no device): remap swaps exchange the bits of the
+    physical positions, a rank whose slice lies outside the support skips its passes."""
+    from paper_2511_03359_b200.distributed import CudaBackend
+    be = CudaBackend.__new__(CudaBackend)
+    be.n, be.n_local, be.track = 6, 4, True
+    be.sup_free, be.sup_val = 0b000011, 0b100100     # global bit 5 fixed at 1, bit 4 fixed at 0
+    for rank, empty in ((0, True), (1, True), (2, False), (3, True)):
+        be.rank = rank
+        assert be._slice_empty() is empty
+    be._swap_bits(((5, 0),))                          # position 5 <-> position 0
+    assert (be.sup_free, be.sup_val) == (0b100010, 0b000101)
+    be.rank = 0
+    assert not be._slice_empty()                      # bit 5 now free, bit 4 fixed at 0
+    be.rank = 1
+    assert be._slice_empty()
+    assert be._pair_is_zero(4) and not be._pair_is_zero(5)
