@@ -206,6 +206,39 @@ class CudaBackend:
         nat.check(nat.load().sv_set_support(self.dev.handle, self.sup_free & lm, self.sup_val & lm))
         return True
 
+    def _fixed_local(self, pairs) -> int:
+        """Local bits the support fixes, outside the swap victims (0: dense swap)."""
+        if not self.track:
+            return 0
+        victims = sum(1 << l for _, l in pairs)
+        return ~self.sup_free & ((1 << self.n_local) - 1) & ~victims
+
+    def _swap_restricted(self, pairs) -> bool:
+        """A remap swap of a state whose support fixes local bits outside the victims: on
+        every rank only the amplitudes whose fixed bits read val can be nonzero, so the swap
+        is the chunk form of the group swap over them alone (svk_swap_group_chunk with the
+        fixed bits as the chunk).  False when nothing is fixed (the dense kernels run)."""
+        cmask = self._fixed_local(pairs)
+        if not cmask:
+            return False
+        L = self.dev.size
+        cpat = self.sup_val & cmask
+        T = L >> (len(pairs) + bin(cmask).count("1"))     # remaining-bit indices per member pair
+        lo = T - T // 2
+        sched = group_schedule(self.rank, pairs, self.n_local, L)
+        self._sync_all()
+        lib = nat.load()
+        for member, vmask, own_pat, peer_pat, t0, cnt in sched:
+            tb, tc = (0, lo) if t0 == 0 else (lo, T - lo)
+            if tc:
+                nat.check(lib.svk_swap_group_chunk(self.dev.ptr, self.peers[member], L, self.dev.mode_code, vmask,
+                                                   own_pat, peer_pat, cmask, cpat, tb, tc, self.dev.stream))
+            self.link_bytes += 2 * tc * self.bpe
+        self._sync_all()
+        self.dev._touch()
+        self._swap_bits(pairs)
+        return True
+
     def apply_local(self, ops):
         if self._restrict():
             self.dev.apply_fused(ops, self.tile_bits)
@@ -321,7 +354,9 @@ class CudaBackend:
         before = list(before)
         first, rest = self._first_pass(ops)
         head, last = self._last_pass(before)
-        bits = self._chunk_bits(pairs, list(first) + list(last)) if self.mode is PrecisionMode.FP64 else []
+        # (a support fixing local bits: the restricted swap moves little, no overlap needed)
+        dense = self.mode is PrecisionMode.FP64 and not self._fixed_local(pairs)
+        bits = self._chunk_bits(pairs, list(first) + list(last)) if dense else []
         if not bits:
             if before:
                 self.apply_local(before)
@@ -395,6 +430,8 @@ class CudaBackend:
         self.dist.barrier()
 
     def swap(self, global_pos: int, local_pos: int):
+        if self._swap_restricted(((global_pos, local_pos),)):
+            return
         bit = global_pos - self.n_local
         partner = self.rank ^ (1 << bit)
         side = (self.rank >> bit) & 1
@@ -416,6 +453,8 @@ class CudaBackend:
         """Batched swap of k global qubits (remap.SwapGroup): one svk_swap_group launch
         per other member of this rank's 2^k group, all ranks concurrently (every
         launch touches a disjoint set of amplitudes)."""
+        if self._swap_restricted(pairs):
+            return
         sched = group_schedule(self.rank, pairs, self.n_local, self.dev.size)
         self._sync_all()
         if self.swap_timing:
@@ -583,6 +622,8 @@ class CudaByteBackend:
         return self.peers[r][c]
 
     def swap(self, global_pos: int, local_pos: int):
+        if self._swap_restricted(((global_pos, local_pos),)):
+            return
         bit = global_pos - self.n_local
         partner = self.rank ^ (1 << bit)
         side = (self.rank >> bit) & 1

@@ -375,3 +375,7 @@ def test_distributed_support_bookkeeping():
     be.rank = 1
     assert be._slice_empty()
     assert be._pair_is_zero(4) and not be._pair_is_zero(5)
+    # local bits a restricted remap swap fixes: the support's fixed local bits minus the victims
+    assert be._fixed_local(((4, 2),)) == 0b1111 & ~0b0010 & ~0b0100
+    be.track = False
+    assert be._fixed_local(((4, 2),)) == 0 and not be._pair_is_zero(4)
