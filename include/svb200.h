@@ -235,6 +235,12 @@ int svk_swap_group_chunk(void* own, void* peer, uint64_t n_local_elems, int mode
  * max_blocks caps the grid (0 = two CTAs per SM). */
 int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, int max_blocks, double* out2,
                  void* stream);
+/* the same over the elements of [0, n_elems) whose bits under chunk_mask equal chunk_pattern,
+ * rest indices [t_begin, t_begin + t_count) (t runs over the bits outside chunk_mask): the
+ * cross term of a global qubit of a state whose tracked support fixes those bits */
+int svk_pair_dot_chunk(const void* a0, const void* a1, uint64_t n_elems, int mode, uint64_t chunk_mask,
+                       uint64_t chunk_pattern, uint64_t t_begin, uint64_t t_count, int max_blocks, double* out2,
+                       void* stream);
 
 /* BYTE multi-GPU: IPC handles of the 4 planes ([buffer][magnitude, phase]),
  * mapped peer planes, byte-plane swap and decoded cross term */

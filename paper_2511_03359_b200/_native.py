@@ -91,6 +91,7 @@ _SIGNATURES = {
     "sv_ipc_unexport_all": ([ctypes.POINTER(_U64)], _I),
     "svk_swap_peer": ([_P, _P, _U64, _I, _I, _I, _P], _I),
     "svk_pair_dot": ([_P, _P, _U64, _I, _I, _D, _P], _I),
+    "svk_pair_dot_chunk": ([_P, _P, _U64, _I, _U64, _U64, _U64, _U64, _I, _D, _P], _I),
     "sv_release_cached": ([], _I),
     "sv_cached_bytes": ([ctypes.POINTER(_U64)], _I),
     "sv_jit_mode": ([_I], _I),

@@ -1677,8 +1677,8 @@ int svk_swap_group_chunk(void* own, void* peer, uint64_t n_local_elems, int mode
     return e == cudaSuccess ? SV_OK : cuda_fail(e, "group swap launch");
 }
 
-int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, int max_blocks, double* out2,
-                 void* stream) {
+static int pair_dot_impl(const void* a0, const void* a1, uint64_t t_begin, uint64_t count, uint64_t cmask,
+                         uint64_t cpat, bool chunk, int mode, int max_blocks, double* out2, void* stream) {
     if (!valid_fp_mode(mode)) return fail(SV_EVALUE, "pair dot needs FP64 or FP32 storage");
     out2[0] = out2[1] = 0.0;
     if (count == 0) return SV_OK;
@@ -1689,7 +1689,8 @@ int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, int m
     double* part = nullptr;
     cudaStream_t st = as_stream(stream);
     CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), 16 * grid, st), "pair dot scratch");
-    cudaError_t e = launch_pair_dot(a0, a1, count, mode, part, grid, st);
+    cudaError_t e = chunk ? launch_pair_dot_chunk(a0, a1, t_begin, count, cmask, cpat, mode, part, grid, st)
+                          : launch_pair_dot(a0, a1, count, mode, part, grid, st);
     std::vector<double> h(2 * grid);
     if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), part, 16 * grid, cudaMemcpyDeviceToHost, st);
     cudaFreeAsync(part, st);
@@ -1697,6 +1698,21 @@ int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, int m
     if (e != cudaSuccess) return cuda_fail(e, "pair dot");
     for (int b = 0; b < grid; ++b) { out2[0] += h[2 * b]; out2[1] += h[2 * b + 1]; }
     return SV_OK;
+}
+
+int svk_pair_dot(const void* a0, const void* a1, uint64_t count, int mode, int max_blocks, double* out2,
+                 void* stream) {
+    return pair_dot_impl(a0, a1, 0, count, 0, 0, false, mode, max_blocks, out2, stream);
+}
+
+int svk_pair_dot_chunk(const void* a0, const void* a1, uint64_t n_elems, int mode, uint64_t chunk_mask,
+                       uint64_t chunk_pattern, uint64_t t_begin, uint64_t t_count, int max_blocks, double* out2,
+                       void* stream) {
+    if (!is_pow2(n_elems) || (chunk_mask & ~(n_elems - 1)) || (chunk_pattern & ~chunk_mask))
+        return fail(SV_EINDEX, "chunk mask / pattern outside the buffer");
+    const uint64_t rest = n_elems >> __builtin_popcountll(chunk_mask);
+    if (t_begin > rest || t_count > rest - t_begin) return fail(SV_EINDEX, "rest range outside the buffer");
+    return pair_dot_impl(a0, a1, t_begin, t_count, chunk_mask, chunk_pattern, true, mode, max_blocks, out2, stream);
 }
 
 int sv_buffer_alloc(int device, uint64_t bytes, void** ptr) {

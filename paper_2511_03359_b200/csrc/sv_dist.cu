@@ -151,6 +151,24 @@ cudaError_t launch_swap_group(void* own, void* peer, uint64_t t0, uint64_t n, in
 
 // 4 independent 32-byte loads of each side per iteration: the remote side is an NVLink read,
 // so enough requests must be in flight per thread to cover its latency
+// deterministic block partial of (re, im): warp shuffles, then warp 0's thread 0 in order
+__device__ __forceinline__ void block_partials(double re, double im, double* partials) {
+    __shared__ double sr[8], si[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        re += __shfl_down_sync(0xffffffffu, re, o);
+        im += __shfl_down_sync(0xffffffffu, im, o);
+    }
+    if ((threadIdx.x & 31) == 0) { sr[threadIdx.x >> 5] = re; si[threadIdx.x >> 5] = im; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += sr[w]; b += si[w]; }
+        partials[2 * blockIdx.x] = a;
+        partials[2 * blockIdx.x + 1] = b;
+    }
+}
+
 template <typename S>
 __global__ void __launch_bounds__(256) k_pair_dot(const S* __restrict__ a0, const S* __restrict__ a1, uint64_t n,
                                                   double* __restrict__ partials) {
@@ -184,20 +202,24 @@ __global__ void __launch_bounds__(256) k_pair_dot(const S* __restrict__ a0, cons
         re += a.re * b.re + a.im * b.im;
         im += a.re * b.im - a.im * b.re;
     }
-    __shared__ double sr[8], si[8];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        re += __shfl_down_sync(0xffffffffu, re, o);
-        im += __shfl_down_sync(0xffffffffu, im, o);
+    block_partials(re, im, partials);
+}
+
+// the same over the amplitudes whose bits under cmask read cpat (a tracked support's fixed
+// bits): element t0 + w of the rest indices is insert_zeros(t0 + w, cmask) | cpat
+template <typename S>
+__global__ void __launch_bounds__(256) k_pair_dot_chunk(const S* __restrict__ a0, const S* __restrict__ a1,
+                                                        uint64_t t0, uint64_t n, uint64_t cmask, uint64_t cpat,
+                                                        double* __restrict__ partials) {
+    double re = 0.0, im = 0.0;
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n; w += step) {
+        const uint64_t i = insert_zeros(t0 + w, cmask) | cpat;
+        const cplx a = Store<S>::get(a0[i]), b = Store<S>::get(a1[i]);
+        re += a.re * b.re + a.im * b.im;
+        im += a.re * b.im - a.im * b.re;
     }
-    if ((threadIdx.x & 31) == 0) { sr[threadIdx.x >> 5] = re; si[threadIdx.x >> 5] = im; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double a = 0.0, b = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += sr[w]; b += si[w]; }
-        partials[2 * blockIdx.x] = a;
-        partials[2 * blockIdx.x + 1] = b;
-    }
+    block_partials(re, im, partials);
 }
 
 template <typename S>
@@ -232,6 +254,18 @@ cudaError_t launch_pair_dot(const void* a0, const void* a1, uint64_t n, int mode
         k_pair_dot<c32s><<<grid, 256, 0, st>>>(static_cast<const c32s*>(a0), static_cast<const c32s*>(a1), n, partials);
     else
         k_pair_dot<c64s><<<grid, 256, 0, st>>>(static_cast<const c64s*>(a0), static_cast<const c64s*>(a1), n, partials);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pair_dot_chunk(const void* a0, const void* a1, uint64_t t0, uint64_t n, uint64_t cmask,
+                                  uint64_t cpat, int mode, double* partials, int grid, cudaStream_t st) {
+    if (mode == SV_FP32)
+        k_pair_dot_chunk<c32s><<<grid, 256, 0, st>>>(static_cast<const c32s*>(a0), static_cast<const c32s*>(a1), t0, n,
+                                                     cmask, cpat, partials);
+    else
+        k_pair_dot_chunk<c64s><<<grid, 256, 0, st>>>(static_cast<const c64s*>(a0), static_cast<const c64s*>(a1), t0, n,
+                                                     cmask, cpat, partials);
     count_launch();
     return cudaGetLastError();
 }

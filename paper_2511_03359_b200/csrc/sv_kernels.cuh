@@ -155,6 +155,8 @@ cudaError_t launch_swap_group(void* own, void* peer, uint64_t t0, uint64_t n, in
                               uint64_t own_pat, uint64_t peer_pat, uint64_t cmask, uint64_t cpat, cudaStream_t st);
 cudaError_t launch_pair_dot(const void* a0, const void* a1, uint64_t n, int mode, double* partials, int grid,
                             cudaStream_t st);
+cudaError_t launch_pair_dot_chunk(const void* a0, const void* a1, uint64_t t0, uint64_t n, uint64_t cmask,
+                                  uint64_t cpat, int mode, double* partials, int grid, cudaStream_t st);
 void count_launch(uint64_t n = 1);
 
 }  // namespace sv

@@ -500,6 +500,27 @@ class CudaBackend:
             return 0.0, np.zeros(n), np.zeros(n, dtype=np.complex128)
         return self.dev.measure()
 
+    def _pair_dot_restricted(self, global_pos: int, stream, max_blocks: int):
+        """The cross sum of a free global qubit when the support fixes local bits: only the
+        amplitudes whose fixed bits read val enter (svk_pair_dot_chunk over the whole slices,
+        the rest indices split between the two ranks); None when nothing is fixed."""
+        cmask = self._fixed_local(())
+        if not cmask:
+            return None
+        bit = global_pos - self.n_local
+        partner = self.rank ^ (1 << bit)
+        low = ((self.rank >> bit) & 1) == 0
+        a0, a1 = (self.dev.ptr, self.peers[partner]) if low else (self.peers[partner], self.dev.ptr)
+        L = self.dev.size
+        T = L >> bin(cmask).count("1")
+        lo = T - T // 2
+        tb, tc = (0, lo) if low else (lo, T - lo)
+        res = np.zeros(2)
+        nat.check(nat.load().svk_pair_dot_chunk(a0, a1, L, self.dev.mode_code, cmask, self.sup_val & cmask, tb, tc,
+                                                max_blocks, nat.dptr(res), stream))
+        self.link_bytes += tc * self.bpe
+        return complex(res[0], res[1])
+
     def _pair_is_zero(self, global_pos: int) -> bool:
         """A fixed global qubit: one amplitude of every pair is zero, the cross sum is 0."""
         return self.track and not (self.sup_free >> global_pos) & 1
@@ -514,6 +535,9 @@ class CudaBackend:
         half = self.dev.size // 2
         esz = np.dtype(self.dev.dtype).itemsize
         self._sync_all()
+        r = self._pair_dot_restricted(global_pos, self.dev.stream, 0)
+        if r is not None:
+            return r
         out = np.zeros(2)
         if low:
             a0, a1 = self.dev.ptr, self.peers[partner]
@@ -543,6 +567,10 @@ class CudaBackend:
         for global_pos in positions:
             if self._pair_is_zero(global_pos):
                 out[global_pos] = 0j
+                continue
+            r = self._pair_dot_restricted(global_pos, stream.ptr, self.PAIR_DOT_BLOCKS)
+            if r is not None:
+                out[global_pos] = r
                 continue
             bit = global_pos - self.n_local
             partner = self.rank ^ (1 << bit)
