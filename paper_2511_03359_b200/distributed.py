@@ -650,8 +650,6 @@ class CudaByteBackend:
         return self.peers[r][c]
 
     def swap(self, global_pos: int, local_pos: int):
-        if self._swap_restricted(((global_pos, local_pos),)):
-            return
         bit = global_pos - self.n_local
         partner = self.rank ^ (1 << bit)
         side = (self.rank >> bit) & 1
