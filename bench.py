@@ -1032,14 +1032,16 @@ def run_b200_multi(args, dist, rank, world, device):
         t_e2e, e2e_bytes = 0.0, 0
         for j in range(args.e2e_steps):
             li = 1 + j % (len(layers) - 1) if len(layers) > 1 else 0
-            circ = pb.Circuit(N, tuple(layers[li]) + (pb.gates.measure_all(),))
+            # the 1-GPU line's e2e circuit: the Hadamard layer on |0..0> (the state dense from
+            # there, whatever the support tracking skips before), one random layer, measure-all
+            circ = pb.Circuit(N, tuple(layers[0]) + tuple(layers[li]) + (pb.gates.measure_all(),))
             dist.barrier()
             t0 = time.perf_counter()
             res = run_circuit_distributed(circ, dist, device=device, tile_bits=args.tile_bits)
             _ = res.report.qz[0]
             dist.barrier()
             t_e2e += time.perf_counter() - t0
-            e2e_bytes += lbytes[li]
+            e2e_bytes += lbytes[0] + lbytes[li]
             res.backend.close()
             res.backend.dev.free()
             del res
@@ -1048,8 +1050,8 @@ def run_b200_multi(args, dist, rank, world, device):
         e2e = {"value": round(e2e_bytes / t_e2e / 1e9, 2), "unit": "GB/s",
                "h2d_bytes_per_step": (h2d1 - h2d0) // args.e2e_steps,
                "d2h_bytes_per_step": (d2h1 - d2h0) // args.e2e_steps,
-               "what": "run_circuit_distributed(layer + M) per step: allocate + zero + IPC map, remapped "
-                       "layer, measure-all, report on every rank; wall clock max over ranks"}
+               "what": "run_circuit_distributed(H layer + layer + M) per step: allocate + zero + IPC map, "
+                       "remapped layers, measure-all, report on every rank; wall clock max over ranks"}
     jit = jit_stats()
     # adder circuit (BASELINE config 3, N=32 FP64, strong scaling) through the public API
     adder = None
