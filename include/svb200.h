@@ -247,6 +247,8 @@ int svk_pair_dot_chunk(const void* a0, const void* a1, uint64_t n_elems, int mod
 int svb_ipc_handles(sv_bhandle h, void* out256);
 int svb_cur(sv_bhandle h);
 int svb_swap_peer(sv_bhandle h, void* peer_mi, void* peer_pi, int l, int side);
+/* zeros into the pending planes (a tracked support after a remap swap of the current planes) */
+int svb_clear_pending(sv_bhandle h);
 /* BYTE planes form of svk_swap_group (current planes of this rank and the peer) */
 int svb_swap_group(sv_bhandle h, void* peer_mi, void* peer_pi, uint64_t victim_mask, uint64_t own_pattern,
                    uint64_t peer_pattern, uint64_t t_begin, uint64_t t_count);

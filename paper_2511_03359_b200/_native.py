@@ -122,6 +122,7 @@ _SIGNATURES = {
     "svb_cur": ([_P], _I),
     "svb_planes": ([_P, ctypes.POINTER(_P), ctypes.POINTER(_P)], _I),
     "svb_swap_peer": ([_P, _P, _P, _I, _I], _I),
+    "svb_clear_pending": ([_P], _I),
     "svb_swap_group": ([_P, _P, _P, _U64, _U64, _U64, _U64, _U64], _I),
     "svb_pair_dot": ([_P, _P, _P, _P, _P, _U64, _D], _I),
     "sv_buffer_alloc": ([_I, _U64, ctypes.POINTER(_P)], _I),

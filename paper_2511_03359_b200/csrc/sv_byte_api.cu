@@ -150,6 +150,15 @@ int svb_zero_state(sv_bhandle h, int64_t unit) {
     return SV_OK;
 }
 
+// zeros into the pending (not current) planes: after a remap swap moved the current planes
+// under a tracked support, the next support-restricted write pass relies on zeros outside it
+int svb_clear_pending(sv_bhandle h) {
+    Guard gd(h->device);
+    const uint64_t n = 1ull << h->n;
+    for (int p = 0; p < 2; ++p) BTRY(cudaMemsetAsync(h->plane[1 - h->cur][p], 0, n, h->stream), "zero pending planes");
+    return SV_OK;
+}
+
 int svb_set_tables(sv_bhandle h, const double* mags, int n_mag, const double* thetas, const double* ux,
                    const double* uy, int n_ph) {
     if (n_mag < 1 || n_mag > 256 || n_ph < 1 || n_ph > 256) return capi_fail(SV_EVALUE, "table size out of range");

@@ -123,7 +123,30 @@ def _prepare_peer_maps(dist, device: int, shape) -> dict:
 _OVERLAP_EVENTS: dict = {}  # (device, rank, world, chunks) -> (stream, own events, peer events)
 
 
-class CudaBackend:
+class _SupportBook:
+    """The global state's support {i : (i & ~sup_free) == sup_val} in physical positions,
+    identical on every rank (the same ops move it everywhere); a remap swap exchanges the
+    bits of its two positions."""
+
+    def _swap_bits(self, pairs) -> None:
+        for a, b in pairs:
+            for name in ("sup_free", "sup_val"):
+                x = getattr(self, name)
+                if ((x >> a) ^ (x >> b)) & 1:
+                    x ^= (1 << a) | (1 << b)
+                setattr(self, name, x)
+
+    def _slice_empty(self) -> bool:
+        """True when a fixed global bit of the support differs from this rank's bit."""
+        gmask = ((1 << self.n) - 1) & ~((1 << self.n_local) - 1)
+        return bool((self.sup_val ^ (self.rank << self.n_local)) & gmask & ~self.sup_free)
+
+    def _pair_is_zero(self, global_pos: int) -> bool:
+        """A fixed global qubit: one amplitude of every pair is zero, the cross sum is 0."""
+        return self.track and not (self.sup_free >> global_pos) & 1
+
+
+class CudaBackend(_SupportBook):
     """This rank's slice in HBM plus IPC-mapped slices of every other rank."""
 
     def __init__(self, dist, n_local: int, mode: PrecisionMode, device: int, tile_bits: int = 12):
@@ -182,19 +205,6 @@ class CudaBackend:
         nat.check(nat.load(require_device=False).sv_support_advance(ops_array(ops), len(ops), ctypes.byref(f),
                                                                     ctypes.byref(v)))
         self.sup_free, self.sup_val = f.value, v.value
-
-    def _swap_bits(self, pairs) -> None:
-        for a, b in pairs:
-            for name in ("sup_free", "sup_val"):
-                x = getattr(self, name)
-                if ((x >> a) ^ (x >> b)) & 1:
-                    x ^= (1 << a) | (1 << b)
-                setattr(self, name, x)
-
-    def _slice_empty(self) -> bool:
-        """True when a fixed global bit of the support differs from this rank's bit."""
-        gmask = ((1 << self.n) - 1) & ~((1 << self.n_local) - 1)
-        return bool((self.sup_val ^ (self.rank << self.n_local)) & gmask & ~self.sup_free)
 
     def _restrict(self) -> bool:
         """Hand this slice's support to the handle; False when the slice can only hold zeros."""
@@ -521,10 +531,6 @@ class CudaBackend:
         self.link_bytes += tc * self.bpe
         return complex(res[0], res[1])
 
-    def _pair_is_zero(self, global_pos: int) -> bool:
-        """A fixed global qubit: one amplitude of every pair is zero, the cross sum is 0."""
-        return self.track and not (self.sup_free >> global_pos) & 1
-
     def pair_dot(self, global_pos: int) -> complex:
         """This rank's share of sum conj(a0) a1 for a global qubit (measure.py:92-99)."""
         if self._pair_is_zero(global_pos):
@@ -596,7 +602,7 @@ class CudaBackend:
         self.peers = {}
 
 
-class CudaByteBackend:
+class CudaByteBackend(_SupportBook):
     """BYTE slice (two uint8 planes, double-buffered) + IPC-mapped peer planes.
 
     Every gate runs the reference's per-gate codebook barrier across ranks: each rank
@@ -639,7 +645,25 @@ class CudaByteBackend:
         self.passes = 0
         self.scan_first = False
         self.host_fixes = 0
+        # support tracking (_SupportBook), monotone as in ByteEngineState: every non-diagonal
+        # gate frees its qubits, so both plane buffers hold zeros outside the support -- after
+        # a remap swap moved the current planes, the pending ones are cleared to keep that
+        self.n = n_local + (self.world.bit_length() - 1)
+        self.track = _DIST_SUPPORT
+        self.sup_free, self.sup_val = 0, 0
         dist.barrier()
+
+    def _tracked(self) -> bool:
+        """Tracking, and the support still fixes some bit (else every pass is dense)."""
+        return self.track and self.sup_free != (1 << self.n) - 1
+
+    def _after_swap(self, pairs) -> None:
+        if not self.track:
+            return
+        tracked = self._tracked()
+        self._swap_bits(pairs)
+        if tracked:
+            nat.check(nat.load().svb_clear_pending(self.st.handle))
 
     def _sync_all(self):
         self.st.synchronize()
@@ -658,6 +682,7 @@ class CudaByteBackend:
         nat.check(nat.load().svb_swap_peer(self.st.handle, pm, pp, local_pos, side))
         self._sync_all()
         self.st.version += 1
+        self._after_swap(((global_pos, local_pos),))
         self.link_bytes += 2 * (self.st.size // 4) * 2
 
     def swap_group(self, pairs) -> None:
@@ -670,6 +695,7 @@ class CudaByteBackend:
             self.link_bytes += 2 * cnt * 2
         self._sync_all()
         self.st.version += 1
+        self._after_swap(pairs)
 
     def _desc(self, gate, phys, pos):
         from .byte_state import SvbGateDesc, _exchange_fields, set_logical_bits
@@ -698,6 +724,13 @@ class CudaByteBackend:
         _exchange_fields(d, gate, self.layout, plan)
         set_logical_bits(d, self.layout, pos, self.rank << n_local)
         d.mag_cut = d.ph_cut = 1e308
+        if self._tracked():   # the passes visit only the slice's support items (an empty slice: one)
+            lm = (1 << n_local) - 1
+            if self._slice_empty():
+                d.sup_fixed, d.sup_val = lm, 0
+            else:
+                d.sup_fixed = ~self.sup_free & lm
+                d.sup_val = self.sup_val & d.sup_fixed
         return d
 
     def _pass(self, d, producer, collect, scan, in_place=False):
@@ -764,11 +797,25 @@ class CudaByteBackend:
                 ui = np.concatenate([u[0] for u in unsure])
                 uv = np.concatenate([u[1] for u in unsure])
         self.host_fixes += self.st.finish_gate(ui, uv, final_in_place)
+        if self.track and not g.is_diagonal(gate):
+            for p in phys:
+                self.sup_free |= 1 << p
 
     def measure_local(self):
-        return self.st.measure_sums()
+        if self._tracked():
+            if self._slice_empty():
+                n = self.n_local
+                return 0.0, np.zeros(n), np.zeros(n, dtype=np.complex128)
+            lm = (1 << self.n_local) - 1
+            self.st.sup_free, self.st.sup_val = self.sup_free & lm, self.sup_val & lm   # svb_measure_support
+        try:
+            return self.st.measure_sums()
+        finally:
+            self.st.sup_free = (1 << self.n_local) - 1
 
     def pair_dot(self, global_pos: int) -> complex:
+        if self._pair_is_zero(global_pos):
+            return 0j
         bit = global_pos - self.n_local
         partner = self.rank ^ (1 << bit)
         low = ((self.rank >> bit) & 1) == 0

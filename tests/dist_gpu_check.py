@@ -94,7 +94,11 @@ def main():
                   ("adder6_be", adder(6, [45, 18])[0]),
                   # rank slices of >= 16 qubits: the tiled BYTE measurement (a rank slice is
                   # dense -- remap swaps move amplitudes between ranks, no support is tracked)
-                  ("bench18_be", benchmark(18)), ("adder9_be", adder(9, [300, 77])[0])]
+                  ("bench18_be", benchmark(18)), ("adder9_be", adder(9, [300, 77])[0]),
+                  # tracked support across ranks (monotone): restricted passes, empty slices,
+                  # pending planes cleared after remap swaps
+                  ("sparse18_be", sparse_circuit(np.random.default_rng(35), 18, 80, 3)),
+                  ("sparse14_be", sparse_circuit(np.random.default_rng(36), 14, 60, 2))]
     for name, circ in byte_cases:
         res = run_circuit_distributed(to_product(circ), dist, mode=PrecisionMode.BYTE, device=dev)
         planes = res.gathered_bytes(dist)
