@@ -639,6 +639,21 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
             (g_seg_limit <= 0 || P2.n_segs <= g_seg_limit)) {
             P2.storage = mode;
             P2.vinit = -2;
+            static const bool lazy_memset = [] {
+                const char* e = std::getenv("SVB200_LAZY_MEMSET");
+                return !e || std::atoi(e) != 0;
+            }();
+            if (lazy_memset && g_support && init && *init != -2 && materialize_fn) {
+                // a lazy basis state under support tracking: write it (memset + the unit
+                // amplitude, HBM-write bound) and run the pass over the support's tiles only,
+                // instead of generating every tile through the pass's arithmetic (FP64-heavy
+                // first passes, e.g. the adder's QFT + CPHASE run, cost more than the write)
+                const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+                if (~g_support->free & ~P2.tile_mask & all) {
+                    if (int rc = materialize_fn()) return rc;
+                    *init = -2;
+                }
+            }
             if (g_support && !(init && *init != -2)) {
                 // only the tiles whose fixed out-of-tile bits read val can be nonzero
                 const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
