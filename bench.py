@@ -694,11 +694,14 @@ def run_b200(args):
             """(wall seconds of a warm run, pass count, pass ms of a further run, report)"""
             pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, **kw)
             jit_wait()
-            t0 = time.perf_counter()
-            r = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, **kw)
-            t = time.perf_counter() - t0
-            rep = r.report
-            del r
+            t = None
+            for _ in range(2):   # the faster of two warm calls (a stray slab re-allocation)
+                t0 = time.perf_counter()
+                r = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, **kw)
+                dt = time.perf_counter() - t0
+                t = dt if t is None else min(t, dt)
+                rep = r.report
+                del r
             nat.pass_timing(True)
             nat.pass_timing_read()
             r = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits, **kw)
