@@ -1025,7 +1025,8 @@ def run_b200_multi(args, dist, rank, world, device):
     be.close()
     be.dev.free()
     del be
-    if args.nccl_probe_gib > 0:
+    shared = int(os.environ.get("SVB200_DEVICES", "0") or 0)
+    if args.nccl_probe_gib > 0 and not (0 < shared < world):   # (NCCL: one rank per GPU)
         nvlink["nccl_baseline"] = nccl_probe(dist, rank, world, device, args.nccl_probe_gib)
     # end to end through the public API: run_circuit_distributed(layer + M) per step
     e2e = None
