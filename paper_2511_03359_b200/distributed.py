@@ -60,6 +60,45 @@ def phys_op(gate, phys: tuple, n_local: int, rank: int):
     return gate_op(nat.SV_OP_2Q, qa=phys[0], qb=phys[1], data=m)
 
 
+def all_gather_candidates(dist, mine):
+    """The per-gate codebook barrier's exchange: every rank's [(magnitudes, phase values)]
+    per reference rank, gathered in rank order -- the result of dist.all_gather_object,
+    built from two tensor all-gathers (lengths, then one padded float64 buffer per rank)
+    instead of pickling on the per-gate path.  Non-gloo groups use all_gather_object."""
+    world = dist.get_world_size()
+    if dist.get_backend() != "gloo":
+        every = [None] * world
+        dist.all_gather_object(every, mine)
+        return every
+    import torch
+    R = len(mine)
+    parts = [np.asarray([len(m) for m, _ in mine] + [len(p) for _, p in mine], dtype=np.float64)]
+    for m, p in mine:
+        parts.append(np.ascontiguousarray(m, dtype=np.float64).ravel())
+        parts.append(np.ascontiguousarray(p, dtype=np.complex128).ravel().view(np.float64))
+    buf = np.concatenate(parts)
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([buf.size], dtype=torch.int64))
+    L = max(int(t.item()) for t in sizes)
+    mine_t = torch.zeros(L, dtype=torch.float64)
+    mine_t[:buf.size] = torch.from_numpy(buf)
+    outs = [torch.empty(L, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(outs, mine_t)
+    every = []
+    for t in outs:
+        a = t.numpy()
+        lm, lp = a[:R].astype(np.int64), a[R:2 * R].astype(np.int64)
+        off, lst = 2 * R, []
+        for r in range(R):
+            m = a[off:off + lm[r]].copy()
+            off += int(lm[r])
+            ph = a[off:off + 2 * lp[r]].copy().view(np.complex128)
+            off += 2 * int(lp[r])
+            lst.append((m, ph))
+        every.append(lst)
+    return every
+
+
 # SVB200_SUPPORT=0: distributed FP runs process every tile of every pass (no support tracking)
 _DIST_SUPPORT = os.environ.get("SVB200_SUPPORT", "1") != "0"
 
@@ -778,8 +817,7 @@ class CudaByteBackend(_SupportBook):
                     mags, ph, u = self._pass(d, r, True, scan)
                     mine.append((mags, ph))
                     unsure.append(u)
-            every = [None] * self.world
-            self.dist.all_gather_object(every, mine)
+            every = all_gather_candidates(self.dist, mine)
             proposals = []
             for r in range(self.layout.rank_count):
                 mags = np.concatenate([every[k][r][0] for k in range(self.world)])

@@ -127,3 +127,48 @@ def test_peer_map_cache_decisions(monkeypatch):
     assert d.barriers == 4 and closed[-1] == (0, "p2")
     D.release_peer_maps(d)
     assert D._PEER_MAPS == {} and d.barriers == 5 and len(unexports) == 5
+
+
+def _gather_worker(rank, world, port, outq):
+    import sys
+    import torch.distributed as dist
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_03359_b200.distributed import all_gather_candidates
+        rng = np.random.default_rng(100 + rank)
+        mine = []
+        for r in range(world):      # ragged, empty and -0.0 entries
+            nm, npp = int(rng.integers(0, 5)) * (r != rank), int(rng.integers(0, 4))
+            mags = rng.random(nm)
+            ph = rng.normal(size=npp) + 1j * rng.normal(size=npp)
+            if npp:
+                ph[0] = complex(-0.0, 0.0)
+            mine.append((mags, ph))
+        fast = all_gather_candidates(dist, mine)
+        ref = [None] * world
+        dist.all_gather_object(ref, mine)
+        same = all(len(a) == len(b) and all(
+            x[0].tobytes() == y[0].tobytes() and x[1].tobytes() == y[1].tobytes() and x[1].dtype == y[1].dtype
+            for x, y in zip(a, b)) for a, b in zip(fast, ref))
+        outq.put((rank, same))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_candidate_all_gather_equals_all_gather_object(world):
+    """The BYTE barrier's tensor all-gather returns exactly what all_gather_object does."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(same for _, same in got), got
