@@ -239,7 +239,28 @@ int classify(const double* m, int dim, uint32_t* mono) {
 struct Support {
     bool on = false;
     uint64_t free = 0, val = 0;
+    // dirty: HBM outside the support was never written (a lazy basis state whose first pass
+    // generated only the support's tiles); passes then load it as zeros (Fused2Params::pfix),
+    // every other reader first zero-fills it (clean_support)
+    bool dirty = false;
 };
+__global__ void k_zero_outside(c64s* __restrict__ psi, uint64_t n, uint64_t fixed, uint64_t val) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        if ((i & fixed) != val) psi[i] = c64s{0.0, 0.0};
+}
+// zeros into the never-written part of a dirty FP64 state (HBM-write bound, like a memset)
+static int clean_support(void* psi, uint64_t n_elems, Support& s, cudaStream_t st) {
+    if (!s.on || !s.dirty) return SV_OK;
+    const uint64_t fixed = ~s.free & (n_elems - 1);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    k_zero_outside<<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(static_cast<c64s*>(psi), n_elems, fixed,
+                                                               s.val & fixed);
+    count_launch();
+    s.dirty = false;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SV_OK : cuda_fail(e, "zero-fill outside the support");
+}
 static thread_local Support* g_support = nullptr;   // the handle's, for one fused_impl call
 struct SupportScope {
     Support* prev;
@@ -643,39 +664,95 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
                 const char* e = std::getenv("SVB200_LAZY_MEMSET");
                 return !e || std::atoi(e) != 0;
             }();
+            static const bool lazy_pred = [] {
+                const char* e = std::getenv("SVB200_LAZY_PRED");
+                return !e || std::atoi(e) != 0;
+            }();
+            const uint64_t allq = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+            // tile-index bits of the support's fixed out-of-tile qubits and their values
+            auto restrict_tiles = [&](uint64_t fixed_out, uint64_t* cm, uint64_t* cp) {
+                *cm = *cp = 0;
+                int j = 0;
+                for (int q = 0; q < n; ++q) {
+                    if ((P2.tile_mask >> q) & 1) continue;
+                    if ((fixed_out >> q) & 1) {
+                        *cm |= 1ull << j;
+                        if ((g_support->val >> q) & 1) *cp |= 1ull << j;
+                    }
+                    ++j;
+                }
+            };
             if (lazy_memset && g_support && init && *init != -2 && materialize_fn) {
-                // a lazy basis state under support tracking: write it (memset + the unit
-                // amplitude, HBM-write bound) and run the pass over the support's tiles only,
-                // instead of generating every tile through the pass's arithmetic (FP64-heavy
-                // first passes, e.g. the adder's QFT + CPHASE run, cost more than the write)
-                const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
-                if (~g_support->free & ~P2.tile_mask & all) {
+                // a lazy basis state under support tracking.  FP64 specialised passes: generate
+                // only the support's tiles and leave the rest of HBM unwritten (dirty: later
+                // passes load it as zeros, other readers zero-fill it first).  Otherwise write
+                // the state (memset + the unit amplitude) and run the pass over the support's
+                // tiles only -- either way no pass generates every tile through its arithmetic
+                const uint64_t fixed_out = ~g_support->free & ~P2.tile_mask & allq;
+                if (fixed_out) {
+                    if (lazy_pred && mode == SV_FP64 && jit_predicable(P2)) {
+                        uint64_t cm, cp;
+                        restrict_tiles(fixed_out, &cm, &cp);
+                        const uint64_t full_tiles = P2.n_tiles;
+                        P2.cmask_t = cm;
+                        P2.cpat_t = cp;
+                        P2.n_tiles >>= __builtin_popcountll(cm);
+                        P2.vinit = *init;
+                        const int jr = jit_launch_fused(psi, P2, st);
+                        if (jr < 0) return cuda_fail(cudaErrorLaunchFailure, "fused pass launch");
+                        if (jr == 0) {
+                            *init = -2;
+                            g_support->dirty = true;
+                            g_support_tiles_skipped += full_tiles - P2.n_tiles;
+                            if (g_timing) {
+                                cudaEventRecord(ev1, st);
+                                std::lock_guard<std::mutex> lk(g_timing_mu);
+                                g_timed.push_back({ev0, ev1, 0.5 * pass_bytes * (double)P2.n_tiles / (double)full_tiles});
+                            }
+                            advance_support();
+                            cur = PassPlan();
+                            return SV_OK;
+                        }
+                        P2.cmask_t = 0;   // not compiled yet: write the state
+                        P2.cpat_t = 0;
+                        P2.n_tiles = full_tiles;
+                        P2.vinit = -2;
+                    }
                     if (int rc = materialize_fn()) return rc;
                     *init = -2;
                 }
             }
+            // a dirty support (unwritten HBM outside it): the plain specialised FP64 passes load
+            // those amplitudes as zeros; any other kernel needs them written first
+            auto predicate = [&]() -> int {
+                if (!g_support || !g_support->dirty) return SV_OK;
+                if (mode == SV_FP64 && jit_predicable(P2)) {
+                    P2.pfix = ~g_support->free & allq;
+                    P2.pval = g_support->val & P2.pfix;
+                    return SV_OK;
+                }
+                return clean_support(psi, n_elems, *g_support, st);
+            };
+            auto unpredicate = [&]() -> int {   // before a generic-kernel fallback
+                P2.pfix = P2.pval = 0;
+                return g_support ? clean_support(psi, n_elems, *g_support, st) : SV_OK;
+            };
             if (g_support && !(init && *init != -2)) {
                 // only the tiles whose fixed out-of-tile bits read val can be nonzero
                 const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
                 const uint64_t fixed_out = ~g_support->free & ~P2.tile_mask & all;
                 if (fixed_out) {
-                    uint64_t cm = 0, cp = 0;
-                    int j = 0;
-                    for (int q = 0; q < n; ++q) {
-                        if ((P2.tile_mask >> q) & 1) continue;
-                        if ((fixed_out >> q) & 1) {
-                            cm |= 1ull << j;
-                            if ((g_support->val >> q) & 1) cp |= 1ull << j;
-                        }
-                        ++j;
-                    }
+                    uint64_t cm, cp;
+                    restrict_tiles(fixed_out, &cm, &cp);
                     const uint64_t full_tiles = P2.n_tiles;
                     P2.cmask_t = cm;
                     P2.cpat_t = cp;
                     P2.n_tiles >>= __builtin_popcountll(cm);
+                    if (int rc = predicate()) return rc;
                     int jr = jit_launch_fused(psi, P2, st);
                     if (jr < 0) return cuda_fail(cudaErrorLaunchFailure, "fused pass launch");
                     if (jr != 0 && mode == SV_FP64) {   // not compiled yet: the generic kernel takes chunks too
+                        if (int rc = unpredicate()) return rc;
                         count_h2d(sizeof(Fused2Params));
                         const cudaError_t eg = launch_fused2(psi, mode, P2, st);
                         if (eg != cudaSuccess) return cuda_fail(eg, "fused pass launch");
@@ -693,6 +770,7 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
                         return SV_OK;
                     }
                     // FP32, specialised kernel not compiled yet: the whole state through v1
+                    if (int rc = unpredicate()) return rc;
                     P2.cmask_t = 0;
                     P2.cpat_t = 0;
                     P2.n_tiles = full_tiles;
@@ -717,18 +795,28 @@ int fused_impl(void* psi, uint64_t n_elems, int mode, const sv_op* ops, int n_op
                 *init = -2;
                 P2.vinit = -2;
             }
+            if (int rc = predicate()) return rc;
             const int jr = jit_launch_fused(psi, P2, st);
             count_h2d(sizeof(Fused2Params));
             if (jr < 0) e = cudaErrorLaunchFailure;
-            else if (jr == 0) e = cudaSuccess;
-            else e = mode == SV_FP64 ? launch_fused2(psi, mode, P2, st) : v1();   // not compiled yet
+            else if (jr == 0) {
+                e = cudaSuccess;
+                if (P2.pfix) g_support->dirty = false;   // every tile written
+            } else {                                     // not compiled yet
+                if (int rc = unpredicate()) return rc;
+                e = mode == SV_FP64 ? launch_fused2(psi, mode, P2, st) : v1();
+            }
         } else if (mode == SV_FP32 && use_v3) {
+            if (g_support)
+                if (int rc = clean_support(psi, n_elems, *g_support, st)) return rc;
             if (init && *init != -2) {
                 if (int rc = materialize_fn ? materialize_fn() : SV_OK) return rc;
                 *init = -2;
             }
             e = v1();
         } else {
+            if (g_support)
+                if (int rc = clean_support(psi, n_elems, *g_support, st)) return rc;
             if (init && *init != -2) {
                 if (int rc = materialize_fn ? materialize_fn() : SV_OK) return rc;
                 *init = -2;
@@ -1307,6 +1395,7 @@ int sv_zero_state(sv_handle h, int64_t unit) {
     h->sup.on = h->track && unit >= 0;
     h->sup.free = 0;
     h->sup.val = unit >= 0 ? (uint64_t)unit : 0;
+    h->sup.dirty = false;
     h->lazy = -2;
     const size_t eb = elem_bytes(h->mode);
     const uint64_t n = 1ull << h->n;
@@ -1332,12 +1421,17 @@ int sv_zero_state_lazy(sv_handle h, int64_t unit) {
     h->sup.on = h->track && unit >= 0;
     h->sup.free = 0;
     h->sup.val = unit >= 0 ? (uint64_t)unit : 0;
+    h->sup.dirty = false;
     return SV_OK;
 }
 
 int sv_set_support_tracking(sv_handle h, int on) {
     h->track = on ? 1 : 0;
-    if (!on) h->sup.on = false;
+    if (!on) {
+        DeviceGuard g(h->device);
+        if (int rc = clean_support(h->ptr, 1ull << h->n, h->sup, h->stream)) return rc;
+        h->sup.on = false;
+    }
     return SV_OK;
 }
 
@@ -1347,6 +1441,7 @@ int sv_set_support(sv_handle h, uint64_t free_mask, uint64_t val) {
     const uint64_t all = h->n >= 64 ? ~0ull : ((1ull << h->n) - 1ull);
     h->track = 1;
     h->sup.on = true;
+    if (int rc = clean_support(h->ptr, 1ull << h->n, h->sup, h->stream)) return rc;
     h->sup.free = free_mask & all;
     h->sup.val = val & ~free_mask & all;
     return SV_OK;
@@ -1379,7 +1474,7 @@ int sv_support_info(sv_handle h, int* on, uint64_t* free_mask, uint64_t* val, ui
 }
 
 static int materialize(sv_handle h) {
-    if (h->lazy == -2) return SV_OK;
+    if (h->lazy == -2) return clean_support(h->ptr, 1ull << h->n, h->sup, h->stream);
     const int64_t u = h->lazy;
     return sv_zero_state(h, u);   // clears h->lazy
 }

@@ -101,6 +101,11 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
 }
+// the same with a source size: 0 fills the 16 shared-memory bytes with zeros, reading nothing
+__device__ __forceinline__ void cp_async16_z(void* smem_dst, const void* gsrc, unsigned bytes) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -192,7 +197,7 @@ __device__ __forceinline__ cplx rmul(double m, cplx a) { return {__dmul_rn(m, a.
 // constant loads ptxas hoists every matrix of the pass out of the tile loop, the
 // uniform registers overflow into ~130 regular registers for a few U4 gates and the
 // kernel spills; a per-use LDC costs one instruction per entry per tile.
-constexpr int kArgsM = 32;   // byte offset of Args::m (after n_tiles, cmask, cpat, vinit)
+constexpr int kArgsM = 48;   // byte offset of Args::m (after n_tiles, cmask, cpat, vinit, pfix, pval)
 
 // tile index t of a chunked launch -> full tile index: zeros inserted at the bits of cm,
 // then the chunk pattern

@@ -52,6 +52,8 @@ struct Fused2Params {
                                         // the remaining tiles); 0, 0 = every tile
     int64_t vinit;                      // -2: read the tiles; -1 / u: generate them (all zeros / |u>),
                                         // specialised kernel only (lazy zero state, first pass)
+    uint64_t pfix, pval;                // pfix != 0: amplitudes with (i & pfix) != pval load as zeros
+                                        // (a tracked support over memory not yet written; cp.async zfill)
     int8_t tq[13];                      // tile position -> qubit (2^13 tiles: config 10)
     uint8_t seg_reg[kMaxSegs][4];       // register bit j -> tile position
     uint8_t seg_thr[kMaxSegs][9];       // thread-id bit j -> tile position
@@ -72,6 +74,7 @@ struct Fused2Params {
 cudaError_t launch_fused2(void* psi, int mode, const Fused2Params& p, cudaStream_t st);
 // run-time specialised form of the same pass (sv_jit.cu): 0 launched, 1 not ready, < 0 error
 int jit_launch_fused(void* psi, const Fused2Params& p, cudaStream_t st);
+bool jit_predicable(const Fused2Params& p);     // the pass's tile loads honour pfix / pval
 int jit_prepare_fused(const Fused2Params& p);   // queue the compile; 1 if a new kernel was queued
 bool jit_enabled();                             // JIT mode != 0 and NVRTC present
 }  // namespace sv
