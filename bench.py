@@ -680,9 +680,14 @@ def run_b200(args):
         t_first = time.perf_counter() - t0
         del res
         jit_wait()                       # the first run queued the adder's pass kernels
-        t0 = time.perf_counter()
-        res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
-        t_adder = time.perf_counter() - t0
+        t_adder = None
+        for rep in range(3):             # warm calls (the fastest: a stray slab re-allocation or
+            if rep:                      # first launch of a helper kernel is not the circuit)
+                del res
+            t0 = time.perf_counter()
+            res = pb.run_circuit(circ, device=device, tile_bits=args.tile_bits)
+            dt = time.perf_counter() - t0
+            t_adder = dt if t_adder is None else min(t_adder, dt)
         kat = all(abs(res.report.qz[q] - 1.0) < 1e-12 for q in regs["R2"])
         rep_support = res.device_stats.get("support")
         rep_exact = res.report

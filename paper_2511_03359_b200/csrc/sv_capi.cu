@@ -245,20 +245,58 @@ struct Support {
     bool dirty = false;
 };
 __global__ void k_zero_outside(c64s* __restrict__ psi, uint64_t n, uint64_t fixed, uint64_t val) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        if ((i & fixed) != val) psi[i] = c64s{0.0, 0.0};
+    const uint64_t step = (uint64_t)gridDim.x * blockDim.x * 4;
+    for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * 4; i < n; i += step) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (i + k < n && ((i + k) & fixed) != val) psi[i + k] = c64s{0.0, 0.0};
+    }
 }
-// zeros into the never-written part of a dirty FP64 state (HBM-write bound, like a memset)
+// the support's amplitudes {deposit(t, free) | val} to / from a compact buffer
+__global__ void k_support_copy(c64s* __restrict__ psi, c64s* __restrict__ buf, uint64_t m, uint64_t freem,
+                               uint64_t val, int to_buf) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < m; t += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t i = val, f = freem, tt = t;
+        while (f) {
+            const uint64_t b = f & (~f + 1ull);
+            if (tt & 1ull) i |= b;
+            tt >>= 1;
+            f &= f - 1ull;
+        }
+        if (to_buf) buf[t] = psi[i];
+        else psi[i] = buf[t];
+    }
+}
+// zeros into the never-written part of a dirty FP64 state.  A small support (<= 2^24
+// amplitudes): saved, the whole state memset (the copy engine's write rate), restored;
+// otherwise a zero-fill kernel over the complement
 static int clean_support(void* psi, uint64_t n_elems, Support& s, cudaStream_t st) {
     if (!s.on || !s.dirty) return SV_OK;
-    const uint64_t fixed = ~s.free & (n_elems - 1);
+    const uint64_t all = n_elems - 1, freem = s.free & all, fixed = ~s.free & all, val = s.val & fixed;
     int dev = 0;
     cudaGetDevice(&dev);
-    k_zero_outside<<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(static_cast<c64s*>(psi), n_elems, fixed,
-                                                               s.val & fixed);
-    count_launch();
+    const unsigned grid = (unsigned)sm_count(dev) * 8;
+    const int nf = __builtin_popcountll(freem);
+    cudaError_t e = cudaSuccess;
+    if (nf <= 24) {
+        const uint64_t m = 1ull << nf;
+        c64s* buf = nullptr;
+        e = cudaMallocAsync(reinterpret_cast<void**>(&buf), m * sizeof(c64s), st);
+        if (e == cudaSuccess) {
+            const unsigned g = (unsigned)std::min<uint64_t>(grid, (m + 255) / 256);
+            k_support_copy<<<g, 256, 0, st>>>(static_cast<c64s*>(psi), buf, m, freem, val, 1);
+            e = cudaMemsetAsync(psi, 0, n_elems * sizeof(c64s), st);
+            if (e == cudaSuccess) k_support_copy<<<g, 256, 0, st>>>(static_cast<c64s*>(psi), buf, m, freem, val, 0);
+            cudaFreeAsync(buf, st);
+            count_launch();
+            count_launch();
+        }
+    } else {
+        k_zero_outside<<<grid, 256, 0, st>>>(static_cast<c64s*>(psi), n_elems, fixed, val);
+        count_launch();
+    }
     s.dirty = false;
-    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? SV_OK : cuda_fail(e, "zero-fill outside the support");
 }
 static thread_local Support* g_support = nullptr;   // the handle's, for one fused_impl call
