@@ -732,8 +732,8 @@ def run_b200(args):
                                   "fp64_floor_ms": d_roof["fp64_floor_ms"], "max_floor_ms": d_roof["max_floor_ms"],
                                   "frac_of_max_floor": d_roof["frac"],
                                   "fp64_per_amplitude": d_roof["fp64_per_amplitude"]},
-                 "what": "run_circuit wall clock incl. allocation, |0..0>, fused passes, measure-all (second "
-                         "run: specialised pass kernels compiled; first_run_seconds: cold).  The adder's state "
+                 "what": "run_circuit wall clock incl. allocation, |0..0>, fused passes, measure-all (fastest "
+                         "of three warm runs: specialised pass kernels compiled; first_run_seconds: cold).  The adder's state "
                          "stays inside a 2^k-amplitude support (basis-state inputs, only one register "
                          "superposed), which run_circuit tracks: passes and measurement read only its tiles "
                          "(support_passes).  dense_*: track_support=False, every tile, with the passes' "
