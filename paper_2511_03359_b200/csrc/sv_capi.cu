@@ -966,6 +966,10 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
         }
         P.n_out = o;
         P.base_const = fixv & ~tmask;                             // and carry the fixed ones
+        if (tracked && sup->dirty && !byte) {                     // unwritten HBM outside the support
+            P.pfix = ~freem & all;
+            P.pval = fixv;
+        }
         P.n_tiles = 1ull << o;
         int b = 0;
         while (b < K && P.tq[b] == b) ++b;
@@ -982,7 +986,7 @@ int measure3_impl(const void* psi, int n, double* norm, double* ones, double* cr
         }
         int n_hi = 0;
         for (int i : cpos) n_hi += i >= 5;
-        P.direct = (denv && !byte && K == 12 && b >= 5 && n_hi >= RB) ? 1 : 0;
+        P.direct = (denv && !byte && !P.pfix && K == 12 && b >= 5 && n_hi >= RB) ? 1 : 0;
         if (P.direct) std::stable_partition(cpos.begin(), cpos.end(), [](int i) { return i >= 5; });
         P.n_segs = (int)((cpos.size() + RB - 1) / RB);
         if (P.n_segs < 1) P.n_segs = 1;
@@ -1670,7 +1674,13 @@ int sv_apply_fused(sv_handle h, const sv_op* ops, int n_ops, int tile_bits) {
 }
 int sv_measure(sv_handle h, double* norm, double* ones, double* cross) {
     DeviceGuard g(h->device);
-    if (int rc = materialize(h)) return rc;
+    // a dirty support (never-written HBM outside it) is read through zero-filled loads by
+    // the register-resident FP64 measurement; any other form writes the zeros first
+    const char* m3 = std::getenv("SVB200_MEASURE3");
+    const bool zfill = h->lazy == -2 && h->sup.on && h->sup.dirty && h->mode == SV_FP64 && h->n >= 16 &&
+                       !(m3 && std::atoi(m3) == 0);
+    if (!zfill)
+        if (int rc = materialize(h)) return rc;
     return measure_impl(h->ptr, 1ull << h->n, h->mode, norm, ones, cross, h->partials, h->partial_cap,
                         h->stream, h->sup.on ? &h->sup : nullptr);
 }
@@ -1704,7 +1714,10 @@ int sv_import(sv_handle h, const void* host, uint64_t first, uint64_t count) {
 
 int sv_synchronize(sv_handle h) {
     DeviceGuard g(h->device);
-    if (int rc = materialize(h)) return rc;
+    // a pending lazy basis state is written; a dirty support's unwritten HBM stays unwritten
+    // (synchronising reads nothing; every reader zero-fills it first)
+    if (h->lazy != -2)
+        if (int rc = materialize(h)) return rc;
     CUDA_TRY(cudaStreamSynchronize(h->stream), "synchronize");
     return SV_OK;
 }

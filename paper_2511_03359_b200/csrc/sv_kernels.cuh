@@ -128,6 +128,7 @@ struct Measure3Params {
     uint64_t pf_go[16];                 // HBM offset of tile element j * threads (prefetch chunks)
     uint64_t base_tab[4][256];          // tile index byte -> local-index bits outside the tile
     uint64_t base_const;                // index bits every tile carries (fixed bits of a tracked support)
+    uint64_t pfix, pval;                // pfix != 0: amplitudes with (i & pfix) != pval load as zeros
     int direct;                         // segment 0 loads its registers from HBM (lanes = qubits 0..4)
     uint64_t seg0_go[16];               // direct: HBM offset of segment-0 register slot i
 };

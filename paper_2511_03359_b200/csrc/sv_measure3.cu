@@ -38,6 +38,11 @@ __device__ __forceinline__ void cp_async16m(void* smem_dst, const void* gsrc) {
 __device__ __forceinline__ void cp_commit_m() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait_m() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+// with a source size (0: 16 zero bytes, nothing read) -- a dirty support's unwritten HBM
+__device__ __forceinline__ void cp_async16mz(void* smem_dst, const void* gsrc, unsigned bytes) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(bytes) : "memory");
+}
 
 constexpr int kOutMax = 52;
 
@@ -103,7 +108,15 @@ __global__ void __launch_bounds__(1 << (KB - RB), MINB)
                p.base_tab[3][(t >> 24) & 255] | p.base_const;
     };
     auto prefetch = [&](uint64_t t, cplx* dst) {
-        const c64s* g = psi + tile_base(t) + go_tid;
+        const uint64_t gb = tile_base(t) + go_tid;
+        const c64s* g = psi + gb;
+        if (p.pfix) {   // amplitudes outside the support were never written: zeros
+#pragma unroll
+            for (int j = 0; j < R; ++j)
+                cp_async16mz(dst + (sw_tid + j * NT), g + p.pf_go[j],
+                             ((gb + p.pf_go[j]) & p.pfix) == p.pval ? 16u : 0u);
+            return;
+        }
 #pragma unroll
         for (int j = 0; j < R; ++j) cp_async16m(dst + (sw_tid + j * NT), g + p.pf_go[j]);
     };
