@@ -1068,7 +1068,7 @@ def run_b200_multi(args, dist, rank, world, device):
         from paper_2511_03359_b200.distributed import run_circuit_distributed
         circ, regs = pb.build_adder(16, [47302, 18233])
         times = []
-        for rep in range(2):
+        for rep in range(4):   # cold, then three warm runs (the fastest is reported)
             dist.barrier()
             t0 = time.perf_counter()
             res = run_circuit_distributed(circ, dist, device=device, tile_bits=args.tile_bits)
@@ -1081,11 +1081,11 @@ def run_b200_multi(args, dist, rank, world, device):
             del res
             jit_wait()
         adder = {"circuit": "build_adder(16, [47302, 18233])", "n_qubits": 32, "gates": len(circ.gates),
-                 "seconds": round(times[1], 4), "first_run_seconds": round(times[0], 4),
-                 "sec_per_gate": round(times[1] / len(circ.gates), 6), "kat_all_ones_R2": kat,
+                 "seconds": round(min(times[1:]), 4), "first_run_seconds": round(times[0], 4),
+                 "sec_per_gate": round(min(times[1:]) / len(circ.gates), 6), "kat_all_ones_R2": kat,
                  "swaps": stats.get("swaps"), "swap_groups": stats.get("swap_groups"),
                  "scaling": "strong (fixed N=32 over the GPUs)",
-                 "what": "run_circuit_distributed wall clock, max over ranks (second run: compiled kernels)"}
+                 "what": "run_circuit_distributed wall clock, max over ranks (fastest of three warm runs: compiled kernels)"}
     # traffic optimizer A/B (BASELINE config 4 circuit): the remap planner vs the reference's
     # per-gate exchange choreography (exchange-fused P2P pair updates), same circuit
     planner_ab = None
